@@ -1,0 +1,163 @@
+/*
+ * psdproj.h — C ABI of libpsdproj.so, the B200 (sm_100a) randomized
+ * PSD-cone projection.  Plain pointers and sizes only; every array argument
+ * is a DEVICE pointer on the plan's device, row-major, with the given leading
+ * dimension (in elements).  Calls are enqueued on `stream` (a cudaStream_t;
+ * NULL = legacy default stream) and synchronise with it only where the
+ * algorithm needs a host decision (symmetry verdict, CholeskyQR breakdown,
+ * rank truncation, effective rank), exactly where the reference raises or
+ * branches.
+ *
+ * Each entry point replaces one function of the reference `psdcone` package
+ * (/root/reference/pkg/src/psdcone, cited file:line below); INTEGRATION.md
+ * shows the ctypes binding a psdcone maintainer would add.
+ */
+#ifndef PSDPROJ_H
+#define PSDPROJ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes, 1:1 with the reference exception hierarchy (errors.py:4-49). */
+enum psd_status {
+  PSD_OK = 0,
+  PSD_ERR_INVALID_PARAMS = 1,  /* InvalidParams          errors.py:28 */
+  PSD_ERR_ASYMMETRIC = 2,      /* AsymmetricMatrixError  errors.py:12 */
+  PSD_ERR_RANK_DEFICIENT = 3,  /* RankDeficientSample    errors.py:20 */
+  PSD_ERR_ALPHA_TOO_SMALL = 4, /* AlphaTooSmall          errors.py:24 */
+  PSD_ERR_CONVERGENCE = 5,     /* ConvergenceFailure     errors.py:16 */
+  PSD_ERR_NONSQUARE = 6,       /* NonSquareError         errors.py:8  */
+  PSD_ERR_CUDA = 7,            /* CUDA runtime failure (no reference analogue) */
+  PSD_ERR_NO_MEMORY = 8        /* device allocation failed */
+};
+
+/* flags for psd_ran_proj / psd_range_finder */
+#define PSD_FLAG_DIAGNOSTICS 1u   /* residual_frob = ||X - Q Q^T X||_F   (projection.py:109-110) */
+#define PSD_FLAG_STRICT 2u        /* RankDeficientSample instead of truncation (sketch.py:86-92) */
+#define PSD_FLAG_SKIP_SYMCHECK 4u /* caller already ran psd_require_symmetric on X */
+#define PSD_FLAG_ASSUME_SYMMETRIC 8u /* X is bitwise symmetric: X^T·P computed as X·P */
+
+typedef struct psd_plan psd_plan;
+
+/* Stages timed by psd_plan_profile (CUDA events on the caller's stream). */
+enum psd_stage {
+  PSD_STAGE_SYMCHECK = 0,    /* require_symmetric pass                       */
+  PSD_STAGE_SKETCH_GEMM = 1, /* each op(X)·P product (n x n · n x w), DMMA     */
+  PSD_STAGE_QR = 2,          /* CholeskyQR (Gram, Cholesky, inverse, apply)  */
+  PSD_STAGE_COMPRESS = 3,    /* T = Q^T (X Q)                                */
+  PSD_STAGE_EIGH = 4,        /* block-Jacobi eigensolve + sort               */
+  PSD_STAGE_RECON = 5,       /* W = Q U, mirrored SYRK reconstruction        */
+  PSD_STAGE_DIAG = 6,        /* residual diagnostics                         */
+  PSD_STAGE_TOTAL = 7,       /* whole psd_ran_proj call                      */
+  PSD_NUM_STAGES = 8
+};
+
+typedef struct psd_report {
+  int32_t effective_rank;  /* ProjectionReport.effective_rank (projection.py:115) */
+  int32_t basis_width;     /* ProjectionReport.basis_width    (projection.py:118) */
+  int32_t used_transpose;  /* 1 if X^T multiplies ran on the transposed-operand kernel */
+  int32_t qr_passes;       /* CholeskyQR passes of the final orthonormalisation */
+  int32_t qr_shifted;      /* 1 if a shifted CholeskyQR pass was needed */
+  int32_t eig_sweeps;      /* block-Jacobi sweeps of the k x k eigensolve */
+  int32_t gpu_launches;    /* kernels this call launched */
+  int32_t reserved;
+  double residual_frob;    /* PSD_FLAG_DIAGNOSTICS only, else NaN */
+  double max_abs;          /* max|x_ij| (symmetric.py:51) */
+  double sym_defect;       /* max|x_ij - x_ji| (symmetric.py:52) */
+  double alpha_used;       /* alpha (ran_proj_scal) or 0 */
+} psd_report;
+
+/* Thread-local description of the last non-OK status. */
+const char* psd_last_error(void);
+const char* psd_version(void);
+
+/* Workspace for problems with dimension <= n and sketch width <= width on
+ * `device`.  A plan is not thread-safe; use one per host thread / stream. */
+int psd_plan_create(psd_plan** plan, int64_t n, int32_t width, int32_t device);
+void psd_plan_destroy(psd_plan* plan);
+/* Bytes of device memory the plan holds. */
+int64_t psd_plan_bytes(const psd_plan* plan);
+/* Stage profiling.  enable: 1 on, 0 off, -1 unchanged.  When ms_out /
+ * counts_out (HOST, PSD_NUM_STAGES each) are non-NULL they receive the
+ * accumulated milliseconds / event pairs per psd_stage; reset != 0 zeroes
+ * the accumulators afterwards. */
+int psd_plan_profile(psd_plan* plan, int32_t enable, double* ms_out, int32_t* counts_out,
+                     int32_t reset);
+
+/* require_symmetric — symmetric.py:39-57.  tol < 0 selects the reference
+ * default 1e-10*max(1, max|x|).  stats_out (HOST, 3 doubles) receives
+ * {max|x|, max|x - x^T|, 1.0 if bitwise symmetric else 0.0}. */
+int psd_require_symmetric(psd_plan* plan, const double* x, int64_t n, int64_t ldx, double tol,
+                          double* stats_out, void* stream);
+
+/* power_iteration — sketch.py:96-114: exactly n_iter normalised products of
+ * (X - shift*I) from v0 (device, length n), returns ||(X - shift I) v||_2, or
+ * 0 when an iterate is annihilated.  result: HOST double. */
+int psd_power_iteration(psd_plan* plan, const double* x, int64_t n, int64_t ldx, double shift,
+                        const double* v0, int32_t n_iter, double* result, void* stream);
+
+/* min_eig_magnitude — sketch.py:117-129 (Alg. 5) with start vectors v1, v2. */
+int psd_min_eig_magnitude(psd_plan* plan, const double* x, int64_t n, int64_t ldx,
+                          const double* v1, const double* v2, int32_t n_iter, double* result,
+                          void* stream);
+
+/* range_finder — sketch.py:53-93: basis (m x width, ld ldb) of the range of
+ * (X X^T)^q X Omega for an m x n X, Omega = omega (n x width, ld ldo).  alpha > 0 sketches
+ * B = (X + alpha I)/alpha instead (projection.py:139-140).  *width_out =
+ * number of columns kept by the 1e-12*||Y||_F truncation. */
+int psd_range_finder(psd_plan* plan, const double* x, int64_t m, int64_t n, int64_t ldx,
+                     const double* omega, int64_t ldo, int32_t width, int32_t q, double alpha,
+                     uint32_t flags, double* basis, int64_t ldb, int32_t* width_out,
+                     void* stream);
+
+/* eigh — symmetric.py:68-86 for an m x m symmetric matrix: values descending,
+ * each vector's largest-|entry| positive.  a is overwritten. */
+int psd_eigh(psd_plan* plan, double* a, int32_t m, int64_t lda, double* values, double* vectors,
+             int64_t ldv, int32_t* sweeps_out, void* stream);
+
+/* ran_proj (alpha == 0) — projection.py:92-119, Alg. 2;
+ * ran_proj_scal (alpha > 0) — projection.py:122-159, Alg. 3.
+ * omega: n x (k+l) Gaussian test matrix (ld ldo) — the reference's draw at
+ * sketch.py:75, passed in so both sides see identical inputs.
+ * result: n x n (ld ldr) or NULL; factors_w: n x (k+l) (ld ldw) or NULL —
+ * the first report->effective_rank columns receive W; factors_d: k+l or NULL.
+ * report: HOST. */
+int psd_ran_proj(psd_plan* plan, const double* x, int64_t n, int64_t ldx, const double* omega,
+                 int64_t ldo, int32_t k, int32_t l, int32_t q, double alpha, uint32_t flags,
+                 double* result, int64_t ldr, double* factors_w, int64_t ldw, double* factors_d,
+                 psd_report* report, void* stream);
+
+/* Dense X = sym(W diag(d) W^T) for W n x r (ld ldw), d[r] — the reconstruction
+ * of projection.py:72-78 (and of exact_psd_projection, symmetric.py:109-114):
+ * lower tiles on the FP64 tensor cores, each tile stored twice (mirrored). */
+int psd_reconstruct(psd_plan* plan, const double* w, int64_t n, int64_t ldw, const double* d,
+                    int32_t r, double* result, int64_t ldr, void* stream);
+
+/* symmetrize — symmetric.py:31-36, in place: a <- (a + a^T)/2 (m x m). */
+int psd_symmetrize(double* a, int64_t m, int64_t lda, void* stream);
+
+/* The FP64 DMMA GEMM itself: C (M x N) = op_A · op_B with
+ * a_layout 0: A[m*lda + k] (row-major M x K), 1: A[k*lda + m] (A^T stored);
+ * b_layout 0: B[k*ldb + n] (row-major K x N), 1: B[n*ldb + k] (B^T stored);
+ * epilogue 0: C = acc; 1: C = (acc + alpha*S)/alpha; 2: C = S - acc;
+ *          3: mirrored lower-tile store (M == N, a_layout 0, b_layout 1).
+ * ws/ws_elems: split-K scratch (may be NULL → no split). */
+int psd_gemm_f64(int32_t a_layout, int32_t b_layout, const double* a, int64_t lda, const double* b,
+                 int64_t ldb, double* c, int64_t ldc, int32_t m, int32_t n, int32_t k,
+                 int32_t epilogue, double alpha, const double* s, int64_t lds, double* ws,
+                 int64_t ws_elems, void* stream);
+
+/* Device-side N(0,1) fill (Philox4x32-10 + Box-Muller) for callers that do
+ * not need the reference's numpy stream (benchmarks, solver loops). */
+int psd_fill_gaussian(double* out, int64_t rows, int32_t cols, int64_t ld, uint64_t seed,
+                      uint64_t offset, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSDPROJ_H */

@@ -1,0 +1,32 @@
+"""paper_2410_19208_b200 — B200-native randomized projection onto the PSD cone.
+
+Drop-in for the hot path of the reference ``psdcone`` package (arXiv
+2410.19208): the same names, signatures, exceptions and RNG draw order, with
+every numeric step in hand-written sm_100a kernels (libpsdproj.so, C ABI in
+include/psdproj.h).  ``install()`` rebinds the reference modules so that
+``psdcone.solve`` and friends run on this path.
+"""
+
+from .errors import (AlphaTooSmall, AsymmetricMatrixError, ConvergenceFailure, DeviceError,
+                     DimensionMismatch, InvalidParams, NonSquareError, PsdconeError,
+                     RankDeficientSample)
+from ._tensors import DeviceRng
+from .projection import (METHODS, ProjectionReport, ProjectorConfig, flops, project, ran_proj,
+                         ran_proj_scal)
+from .sketch import (RangeParams, min_eig_magnitude, orthonormality_defect, power_iteration,
+                     range_finder)
+from .symmetric import (EigenDecomposition, eigh, exact_psd_projection, frobenius_norm,
+                        gaussian_matrix, require_symmetric, rng_from_seed, symmetrize)
+from .install import install, uninstall
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AlphaTooSmall", "AsymmetricMatrixError", "ConvergenceFailure", "DeviceError",
+    "DimensionMismatch", "InvalidParams", "NonSquareError", "PsdconeError", "RankDeficientSample",
+    "DeviceRng", "METHODS", "ProjectionReport", "ProjectorConfig", "flops", "project", "ran_proj",
+    "ran_proj_scal", "RangeParams", "min_eig_magnitude", "orthonormality_defect",
+    "power_iteration", "range_finder", "EigenDecomposition", "eigh", "exact_psd_projection",
+    "frobenius_norm", "gaussian_matrix", "require_symmetric", "rng_from_seed", "symmetrize",
+    "install", "uninstall",
+]

@@ -1,0 +1,900 @@
+// C ABI (include/psdproj.h) and the host-side orchestration of the randomized
+// PSD projection on one B200.  Every numeric step runs in the sm_100a kernels
+// of this library; the host only sequences launches and takes the decisions
+// the reference takes on the host (raise / truncate / count).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "launch.h"
+#include "psdproj.h"
+
+using ll = long long;
+
+namespace psd {
+thread_local int g_launch_count = 0;
+}
+
+struct psd_plan {
+  int device = 0;
+  ll n = 0;
+  int w = 0;
+  ll ldp = 0;  // leading dimension of n×w panels
+  double* panel[6] = {};
+  double *G = nullptr, *L = nullptr, *Rinv = nullptr, *T = nullptr, *V = nullptr, *U = nullptr;
+  double *vals = nullptr, *vals_sorted = nullptr, *rdiag = nullptr, *dvec = nullptr;
+  int* ints = nullptr;  // perm[w], npos, info, flags
+  double* ws = nullptr;
+  size_t ws_elems = 0;
+  double* jws = nullptr;
+  size_t jws_elems = 0;
+  double *gy = nullptr, *gv = nullptr, *gpart = nullptr, *stats = nullptr, *scal = nullptr;
+  int gparts = 0;
+  double* rpart = nullptr;
+  ll rparts = 0;
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+  // stage profiling (psd_plan_profile): CUDA events on the caller's stream
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  double stage_ms[PSD_NUM_STAGES] = {};
+  int stage_cnt[PSD_NUM_STAGES] = {};
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+cudaEvent_t take_event(psd_plan* p) {
+  cudaEvent_t e;
+  if (!p->ev_pool.empty()) {
+    e = p->ev_pool.back();
+    p->ev_pool.pop_back();
+  } else {
+    cudaEventCreate(&e);
+  }
+  return e;
+}
+
+// RAII stage marker: records start/stop events on `st` when profiling is on.
+struct Stage {
+  psd_plan* p;
+  int id;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  Stage(psd_plan* p_, int id_, cudaStream_t st_) : p(p_), id(id_), st(st_) {
+    if (p->prof) {
+      a = take_event(p);
+      cudaEventRecord(a, st);
+    }
+  }
+  void close() {
+    if (p->prof && a) {
+      cudaEvent_t b = take_event(p);
+      cudaEventRecord(b, st);
+      p->marks.push_back({id, {a, b}});
+      a = nullptr;
+    }
+  }
+  ~Stage() { close(); }
+};
+
+// Fold recorded marks into the per-stage totals (stream must be synchronised).
+void collect_marks(psd_plan* p) {
+  for (auto& m : p->marks) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, m.second.first, m.second.second) == cudaSuccess) {
+      p->stage_ms[m.first] += ms;
+      p->stage_cnt[m.first] += 1;
+    }
+    p->ev_pool.push_back(m.second.first);
+    p->ev_pool.push_back(m.second.second);
+  }
+  p->marks.clear();
+}
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(PSD_ERR_CUDA, "CUDA error in %s: %s", where, cudaGetErrorString(e));
+}
+
+#define PSD_CUDA_CHECK(expr, where)                \
+  do {                                             \
+    cudaError_t _e = (expr);                       \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+#define PSD_TRY(expr)          \
+  do {                         \
+    int _s = (expr);           \
+    if (_s != PSD_OK) return _s; \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+double* alloc(psd_plan* p, size_t elems) {
+  void* ptr = nullptr;
+  const size_t b = std::max<size_t>(elems, 2) * sizeof(double);
+  if (cudaMalloc(&ptr, b) != cudaSuccess) return nullptr;
+  p->allocs.push_back(ptr);
+  p->bytes += b;
+  return static_cast<double*>(ptr);
+}
+
+int sync(cudaStream_t st, const char* where) {
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, where);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, where);
+  return PSD_OK;
+}
+
+int launched(int k) {
+  if (k > 0) psd::count_launch(k);
+  return k;
+}
+
+// C = op(X)·P  (op = X or Xᵀ); alpha > 0 fuses B = (X + αI)/α: C = (acc + α·P)/α
+// X is rows×cols; op(X) = X (M=rows, K=cols) or Xᵀ (M=cols, K=rows).
+int xmul_rect(psd_plan* p, const double* x, ll rows, ll cols, ll ldx, const double* P, ll ldP,
+              int w, double* out, ll ldo, double alpha, bool transpose, cudaStream_t st) {
+  Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
+  psd::GemmOp op;
+  op.a_layout = transpose ? psd::A_KM : psd::A_MK;
+  op.b_layout = psd::B_KN;
+  op.A = x;
+  op.lda = ldx;
+  op.B = P;
+  op.ldb = ldP;
+  op.C = out;
+  op.ldc = ldo;
+  op.M = (int)(transpose ? cols : rows);
+  op.N = w;
+  op.K = (int)(transpose ? rows : cols);
+  op.epi = alpha > 0.0 ? psd::EPI_SHIFT : psd::EPI_STORE;
+  op.alpha = alpha;
+  op.S = P;
+  op.lds = ldP;
+  op.max_splits = 4;
+  const int r = psd::gemm_f64(op, p->ws, p->ws_elems, st);
+  if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "unsupported GEMM layout");
+  return PSD_OK;
+}
+
+int xmul(psd_plan* p, const double* x, ll n, ll ldx, const double* P, ll ldP, int w, double* out,
+         ll ldo, double alpha, bool transpose, cudaStream_t st) {
+  return xmul_rect(p, x, n, n, ldx, P, ldP, w, out, ldo, alpha, transpose, st);
+}
+
+// G (w×w, ld w) = Aᵀ·B for n×w panels A, B (symmetrised when A == B or sym)
+int panel_tn(psd_plan* p, const double* A, const double* B, ll ld, ll n, int w, double* G,
+             bool sym, cudaStream_t st) {
+  psd::GemmOp op;
+  op.a_layout = psd::A_KM;
+  op.b_layout = psd::B_KN;
+  op.A = A;
+  op.lda = ld;
+  op.B = B;
+  op.ldb = ld;
+  op.C = G;
+  op.ldc = w;
+  op.M = w;
+  op.N = w;
+  op.K = (int)n;
+  op.epi = psd::EPI_STORE;
+  op.max_splits = 256;
+  const int r = psd::gemm_f64(op, p->ws, p->ws_elems, st);
+  if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "unsupported GEMM layout");
+  if (sym) {
+    psd::symmetrize_small(G, w, w, st);
+  }
+  return PSD_OK;
+}
+
+// out (n×N) = A (n×K, lda) · B (K×N, ldb)
+int panel_nn(psd_plan* p, const double* A, ll lda, const double* B, ll ldb, double* out, ll ldo,
+             ll n, int K, int N, cudaStream_t st) {
+  psd::GemmOp op;
+  op.a_layout = psd::A_MK;
+  op.b_layout = psd::B_KN;
+  op.A = A;
+  op.lda = lda;
+  op.B = B;
+  op.ldb = ldb;
+  op.C = out;
+  op.ldc = ldo;
+  op.M = (int)n;
+  op.N = N;
+  op.K = K;
+  op.epi = psd::EPI_STORE;
+  op.max_splits = 1;
+  const int r = psd::gemm_f64(op, p->ws, p->ws_elems, st);
+  if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "unsupported GEMM layout");
+  return PSD_OK;
+}
+
+__global__ void fill_value_kernel(double* a, int m, double v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) a[i] = v;
+}
+
+__global__ void clip_values_kernel(const double* vals, int m, double offset, double scale,
+                                   double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = (vals[i] - offset) * scale;
+}
+
+struct QrInfo {
+  int passes = 0;
+  int shifted = 0;
+  double frob = 0.0;  // ‖Y‖_F of the input panel
+  bool zero = false;  // Y == 0
+};
+
+// CholeskyQR2 with shifted passes (shifted CholeskyQR3 when ill-conditioned).
+// Orthonormalises the n×w panel in `bufs[cur]`; `bufs[tmp]` is scratch.
+// On return *qidx is the buffer index holding Q; rdiag (if non-null) holds
+// Π_pass |L_ii| = |R_ii| of Y = Q·R.
+int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rdiag, int* qidx,
+           QrInfo* info, cudaStream_t st) {
+  Stage mark(p, PSD_STAGE_QR, st);
+  const ll ld = p->ldp;
+  int* dinfo = p->ints + p->w + 1;
+  if (rdiag) {
+    fill_value_kernel<<<(w + 255) / 256, 256, 0, st>>>(rdiag, w, 1.0);
+    launched(1);
+  }
+  std::vector<double> hdiag(w);
+  int hinfo = 0;
+  int unshifted_run = 0;
+  double kest0 = 0.0;
+  bool verified = false;
+  const double u = 1.1102230246251565e-16;
+  for (int pass = 0; pass < 10; ++pass) {
+    PSD_TRY(panel_tn(p, bufs[cur], bufs[cur], ld, n, w, p->G, true, st));
+    PSD_CUDA_CHECK(cudaMemcpy2DAsync(hdiag.data(), sizeof(double), p->G, (w + 1) * sizeof(double),
+                                     sizeof(double), w, cudaMemcpyDeviceToHost, st),
+                   "gram diag");
+    PSD_TRY(sync(st, "gram"));
+    double trace = 0.0;
+    for (int i = 0; i < w; ++i) trace += hdiag[i];
+    if (pass == 0) {
+      info->frob = std::sqrt(std::max(trace, 0.0));
+      if (trace == 0.0) {
+        info->zero = true;
+        *qidx = cur;
+        return PSD_OK;
+      }
+    }
+    if (!std::isfinite(trace)) return fail(PSD_ERR_CONVERGENCE, "non-finite Gram matrix in QR");
+    if (unshifted_run >= 2) {
+      // verification Gram of an ill-conditioned input: accept if ‖QᵀQ − I‖_max small
+      std::vector<double> hg((size_t)w * w);
+      PSD_CUDA_CHECK(cudaMemcpyAsync(hg.data(), p->G, hg.size() * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st),
+                     "gram copy");
+      PSD_TRY(sync(st, "gram copy"));
+      double dev = 0.0;
+      for (int i = 0; i < w; ++i)
+        for (int j = 0; j < w; ++j) dev = std::max(dev, std::fabs(hg[(size_t)i * w + j] - (i == j)));
+      if (dev <= 1e-13 * std::max(1, w)) {
+        verified = true;
+        break;
+      }
+    }
+    psd::copy_matrix(p->G, w, p->L, w, w, w, st);
+    psd::cholesky_lower(p->L, w, w, dinfo, p->ws, p->ws_elems, st);
+    PSD_CUDA_CHECK(cudaMemcpy2DAsync(hdiag.data(), sizeof(double), p->L, (w + 1) * sizeof(double),
+                                     sizeof(double), w, cudaMemcpyDeviceToHost, st),
+                   "chol diag");
+    PSD_CUDA_CHECK(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st), "info");
+    PSD_TRY(sync(st, "cholesky"));
+    bool bad = hinfo != 0;
+    double dmax = 0.0, dmin = INFINITY;
+    for (int i = 0; i < w; ++i) {
+      if (!std::isfinite(hdiag[i])) bad = true;
+      dmax = std::max(dmax, hdiag[i]);
+      dmin = std::min(dmin, hdiag[i]);
+    }
+    const double kest = (dmin > 0.0) ? dmax / dmin : INFINITY;
+    if (pass == 0) kest0 = kest;
+    const bool shift = bad || kest > 3e6;
+    if (shift) {
+      // Fukaya et al. shifted CholeskyQR: s = 11(mn + n(n+1))·u·‖Y‖²
+      const double s = 11.0 * ((double)n * w + (double)w * (w + 1)) * u * trace;
+      psd::copy_matrix(p->G, w, p->L, w, w, w, st);
+      psd::add_diag(p->L, w, w, s, st);
+      psd::cholesky_lower(p->L, w, w, dinfo, p->ws, p->ws_elems, st);
+      PSD_CUDA_CHECK(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st),
+                     "info");
+      PSD_TRY(sync(st, "shifted cholesky"));
+      if (hinfo != 0) return fail(PSD_ERR_CONVERGENCE, "shifted CholeskyQR broke down (pivot %d)", hinfo);
+      info->shifted = 1;
+    }
+    psd::tri_inv_upper_from_lower(p->L, w, w, p->Rinv, w, st);
+    if (rdiag) {
+      psd::accumulate_diag(p->L, w, w, rdiag, st);
+    }
+    PSD_TRY(panel_nn(p, bufs[cur], ld, p->Rinv, w, bufs[tmp], ld, n, w, w, st));
+    std::swap(cur, tmp);
+    info->passes++;
+    unshifted_run = shift ? 0 : unshifted_run + 1;
+    if (unshifted_run >= 2 && kest0 <= 1e4) {
+      verified = true;
+      break;
+    }
+  }
+  if (!verified) return fail(PSD_ERR_CONVERGENCE, "CholeskyQR did not reach orthogonality");
+  *qidx = cur;
+  return PSD_OK;
+}
+
+struct SymInfo {
+  double max_abs = 0.0, defect = 0.0;
+  bool bitwise = true, nonfinite = false;
+};
+
+int symcheck(psd_plan* p, const double* x, ll n, ll ldx, SymInfo* si, cudaStream_t st) {
+  {
+    Stage mark(p, PSD_STAGE_SYMCHECK, st);
+    psd::sym_stats(x, n, ldx, p->stats, st);
+  }
+  double h[3];
+  PSD_CUDA_CHECK(cudaMemcpyAsync(h, p->stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st),
+                 "stats");
+  PSD_TRY(sync(st, "symmetry check"));
+  int flags = 0;
+  std::memcpy(&flags, &h[2], sizeof(int));
+  si->max_abs = h[0];
+  si->defect = h[1];
+  si->bitwise = (flags & 1) == 0;
+  si->nonfinite = (flags & 2) != 0;
+  return PSD_OK;
+}
+
+// Range finder core (sketch.py:53-93).  Returns index of the buffer holding
+// the basis (columns compacted to *width_out).  bufs: 3 panel buffers.
+// X is m×n (m == n for the projections); Ω is n×w; the basis is m×w.
+int range_finder_core(psd_plan* p, const double* x, ll m, ll n, ll ldx, const double* omega,
+                      ll ldo, int w, int q, double alpha, bool use_t, bool strict, double** bufs,
+                      int* qidx, int* width_out, QrInfo* qi, cudaStream_t st) {
+  const ll ld = p->ldp;
+  const bool stabilize = q >= 2;                                   // sketch.py:74
+  int y = 0;
+  PSD_TRY(xmul_rect(p, x, m, n, ldx, omega, ldo, w, bufs[0], ld, alpha, false, st));  // :75
+  for (int it = 0; it < q; ++it) {                                 // :76-82
+    QrInfo tmp;
+    if (stabilize) PSD_TRY(cholqr(p, bufs, y, (y + 1) % 3, m, w, nullptr, &y, &tmp, st));
+    const int z = (y + 1) % 3;
+    // z = xᵀ @ y (sketch.py:79); for bitwise-symmetric X this equals X·Y exactly
+    PSD_TRY(xmul_rect(p, x, m, n, ldx, bufs[y], ld, w, bufs[z], ld, alpha, use_t, st));
+    int zq = z;
+    if (stabilize) PSD_TRY(cholqr(p, bufs, z, (z + 1) % 3, n, w, nullptr, &zq, &tmp, st));
+    const int ny = (zq + 1) % 3;
+    PSD_TRY(xmul_rect(p, x, m, n, ldx, bufs[zq], ld, w, bufs[ny], ld, alpha, false, st));
+    y = ny;
+  }
+  n = m;  // the final QR and gather act on the m×w sample
+  int qb = y;
+  PSD_TRY(cholqr(p, bufs, y, (y + 1) % 3, n, w, p->rdiag, &qb, qi, st));   // :84-85
+  if (qi->zero) {
+    *width_out = 0;
+    *qidx = qb;
+    return PSD_OK;
+  }
+  std::vector<double> rd(w);
+  PSD_CUDA_CHECK(cudaMemcpyAsync(rd.data(), p->rdiag, w * sizeof(double), cudaMemcpyDeviceToHost, st),
+                 "rdiag");
+  PSD_TRY(sync(st, "rdiag"));
+  std::vector<int> keep;
+  for (int i = 0; i < w; ++i)
+    if (rd[i] > 1e-12 * qi->frob) keep.push_back(i);               // :86
+  if ((int)keep.size() < w) {
+    if (strict)
+      return fail(PSD_ERR_RANK_DEFICIENT, "sampled matrix has numerical rank %d < %d",
+                  (int)keep.size(), w);
+    if (!keep.empty()) {
+      int* didx = p->ints;  // perm area reused
+      PSD_CUDA_CHECK(cudaMemcpyAsync(didx, keep.data(), keep.size() * sizeof(int),
+                                     cudaMemcpyHostToDevice, st),
+                     "keep idx");
+      const int dst = (qb + 1) % 3;
+      psd::gather_columns(bufs[qb], ld, didx, (int)keep.size(), bufs[dst], ld, n, st);
+      qb = dst;
+    }
+  }
+  *width_out = (int)keep.size();
+  *qidx = qb;
+  return PSD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* psd_last_error(void) { return g_err.c_str(); }
+
+const char* psd_version(void) { return "psdproj 0.1.0 (sm_100a, FP64 DMMA)"; }
+
+int psd_plan_create(psd_plan** out, int64_t n, int32_t width, int32_t device) {
+  if (!out) return fail(PSD_ERR_INVALID_PARAMS, "null plan pointer");
+  if (n < 1 || width < 1 || width > n)
+    return fail(PSD_ERR_INVALID_PARAMS, "plan needs 1 <= width <= n (n=%lld, width=%d)", (ll)n, width);
+  DeviceGuard g(device);
+  psd_plan* p = new psd_plan();
+  p->device = device;
+  p->n = n;
+  p->w = width;
+  p->ldp = (width + 1) / 2 * 2;
+  const size_t panel = (size_t)n * p->ldp;
+  const size_t sq = (size_t)width * width;
+  bool ok = true;
+  for (int i = 0; i < 6; ++i) ok &= (p->panel[i] = alloc(p, panel)) != nullptr;
+  ok &= (p->G = alloc(p, sq)) != nullptr;
+  ok &= (p->L = alloc(p, sq)) != nullptr;
+  ok &= (p->Rinv = alloc(p, sq)) != nullptr;
+  ok &= (p->T = alloc(p, sq)) != nullptr;
+  ok &= (p->V = alloc(p, sq)) != nullptr;
+  ok &= (p->U = alloc(p, sq)) != nullptr;
+  ok &= (p->vals = alloc(p, width)) != nullptr;
+  ok &= (p->vals_sorted = alloc(p, width)) != nullptr;
+  ok &= (p->rdiag = alloc(p, width)) != nullptr;
+  ok &= (p->dvec = alloc(p, width)) != nullptr;
+  ok &= (p->ints = reinterpret_cast<int*>(alloc(p, width + 8))) != nullptr;
+  p->ws_elems = std::max<size_t>((size_t)4 * n * p->ldp, (size_t)256 * width * p->ldp);
+  p->ws_elems = std::max<size_t>(p->ws_elems, 1 << 20);
+  ok &= (p->ws = alloc(p, p->ws_elems)) != nullptr;
+  p->jws_elems = psd::jacobi_ws_elems(width);
+  ok &= (p->jws = alloc(p, p->jws_elems)) != nullptr;
+  p->gparts = psd::gemv_blocks(n);
+  ok &= (p->gy = alloc(p, n)) != nullptr;
+  ok &= (p->gv = alloc(p, n)) != nullptr;
+  ok &= (p->gpart = alloc(p, p->gparts)) != nullptr;
+  ok &= (p->stats = alloc(p, 4)) != nullptr;
+  ok &= (p->scal = alloc(p, 8)) != nullptr;
+  psd::GemmOp rop;
+  rop.M = (int)n;
+  rop.N = (int)n;
+  p->rparts = psd::gemm_resid_ctas(rop);
+  ok &= (p->rpart = alloc(p, p->rparts)) != nullptr;
+  if (!ok) {
+    psd_plan_destroy(p);
+    return fail(PSD_ERR_NO_MEMORY, "device allocation failed for plan n=%lld width=%d", (ll)n, width);
+  }
+  *out = p;
+  return PSD_OK;
+}
+
+void psd_plan_destroy(psd_plan* p) {
+  if (!p) return;
+  DeviceGuard g(p->device);
+  for (auto& m : p->marks) {
+    p->ev_pool.push_back(m.second.first);
+    p->ev_pool.push_back(m.second.second);
+  }
+  for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+  for (void* a : p->allocs) cudaFree(a);
+  delete p;
+}
+
+int64_t psd_plan_bytes(const psd_plan* p) { return p ? (int64_t)p->bytes : 0; }
+
+int psd_require_symmetric(psd_plan* p, const double* x, int64_t n, int64_t ldx, double tol,
+                          double* stats_out, void* stream) {
+  if (!p || !x) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  if (n < 1) return fail(PSD_ERR_NONSQUARE, "matrix dimension must be at least 1");
+  DeviceGuard g(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SymInfo si;
+  PSD_TRY(symcheck(p, x, n, ldx, &si, st));
+  if (stats_out) {
+    stats_out[0] = si.max_abs;
+    stats_out[1] = si.defect;
+    stats_out[2] = si.bitwise ? 1.0 : 0.0;
+  }
+  if (si.nonfinite) return fail(PSD_ERR_CONVERGENCE, "matrix has non-finite entries");
+  if (tol < 0.0) tol = 1e-10 * std::max(1.0, si.max_abs);
+  if (si.defect > tol)
+    return fail(PSD_ERR_ASYMMETRIC,
+                "matrix is not symmetric: max asymmetry %.3e exceeds tolerance %.3e", si.defect, tol);
+  return PSD_OK;
+}
+
+static int power_iteration_impl(psd_plan* p, const double* x, ll n, ll ldx, double shift,
+                                const double* v0, int n_iter, double* result, cudaStream_t st) {
+  const double floor = 2.2250738585072014e-308 * (double)n;  // finfo.tiny·n (sketch.py:107)
+  int* flag = p->ints + p->w + 2;
+  PSD_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int), st), "flag");
+  const double* v = v0;
+  for (int it = 0; it < n_iter; ++it) {
+    const int nb = psd::gemv_shift(x, n, ldx, v, shift, p->gy, p->gpart, st);
+    psd::normalize(p->gy, p->gpart, nb, n, floor, p->gv, p->scal, flag, st);
+    v = p->gv;
+  }
+  const int nb = psd::gemv_shift(x, n, ldx, v, shift, p->gy, p->gpart, st);
+  psd::sum_partials(p->gpart, nb, p->scal + 1, 1, st);
+  double h[2];
+  int hflag = 0;
+  PSD_CUDA_CHECK(cudaMemcpyAsync(h, p->scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "pi");
+  PSD_CUDA_CHECK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "pi flag");
+  PSD_TRY(sync(st, "power iteration"));
+  *result = hflag ? 0.0 : h[1];
+  return PSD_OK;
+}
+
+int psd_power_iteration(psd_plan* p, const double* x, int64_t n, int64_t ldx, double shift,
+                        const double* v0, int32_t n_iter, double* result, void* stream) {
+  if (!p || !x || !v0 || !result) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  if (n_iter < 1) return fail(PSD_ERR_INVALID_PARAMS, "power iteration needs n_iter >= 1, got %d", n_iter);
+  if (n < 1 || n > p->n) return fail(PSD_ERR_INVALID_PARAMS, "n=%lld outside plan", (ll)n);
+  DeviceGuard g(p->device);
+  return power_iteration_impl(p, x, n, ldx, shift, v0, n_iter, result,
+                              static_cast<cudaStream_t>(stream));
+}
+
+int psd_min_eig_magnitude(psd_plan* p, const double* x, int64_t n, int64_t ldx, const double* v1,
+                          const double* v2, int32_t n_iter, double* result, void* stream) {
+  if (!p || !x || !v1 || !v2 || !result) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  if (n_iter < 1) return fail(PSD_ERR_INVALID_PARAMS, "power iteration needs n_iter >= 1, got %d", n_iter);
+  if (n < 1 || n > p->n) return fail(PSD_ERR_INVALID_PARAMS, "n=%lld outside plan", (ll)n);
+  DeviceGuard g(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double s1 = 0.0, s2 = 0.0;
+  PSD_TRY(power_iteration_impl(p, x, n, ldx, 0.0, v1, n_iter, &s1, st));   // sketch.py:126
+  PSD_TRY(power_iteration_impl(p, x, n, ldx, s1, v2, n_iter, &s2, st));    // sketch.py:127-128
+  *result = std::fabs(s1 - s2);
+  return PSD_OK;
+}
+
+int psd_range_finder(psd_plan* p, const double* x, int64_t m, int64_t n, int64_t ldx,
+                     const double* omega, int64_t ldo, int32_t width, int32_t q, double alpha,
+                     uint32_t flags, double* basis, int64_t ldb, int32_t* width_out,
+                     void* stream) {
+  if (!p || !x || !omega || !basis || !width_out) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  if (q < 0) return fail(PSD_ERR_INVALID_PARAMS, "power exponent q must be >= 0, got %d", q);
+  if (m < 1 || n < 1) return fail(PSD_ERR_INVALID_PARAMS, "expected a matrix, got shape (%lld, %lld)", (ll)m, (ll)n);
+  if (width < 1 || width > std::min(m, n))
+    return fail(PSD_ERR_INVALID_PARAMS, "k+l = %d exceeds min(m, n) = %lld", width, (ll)std::min(m, n));
+  if (std::max(m, n) > p->n || width > p->w)
+    return fail(PSD_ERR_INVALID_PARAMS, "problem exceeds plan capacity");
+  if (alpha > 0.0 && m != n) return fail(PSD_ERR_INVALID_PARAMS, "scaled sketch needs a square matrix");
+  DeviceGuard g(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  psd::g_launch_count = 0;
+  bool use_t = (m != n) || !(flags & PSD_FLAG_ASSUME_SYMMETRIC);
+  if (use_t && m == n) {
+    SymInfo si;
+    PSD_TRY(symcheck(p, x, n, ldx, &si, st));
+    use_t = !si.bitwise;
+  }
+  double* bufs[3] = {p->panel[0], p->panel[1], p->panel[2]};
+  int qb = 0, wk = 0;
+  QrInfo qi;
+  PSD_TRY(range_finder_core(p, x, m, n, ldx, omega, ldo, width, q, alpha, use_t,
+                            (flags & PSD_FLAG_STRICT) != 0, bufs, &qb, &wk, &qi, st));
+  if (wk > 0) {
+    psd::copy_matrix(bufs[qb], p->ldp, basis, ldb, m, wk, st);
+  }
+  *width_out = wk;
+  return sync(st, "range finder");
+}
+
+int psd_eigh(psd_plan* p, double* a, int32_t m, int64_t lda, double* values, double* vectors,
+             int64_t ldv, int32_t* sweeps_out, void* stream) {
+  if (!p || !a || !values || !vectors) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  if (m < 1 || m > p->w) return fail(PSD_ERR_INVALID_PARAMS, "eigh size %d outside plan", m);
+  DeviceGuard g(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  psd::symmetrize_small(a, m, lda, st);  // eigh validates/uses the symmetric part
+  const int sw = psd::jacobi_eigh(a, lda, m, p->vals, p->V, m, p->jws, p->jws_elems,
+                                  p->ints + p->w + 3, st);
+  if (sw < 0) return fail(PSD_ERR_CONVERGENCE, "Jacobi eigensolver did not converge");
+  psd::sort_eigs(p->vals, p->V, m, m, 0.0, values, vectors, ldv, p->ints + p->w, p->ints, st);
+  if (sweeps_out) *sweeps_out = sw;
+  return sync(st, "eigh");
+}
+
+static int ran_proj_impl(psd_plan* p, const double* x, int64_t n, int64_t ldx,
+                         const double* omega, int64_t ldo, int32_t k, int32_t l, int32_t q,
+                         double alpha, uint32_t flags, double* result, int64_t ldr,
+                         double* factors_w, int64_t ldw, double* factors_d, psd_report* rep,
+                         void* stream) {
+  if (k < 1) return fail(PSD_ERR_INVALID_PARAMS, "target rank k must be >= 1, got %d", k);
+  if (l < 0) return fail(PSD_ERR_INVALID_PARAMS, "oversampling l must be >= 0, got %d", l);
+  if (q < 0) return fail(PSD_ERR_INVALID_PARAMS, "power exponent q must be >= 0, got %d", q);
+  if (n < 1) return fail(PSD_ERR_NONSQUARE, "matrix dimension must be at least 1");
+  const int w = k + l;
+  if (n > p->n || std::min<ll>(w, n) > p->w)
+    return fail(PSD_ERR_INVALID_PARAMS, "problem exceeds plan capacity");
+  DeviceGuard g(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  psd::g_launch_count = 0;
+  psd_report r{};
+  r.residual_frob = NAN;
+  r.alpha_used = alpha;
+
+  // require_symmetric (projection.py:100 / :132) + alpha_tol (projection.py:133-137)
+  // With PSD_FLAG_SKIP_SYMCHECK the caller has run require_symmetric and the
+  // alpha_tol test itself and tells us via PSD_FLAG_ASSUME_SYMMETRIC whether
+  // X is bitwise symmetric (then Xᵀ·P == X·P exactly).
+  bool use_t = !(flags & PSD_FLAG_ASSUME_SYMMETRIC);
+  if (!(flags & PSD_FLAG_SKIP_SYMCHECK)) {
+    SymInfo si;
+    PSD_TRY(symcheck(p, x, n, ldx, &si, st));
+    r.max_abs = si.max_abs;
+    r.sym_defect = si.defect;
+    if (si.nonfinite) return fail(PSD_ERR_CONVERGENCE, "matrix has non-finite entries");
+    const double tol = 1e-10 * std::max(1.0, si.max_abs);
+    if (si.defect > tol)
+      return fail(PSD_ERR_ASYMMETRIC,
+                  "matrix is not symmetric: max asymmetry %.3e exceeds tolerance %.3e", si.defect,
+                  tol);
+    if (alpha > 0.0) {
+      const double alpha_tol = 1e-12 * std::max(1.0, si.max_abs);
+      if (alpha <= alpha_tol)
+        return fail(PSD_ERR_ALPHA_TOO_SMALL,
+                    "alpha = %.3e is at or below tolerance %.3e; input is numerically PSD", alpha,
+                    alpha_tol);
+    }
+    use_t = use_t && !si.bitwise;
+  }
+  if (w > n) return fail(PSD_ERR_INVALID_PARAMS, "k+l = %d exceeds min(m, n) = %lld", w, (ll)n);
+  r.used_transpose = use_t ? 1 : 0;
+
+  const ll ld = p->ldp;
+  double* bufs[3] = {p->panel[0], p->panel[1], p->panel[2]};
+  int qb = 0, wk = 0;
+  QrInfo qi;
+  PSD_TRY(range_finder_core(p, x, n, n, ldx, omega, ldo, w, q, alpha, use_t,
+                            (flags & PSD_FLAG_STRICT) != 0, bufs, &qb, &wk, &qi, st));
+  r.qr_passes = qi.passes;
+  r.qr_shifted = qi.shifted;
+  r.basis_width = wk;
+  if (wk == 0) {  // _zero_report (projection.py:81-89)
+    if (result) {
+      psd::fill_zero(result, ldr, n, n, st);
+    }
+    r.effective_rank = 0;
+    r.gpu_launches = psd::g_launch_count;
+    if (rep) *rep = r;
+    return sync(st, "zero report");
+  }
+  double* Q = bufs[qb];
+  double* C = p->panel[3];
+  double* W = p->panel[4];
+  double* WD = p->panel[5];
+
+  // compression T = sym(Qᵀ X Q) or sym(Qᵀ B Q)  (projection.py:104 / :143)
+  PSD_TRY(xmul(p, x, n, ldx, Q, ld, wk, C, ld, alpha, false, st));
+  {
+    Stage mark(p, PSD_STAGE_COMPRESS, st);
+    PSD_TRY(panel_tn(p, Q, C, ld, n, wk, p->T, true, st));
+  }
+  // eigh (projection.py:105 → symmetric.py:68-86)
+  Stage eig_mark(p, PSD_STAGE_EIGH, st);
+  const int sweeps = psd::jacobi_eigh(p->T, wk, wk, p->vals, p->V, wk, p->jws, p->jws_elems,
+                                      p->ints + p->w + 3, st);
+  if (sweeps < 0) return fail(PSD_ERR_CONVERGENCE, "eigen-decomposition failed: Jacobi did not converge");
+  r.eig_sweeps = sweeps;
+  const double offset = alpha > 0.0 ? 1.0 : 0.0;  // max(D − 1, 0) for Alg. 3
+  psd::sort_eigs(p->vals, p->V, wk, wk, offset, p->vals_sorted, p->U, wk, p->ints + p->w,
+                 p->ints, st);
+  int npos = 0;
+  PSD_CUDA_CHECK(cudaMemcpyAsync(&npos, p->ints + p->w, sizeof(int), cudaMemcpyDeviceToHost, st),
+                 "npos");
+  PSD_TRY(sync(st, "eigh"));
+  eig_mark.close();
+  r.effective_rank = npos;
+  Stage recon_mark(p, PSD_STAGE_RECON, st);
+  // d = clipped[keep]·scale (projection.py:75-77)
+  clip_values_kernel<<<(wk + 255) / 256, 256, 0, st>>>(p->vals_sorted, wk, offset,
+                                                        alpha > 0.0 ? alpha : 1.0, p->dvec);
+  launched(1);
+  if (npos > 0) {
+    // W = Q·U₊ ; WD = W·diag(d) ; X̂₊ = WD·Wᵀ on lower tiles, mirrored
+    PSD_TRY(panel_nn(p, Q, ld, p->U, wk, W, ld, n, wk, npos, st));
+    if (result) {
+      psd::scale_columns(W, ld, p->dvec, WD, ld, n, npos, st);
+      psd::GemmOp op;
+      op.a_layout = psd::A_MK;
+      op.b_layout = psd::B_NK;
+      op.A = WD;
+      op.lda = ld;
+      op.B = W;
+      op.ldb = ld;
+      op.C = result;
+      op.ldc = ldr;
+      op.M = (int)n;
+      op.N = (int)n;
+      op.K = npos;
+      op.epi = psd::EPI_MIRROR;
+      op.max_splits = 1;
+      psd::gemm_f64(op, p->ws, p->ws_elems, st);
+    }
+    if (factors_w) {
+      psd::copy_matrix(W, ld, factors_w, ldw, n, npos, st);
+    }
+    if (factors_d) {
+      PSD_CUDA_CHECK(cudaMemcpyAsync(factors_d, p->dvec, npos * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, st),
+                     "factors d");
+    }
+  } else if (result) {
+    psd::fill_zero(result, ldr, n, n, st);
+  }
+  recon_mark.close();
+  if (flags & PSD_FLAG_DIAGNOSTICS) {
+    Stage diag_mark(p, PSD_STAGE_DIAG, st);
+    // ‖X − Q(QᵀX)‖_F with QᵀX = (XᵀQ)ᵀ (projection.py:110)
+    PSD_TRY(xmul(p, x, n, ldx, Q, ld, wk, C, ld, 0.0, use_t, st));
+    psd::GemmOp op;
+    op.a_layout = psd::A_MK;
+    op.b_layout = psd::B_NK;
+    op.A = Q;
+    op.lda = ld;
+    op.B = C;
+    op.ldb = ld;
+    op.C = nullptr;
+    op.M = (int)n;
+    op.N = (int)n;
+    op.K = wk;
+    op.epi = psd::EPI_RESID;
+    op.S = x;
+    op.lds = ldx;
+    op.partials = p->rpart;
+    op.max_splits = 1;
+    psd::gemm_f64(op, p->ws, p->ws_elems, st);
+    psd::sum_partials(p->rpart, psd::gemm_resid_ctas(op), p->scal + 2, 1, st);
+    PSD_CUDA_CHECK(cudaMemcpyAsync(&r.residual_frob, p->scal + 2, sizeof(double),
+                                   cudaMemcpyDeviceToHost, st),
+                   "residual");
+  }
+  PSD_TRY(sync(st, "ran_proj"));
+  r.gpu_launches = psd::g_launch_count;
+  if (rep) *rep = r;
+  return PSD_OK;
+}
+
+int psd_ran_proj(psd_plan* p, const double* x, int64_t n, int64_t ldx, const double* omega,
+                 int64_t ldo, int32_t k, int32_t l, int32_t q, double alpha, uint32_t flags,
+                 double* result, int64_t ldr, double* factors_w, int64_t ldw, double* factors_d,
+                 psd_report* rep, void* stream) {
+  if (!p || !x || !omega) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  DeviceGuard g(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int status;
+  {
+    Stage total(p, PSD_STAGE_TOTAL, st);
+    status = ran_proj_impl(p, x, n, ldx, omega, ldo, k, l, q, alpha, flags, result, ldr,
+                           factors_w, ldw, factors_d, rep, stream);
+  }
+  if (p->prof) {
+    cudaStreamSynchronize(st);
+    collect_marks(p);
+  }
+  return status;
+}
+
+int psd_plan_profile(psd_plan* p, int32_t enable, double* ms_out, int32_t* counts_out,
+                     int32_t reset) {
+  if (!p) return fail(PSD_ERR_INVALID_PARAMS, "null plan");
+  if (enable >= 0) p->prof = enable != 0;
+  for (int i = 0; i < PSD_NUM_STAGES; ++i) {
+    if (ms_out) ms_out[i] = p->stage_ms[i];
+    if (counts_out) counts_out[i] = p->stage_cnt[i];
+    if (reset) {
+      p->stage_ms[i] = 0.0;
+      p->stage_cnt[i] = 0;
+    }
+  }
+  return PSD_OK;
+}
+
+int psd_reconstruct(psd_plan* p, const double* w, int64_t n, int64_t ldw, const double* d,
+                    int32_t r, double* result, int64_t ldr, void* stream) {
+  if (!p || !w || !d || !result) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  if (n < 1 || n > p->n || r < 0 || r > p->w) return fail(PSD_ERR_INVALID_PARAMS, "reconstruct shape outside plan");
+  DeviceGuard g(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (r == 0) {
+    psd::fill_zero(result, ldr, n, n, st);
+    return sync(st, "reconstruct");
+  }
+  double* WD = p->panel[5];
+  psd::scale_columns(w, ldw, d, WD, p->ldp, n, r, st);
+  psd::GemmOp op;
+  op.a_layout = psd::A_MK;
+  op.b_layout = psd::B_NK;
+  op.A = WD;
+  op.lda = p->ldp;
+  op.B = w;
+  op.ldb = ldw;
+  op.C = result;
+  op.ldc = ldr;
+  op.M = (int)n;
+  op.N = (int)n;
+  op.K = r;
+  op.epi = psd::EPI_MIRROR;
+  op.max_splits = 1;
+  psd::gemm_f64(op, p->ws, p->ws_elems, st);
+  return sync(st, "reconstruct");
+}
+
+int psd_symmetrize(double* a, int64_t m, int64_t lda, void* stream) {
+  if (!a || m < 1) return fail(PSD_ERR_NONSQUARE, "expected a square matrix");
+  psd::symmetrize_small(a, (int)m, lda, static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "symmetrize");
+  return PSD_OK;
+}
+
+int psd_gemm_f64(int32_t a_layout, int32_t b_layout, const double* a, int64_t lda, const double* b,
+                 int64_t ldb, double* c, int64_t ldc, int32_t m, int32_t n, int32_t k,
+                 int32_t epilogue, double alpha, const double* s, int64_t lds, double* ws,
+                 int64_t ws_elems, void* stream) {
+  if (!a || !b || !c || m < 0 || n < 0 || k < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad gemm arguments");
+  if (epilogue < 0 || epilogue > 3) return fail(PSD_ERR_INVALID_PARAMS, "bad epilogue %d", epilogue);
+  if ((epilogue == 1 || epilogue == 2) && !s) return fail(PSD_ERR_INVALID_PARAMS, "epilogue needs S");
+  if (epilogue == 3 && (m != n || a_layout != 0 || b_layout != 1))
+    return fail(PSD_ERR_INVALID_PARAMS, "mirrored store needs M == N, A row-major, B^T stored");
+  psd::GemmOp op;
+  op.a_layout = a_layout;
+  op.b_layout = b_layout;
+  op.A = a;
+  op.lda = lda;
+  op.B = b;
+  op.ldb = ldb;
+  op.C = c;
+  op.ldc = ldc;
+  op.M = m;
+  op.N = n;
+  op.K = k;
+  op.epi = epilogue;
+  op.alpha = alpha;
+  op.S = s;
+  op.lds = lds;
+  op.max_splits = (ws && ws_elems > 0 && epilogue <= 1) ? 256 : 1;
+  const int r = psd::gemm_f64(op, ws, ws ? (size_t)ws_elems : 0, static_cast<cudaStream_t>(stream));
+  if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "unsupported layout pair (%d, %d)", a_layout, b_layout);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "gemm");
+  return PSD_OK;
+}
+
+int psd_fill_gaussian(double* out, int64_t rows, int32_t cols, int64_t ld, uint64_t seed,
+                      uint64_t offset, void* stream) {
+  if (!out || rows < 1 || cols < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad gaussian fill");
+  psd::philox_normal(out, rows, cols, ld, seed, offset, static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "philox");
+  return PSD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,416 @@
+// Memory-bound kernels of the projection path (HBM roofline): symmetry
+// validation, Gaussian test-matrix generation, the power-iteration GEMV,
+// split-K reduction and small panel utilities.
+#include <algorithm>
+#include <cmath>
+
+#include "launch.h"
+
+namespace psd {
+
+// ---------------------------------------------------------------------------
+// a1 — require_symmetric (symmetric.py:39-57).  One pass over (I,J)/(J,I)
+// 32×32 tile pairs (I ≤ J): max|x|, max|x − xᵀ| and "bitwise symmetric".
+// ---------------------------------------------------------------------------
+constexpr int kSymT = 32;
+
+__global__ void __launch_bounds__(256) sym_stats_kernel(const double* __restrict__ x, long long n,
+                                                        long long ldx, double* stats) {
+  __shared__ double tj[kSymT][kSymT + 1];
+  const long long nt = (n + kSymT - 1) / kSymT;
+  // linear index over lower-triangular pairs (ti ≥ tj) → tile (ti, tj)
+  const long long b = blockIdx.x;
+  long long ti = (long long)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+  while ((ti + 1) * (ti + 2) / 2 <= b) ++ti;
+  while (ti * (ti + 1) / 2 > b) --ti;
+  const long long tjx = b - ti * (ti + 1) / 2;
+  (void)nt;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows per pass
+  const long long r0 = ti * kSymT, c0 = tjx * kSymT;
+  // load tile (tj, ti) = x[c0.., r0..] into smem
+  for (int r = ty; r < kSymT; r += 8) {
+    const long long gr = c0 + r, gc = r0 + tx;
+    tj[r][tx] = (gr < n && gc < n) ? x[gr * ldx + gc] : 0.0;
+  }
+  __syncthreads();
+  double mabs = 0.0, mdef = 0.0;
+  int flags = 0;
+  for (int r = ty; r < kSymT; r += 8) {
+    const long long gr = r0 + r, gc = c0 + tx;
+    if (gr < n && gc < n) {
+      const double a = x[gr * ldx + gc];   // x[i][j]
+      const double bt = tj[tx][r];         // x[j][i]
+      if (!isfinite(a) || !isfinite(bt)) flags |= 2;
+      mabs = fmax(mabs, fmax(fabs(a), fabs(bt)));
+      const double d = fabs(a - bt);
+      mdef = fmax(mdef, d);
+      if (a != bt) flags |= 1;
+    }
+  }
+  mabs = warp_max(mabs);
+  mdef = warp_max(mdef);
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (tx == 0) {
+    if (mabs > 0.0) atomic_max_nonneg(&stats[0], mabs);
+    if (mdef > 0.0) atomic_max_nonneg(&stats[1], mdef);
+    if (flags) atomicOr(reinterpret_cast<int*>(stats + 2), flags);
+  }
+}
+
+void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st) {
+  cudaMemsetAsync(stats, 0, 3 * sizeof(double), st);
+  const long long nt = (n + kSymT - 1) / kSymT;
+  const long long blocks = nt * (nt + 1) / 2;
+  sym_stats_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, stats);
+  count_launch();
+}
+
+// T ← (T + Tᵀ)/2 for a small matrix; each (i,j), i>j pair written by one thread.
+__global__ void symmetrize_small_kernel(double* x, int m, long long ld) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)m * m) return;
+  const int i = (int)(idx / m), j = (int)(idx % m);
+  if (i <= j) return;
+  const double v = (x[(long long)i * ld + j] + x[(long long)j * ld + i]) / 2.0;
+  x[(long long)i * ld + j] = v;
+  x[(long long)j * ld + i] = v;
+}
+
+void symmetrize_small(double* x, int m, long long ld, cudaStream_t st) {
+  const long long tot = (long long)m * m;
+  symmetrize_small_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(x, m, ld);
+  count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// Ω on device: Philox4x32-10 → 2×53-bit uniforms → Box–Muller.
+// Used only when the caller does not supply Ω (perf mode); parity runs pass
+// the host numpy Ω (symmetric.py:135) instead.
+// ---------------------------------------------------------------------------
+PSD_DEVINL void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, uint32_t k0,
+                             uint32_t k1) {
+  const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+  const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+  const uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+  c0 = n0;
+  c1 = n1;
+  c2 = n2;
+  c3 = n3;
+}
+
+__global__ void philox_normal_kernel(double* out, long long rows, int cols, long long ld,
+                                     uint64_t seed, uint64_t offset) {
+  const long long total = rows * (long long)cols;
+  const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (2 * pair >= total) return;
+  uint32_t c0 = (uint32_t)(pair + offset), c1 = (uint32_t)((pair + offset) >> 32), c2 = 0x5053u,
+           c3 = 0x44u;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    philox_round(c0, c1, c2, c3, k0, k1);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  const double two53 = 1.0 / 9007199254740992.0;
+  const uint64_t b1 = ((uint64_t)c0 << 21) | (uint64_t)(c1 >> 11);  // 53 bits
+  const uint64_t b2 = ((uint64_t)c2 << 21) | (uint64_t)(c3 >> 11);
+  const double u1 = ((double)b1 + 0.5) * two53;  // (0, 1)
+  const double u2 = (double)b2 * two53;          // [0, 1)
+  const double r = sqrt(-2.0 * log(u1));
+  double s, c;
+  sincospi(2.0 * u2, &s, &c);
+  const long long e0 = 2 * pair, e1 = 2 * pair + 1;
+  out[(e0 / cols) * ld + (e0 % cols)] = r * c;
+  if (e1 < total) out[(e1 / cols) * ld + (e1 % cols)] = r * s;
+}
+
+void philox_normal(double* out, long long rows, int cols, long long ld, uint64_t seed,
+                   uint64_t offset, cudaStream_t st) {
+  const long long pairs = (rows * (long long)cols + 1) / 2;
+  philox_normal_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, st>>>(out, rows, cols, ld, seed,
+                                                                        offset);
+  count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// a8 — power_iteration GEMV (sketch.py:109,114): y = (X − σI)v, HBM-bound.
+// One warp per 4 rows, 16-byte loads, per-block partial Σy² (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int kGemvRowsPerWarp = 4;
+constexpr int kGemvWarps = 8;
+
+__global__ void __launch_bounds__(256) gemv_kernel(const double* __restrict__ x, long long n,
+                                                   long long ldx, const double* __restrict__ v,
+                                                   double shift, double* __restrict__ y,
+                                                   double* __restrict__ partials, int vec) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long row0 = ((long long)blockIdx.x * kGemvWarps + warp) * kGemvRowsPerWarp;
+  double acc[kGemvRowsPerWarp] = {0.0, 0.0, 0.0, 0.0};
+  if (vec) {
+    for (long long c = 2 * lane; c + 1 < n; c += 64) {
+      const double2 vv = *reinterpret_cast<const double2*>(v + c);
+#pragma unroll
+      for (int r = 0; r < kGemvRowsPerWarp; ++r) {
+        const long long row = row0 + r;
+        if (row < n) {
+          const double2 xx = __ldcs(reinterpret_cast<const double2*>(x + row * ldx + c));
+          acc[r] = fma(xx.x, vv.x, acc[r]);
+          acc[r] = fma(xx.y, vv.y, acc[r]);
+        }
+      }
+    }
+    if ((n & 1) && lane == 0) {
+      const long long c = n - 1;
+#pragma unroll
+      for (int r = 0; r < kGemvRowsPerWarp; ++r)
+        if (row0 + r < n) acc[r] = fma(x[(row0 + r) * ldx + c], v[c], acc[r]);
+    }
+  } else {
+    for (long long c = lane; c < n; c += 32) {
+      const double vv = v[c];
+#pragma unroll
+      for (int r = 0; r < kGemvRowsPerWarp; ++r)
+        if (row0 + r < n) acc[r] = fma(x[(row0 + r) * ldx + c], vv, acc[r]);
+    }
+  }
+  double sq = 0.0;
+#pragma unroll
+  for (int r = 0; r < kGemvRowsPerWarp; ++r) {
+    double s = warp_sum(acc[r]);
+    const long long row = row0 + r;
+    if (row < n) {
+      s = s - shift * v[row];
+      if (lane == 0) y[row] = s;
+      sq = fma(s, s, sq);
+    }
+  }
+  __shared__ double red[kGemvWarps];
+  if (lane == 0) red[warp] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < kGemvWarps; ++w) tot += red[w];
+    partials[blockIdx.x] = tot;
+  }
+}
+
+int gemv_blocks(long long n) {
+  const long long rows_per_block = kGemvWarps * kGemvRowsPerWarp;
+  return (int)((n + rows_per_block - 1) / rows_per_block);
+}
+
+int gemv_shift(const double* x, long long n, long long ldx, const double* v, double shift,
+               double* y, double* partials, cudaStream_t st) {
+  const int blocks = gemv_blocks(n);
+  const int vec = ((uintptr_t)x % 16 == 0) && (ldx % 2 == 0) && ((uintptr_t)v % 16 == 0);
+  gemv_kernel<<<blocks, 256, 0, st>>>(x, n, ldx, v, shift, y, partials, vec);
+  count_launch();
+  return blocks;
+}
+
+__global__ void normalize_kernel(const double* __restrict__ y, const double* __restrict__ partials,
+                                 int nparts, long long n, double floor, double* __restrict__ v,
+                                 double* out, int* flag) {
+  __shared__ double red[32];
+  __shared__ double nrm_s;
+  double s = 0.0;
+  // fixed-order reduction so every launch (and every block) gets the same value
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += partials[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    nrm_s = sqrt(t);
+    if (blockIdx.x == 0) {
+      if (out) out[0] = nrm_s;
+      if (flag && !(nrm_s > floor)) *flag = 1;
+    }
+  }
+  __syncthreads();
+  const double nrm = nrm_s;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v[i] = y[i] / nrm;
+}
+
+void normalize(const double* y, const double* partials, int nparts, long long n, double floor,
+               double* v, double* out, int* flag, cudaStream_t st) {
+  int blocks = (int)std::min<long long>((n + 1023) / 1024, 64);
+  if (blocks < 1) blocks = 1;
+  normalize_kernel<<<blocks, 1024, 0, st>>>(y, partials, nparts, n, floor, v, out, flag);
+  count_launch();
+}
+
+__global__ void sum_partials_kernel(const double* partials, long long nparts, double* out,
+                                    int do_sqrt) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < nparts; i += blockDim.x) s += partials[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    out[0] = do_sqrt ? sqrt(t) : t;
+  }
+}
+
+void sum_partials(const double* partials, long long nparts, double* out, int do_sqrt,
+                  cudaStream_t st) {
+  sum_partials_kernel<<<1, 1024, 0, st>>>(partials, nparts, out, do_sqrt);
+  count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// split-K reduction + epilogue
+// ---------------------------------------------------------------------------
+__global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits,
+                                     long long split_stride, int M, int N, long long ldw,
+                                     double* C, long long ldc, int mode, double alpha,
+                                     const double* S, long long lds) {
+  const long long total = (long long)M * N;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(idx / N), n = (int)(idx % N);
+    double v = 0.0;
+    for (int s = 0; s < splits; ++s) v += ws[s * split_stride + (long long)m * ldw + n];
+    if (mode == 10) {  // symmetric part of a square result: (T + Tᵀ)/2
+      if (m < n) continue;
+      double u = 0.0;
+      for (int s = 0; s < splits; ++s) u += ws[s * split_stride + (long long)n * ldw + m];
+      const double sv = (v + u) / 2.0;
+      C[(long long)m * ldc + n] = sv;
+      C[(long long)n * ldc + m] = sv;
+      continue;
+    }
+    if (mode == EPI_SHIFT) v = (v + alpha * S[(long long)m * lds + n]) / alpha;
+    else if (mode == EPI_SUB) v = S[(long long)m * lds + n] - v;
+    C[(long long)m * ldc + n] = v;
+  }
+}
+
+void splitk_reduce(const double* ws, int splits, long long split_stride, int M, int N,
+                   long long ldw, double* C, long long ldc, int mode, double alpha,
+                   const double* S, long long lds, cudaStream_t st) {
+  const long long total = (long long)M * N;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, splits, split_stride, M, N, ldw, C, ldc, mode,
+                                               alpha, S, lds);
+  count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// panel utilities
+// ---------------------------------------------------------------------------
+__global__ void copy_matrix_kernel(const double* src, long long lds, double* dst, long long ldd,
+                                   long long rows, int cols) {
+  const long long total = rows * cols;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cols;
+    const int c = (int)(i % cols);
+    dst[r * ldd + c] = src[r * lds + c];
+  }
+}
+
+void copy_matrix(const double* src, long long lds, double* dst, long long ldd, long long rows,
+                 int cols, cudaStream_t st) {
+  const long long total = rows * cols;
+  if (total == 0) return;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+  copy_matrix_kernel<<<blocks, 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
+  count_launch();
+}
+
+__global__ void fill_zero_kernel(double* dst, long long ld, long long rows, long long cols) {
+  const long long total = rows * cols;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[(i / cols) * ld + (i % cols)] = 0.0;
+}
+
+void fill_zero(double* dst, long long ld, long long rows, long long cols, cudaStream_t st) {
+  if (ld == cols) {
+    cudaMemsetAsync(dst, 0, (size_t)rows * cols * sizeof(double), st);
+    return;
+  }
+  const long long total = rows * cols;
+  if (total == 0) return;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+  fill_zero_kernel<<<blocks, 256, 0, st>>>(dst, ld, rows, cols);
+  count_launch();
+}
+
+// out[m][k] = w[m][k] · d[k]  — (w_kept * d_kept) of projection.py:77
+__global__ void scale_columns_kernel(const double* w, long long ldw, const double* d, double* out,
+                                     long long ldo, long long rows, int cols) {
+  const long long total = rows * cols;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cols;
+    const int c = (int)(i % cols);
+    out[r * ldo + c] = w[r * ldw + c] * d[c];
+  }
+}
+
+void scale_columns(const double* w, long long ldw, const double* d, double* out, long long ldo,
+                   long long rows, int cols, cudaStream_t st) {
+  const long long total = rows * cols;
+  if (total == 0) return;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+  scale_columns_kernel<<<blocks, 256, 0, st>>>(w, ldw, d, out, ldo, rows, cols);
+  count_launch();
+}
+
+__global__ void gather_columns_kernel(const double* src, long long lds, const int* idx, int ncols,
+                                      double* dst, long long ldd, long long rows) {
+  const long long total = rows * ncols;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / ncols;
+    const int c = (int)(i % ncols);
+    dst[r * ldd + c] = src[r * lds + idx[c]];
+  }
+}
+
+void gather_columns(const double* src, long long lds, const int* idx, int ncols, double* dst,
+                    long long ldd, long long rows, cudaStream_t st) {
+  const long long total = rows * ncols;
+  if (total == 0) return;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+  gather_columns_kernel<<<blocks, 256, 0, st>>>(src, lds, idx, ncols, dst, ldd, rows);
+  count_launch();
+}
+
+__global__ void add_diag_kernel(double* a, long long ld, int m, double s) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) a[(long long)i * ld + i] += s;
+}
+
+void add_diag(double* a, long long ld, int m, double s, cudaStream_t st) {
+  add_diag_kernel<<<(m + 255) / 256, 256, 0, st>>>(a, ld, m, s);
+  count_launch();
+}
+
+__global__ void set_identity_kernel(double* a, long long ld, int m) {
+  const long long total = (long long)m * m;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / m), c = (int)(i % m);
+    a[(long long)r * ld + c] = (r == c) ? 1.0 : 0.0;
+  }
+}
+
+void set_identity(double* a, long long ld, int m, cudaStream_t st) {
+  const long long total = (long long)m * m;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 4096);
+  set_identity_kernel<<<blocks, 256, 0, st>>>(a, ld, m);
+  count_launch();
+}
+
+}  // namespace psd

@@ -1,0 +1,97 @@
+// Host-side launchers for the sm_100a kernels (internal to libpsdproj.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gemm_f64.cuh"
+
+namespace psd {
+
+// Kernels launched by this library on the calling thread (reported to callers
+// as psd_report.gpu_launches).
+extern thread_local int g_launch_count;
+inline void count_launch(int k = 1) { g_launch_count += k; }
+
+struct DeviceInfo {
+  int sms = 148;
+  size_t max_smem = 227 * 1024;
+};
+const DeviceInfo& device_info();
+
+// ---- GEMM (DMMA) ------------------------------------------------------------
+struct GemmOp {
+  int a_layout = A_MK, b_layout = B_KN;
+  const double* A = nullptr;
+  long long lda = 0;
+  const double* B = nullptr;
+  long long ldb = 0;
+  double* C = nullptr;
+  long long ldc = 0;
+  int M = 0, N = 0, K = 0;
+  int epi = EPI_STORE;
+  double alpha = 1.0;
+  const double* S = nullptr;
+  long long lds = 0;
+  double* partials = nullptr;  // EPI_RESID: one double per CTA
+  int max_splits = 256;        // 1 forces a single pass (required for SUB/MIRROR/RESID)
+};
+// Launches the DMMA GEMM, splitting K when that shortens the critical path.
+// `ws` must hold ws_elems doubles for split-K partials.  Returns the number
+// of kernel launches issued (1 or 2), or <0 on error.
+int gemm_f64(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st);
+// Number of CTAs a RESID launch uses (size of `partials`).
+long long gemm_resid_ctas(const GemmOp& op);
+
+// ---- memory-bound kernels --------------------------------------------------
+// stats[0] = max|x|, stats[1] = max|x - xᵀ|, ((int*)(stats+2))[0] = flags
+// (bit0: not bitwise symmetric, bit1: NaN/Inf present). stats zeroed inside.
+void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st);
+// x ← (x + xᵀ)/2 for a small m×m matrix (in place, exact mirror).
+void symmetrize_small(double* x, int m, long long ld, cudaStream_t st);
+void philox_normal(double* out, long long rows, int cols, long long ld, uint64_t seed,
+                   uint64_t offset, cudaStream_t st);
+// y = (X − shift·I)·v ; partials[b] = Σ_{rows of block b} y²; returns #blocks.
+int gemv_shift(const double* x, long long n, long long ldx, const double* v, double shift,
+               double* y, double* partials, cudaStream_t st);
+int gemv_blocks(long long n);
+// nrm = sqrt(Σ partials); if nrm ≤ floor set *flag; v = y / nrm. out[0] = nrm.
+void normalize(const double* y, const double* partials, int nparts, long long n, double floor,
+               double* v, double* out, int* flag, cudaStream_t st);
+void sum_partials(const double* partials, long long nparts, double* out, int do_sqrt,
+                  cudaStream_t st);
+// Split-K reduction with the GEMM epilogues; mode EPI_STORE/SHIFT/SUB or 10 (= symmetric).
+void splitk_reduce(const double* ws, int splits, long long split_stride, int M, int N,
+                   long long ldw, double* C, long long ldc, int mode, double alpha,
+                   const double* S, long long lds, cudaStream_t st);
+void copy_matrix(const double* src, long long lds, double* dst, long long ldd, long long rows,
+                 int cols, cudaStream_t st);
+void fill_zero(double* dst, long long ld, long long rows, long long cols, cudaStream_t st);
+void scale_columns(const double* w, long long ldw, const double* d, double* out, long long ldo,
+                   long long rows, int cols, cudaStream_t st);
+void gather_columns(const double* src, long long lds, const int* idx, int ncols, double* dst,
+                    long long ldd, long long rows, cudaStream_t st);
+void add_diag(double* a, long long ld, int m, double s, cudaStream_t st);
+void set_identity(double* a, long long ld, int m, cudaStream_t st);
+
+// ---- small dense (w×w) kernels ---------------------------------------------
+// Blocked right-looking Cholesky A = L Lᵀ in place (lower), ld = lda.
+// info[0] = 0 ok, j+1 = first failing pivot.  Upper triangle zeroed.
+int cholesky_lower(double* a, long long lda, int m, int* info, double* ws, size_t ws_elems,
+                   cudaStream_t st);
+// rinv = (Lᵀ)⁻¹ (upper triangular), from lower-triangular L.
+void tri_inv_upper_from_lower(const double* l, long long ldl, int m, double* rinv,
+                              long long ldr, cudaStream_t st);
+// rdiag[i] *= L[i][i]
+void accumulate_diag(const double* l, long long ldl, int m, double* rdiag, cudaStream_t st);
+// Symmetric eigensolver (block Jacobi).  a (m×m, destroyed), values[m], v (m×m).
+// Returns number of sweeps (>0) or −1 on non-convergence.
+int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long long ldv,
+                double* ws, size_t ws_elems, int* dflags, cudaStream_t st);
+size_t jacobi_ws_elems(int m);
+// Sort eigenpairs descending, sign-fix columns (symmetric.py:80-85).
+// vals_out[m], vecs_out (m×m, ld), npos[0] = #(vals − offset > 0).
+void sort_eigs(const double* vals, const double* vecs, long long ldv, int m, double offset,
+               double* vals_out, double* vecs_out, long long ldo, int* npos, int* perm,
+               cudaStream_t st);
+
+}  // namespace psd

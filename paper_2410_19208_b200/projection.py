@@ -1,0 +1,219 @@
+"""Randomized PSD projections on the GPU — drop-in for psdcone/projection.py.
+
+``ran_proj`` (Alg. 2, projection.py:92-119), ``ran_proj_scal`` (Alg. 3,
+projection.py:122-159) and the ``project`` dispatcher (projection.py:180-223)
+keep the reference signatures, validation order, RNG draw order and report
+fields.  All arithmetic runs in libpsdproj.so (FP64 DMMA tensor-core GEMMs,
+CholeskyQR, block-Jacobi eigensolver, mirrored SYRK reconstruction); numpy
+inputs are uploaded once and results copied back, torch CUDA inputs stay on
+the device.  Extra keyword-only arguments: ``omega=`` (inject Ω),
+``assume_symmetric=`` (skip the validation pass for inputs known to be
+bitwise symmetric).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native, errors
+from ._tensors import as_device, draw_gaussian, require_square
+from .sketch import RangeParams, min_eig_magnitude_device
+from .symmetric import (SymStats, check_symmetric_device, eigh_device, reconstruct_device,
+                        rng_from_seed)
+
+METHODS = ("exact", "polar", "randomized", "scaled_randomized")  # projection.py:21
+ALPHA_TOL_FACTOR = 1e-12  # projection.py:133
+
+
+@dataclass
+class ProjectorConfig:
+    """projection.py:24-49."""
+
+    method: str = "exact"
+    params: RangeParams | None = None
+    power_N: int = 10
+    alpha_override: float | None = None
+    scale_factor: float = 1.0
+    collect_diagnostics: bool = False
+    return_factors: bool = False
+
+    def __post_init__(self):
+        if self.method not in METHODS:
+            raise errors.error("InvalidParams", f"unknown projection method {self.method!r}")
+        if self.method in ("randomized", "scaled_randomized") and self.params is None:
+            raise errors.error("InvalidParams", f"method {self.method!r} requires RangeParams")
+        if self.method == "scaled_randomized" and self.alpha_override is None and self.power_N < 1:
+            raise errors.error("InvalidParams", "scaled method needs power_N >= 1 or alpha_override")
+
+
+@dataclass
+class ProjectionReport:
+    """projection.py:52-69 (+ ``device_info``: kernel-side diagnostics)."""
+
+    result: object
+    method: str
+    effective_rank: int
+    alpha_used: float | None = None
+    residual_frob: float | None = None
+    wall_time: float = 0.0
+    factors: tuple | None = None
+    fallback: bool = False
+    basis_width: int = 0
+    device_info: dict | None = field(default=None, repr=False)
+
+
+def _stats_for(op, assume_symmetric):
+    if assume_symmetric:
+        return None
+    return check_symmetric_device(op)
+
+
+def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, method, t0):
+    width = params.width
+    lib = _native.load_library()
+    plan = _native.get_plan(n, width, op.device)
+    dev = op.device
+    result = torch.empty((n, n), dtype=torch.float64, device=dev)
+    fw = torch.empty((n, width), dtype=torch.float64, device=dev) if return_factors else None
+    fd = torch.empty(width, dtype=torch.float64, device=dev) if return_factors else None
+    flags = _native.FLAG_SKIP_SYMCHECK
+    if stats is None or stats.bitwise:
+        flags |= _native.FLAG_ASSUME_SYMMETRIC
+    if collect_diagnostics:
+        flags |= _native.FLAG_DIAGNOSTICS
+    rep = _native.PsdReport()
+    _native.check(lib.psd_ran_proj(plan.handle, _native.ptr(op.t), n, n, _native.ptr(om),
+                                   om.stride(0), params.k, params.l, params.q, float(alpha), flags,
+                                   _native.ptr(result), n, _native.ptr(fw), width, _native.ptr(fd),
+                                   ctypes.byref(rep), _native.stream_handle(dev)))
+    r = rep.effective_rank
+    factors = None
+    if return_factors:
+        factors = (op.give_back(fw[:, :r].contiguous()), op.give_back(fd[:r].contiguous()))
+    info = rep.as_dict()
+    if stats is not None:
+        info["max_abs"], info["sym_defect"] = stats.max_abs, stats.defect
+    return ProjectionReport(
+        result=op.give_back(result),
+        method=method,
+        effective_rank=int(r),
+        alpha_used=float(alpha) if alpha > 0 else None,
+        residual_frob=float(rep.residual_frob) if collect_diagnostics else None,
+        wall_time=time.perf_counter() - t0,
+        factors=factors,
+        basis_width=int(rep.basis_width),
+        device_info=info,
+    )
+
+
+def _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, stats, t0):
+    n = require_square(op)
+    width = params.width
+    if width > n:                                               # sketch.py:67-69
+        raise errors.error("InvalidParams", f"k+l = {width} exceeds min(m, n) = {n}")
+    om = as_device(omega, op.device).t if omega is not None else draw_gaussian(rng, (n, width), op.device)
+    return _run(op, n, params, om, 0.0, stats, collect_diagnostics, return_factors, "randomized", t0)
+
+
+def ran_proj(x, params, rng, collect_diagnostics=False, return_factors=False, *, omega=None,
+             assume_symmetric=False):
+    """projection.py:92-119 (Alg. 2): X̂₊ = Q U D₊ Uᵀ Qᵀ."""
+    t0 = time.perf_counter()
+    op = as_device(x)
+    require_square(op)
+    stats = _stats_for(op, assume_symmetric)                   # projection.py:100
+    return _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, stats, t0)
+
+
+def _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factors, omega, stats, t0):
+    n = require_square(op)
+    if stats is None:  # assume_symmetric: still need max|x| for alpha_tol (one HBM pass)
+        stats = check_symmetric_device(op)
+    max_abs = stats.max_abs
+    alpha_tol = ALPHA_TOL_FACTOR * max(1.0, max_abs)            # projection.py:133
+    if alpha <= alpha_tol:
+        raise errors.error(
+            "AlphaTooSmall",
+            f"alpha = {alpha:.3e} is at or below tolerance {alpha_tol:.3e}; input is numerically PSD")
+    width = params.width
+    if width > n:
+        raise errors.error("InvalidParams", f"k+l = {width} exceeds min(m, n) = {n}")
+    om = as_device(omega, op.device).t if omega is not None else draw_gaussian(rng, (n, width), op.device)
+    return _run(op, n, params, om, float(alpha), stats, collect_diagnostics, return_factors,
+                "scaled_randomized", t0)
+
+
+def ran_proj_scal(x, params, alpha, rng, collect_diagnostics=False, return_factors=False, *,
+                  omega=None, assume_symmetric=False):
+    """projection.py:122-159 (Alg. 3) through B = (X + αI)/α (fused in the GEMM epilogues)."""
+    t0 = time.perf_counter()
+    op = as_device(x)
+    require_square(op)
+    stats = _stats_for(op, assume_symmetric)
+    return _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factors, omega,
+                             stats, t0)
+
+
+def _exact_report(op, method, t0):
+    """projection.py:162-177 on the GPU (eigh + mirrored reconstruction)."""
+    n = op.t.shape[0]
+    vals, vecs = eigh_device(op, validate=False)
+    r = int((vals > 0.0).sum().item())
+    if method == "exact":
+        result = reconstruct_device(vecs[:, :r], vals[:r], n, op.device)
+    else:
+        # polar form (X + (XᵀX)^½)/2 = (X + V|Λ|Vᵀ)/2 for symmetric X (symmetric.py:117-128)
+        absr = reconstruct_device(vecs, vals.abs(), n, op.device)
+        result = (op.t + absr) / 2.0
+        result = (result + result.T) / 2.0
+    factors = None
+    if method == "exact":
+        factors = (op.give_back(vecs[:, :r].contiguous()), op.give_back(vals[:r].contiguous()))
+    return ProjectionReport(result=op.give_back(result), method=method, effective_rank=r,
+                            wall_time=time.perf_counter() - t0, factors=factors, basis_width=n)
+
+
+def project(x, cfg, rng=None, *, omega=None, assume_symmetric=False):
+    """projection.py:180-223: dispatcher with the scaled → unscaled AlphaTooSmall fallback."""
+    t0 = time.perf_counter()
+    op = as_device(x)
+    require_square(op)
+    stats = _stats_for(op, assume_symmetric)                   # projection.py:189
+    if cfg.method in ("exact", "polar"):
+        return _exact_report(op, cfg.method, t0)
+
+    rng = rng_from_seed(rng if rng is not None else (cfg.params.seed if cfg.params else None))
+    if cfg.method == "randomized":
+        report = _ran_proj_op(op, cfg.params, rng, cfg.collect_diagnostics, cfg.return_factors,
+                              omega, stats, t0)
+        report.wall_time = time.perf_counter() - t0
+        return report
+
+    if cfg.alpha_override is not None:
+        alpha = float(cfg.alpha_override)
+    else:
+        alpha = min_eig_magnitude_device(op, cfg.power_N, rng)   # projection.py:206
+    alpha *= cfg.scale_factor
+    try:
+        report = _ran_proj_scal_op(op, cfg.params, alpha, rng, cfg.collect_diagnostics,
+                                   cfg.return_factors, omega, stats, t0)
+    except errors.REGISTRY["AlphaTooSmall"]:
+        report = _ran_proj_op(op, cfg.params, rng, cfg.collect_diagnostics, cfg.return_factors,
+                              omega, stats, t0)
+        report.fallback = True
+        report.alpha_used = float(alpha)
+    report.wall_time = time.perf_counter() - t0
+    return report
+
+
+def flops(n, params, effective_rank):
+    """Algorithmic FLOPs of one projection: 2n²w(2q+2) + n²r₊."""
+    return 2.0 * n * n * params.width * (2 * params.q + 2) + float(n) * n * effective_rank
+
+
+__all__ = ["METHODS", "ProjectorConfig", "ProjectionReport", "ran_proj", "ran_proj_scal",
+           "project", "flops"]

@@ -1,0 +1,143 @@
+"""Kernel-level GPU tests: the FP64 DMMA GEMM in every layout / epilogue
+against a torch fp64 reference, the symmetric eigensolver, the Philox
+Gaussian fill and the symmetry-statistics pass."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    import paper_2410_19208_b200 as psd
+    lib = psd._native.load_library()
+    return torch, psd, lib
+
+
+def _gemm(env, a_layout, b_layout, A, B, M, N, K, epi=0, alpha=1.0, S=None, ws=True, C=None):
+    torch, psd, lib = env
+    dev = A.device
+    if C is None:
+        C = torch.full((M, N), np.nan, dtype=torch.float64, device=dev)
+    wsb = torch.empty(64 * max(M, 1) * (N + 1) + (1 << 20), dtype=torch.float64, device=dev) if ws else None
+    st = psd._native.check(lib.psd_gemm_f64(
+        a_layout, b_layout, psd._native.ptr(A), A.stride(0), psd._native.ptr(B), B.stride(0),
+        psd._native.ptr(C), C.stride(0), M, N, K, epi, alpha,
+        psd._native.ptr(S) if S is not None else ctypes.c_void_p(0), S.stride(0) if S is not None else 0,
+        psd._native.ptr(wsb) if wsb is not None else ctypes.c_void_p(0), wsb.numel() if wsb is not None else 0,
+        psd._native.stream_handle(dev)))
+    torch.cuda.synchronize()
+    return C
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (64, 288, 16), (200, 272, 1000),
+                                   (1000, 50, 1000), (333, 544, 257), (130, 9, 4099)])
+@pytest.mark.parametrize("al,bl", [(0, 0), (1, 0), (0, 1)])
+def test_gemm_layouts(env, M, N, K, al, bl):
+    torch = env[0]
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
+    a = torch.randn(M, K, dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn(K, N, dtype=torch.float64, device="cuda", generator=g)
+    A = a if al == 0 else a.T.contiguous()
+    B = b if bl == 0 else b.T.contiguous()
+    C = _gemm(env, al, bl, A, B, M, N, K)
+    ref = a @ b
+    err = (C - ref).abs().max().item() / max(ref.abs().max().item(), 1e-300)
+    assert err < 1e-13, err
+
+
+def test_gemm_odd_leading_dimensions(env):
+    torch = env[0]
+    base = torch.randn(301, 303, dtype=torch.float64, device="cuda")
+    A = base[:, :77]             # lda = 303 (odd) → 8-byte cp.async path
+    B = torch.randn(77, 41, dtype=torch.float64, device="cuda")
+    C = _gemm(env, 0, 0, A, B, 301, 41, 77)
+    assert (C - A @ B).abs().max().item() < 1e-12
+
+
+def test_gemm_shift_and_sub_epilogues(env):
+    torch = env[0]
+    n, w = 513, 40
+    X = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    P = torch.randn(n, w, dtype=torch.float64, device="cuda")
+    alpha = 0.37
+    C = _gemm(env, 0, 0, X, P, n, w, n, epi=1, alpha=alpha, S=P)
+    ref = (X @ P + alpha * P) / alpha
+    assert ((C - ref).abs().max() / ref.abs().max()).item() < 1e-13
+    S = torch.randn(n, w, dtype=torch.float64, device="cuda")
+    C2 = _gemm(env, 0, 0, X, P, n, w, n, epi=2, S=S, ws=False)
+    assert ((C2 - (S - X @ P)).abs().max()).item() < 1e-11
+
+
+def test_gemm_mirrored_store_is_exactly_symmetric(env):
+    torch = env[0]
+    n, r = 700, 37
+    W = torch.randn(n, r, dtype=torch.float64, device="cuda")
+    d = torch.rand(r, dtype=torch.float64, device="cuda")
+    WD = W * d
+    C = _gemm(env, 0, 1, WD, W, n, n, r, epi=3, ws=False)
+    assert torch.equal(C, C.T)
+    ref = WD @ W.T
+    assert ((C - ref).abs().max() / ref.abs().max()).item() < 1e-13
+
+
+@pytest.mark.parametrize("m", [1, 2, 17, 50, 64, 144, 272])
+def test_eigh_vs_lapack(env, m):
+    torch, psd, _ = env
+    rng = np.random.default_rng(m)
+    g = rng.standard_normal((m, m))
+    a = (g + g.T) / 2
+    dec = psd.eigh(a)
+    ref = np.linalg.eigvalsh(a)[::-1]
+    np.testing.assert_allclose(dec.values, ref, atol=1e-12 * max(1, np.abs(ref).max()))
+    v = dec.vectors
+    assert np.abs(v.T @ v - np.eye(m)).max() < 1e-12 * m
+    assert np.abs(v @ np.diag(dec.values) @ v.T - a).max() < 1e-12 * m
+    # sign convention: largest-|entry| of each column is positive
+    idx = np.argmax(np.abs(v), axis=0)
+    assert np.all(v[idx, np.arange(m)] > 0)
+
+
+def test_eigh_clustered_and_degenerate(env):
+    torch, psd, _ = env
+    rng = np.random.default_rng(5)
+    q, _ = np.linalg.qr(rng.standard_normal((120, 120)))
+    lam = np.concatenate([np.full(40, 2.0), np.full(40, -1.0), 1e-14 * rng.standard_normal(40)])
+    a = (q * lam) @ q.T
+    a = (a + a.T) / 2
+    dec = psd.eigh(a)
+    np.testing.assert_allclose(np.sort(dec.values), np.sort(np.linalg.eigvalsh(a)), atol=1e-13)
+    assert np.abs(dec.vectors @ np.diag(dec.values) @ dec.vectors.T - a).max() < 1e-12
+
+
+def test_gaussian_fill_statistics(env):
+    torch, psd, _ = env
+    g = psd.DeviceRng(123)
+    x = g.normal((1000, 1000), torch.device("cuda"))
+    m, v = x.mean().item(), x.var().item()
+    assert abs(m) < 0.01 and abs(v - 1) < 0.01
+    y = psd.DeviceRng(123).normal((1000, 1000), torch.device("cuda"))
+    assert torch.equal(x, y)
+
+
+def test_require_symmetric_stats(env):
+    torch, psd, _ = env
+    rng = np.random.default_rng(3)
+    g = rng.standard_normal((333, 333))
+    a = (g + g.T) / 2
+    assert psd.require_symmetric(a) is not None
+    b = a.copy()
+    b[5, 7] += 1e-6
+    with pytest.raises(psd.AsymmetricMatrixError):
+        psd.require_symmetric(b)
+    c = a.copy()
+    c[5, 7] += 1e-12 * np.abs(a).max()   # within tolerance: accepted
+    op = psd._tensors.as_device(c)
+    st = psd.symmetric.check_symmetric_device(op)
+    assert not st.bitwise and st.defect == pytest.approx(abs(c[5, 7] - c[7, 5]))
+    assert st.max_abs == np.abs(c).max()
