@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark: randomized PSD projections/s at BASELINE config 3
+(n=32768, k=256, p=16, q=1, fp64) on B200, with FP64 tensor-core roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one projection (``ran_proj``, Alg. 2) of a seeded C3 matrix that is
+already resident in HBM; the K timed steps cycle through a pool of distinct
+matrices (8.6 GB each ≫ 126 MB L2, so no L2 flush is needed).  Ω is drawn on
+the device each step (Philox).  Multi-GPU: independent replicas, one process
+per GPU (the C3 projections are independent), value
+= all ranks' projections / max-over-ranks device time.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port in oracle/psd_oracle.py — same numpy/OpenBLAS calls as
+psdcone.ran_proj) on this box's host cores, on a bounded sample (n=8192 with
+C3's k, p, q), scaled by (8192/32768)² to the metric's unit.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "rand-PSD projections/s at n=32768,k=256 fp64; % of FP64 tensor-core roofline"
+UNIT = "projections/s"
+CPU_SAMPLE_N = 8192
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=16)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--k", type=int, default=256)
+    ap.add_argument("--p", type=int, default=16)
+    ap.add_argument("--q", type=int, default=1)
+    ap.add_argument("--pool", type=int, default=4, help="distinct X matrices cycled per rank")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(a, n_gpus):
+    return {
+        "workload": f"BASELINE config 3: ran_proj (Alg. 2) n={a.n}, k={a.k}, p={a.p}, q={a.q}, fp64, "
+                    f"{a.steps} sequential projections per rank",
+        "n": a.n, "k": a.k, "p": a.p, "q": a.q, "width": a.k + a.p,
+        "x_pool": a.pool,
+        "l2": "inputs larger than L2 (each X is 8·n² bytes ≫ 126 MB)",
+        "omega": "device Philox N(0,1) per projection",
+        "parallelism": f"replicas x{n_gpus}" if n_gpus > 1 else "single GPU",
+    }
+
+
+# --------------------------------------------------------------------- CPU ---
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        nt = max((d.get("num_threads") or 0) for d in threadpool_info() if d.get("user_api") == "blas")
+        return int(nt) if nt else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_sample(a, reps=1):
+    """Oracle port (same numpy calls as psdcone.ran_proj) at n=CPU_SAMPLE_N; returns
+    (projections/s scaled to n=a.n, seconds per sample)."""
+    import numpy as np
+
+    from oracle import psd_oracle as orc
+    ns = min(CPU_SAMPLE_N, a.n)
+    x = orc.c3_matrix(ns, seed=11)
+    best = 1e300
+    for r in range(reps):
+        om = np.random.default_rng(100 + r).standard_normal((ns, a.k + a.p))
+        t0 = time.perf_counter()
+        orc.ran_proj(x, a.k, a.p, a.q, omega=om)
+        best = min(best, time.perf_counter() - t0)
+    scale = (ns / a.n) ** 2  # every stage of the path is O(n²) at fixed width
+    return scale / best, best, ns
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    n_gpus = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
+    if rank != 0:
+        return
+    for _ in range(max(a.warmup, 0)):
+        cpu_sample(a)
+    vals, secs = [], []
+    for _ in range(a.steps):
+        v, s, ns = cpu_sample(a)
+        vals.append(v)
+        secs.append(s)
+    value = a.steps / sum(s / ((ns / a.n) ** 2) for s in secs)
+    cores = cpu_cores()
+    sample = (f"oracle port of psdcone.ran_proj (numpy/OpenBLAS, {cores} threads) on a C3 matrix at "
+              f"n={CPU_SAMPLE_N}, k={a.k}, p={a.p}, q={a.q}; time × (n/{CPU_SAMPLE_N})² per step")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": n_gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded C3 matrix, host numpy)",
+        "config": workload_config(a, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ clocks ---
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------- ours ---
+
+def fp64_peak(torch, dev):
+    """cuBLAS DGEMM 8192³ burst rate (MEASURED_PEAKS.json carries no FP64 entry)."""
+    a = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    b = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize(dev)
+    best = 1e9
+    for _ in range(5):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize(dev)
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * 8192 ** 3 / best / 1e9
+
+
+def load_traffic():
+    path = os.path.join(REPO, "profiles", "gemm_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_19208_b200 as psd
+    from paper_2410_19208_b200 import workloads
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    n, params = a.n, psd.RangeParams(k=a.k, l=a.p, q=a.q)
+
+    peak = fp64_peak(torch, dev) if rank == 0 else None
+    nominal = 148 * 128 * 1.965  # GFLOP/s: 148 SMs × 64 DMMA FMA/clk × 2 × 1965 MHz
+
+    pool = [workloads.c3_device(n, seed=1000 * rank + i, device=dev) for i in range(a.pool)]
+    rng = psd.DeviceRng(seed=4242 + rank)
+    plan = psd._native.get_plan(n, params.width, dev)
+
+    for i in range(max(a.warmup, 3 if a.warmup >= 3 else a.warmup)):
+        psd.ran_proj(pool[i % a.pool], params, rng)
+    torch.cuda.synchronize(dev)
+    plan.profile(enable=True, reset=True)
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    ranks = []
+    e0.record()
+    for i in range(a.steps):
+        rep = psd.ran_proj(pool[i % a.pool], params, rng)
+        launches += rep.device_info["gpu_launches"]
+        ranks.append(rep.effective_rank)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    prof = plan.profile(enable=False, reset=True)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * a.steps / (ms / 1000.0)
+
+    # FP64 roofline of the dominant kernel: the op(X)·P DMMA GEMM (2n²w flops per launch)
+    g_ms, g_cnt = prof["sketch_gemm"]
+    gemm_ms = g_ms / max(g_cnt, 1)
+    gemm_tf = 2.0 * n * n * params.width / (gemm_ms / 1000.0) / 1e12
+    r_plus = statistics.median(ranks) if ranks else 0
+    flops = psd.flops(n, params, r_plus)
+    traffic = load_traffic()
+    stages = {k: round(v[0] / a.steps, 3) for k, v in prof.items() if v[1]}
+
+    e2e = None
+    if rank == 0 and not a.no_e2e:
+        e2e = run_e2e(a, torch, psd, pool[0], params, dev)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        v, s, ns = cpu_sample(a, reps=1)
+        cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+               "sample": f"1 projection of a C3 matrix at n={ns} (k={a.k}, p={a.p}, q={a.q}) "
+                         f"by the oracle port of psdcone.ran_proj on host cores in {s:.2f} s, "
+                         f"scaled by ({ns}/{a.n})²"}
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    peak_tf = (peak or nominal) / 1000.0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE config-3 matrices generated in HBM)",
+        "config": workload_config(a, world),
+        "roofline": {
+            "bound": "tensor", "achieved": gemm_tf, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": gemm_tf / peak_tf, "traffic": traffic.get("bytes_per_launch") if traffic else None,
+            "kernel": "gemm_f64_kernel<64x288 DMMA, A row-major, B row-major> — op(X)·P "
+                      f"(n×n·n×w), {2 * n * n * params.width / 1e9:.0f} GFLOP per launch, "
+                      f"{gemm_ms:.2f} ms avg over {g_cnt} launches (CUDA events, timed region)",
+            "peak_source": "cuBLAS DGEMM 8192³ burst measured in this run (MEASURED_PEAKS.json has "
+                           f"no FP64 entry); nominal DMMA peak at 1965 MHz = {nominal / 1000:.1f}",
+            "traffic_source": traffic.get("source") if traffic else None,
+        },
+        "projection_tflops": flops * value / world / 1e12,
+        "projection_roofline_frac": flops * value / world / 1e12 / peak_tf,
+        "flops_per_projection": flops,
+        "effective_rank": r_plus,
+        "stages_ms_per_projection": stages,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if e2e:
+        line["e2e"] = e2e
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(a, torch, psd, x_dev, params, dev):
+    """Same metric through the public API with HOST buffers: pinned X → HBM,
+    projection, result → pinned host, all inside the timed region."""
+    n = a.n
+    try:
+        hx = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        hr = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    except Exception as exc:  # pragma: no cover - host RAM
+        return {"value": None, "unit": UNIT, "error": f"pinned alloc failed: {exc}"}
+    hx.copy_(x_dev.cpu())
+    dx = torch.empty((n, n), dtype=torch.float64, device=dev)
+    rng = psd.DeviceRng(seed=777)
+    steps = max(1, a.e2e_steps)
+
+    def one():
+        dx.copy_(hx, non_blocking=True)
+        rep = psd.ran_proj(dx, params, rng)
+        hr.copy_(rep.result, non_blocking=True)
+        return rep
+
+    one()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    del dx
+    return {"value": steps / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": 8 * n * n,
+            "d2h_bytes_per_step": 8 * n * n, "steps": steps,
+            "path": "pinned host X → cudaMemcpyAsync → paper_2410_19208_b200.ran_proj → pinned host result"}
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -18,6 +18,7 @@ from .sketch import (RangeParams, min_eig_magnitude, orthonormality_defect, powe
 from .symmetric import (EigenDecomposition, eigh, exact_psd_projection, frobenius_norm,
                         gaussian_matrix, require_symmetric, rng_from_seed, symmetrize)
 from .install import install, uninstall
+from . import workloads  # noqa: E402  (seeded HBM generators for the BASELINE configs)
 
 __version__ = "0.1.0"
 

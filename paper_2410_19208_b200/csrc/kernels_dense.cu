@@ -67,19 +67,21 @@ __global__ void zero_upper_kernel(double* a, long long lda, int m) {
 
 int cholesky_lower(double* a, long long lda, int m, int* info, double* ws, size_t ws_elems,
                    cudaStream_t st) {
-  static bool attr_done[16] = {};
+  static size_t attr_bytes[16] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!attr_done[dev]) {
-    cudaFuncSetAttribute(chol_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)device_info().max_smem);
-    attr_done[dev] = true;
+  const size_t need = (size_t)m * (kCholNB + 1) * sizeof(double);
+  if (need > device_info().max_smem - 1024) return -1;
+  if (need > attr_bytes[dev]) {
+    if (cudaFuncSetAttribute(chol_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)need) != cudaSuccess)
+      return -1;
+    attr_bytes[dev] = need;
   }
   cudaMemsetAsync(info, 0, sizeof(int), st);
   for (int p0 = 0; p0 < m; p0 += kCholNB) {
     const int nb = std::min(kCholNB, m - p0);
     const size_t smem = (size_t)(m - p0) * (nb + 1) * sizeof(double);
-    if (smem > device_info().max_smem) return -1;
     chol_panel_kernel<<<1, 512, smem, st>>>(a, lda, m, p0, nb, info);
     count_launch();
     const int rest = m - p0 - nb;
@@ -136,13 +138,12 @@ void tri_inv_upper_from_lower(const double* l, long long ldl, int m, double* rin
                               long long ldr, cudaStream_t st) {
   const int warps = 8;
   const size_t smem = (size_t)warps * m * sizeof(double);
-  static bool attr_done[16] = {};
+  static size_t attr_bytes[16] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!attr_done[dev]) {
-    cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)device_info().max_smem);
-    attr_done[dev] = true;
+  if (smem > 48 * 1024 && smem > attr_bytes[dev]) {
+    cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_bytes[dev] = smem;
   }
   tri_inv_kernel<<<(m + warps - 1) / warps, warps * 32, smem, st>>>(l, ldl, m, rinv, ldr);
   count_launch();
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(256) jacobi_solve_kernel(const double* __restr
                                                            long long lda, int m, int nblk,
                                                            int round, int sweeps,
                                                            const double* norm, double* jbuf,
-                                                           int* dflags) {
+                                                           double* sbuf, int* dflags) {
   __shared__ double S[kSub][kSub + 1];
   __shared__ double V[kSub][kSub + 1];
   __shared__ double cs[kSub / 2], sn[kSub / 2], tt[kSub / 2];
@@ -283,7 +284,11 @@ __global__ void __launch_bounds__(256) jacobi_solve_kernel(const double* __restr
   const double abs_tol = 1e-18 * norm[0];
   const int rots = inner_jacobi(S, V, sweeps, abs_tol, cs, sn, tt);
   double* J = jbuf + (size_t)pair * kSub * kSub;
-  for (int e = threadIdx.x; e < kSub * kSub; e += blockDim.x) J[e] = V[e / kSub][e % kSub];
+  double* Sout = sbuf + (size_t)pair * kSub * kSub;
+  for (int e = threadIdx.x; e < kSub * kSub; e += blockDim.x) {
+    J[e] = V[e / kSub][e % kSub];
+    Sout[e] = S[e / kSub][e % kSub];
+  }
   if (threadIdx.x == 0 && rots > 0) atomicAdd(dflags, rots);
 }
 
@@ -293,6 +298,7 @@ __global__ void __launch_bounds__(256) jacobi_apply_kernel(const double* __restr
                                                            long long ldn, int m,
                                                            int nblk, int round,
                                                            const double* __restrict__ jbuf,
+                                                           const double* __restrict__ sbuf,
                                                            double* v, long long ldv) {
   __shared__ double T[kSub][kSub + 1];
   __shared__ double U[kSub][kSub + 1];
@@ -307,6 +313,16 @@ __global__ void __launch_bounds__(256) jacobi_apply_kernel(const double* __restr
       ib[threadIdx.x] = sub_index(nblk, round, pb, threadIdx.x);
     }
     __syncthreads();
+    if (pa == pb) {
+      // the solve kernel's rotated subproblem: exact zeros on rotated pairs,
+      // no GEMM rounding mixed into the diagonal block
+      const double* Sp = sbuf + (size_t)pa * kSub * kSub;
+      for (int e = threadIdx.x; e < kSub * kSub; e += blockDim.x) {
+        const int gi = ia[e / kSub], gj = ib[e % kSub];
+        if (gi < m && gj < m) anew[(long long)gi * ldn + gj] = Sp[e];
+      }
+      return;
+    }
     const double* Ja = jbuf + (size_t)pa * kSub * kSub;
     const double* Jbp = jbuf + (size_t)pb * kSub * kSub;
     for (int e = threadIdx.x; e < kSub * kSub; e += blockDim.x) {
@@ -398,7 +414,7 @@ size_t jacobi_ws_elems(int m) {
   const int nblk0 = (m + kJB - 1) / kJB;
   const int nblk = nblk0 + (nblk0 & 1);
   const int P = std::max(1, nblk / 2);
-  return (size_t)m * m + (size_t)P * kSub * kSub + 8;
+  return (size_t)m * m + (size_t)2 * P * kSub * kSub + 8;
 }
 
 int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long long ldv,
@@ -413,8 +429,9 @@ int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long
   const int P = nblk / 2;
   if (ws_elems < jacobi_ws_elems(m)) return -2;
   double* anew = ws;                       // m×m, ld m
-  double* jbuf = ws + (size_t)m * m;       // P × kSub²
-  double* norm = jbuf + (size_t)P * kSub * kSub;
+  double* jbuf = ws + (size_t)m * m;       // P × kSub² rotations
+  double* sbuf = jbuf + (size_t)P * kSub * kSub;  // P × kSub² rotated subproblems
+  double* norm = sbuf + (size_t)P * kSub * kSub;
   set_identity(v, ldv, m, st);
   frob_norm_kernel<<<1, 1024, 0, st>>>(a, lda, m, norm);
   count_launch();
@@ -431,10 +448,11 @@ int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long
   for (sweep = 0; sweep < 40 && !converged; ++sweep) {
     cudaMemsetAsync(dflags, 0, sizeof(int), st);
     for (int r = 0; r < rounds; ++r) {
-      jacobi_solve_kernel<<<P, 256, 0, st>>>(cur, ldcur, m, nblk, r, inner, norm, jbuf, dflags);
+      jacobi_solve_kernel<<<P, 256, 0, st>>>(cur, ldcur, m, nblk, r, inner, norm, jbuf, sbuf,
+                                             dflags);
       count_launch();
       jacobi_apply_kernel<<<P * P + P * vchunks, 256, 0, st>>>(cur, ldcur, nxt, ldnxt, m, nblk, r,
-                                                               jbuf, v, ldv);
+                                                               jbuf, sbuf, v, ldv);
       count_launch();
       std::swap(cur, nxt);
       std::swap(ldcur, ldnxt);
