@@ -291,7 +291,7 @@ def run_ours(a):
         dist.destroy_process_group()
     if rank != 0:
         return
-    peak_tf = (peak or nominal) / 1000.0
+    peak_tf = peak if peak else nominal / 1000.0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,

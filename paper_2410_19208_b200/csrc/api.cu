@@ -770,6 +770,8 @@ static int ran_proj_impl(psd_plan* p, const double* x, int64_t n, int64_t ldx,
     op.lds = ldx;
     op.partials = p->rpart;
     op.max_splits = 1;
+    PSD_CUDA_CHECK(cudaMemsetAsync(p->rpart, 0, psd::gemm_resid_ctas(op) * sizeof(double), st),
+                   "resid partials");
     psd::gemm_f64(op, p->ws, p->ws_elems, st);
     psd::sum_partials(p->rpart, psd::gemm_resid_ctas(op), p->scal + 2, 1, st);
     PSD_CUDA_CHECK(cudaMemcpyAsync(&r.residual_frob, p->scal + 2, sizeof(double),

@@ -1,6 +1,7 @@
 // Instantiations and the split-K / tiling policy for the DMMA GEMM.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "launch.h"
@@ -136,8 +137,21 @@ static int launch_cfg(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_
   return 1;
 }
 
+static bool legacy_forced() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PSD_GEMM");
+    v = (e && e[0] == 'l') ? 1 : 0;  // PSD_GEMM=legacy → cp.async kernel only (A/B testing)
+  }
+  return v == 1;
+}
+
 int gemm_f64(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st) {
   if (op.M <= 0 || op.N <= 0) return 0;
+  if (!legacy_forced()) {
+    const int r = gemm_f64_tma(op, ws, ws_elems, st);
+    if (r != -2) return r;
+  }
   if (op.a_layout == A_MK && op.b_layout == B_KN) return launch_cfg<CfgPanelNN>(op, ws, ws_elems, st);
   if (op.a_layout == A_KM && op.b_layout == B_KN) return launch_cfg<CfgPanelTN>(op, ws, ws_elems, st);
   if (op.a_layout == A_MK && op.b_layout == B_NK) return launch_cfg<CfgSquareNT>(op, ws, ws_elems, st);
@@ -147,7 +161,7 @@ int gemm_f64(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st) {
 long long gemm_resid_ctas(const GemmOp& op) {
   int m_tiles, n_tiles, nb;
   tiling<CfgSquareNT>(op, m_tiles, n_tiles, nb);
-  return (long long)m_tiles * n_tiles;
+  return std::max<long long>((long long)m_tiles * n_tiles, gemm_tma_resid_parts(op));
 }
 
 }  // namespace psd

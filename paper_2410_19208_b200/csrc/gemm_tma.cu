@@ -1,0 +1,177 @@
+// Host side of the TMA-fed DMMA GEMM: tensor-map encoding, configuration
+// choice, split-K / persistent-grid policy.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "gemm_tma.cuh"
+#include "launch.h"
+
+namespace psd {
+
+// X·P / Y·R⁻¹ / Q·U (A row-major, B row-major), BM = 64, BN = 2·8·N8W
+template <int N8W, int ST>
+using TmaNN = TmaCfg<A_MK, B_KN, 64, 4, 2, 2, N8W, ST>;
+// Gram YᵀY, Qᵀ(XQ), Xᵀ·P (Aᵀ stored, B row-major)
+template <int N8W, int ST>
+using TmaTN = TmaCfg<A_KM, B_KN, 64, 4, 2, 2, N8W, ST>;
+// (W·D)·Wᵀ mirrored SYRK, residual, Cholesky trailing update (A row-major, Bᵀ stored)
+using TmaNT = TmaCfg<A_MK, B_NK, 128, 4, 2, 4, 8, 6>;
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D row-major tensor: `rows` rows of `cols` doubles, row stride ld.
+bool make_map(CUtensorMap* map, const double* ptr, long long cols, long long rows, long long ld,
+              int box_cols, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_ok(const void* p, long long ld) {
+  return p != nullptr && ((uintptr_t)p % 16 == 0) && (ld % 2 == 0) && ld > 0;
+}
+
+template <class Cfg>
+void ensure_attr() {
+  static bool done[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!done[dev]) {
+    cudaFuncSetAttribute(gemm_tma_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg::kSmem);
+    done[dev] = true;
+  }
+}
+
+template <class Cfg>
+int launch(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st) {
+  ensure_attr<Cfg>();
+  CUtensorMap ma, mb;
+  bool ok;
+  if (Cfg::AL == A_MK) ok = make_map(&ma, op.A, op.K, op.M, op.lda, 16, Cfg::BM);
+  else ok = make_map(&ma, op.A, op.M, op.K, op.lda, 16, 16);
+  if (Cfg::BL == B_KN) ok = ok && make_map(&mb, op.B, op.N, op.K, op.ldb, 16, 16);
+  else ok = ok && make_map(&mb, op.B, op.K, op.N, op.ldb, 16, Cfg::BN);
+  if (!ok) return -2;
+
+  TmaParams p{};
+  p.C = op.C;
+  p.ldc = op.ldc;
+  p.M = op.M;
+  p.N = op.N;
+  p.K = op.K;
+  p.epi = op.epi;
+  p.alpha = op.alpha;
+  p.S = op.S;
+  p.lds = op.lds;
+  p.partials = op.partials;
+  p.m_tiles = (op.M + Cfg::BM - 1) / Cfg::BM;
+  p.n_tiles = (op.N + Cfg::BN - 1) / Cfg::BN;
+  const int sms = device_info().sms;
+  constexpr int BK = Cfg::BK;
+  const long long ldw = (op.N + 1) / 2 * 2;
+  int splits = 1;
+  long long units;
+  if (op.epi == EPI_MIRROR) {
+    units = (long long)p.m_tiles * (p.m_tiles + 1) / 2;
+  } else {
+    const long long tiles = (long long)p.m_tiles * p.n_tiles;
+    if ((op.epi == EPI_STORE || op.epi == EPI_SHIFT) && op.max_splits > 1 && ws != nullptr) {
+      double best = 1e300;
+      const int smax = (int)std::min<long long>(op.max_splits, std::max(1, op.K / (4 * BK)));
+      for (int s = 1; s <= smax; ++s) {
+        const long long kc = ((op.K + s - 1) / s + BK - 1) / BK * BK;
+        if ((op.K + kc - 1) / kc != s) continue;
+        if (s > 1 && (size_t)s * op.M * ldw > ws_elems) break;
+        const long long waves = (tiles * s + sms - 1) / sms;
+        const double cost = (double)waves * (double)kc + (s > 1 ? 96.0 : 0.0);
+        if (cost < best * 0.995) {
+          best = cost;
+          splits = s;
+        }
+      }
+    }
+    units = tiles * splits;
+  }
+  p.splits = splits;
+  p.units = (int)units;
+  if (splits > 1) {
+    p.k_chunk = (int)(((op.K + splits - 1) / splits + BK - 1) / BK * BK);
+    p.C = ws;
+    p.ldc = ldw;
+    p.split_stride = (long long)op.M * ldw;
+    p.epi = EPI_STORE;
+  } else {
+    p.k_chunk = std::max(op.K, 1);
+  }
+  if (units == 0) return 0;
+  const int grid = (int)std::min<long long>(units, sms);
+  gemm_tma_kernel<Cfg><<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(ma, mb, p);
+  count_launch();
+  if (splits > 1) {
+    splitk_reduce(ws, splits, p.split_stride, op.M, op.N, ldw, op.C, op.ldc, op.epi, op.alpha,
+                  op.S, op.lds, st);
+    return 2;
+  }
+  return 1;
+}
+
+// pick the N tile (272 / 144 / 64 wide) with the least padding, ties → wider
+template <template <int, int> class Tpl>
+int launch_panel(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st) {
+  const int cand[3] = {272, 144, 64};
+  int best = 0;
+  long long best_waste = 1LL << 62;
+  for (int c = 0; c < 3; ++c) {
+    const long long tiles = (op.N + cand[c] - 1) / cand[c];
+    const long long waste = tiles * cand[c] - op.N;
+    if (waste < best_waste) {
+      best_waste = waste;
+      best = c;
+    }
+  }
+  if (best == 0) return launch<Tpl<17, 5>>(op, ws, ws_elems, st);
+  if (best == 1) return launch<Tpl<9, 7>>(op, ws, ws_elems, st);
+  return launch<Tpl<4, 8>>(op, ws, ws_elems, st);
+}
+
+}  // namespace
+
+// Returns launches issued, −1 unsupported layout, −2 when TMA cannot be used
+// (alignment) so the caller falls back to the cp.async kernel.
+int gemm_f64_tma(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st) {
+  if (!tma_ok(op.A, op.lda) || !tma_ok(op.B, op.ldb)) return -2;
+  if (op.a_layout == A_MK && op.b_layout == B_KN) return launch_panel<TmaNN>(op, ws, ws_elems, st);
+  if (op.a_layout == A_KM && op.b_layout == B_KN) return launch_panel<TmaTN>(op, ws, ws_elems, st);
+  if (op.a_layout == A_MK && op.b_layout == B_NK) return launch<TmaNT>(op, ws, ws_elems, st);
+  return -1;
+}
+
+long long gemm_tma_resid_parts(const GemmOp& op) {
+  const long long mt = (op.M + TmaNT::BM - 1) / TmaNT::BM;
+  const long long nt = (op.N + TmaNT::BN - 1) / TmaNT::BN;
+  return mt * nt * TmaNT::kConsumers;
+}
+
+}  // namespace psd

@@ -39,8 +39,11 @@ struct GemmOp {
 // `ws` must hold ws_elems doubles for split-K partials.  Returns the number
 // of kernel launches issued (1 or 2), or <0 on error.
 int gemm_f64(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st);
-// Number of CTAs a RESID launch uses (size of `partials`).
+// Number of partial sums a RESID launch may write (size of `partials`; zero it first).
 long long gemm_resid_ctas(const GemmOp& op);
+// TMA-fed warp-specialised path (gemm_tma.cu); −2 = operands not TMA-aligned.
+int gemm_f64_tma(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st);
+long long gemm_tma_resid_parts(const GemmOp& op);
 
 // ---- memory-bound kernels --------------------------------------------------
 // stats[0] = max|x|, stats[1] = max|x - xᵀ|, ((int*)(stats+2))[0] = flags
