@@ -1,0 +1,474 @@
+// Symmetric eigensolver for the k×k compressed matrix T = sym(QᵀXQ)
+// (symmetric.py:68-86 via projection.py:105): block-cyclic two-sided Jacobi
+// in ONE persistent cooperative kernel.
+//
+// The m×m matrix is cut into 16-index blocks; every round the circle method
+// pairs the blocks and each pair's 32×32 principal submatrix is rotated by
+// one CTA in shared memory.  A parallel Jacobi step is one phase with one
+// barrier: every warp recomputes the step's 16 rotations redundantly (lane
+// l ↔ pair l, broadcast by shuffles, no shared-memory hand-off), then each
+// thread applies J_kᵀ·[2×2 block]·J_l to its block and to two (row, pair)
+// slots of the local rotation product, reading one buffer and writing the
+// other.  The CTA's rotation product J_P is applied to the whole matrix
+// (A ← Jᵀ A J, V ← V J) by all CTAs as 32×32 DMMA tile products.  Grid-wide
+// barriers separate solve and apply; convergence (a sweep with no rotation
+// above threshold) is decided on the device: one launch, one host sync.
+//
+// Per-pair threshold: rotate (p,q) iff |a_pq| > 1e-15·sqrt(|a_pp a_qq|) and
+// |a_pq| > 1e-15·‖A‖_F.  Off-diagonal mass left below that bound perturbs
+// the reconstructed T₊ by ≲ m·1e-15·‖A‖_F (≈3e-13 relative at m = 272).
+// Diagonal sub-blocks are copied from the solve CTA (exact zeros on rotated
+// pairs) instead of being re-multiplied.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "launch.h"
+
+namespace psd {
+
+constexpr int kJB = 16;          // indices per block
+constexpr int kJS = 2 * kJB;     // subproblem size (32)
+constexpr int kJT = 256;         // threads per CTA
+constexpr int kJLd = kJS + 4;    // smem row stride ≡ 4 (mod 16): conflict-free DMMA fragments
+constexpr int kJTile = kJS * kJLd;
+
+struct JacobiArgs {
+  double* a;        // m×m, ld lda (input; may end up holding the result)
+  long long lda;
+  double* b;        // m×m scratch, ld m
+  double* v;        // m×m eigenvectors, ld ldv
+  long long ldv;
+  double* jbuf;     // P × kJS²
+  double* sbuf;     // P × kJS²
+  int* counters;    // per-sweep rotation counts (zeroed)
+  unsigned* barrier;  // grid barrier counter (zeroed)
+  double* norm;     // [0] = ‖A‖_F
+  int* out;         // [0] = sweeps (or −1), [1] = 1 if result is in b
+  int m, nblk, max_sweeps;
+  long long* timers;  // optional: block 0 clock64 per phase [solve, bar1, apply, bar2]
+};
+
+PSD_DEVINL void circle_pair(int nplayers, int r, int i, int& a, int& b) {
+  const int M = nplayers - 1;
+  if (i == 0) {
+    a = M;
+    b = r % M;
+  } else {
+    a = (r + i) % M;
+    b = (r - i + M) % M;
+  }
+}
+
+PSD_DEVINL int sub_index(int nblk, int r, int pair, int k) {
+  int a, b;
+  circle_pair(nblk, r, pair, a, b);
+  return (k < kJB) ? a * kJB + k : b * kJB + (k - kJB);
+}
+
+__device__ void grid_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    gen += 1;
+    const unsigned target = gen * gridDim.x;
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(seen) : "l"(bar) : "memory");
+    } while (seen < target);
+  }
+  __syncthreads();
+}
+
+// Rotation for pair (p,q) (GVL sym.schur2; one sqrt, one division, one rsqrt).
+PSD_DEVINL bool rotation(double app, double aqq, double apq, double abs_tol, double& c, double& s,
+                         double& t) {
+  c = 1.0;
+  s = 0.0;
+  t = 0.0;
+  if (!(fabs(apq) > abs_tol) || !(apq * apq > 1e-30 * fabs(app * aqq))) return false;
+  const double d = aqq - app, e = 2.0 * apq;
+  const double r = sqrt(fma(d, d, e * e));
+  t = (d >= 0.0 ? e : -e) / (fabs(d) + r);  // tan θ
+  c = rsqrt(fma(t, t, 1.0));
+  s = t * c;
+  return true;
+}
+
+// Pair k of inner step ir: full sweep = circle method over 32 indices
+// (31 steps), cross sweep = (k, 16 + (k + ir) mod 16) (16 steps).
+PSD_DEVINL void step_pair(bool full, int ir, int k, int& p, int& q) {
+  if (full) {
+    if (k == 0) {
+      p = kJS - 1;
+      q = ir;
+    } else {
+      p = ir + k;
+      if (p >= kJS - 1) p -= kJS - 1;
+      q = ir - k + kJS - 1;
+      if (q >= kJS - 1) q -= kJS - 1;
+    }
+  } else {
+    p = k;
+    q = kJB + ((k + ir) & (kJB - 1));
+  }
+}
+
+// One parallel step: reads (Sc, Vc), writes every element of (Sn, Vn).
+// Returns #rotations (block-uniform); 0 ⇒ nothing written.
+__device__ int jacobi_step(const double* Sc, const double* Vc, double* Sn, double* Vn, bool full,
+                           int ir, double abs_tol) {
+  const int lane = threadIdx.x & 31;
+  const int l = lane & 15;
+  int p, q;
+  step_pair(full, ir, l, p, q);
+  double c, s, t;
+  const bool r = rotation(Sc[p * kJLd + p], Sc[q * kJLd + q], Sc[p * kJLd + q], abs_tol, c, s, t);
+  const int nrot = __popc(__ballot_sync(0xffffffffu, r) & 0xffffu);
+  if (nrot == 0) return 0;
+  // thread → (k, l): rows {p_k, q_k} × cols {p_l, q_l}
+  const int k = ((threadIdx.x >> 5) << 1) | (lane >> 4);
+  const double ck = __shfl_sync(0xffffffffu, c, k);
+  const double sk = __shfl_sync(0xffffffffu, s, k);
+  const double tk = __shfl_sync(0xffffffffu, t, k);
+  int pk, qk;
+  step_pair(full, ir, k, pk, qk);
+  double b00 = Sc[pk * kJLd + p], b01 = Sc[pk * kJLd + q];
+  double b10 = Sc[qk * kJLd + p], b11 = Sc[qk * kJLd + q];
+  const double r00 = ck * b00 - sk * b10, r01 = ck * b01 - sk * b11;
+  const double r10 = sk * b00 + ck * b10, r11 = sk * b01 + ck * b11;
+  b00 = c * r00 - s * r01;
+  b01 = s * r00 + c * r01;
+  b10 = c * r10 - s * r11;
+  b11 = s * r10 + c * r11;
+  if (k == l && sk != 0.0) {  // the rotated pair itself: exact form
+    const double apq = Sc[pk * kJLd + qk];
+    b00 = Sc[pk * kJLd + pk] - tk * apq;
+    b11 = Sc[qk * kJLd + qk] + tk * apq;
+    b01 = 0.0;
+    b10 = 0.0;
+  }
+  Sn[pk * kJLd + p] = b00;
+  Sn[pk * kJLd + q] = b01;
+  Sn[qk * kJLd + p] = b10;
+  Sn[qk * kJLd + q] = b11;
+  // V ← V J for rows (tid>>4) and (tid>>4)+16, pair l
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int row = (threadIdx.x >> 4) + 16 * h;
+    const double a0 = Vc[row * kJLd + p], a1 = Vc[row * kJLd + q];
+    Vn[row * kJLd + p] = c * a0 - s * a1;
+    Vn[row * kJLd + q] = s * a0 + c * a1;
+  }
+  __syncthreads();
+  return nrot;
+}
+
+// C (32×32) = op(A)·B for A, B in shared memory (row stride kJLd) on the FP64
+// tensor cores: warp w owns rows (w&3)·8 … +8, cols (w>>2)·16 … +16.
+// aT: A is stored transposed (A[m][k] = Asmem[k][m]).
+PSD_DEVINL void mm32_dmma(const double* A, bool aT, const double* B, double (&c)[2][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int m0 = (warp & 3) * 8, n0 = (warp >> 2) * 16;
+  c[0][0] = c[0][1] = c[1][0] = c[1][1] = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < kJS; k0 += 4) {
+    const double a = aT ? A[(k0 + t) * kJLd + m0 + g] : A[(m0 + g) * kJLd + k0 + t];
+    const double b0 = B[(k0 + t) * kJLd + n0 + g];
+    const double b1 = B[(k0 + t) * kJLd + n0 + 8 + g];
+    dmma_8x8x4(c[0][0], c[0][1], a, b0);
+    dmma_8x8x4(c[1][0], c[1][1], a, b1);
+  }
+}
+
+// (row, col) within the 32×32 tile of accumulator (j, e) of this thread
+PSD_DEVINL void mm32_coord(int j, int e, int& row, int& col) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  row = (warp & 3) * 8 + (lane >> 2);
+  col = (warp >> 2) * 16 + 8 * j + 2 * (lane & 3) + e;
+}
+
+__global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
+  __shared__ __align__(16) double sm[5 * kJTile];
+  double* S0 = sm;
+  double* V0 = sm + kJTile;
+  double* S1 = sm + 2 * kJTile;
+  double* V1 = sm + 3 * kJTile;
+  double* X = sm + 4 * kJTile;
+  __shared__ int ia[kJS], ib[kJS];
+  __shared__ int stop_flag;
+  const int m = A.m, nblk = A.nblk, P = nblk / 2, rounds = nblk - 1;
+  const double abs_tol = 1e-15 * A.norm[0];
+  unsigned gen = 0;
+  double* cur = A.a;
+  long long ldcur = A.lda;
+  double* nxt = A.b;
+  long long ldnxt = m;
+  int in_b = 0;
+  int sweeps_done = -1;
+  for (int sweep = 0; sweep < A.max_sweeps; ++sweep) {
+    for (int r = 0; r < rounds; ++r) {
+      const long long t0 = clock64();
+      // ------------------------------------------------------------- solve
+      if ((int)blockIdx.x < P) {
+        const int pair = blockIdx.x;
+        if (threadIdx.x < kJS) ia[threadIdx.x] = sub_index(nblk, r, pair, threadIdx.x);
+        __syncthreads();
+        for (int e = threadIdx.x; e < kJS * kJS; e += kJT) {
+          const int i = e / kJS, j = e % kJS;
+          const int gi = ia[i], gj = ia[j];
+          S0[i * kJLd + j] = (gi < m && gj < m) ? cur[(long long)gi * ldcur + gj] : 0.0;
+          V0[i * kJLd + j] = (i == j) ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        int rots = 0;
+        const bool full = (r == 0) || (P == 1);
+        const int inner_sweeps = (P == 1) ? 40 : 1;
+        double *Sc = S0, *Vc = V0, *Sn = S1, *Vn = V1;
+        for (int isw = 0; isw < inner_sweeps; ++isw) {
+          int srot = 0;
+          const int nsteps = full ? kJS - 1 : kJB;
+          for (int ir = 0; ir < nsteps; ++ir) {
+            const int nr = jacobi_step(Sc, Vc, Sn, Vn, full, ir, abs_tol);
+            if (nr) {
+              double* tp = Sc;
+              Sc = Sn;
+              Sn = tp;
+              tp = Vc;
+              Vc = Vn;
+              Vn = tp;
+            }
+            srot += nr;
+          }
+          rots += srot;
+          if (srot == 0) break;
+        }
+        double* J = A.jbuf + (size_t)pair * kJS * kJS;
+        double* So = A.sbuf + (size_t)pair * kJS * kJS;
+        for (int e = threadIdx.x; e < kJS * kJS; e += kJT) {
+          J[e] = Vc[(e / kJS) * kJLd + e % kJS];
+          So[e] = Sc[(e / kJS) * kJLd + e % kJS];
+        }
+        if (threadIdx.x == 0 && rots > 0) atomicAdd(&A.counters[sweep], rots);
+      }
+      const long long t1 = clock64();
+      grid_barrier(A.barrier, gen);
+      const long long t2 = clock64();
+      // ------------------------------------------------------------- apply
+      const int vchunks = (m + kJS - 1) / kJS;
+      const int items = P * P + P * vchunks;
+      for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        double c[2][2];
+        if (it < P * P) {
+          const int pa = it / P, pb = it % P;
+          if (threadIdx.x < kJS) {
+            ia[threadIdx.x] = sub_index(nblk, r, pa, threadIdx.x);
+            ib[threadIdx.x] = sub_index(nblk, r, pb, threadIdx.x);
+          }
+          __syncthreads();
+          if (pa == pb) {
+            const double* Sp = A.sbuf + (size_t)pa * kJS * kJS;
+            for (int e = threadIdx.x; e < kJS * kJS; e += kJT) {
+              const int gi = ia[e / kJS], gj = ib[e % kJS];
+              if (gi < m && gj < m) nxt[(long long)gi * ldnxt + gj] = Sp[e];
+            }
+          } else {
+            const double* Ja = A.jbuf + (size_t)pa * kJS * kJS;
+            const double* Jb = A.jbuf + (size_t)pb * kJS * kJS;
+            for (int e = threadIdx.x; e < kJS * kJS; e += kJT) {
+              const int i = e / kJS, j = e % kJS;
+              const int gi = ia[i], gj = ib[j];
+              S0[i * kJLd + j] = (gi < m && gj < m) ? cur[(long long)gi * ldcur + gj] : 0.0;
+              V0[i * kJLd + j] = Ja[e];
+              X[i * kJLd + j] = Jb[e];
+            }
+            __syncthreads();
+            mm32_dmma(V0, true, S0, c);  // J_aᵀ T
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                int row, col;
+                mm32_coord(j, e, row, col);
+                S1[row * kJLd + col] = c[j][e];
+              }
+            __syncthreads();
+            mm32_dmma(S1, false, X, c);  // (J_aᵀ T) J_b
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                int row, col;
+                mm32_coord(j, e, row, col);
+                const int gi = ia[row], gj = ib[col];
+                if (gi < m && gj < m) nxt[(long long)gi * ldnxt + gj] = c[j][e];
+              }
+          }
+        } else {
+          const int vb = it - P * P;
+          const int pb = vb % P;
+          const int r0 = (vb / P) * kJS;
+          if (threadIdx.x < kJS) ib[threadIdx.x] = sub_index(nblk, r, pb, threadIdx.x);
+          __syncthreads();
+          const double* Jb = A.jbuf + (size_t)pb * kJS * kJS;
+          for (int e = threadIdx.x; e < kJS * kJS; e += kJT) {
+            const int i = e / kJS, j = e % kJS;
+            const int gr = r0 + i, gj = ib[j];
+            S0[i * kJLd + j] = (gr < m && gj < m) ? A.v[(long long)gr * A.ldv + gj] : 0.0;
+            X[i * kJLd + j] = Jb[e];
+          }
+          __syncthreads();
+          mm32_dmma(S0, false, X, c);
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              int row, col;
+              mm32_coord(j, e, row, col);
+              const int gr = r0 + row, gj = ib[col];
+              if (gr < m && gj < m) A.v[(long long)gr * A.ldv + gj] = c[j][e];
+            }
+        }
+        __syncthreads();
+      }
+      const long long t3 = clock64();
+      grid_barrier(A.barrier, gen);
+      if (A.timers && blockIdx.x == 0 && threadIdx.x == 0) {
+        A.timers[0] += t1 - t0;
+        A.timers[1] += t2 - t1;
+        A.timers[2] += t3 - t2;
+        A.timers[3] += clock64() - t3;
+      }
+      double* tp = cur;
+      cur = nxt;
+      nxt = tp;
+      const long long tl = ldcur;
+      ldcur = ldnxt;
+      ldnxt = tl;
+      in_b ^= 1;
+    }
+    if (threadIdx.x == 0) stop_flag = (*((volatile int*)&A.counters[sweep]) == 0);
+    __syncthreads();
+    if (stop_flag) {
+      sweeps_done = sweep + 1;
+      break;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.out[0] = sweeps_done;
+    A.out[1] = in_b;
+  }
+}
+
+__global__ void jacobi_norm_kernel(const double* a, long long lda, int m, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
+    const double x = a[(e / m) * lda + e % m];
+    s = fma(x, x, s);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    out[0] = sqrt(t);
+  }
+}
+
+__global__ void jacobi_diag_kernel(const double* a, long long lda, const double* b, int m,
+                                   const int* out, double* vals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  vals[i] = out[1] ? b[(long long)i * m + i] : a[(long long)i * lda + i];
+}
+
+constexpr int kJacobiMaxSweeps = 40;
+
+static void jacobi_geometry(int m, int& nblk, int& P) {
+  const int nb0 = (m + kJB - 1) / kJB;
+  nblk = std::max(2, nb0 + (nb0 & 1));
+  P = nblk / 2;
+}
+
+size_t jacobi_ws_elems(int m) {
+  int nblk, P;
+  jacobi_geometry(m, nblk, P);
+  return (size_t)m * m + (size_t)2 * P * kJS * kJS + 8 + kJacobiMaxSweeps + 8;
+}
+
+int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long long ldv,
+                double* ws, size_t ws_elems, int* dflags, cudaStream_t st) {
+  (void)dflags;
+  if (m == 1) {
+    cudaMemcpyAsync(values, a, sizeof(double), cudaMemcpyDeviceToDevice, st);
+    set_identity(v, ldv, 1, st);
+    return 1;
+  }
+  if (ws_elems < jacobi_ws_elems(m)) return -2;
+  int nblk, P;
+  jacobi_geometry(m, nblk, P);
+  JacobiArgs A{};
+  A.a = a;
+  A.lda = lda;
+  A.b = ws;
+  A.v = v;
+  A.ldv = ldv;
+  A.jbuf = ws + (size_t)m * m;
+  A.sbuf = A.jbuf + (size_t)P * kJS * kJS;
+  A.norm = A.sbuf + (size_t)P * kJS * kJS;
+  int* ints = reinterpret_cast<int*>(A.norm + 8);
+  A.counters = ints;
+  A.barrier = reinterpret_cast<unsigned*>(ints + kJacobiMaxSweeps);
+  A.out = ints + kJacobiMaxSweeps + 2;
+  A.m = m;
+  A.nblk = nblk;
+  A.max_sweeps = kJacobiMaxSweeps;
+  A.timers = nullptr;
+  static long long* dtimers = nullptr;
+  if (getenv("PSD_JACOBI_TIMERS")) {
+    if (!dtimers) cudaMalloc(&dtimers, 4 * sizeof(long long));
+    cudaMemsetAsync(dtimers, 0, 4 * sizeof(long long), st);
+    A.timers = dtimers;
+  }
+  cudaMemsetAsync(ints, 0, (kJacobiMaxSweeps + 4) * sizeof(int), st);
+  set_identity(v, ldv, m, st);
+  jacobi_norm_kernel<<<1, 1024, 0, st>>>(a, lda, m, A.norm);
+  count_launch();
+
+  static int max_blocks[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!max_blocks[dev]) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_persistent_kernel, kJT, 0);
+    max_blocks[dev] = std::max(1, per_sm) * device_info().sms;
+  }
+  const int vchunks = (m + kJS - 1) / kJS;
+  const int items = P * P + P * vchunks;
+  const int grid = std::max(P, std::min({items, max_blocks[dev], device_info().sms}));
+  void* args[] = {&A};
+  if (cudaLaunchCooperativeKernel((const void*)jacobi_persistent_kernel, dim3(grid), dim3(kJT),
+                                  args, 0, st) != cudaSuccess)
+    return -3;
+  count_launch();
+  int out[2] = {0, 0};
+  cudaMemcpyAsync(out, A.out, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  jacobi_diag_kernel<<<(m + 255) / 256, 256, 0, st>>>(a, lda, ws, m, A.out, values);
+  count_launch();
+  if (out[1]) copy_matrix(ws, m, a, lda, m, m, st);
+  if (A.timers) {
+    long long h[4];
+    cudaMemcpy(h, A.timers, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "jacobi m=%d sweeps=%d grid=%d cycles: solve %lld bar1 %lld apply %lld bar2 %lld\n",
+            m, out[0], grid, h[0], h[1], h[2], h[3]);
+  }
+  return out[0];
+}
+
+}  // namespace psd

@@ -12,73 +12,124 @@ namespace psd {
 // a1 — require_symmetric (symmetric.py:39-57).  One pass over (I,J)/(J,I)
 // 32×32 tile pairs (I ≤ J): max|x|, max|x − xᵀ| and "bitwise symmetric".
 // ---------------------------------------------------------------------------
-constexpr int kSymT = 32;
+constexpr int kSymT = 64;
 
+// Persistent blocks walk the lower-triangular list of 64×64 tile pairs
+// (I ≥ J): tile (J,I) is staged transposed through shared memory, tile (I,J)
+// is read straight into registers, so every element of X is read once
+// (diagonal tiles twice).  One atomic per block per statistic at the end.
 __global__ void __launch_bounds__(256) sym_stats_kernel(const double* __restrict__ x, long long n,
-                                                        long long ldx, double* stats) {
+                                                        long long ldx, long long npairs,
+                                                        double* stats) {
   __shared__ double tj[kSymT][kSymT + 1];
-  const long long nt = (n + kSymT - 1) / kSymT;
-  // linear index over lower-triangular pairs (ti ≥ tj) → tile (ti, tj)
-  const long long b = blockIdx.x;
-  long long ti = (long long)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
-  while ((ti + 1) * (ti + 2) / 2 <= b) ++ti;
-  while (ti * (ti + 1) / 2 > b) --ti;
-  const long long tjx = b - ti * (ti + 1) / 2;
-  (void)nt;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows per pass
-  const long long r0 = ti * kSymT, c0 = tjx * kSymT;
-  // load tile (tj, ti) = x[c0.., r0..] into smem
-  for (int r = ty; r < kSymT; r += 8) {
-    const long long gr = c0 + r, gc = r0 + tx;
-    tj[r][tx] = (gr < n && gc < n) ? x[gr * ldx + gc] : 0.0;
-  }
-  __syncthreads();
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
   double mabs = 0.0, mdef = 0.0;
   int flags = 0;
-  for (int r = ty; r < kSymT; r += 8) {
-    const long long gr = r0 + r, gc = c0 + tx;
-    if (gr < n && gc < n) {
-      const double a = x[gr * ldx + gc];   // x[i][j]
-      const double bt = tj[tx][r];         // x[j][i]
-      if (!isfinite(a) || !isfinite(bt)) flags |= 2;
-      mabs = fmax(mabs, fmax(fabs(a), fabs(bt)));
-      const double d = fabs(a - bt);
-      mdef = fmax(mdef, d);
-      if (a != bt) flags |= 1;
+  for (long long b = blockIdx.x; b < npairs; b += gridDim.x) {
+    long long ti = (long long)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= b) ++ti;
+    while (ti * (ti + 1) / 2 > b) --ti;
+    const long long tjx = b - ti * (ti + 1) / 2;
+    const long long r0 = ti * kSymT, c0 = tjx * kSymT;
+    double a[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = ty + 8 * q;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = tx + 32 * h;
+        // x[c0 + r][r0 + c] → smem (tile (J, I)); x[r0 + r][c0 + c] → registers (tile (I, J))
+        const long long gr = c0 + r, gc = r0 + c;
+        tj[r][c] = (gr < n && gc < n) ? __ldcs(x + gr * ldx + gc) : 0.0;
+        const long long ar = r0 + r, ac = c0 + c;
+        a[q][h] = (ar < n && ac < n) ? __ldcs(x + ar * ldx + ac) : 0.0;
+      }
     }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = ty + 8 * q;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = tx + 32 * h;
+        const double av = a[q][h];
+        const double bt = tj[c][r];  // x[c0 + c][r0 + r] = x[j][i]
+        if (!isfinite(av) || !isfinite(bt)) flags |= 2;
+        mabs = fmax(mabs, fmax(fabs(av), fabs(bt)));
+        mdef = fmax(mdef, fabs(av - bt));
+        if (av != bt) flags |= 1;
+      }
+    }
+    __syncthreads();
   }
+  __shared__ double rmax[8], rdef[8];
+  __shared__ int rfl[8];
   mabs = warp_max(mabs);
   mdef = warp_max(mdef);
   flags = __reduce_or_sync(0xffffffffu, flags);
   if (tx == 0) {
-    if (mabs > 0.0) atomic_max_nonneg(&stats[0], mabs);
-    if (mdef > 0.0) atomic_max_nonneg(&stats[1], mdef);
-    if (flags) atomicOr(reinterpret_cast<int*>(stats + 2), flags);
+    rmax[ty] = mabs;
+    rdef[ty] = mdef;
+    rfl[ty] = flags;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m1 = 0.0, m2 = 0.0;
+    int f = 0;
+    for (int w = 0; w < 8; ++w) {
+      m1 = fmax(m1, rmax[w]);
+      m2 = fmax(m2, rdef[w]);
+      f |= rfl[w];
+    }
+    if (m1 > 0.0) atomic_max_nonneg(&stats[0], m1);
+    if (m2 > 0.0) atomic_max_nonneg(&stats[1], m2);
+    if (f) atomicOr(reinterpret_cast<int*>(stats + 2), f);
   }
 }
 
 void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st) {
   cudaMemsetAsync(stats, 0, 3 * sizeof(double), st);
   const long long nt = (n + kSymT - 1) / kSymT;
-  const long long blocks = nt * (nt + 1) / 2;
-  sym_stats_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, stats);
+  const long long npairs = nt * (nt + 1) / 2;
+  const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * 4);
+  sym_stats_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats);
   count_launch();
 }
 
-// T ← (T + Tᵀ)/2 for a small matrix; each (i,j), i>j pair written by one thread.
-__global__ void symmetrize_small_kernel(double* x, int m, long long ld) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)m * m) return;
-  const int i = (int)(idx / m), j = (int)(idx % m);
-  if (i <= j) return;
-  const double v = (x[(long long)i * ld + j] + x[(long long)j * ld + i]) / 2.0;
-  x[(long long)i * ld + j] = v;
-  x[(long long)j * ld + i] = v;
+// A ← (A + Aᵀ)/2 in place (symmetric.py:31-36): one 32×32 tile pair (I ≥ J)
+// per block, both tiles staged through shared memory so reads and writes
+// stay coalesced; the mirrored pair is written with one value (exactly
+// symmetric result).
+__global__ void __launch_bounds__(256) symmetrize_kernel(double* x, long long m, long long ld) {
+  __shared__ double ta[32][33], tb[32][33];
+  const long long b = blockIdx.x;
+  long long ti = (long long)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+  while ((ti + 1) * (ti + 2) / 2 <= b) ++ti;
+  while (ti * (ti + 1) / 2 > b) --ti;
+  const long long tj = b - ti * (ti + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const long long r0 = ti * 32, c0 = tj * 32;
+  for (int r = ty; r < 32; r += 8) {
+    const long long ar = r0 + r, ac = c0 + tx;
+    ta[r][tx] = (ar < m && ac < m) ? x[ar * ld + ac] : 0.0;   // tile (I, J)
+    const long long br = c0 + r, bc = r0 + tx;
+    tb[r][tx] = (br < m && bc < m) ? x[br * ld + bc] : 0.0;   // tile (J, I)
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const long long ar = r0 + r, ac = c0 + tx;
+    // (A + Aᵀ)/2 at (r0 + r, c0 + tx) uses x[c0 + tx][r0 + r] = tb[tx][r]
+    const double v = (ta[r][tx] + tb[tx][r]) / 2.0;
+    const double w = (tb[r][tx] + ta[tx][r]) / 2.0;   // value at (c0 + r, r0 + tx)
+    if (ar < m && ac < m) x[ar * ld + ac] = v;
+    const long long br = c0 + r, bc = r0 + tx;
+    if (ti != tj && br < m && bc < m) x[br * ld + bc] = w;
+  }
 }
 
 void symmetrize_small(double* x, int m, long long ld, cudaStream_t st) {
-  const long long tot = (long long)m * m;
-  symmetrize_small_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(x, m, ld);
+  const long long nt = ((long long)m + 31) / 32;
+  symmetrize_kernel<<<(unsigned)(nt * (nt + 1) / 2), 256, 0, st>>>(x, m, ld);
   count_launch();
 }
 
