@@ -35,6 +35,7 @@ struct psd_plan {
   double* jws = nullptr;
   size_t jws_elems = 0;
   double *gy = nullptr, *gv = nullptr, *gpart = nullptr, *stats = nullptr, *scal = nullptr;
+  double* qrstat = nullptr;
   int gparts = 0;
   double* rpart = nullptr;
   ll rparts = 0;
@@ -266,25 +267,22 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
            QrInfo* info, cudaStream_t st) {
   Stage mark(p, PSD_STAGE_QR, st);
   const ll ld = p->ldp;
-  int* dinfo = p->ints + p->w + 1;
   if (rdiag) {
     fill_value_kernel<<<(w + 255) / 256, 256, 0, st>>>(rdiag, w, 1.0);
     launched(1);
   }
-  std::vector<double> hdiag(w);
-  int hinfo = 0;
   int unshifted_run = 0;
   double kest0 = 0.0;
   bool verified = false;
   const double u = 1.1102230246251565e-16;
+  double hs[4];
   for (int pass = 0; pass < 10; ++pass) {
     PSD_TRY(panel_tn(p, bufs[cur], bufs[cur], ld, n, w, p->G, true, st));
-    PSD_CUDA_CHECK(cudaMemcpy2DAsync(hdiag.data(), sizeof(double), p->G, (w + 1) * sizeof(double),
-                                     sizeof(double), w, cudaMemcpyDeviceToHost, st),
-                   "gram diag");
-    PSD_TRY(sync(st, "gram"));
-    double trace = 0.0;
-    for (int i = 0; i < w; ++i) trace += hdiag[i];
+    if (psd::chol_inv(p->G, w, w, 0.0, p->L, w, p->Rinv, w, p->T, p->qrstat, st) != 0)
+      return fail(PSD_ERR_INVALID_PARAMS, "width %d too large for the CholeskyQR kernel", w);
+    PSD_CUDA_CHECK(cudaMemcpyAsync(hs, p->qrstat, sizeof(hs), cudaMemcpyDeviceToHost, st), "qr status");
+    PSD_TRY(sync(st, "cholesky"));
+    const double trace = hs[1];
     if (pass == 0) {
       info->frob = std::sqrt(std::max(trace, 0.0));
       if (trace == 0.0) {
@@ -309,39 +307,22 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
         break;
       }
     }
-    psd::copy_matrix(p->G, w, p->L, w, w, w, st);
-    psd::cholesky_lower(p->L, w, w, dinfo, p->ws, p->ws_elems, st);
-    PSD_CUDA_CHECK(cudaMemcpy2DAsync(hdiag.data(), sizeof(double), p->L, (w + 1) * sizeof(double),
-                                     sizeof(double), w, cudaMemcpyDeviceToHost, st),
-                   "chol diag");
-    PSD_CUDA_CHECK(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st), "info");
-    PSD_TRY(sync(st, "cholesky"));
-    bool bad = hinfo != 0;
-    double dmax = 0.0, dmin = INFINITY;
-    for (int i = 0; i < w; ++i) {
-      if (!std::isfinite(hdiag[i])) bad = true;
-      dmax = std::max(dmax, hdiag[i]);
-      dmin = std::min(dmin, hdiag[i]);
-    }
-    const double kest = (dmin > 0.0) ? dmax / dmin : INFINITY;
+    const bool bad = hs[0] != 0.0 || !std::isfinite(hs[2]) || !std::isfinite(hs[3]);
+    const double kest = (hs[2] > 0.0) ? hs[3] / hs[2] : INFINITY;
     if (pass == 0) kest0 = kest;
     const bool shift = bad || kest > 3e6;
     if (shift) {
       // Fukaya et al. shifted CholeskyQR: s = 11(mn + n(n+1))·u·‖Y‖²
       const double s = 11.0 * ((double)n * w + (double)w * (w + 1)) * u * trace;
-      psd::copy_matrix(p->G, w, p->L, w, w, w, st);
-      psd::add_diag(p->L, w, w, s, st);
-      psd::cholesky_lower(p->L, w, w, dinfo, p->ws, p->ws_elems, st);
-      PSD_CUDA_CHECK(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st),
-                     "info");
+      psd::chol_inv(p->G, w, w, s, p->L, w, p->Rinv, w, p->T, p->qrstat, st);
+      PSD_CUDA_CHECK(cudaMemcpyAsync(hs, p->qrstat, sizeof(hs), cudaMemcpyDeviceToHost, st),
+                     "qr status");
       PSD_TRY(sync(st, "shifted cholesky"));
-      if (hinfo != 0) return fail(PSD_ERR_CONVERGENCE, "shifted CholeskyQR broke down (pivot %d)", hinfo);
+      if (hs[0] != 0.0)
+        return fail(PSD_ERR_CONVERGENCE, "shifted CholeskyQR broke down (pivot %d)", (int)hs[0]);
       info->shifted = 1;
     }
-    psd::tri_inv_upper_from_lower(p->L, w, w, p->Rinv, w, st);
-    if (rdiag) {
-      psd::accumulate_diag(p->L, w, w, rdiag, st);
-    }
+    if (rdiag) psd::accumulate_diag(p->L, w, w, rdiag, st);
     PSD_TRY(panel_nn(p, bufs[cur], ld, p->Rinv, w, bufs[tmp], ld, n, w, w, st));
     std::swap(cur, tmp);
     info->passes++;
@@ -479,6 +460,7 @@ int psd_plan_create(psd_plan** out, int64_t n, int32_t width, int32_t device) {
   ok &= (p->gpart = alloc(p, p->gparts)) != nullptr;
   ok &= (p->stats = alloc(p, 4)) != nullptr;
   ok &= (p->scal = alloc(p, 8)) != nullptr;
+  ok &= (p->qrstat = alloc(p, 8)) != nullptr;
   psd::GemmOp rop;
   rop.M = (int)n;
   rop.N = (int)n;

@@ -219,3 +219,233 @@ void sort_eigs(const double* vals, const double* vecs, long long ldv, int m, dou
 }
 
 }  // namespace psd
+
+namespace psd {
+
+// ---------------------------------------------------------------------------
+// One-launch CholeskyQR pass kernel (single CTA, 1024 threads):
+//   L = chol(G + shift·I) (right-looking, 32-column panels in shared memory,
+//   trailing update on the FP64 tensor cores), then Rinv = L⁻ᵀ by block
+//   forward substitution.  G is read, not modified.
+//   status = {info, trace(G), min L_ii, max L_ii} (info = first failing
+//   pivot + 1, 0 if none).  Everything stays in L2 (m ≤ 544 → ≤ 2.4 MB).
+// ---------------------------------------------------------------------------
+constexpr int kCI_NB = 32;
+constexpr int kCI_LD = kCI_NB + 4;  // panel stride ≡ 4 (mod 16): conflict-free DMMA fragments
+
+__global__ void __launch_bounds__(1024, 1)
+    chol_inv_kernel(const double* __restrict__ G, long long ldg, int m, double shift, double* L,
+                    long long ldl, double* Rinv, long long ldr, double* Xs, long long ldx,
+                    double* status) {
+  extern __shared__ double sm[];
+  double* P = sm;  // panel: rows × kCI_LD
+  __shared__ double piv_s;
+  __shared__ int info_s;
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // trace of G and copy G (+ shift on the diagonal) → L (full square, lower used)
+  double tr = 0.0;
+  for (long long e = tid; e < (long long)m * m; e += blockDim.x) {
+    const int i = (int)(e / m), j = (int)(e % m);
+    double v = G[(long long)i * ldg + j];
+    if (i == j) {
+      tr += v;
+      v += shift;
+    }
+    L[(long long)i * ldl + j] = v;
+  }
+  tr = warp_sum(tr);
+  if (lane == 0) red[warp] = tr;
+  if (tid == 0) info_s = 0;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 32; ++w) t += red[w];
+    status[1] = t;
+  }
+
+  // ---------------------------------------------------------------- Cholesky
+  for (int p0 = 0; p0 < m; p0 += kCI_NB) {
+    const int nb = min(kCI_NB, m - p0);
+    const int rows = m - p0;
+    for (int e = tid; e < rows * kCI_NB; e += blockDim.x) {
+      const int r = e / kCI_NB, c = e % kCI_NB;
+      P[r * kCI_LD + c] = (c < nb) ? L[(long long)(p0 + r) * ldl + p0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < nb; ++j) {
+      if (tid == 0) {
+        const double d = P[j * kCI_LD + j];
+        if ((!(d > 0.0) || !isfinite(d)) && info_s == 0) info_s = p0 + j + 1;
+        const double pv = sqrt(fmax(d, 0.0));
+        P[j * kCI_LD + j] = pv;
+        piv_s = pv;
+      }
+      __syncthreads();
+      const double pv = piv_s;
+      for (int r = j + 1 + tid; r < rows; r += blockDim.x) P[r * kCI_LD + j] /= pv;
+      __syncthreads();
+      const int nc = nb - j - 1;
+      if (nc > 0) {
+        const int cnt = (rows - j - 1) * nc;
+        for (int idx = tid; idx < cnt; idx += blockDim.x) {
+          const int r = j + 1 + idx / nc, c = j + 1 + idx % nc;
+          if (r >= c) P[r * kCI_LD + c] -= P[r * kCI_LD + j] * P[c * kCI_LD + j];
+        }
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < rows * nb; e += blockDim.x) {
+      const int r = e / nb, c = e % nb;
+      L[(long long)(p0 + r) * ldl + p0 + c] = (r >= c) ? P[r * kCI_LD + c] : 0.0;
+    }
+    // trailing update A22 −= L21 L21ᵀ (lower 8×8 blocks) with DMMA, K = 32
+    const int t0 = p0 + nb;
+    const int tn = m - t0;
+    if (tn > 0) {
+      const int tb = (tn + 7) / 8;
+      const long long nblocks = (long long)tb * (tb + 1) / 2;
+      const int g = lane >> 2, t = lane & 3;
+      for (long long b = warp; b < nblocks; b += 32) {
+        int bi = (int)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+        while ((long long)(bi + 1) * (bi + 2) / 2 <= b) ++bi;
+        while ((long long)bi * (bi + 1) / 2 > b) --bi;
+        const int bj = (int)(b - (long long)bi * (bi + 1) / 2);
+        // panel rows of this block: (t0 − p0) + 8·bi + g
+        const int ra = nb + 8 * bi + g, rb = nb + 8 * bj + g;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int k0 = 0; k0 < kCI_NB; k0 += 4) {
+          const double a = (ra < rows) ? P[ra * kCI_LD + k0 + t] : 0.0;
+          const double bb = (rb < rows) ? P[rb * kCI_LD + k0 + t] : 0.0;
+          dmma_8x8x4(c0, c1, a, bb);
+        }
+        const int gi = t0 + 8 * bi + g;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int gj = t0 + 8 * bj + 2 * t + e;
+          if (gi < m && gj < m && gi >= gj) L[(long long)gi * ldl + gj] -= (e ? c1 : c0);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // zero the strict upper triangle (trailing updates left stale values there)
+  for (long long e = tid; e < (long long)m * m; e += blockDim.x) {
+    const int i = (int)(e / m), j = (int)(e % m);
+    if (j > i) L[(long long)i * ldl + j] = 0.0;
+  }
+  __syncthreads();
+
+  // diagonal statistics + R diagonal accumulation
+  double dmin = INFINITY, dmax = 0.0;
+  for (int i = tid; i < m; i += blockDim.x) {
+    const double d = L[(long long)i * ldl + i];
+    dmin = fmin(dmin, d);
+    dmax = fmax(dmax, d);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  }
+  __shared__ double rmin[32], rmax[32];
+  if (lane == 0) {
+    rmin[warp] = dmin;
+    rmax[warp] = dmax;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = INFINITY, b2 = 0.0;
+    for (int w = 0; w < 32; ++w) {
+      a = fmin(a, rmin[w]);
+      b2 = fmax(b2, rmax[w]);
+    }
+    status[0] = (double)info_s;
+    status[2] = a;
+    status[3] = b2;
+  }
+  if (info_s != 0) return;  // caller retries with a shift; Rinv not needed
+
+  // ------------------------------------------- Rinv = L⁻ᵀ by block rows of X = L⁻¹
+  // X row-block i: X_i = inv(L_ii) (E_i − Σ_{k<i} L_ik X_k).  X is kept
+  // row-major in Xs (coalesced reads across lanes), Rinv[c][r] = X[r][c].
+  double* Dl = sm;                              // L_ii   32 × 33
+  double* Dinv = sm + kCI_NB * (kCI_NB + 1);    // inv    32 × 33
+  double* Z = sm + 2 * kCI_NB * (kCI_NB + 1);   // 32 × m
+  for (int r0 = 0; r0 < m; r0 += kCI_NB) {
+    const int rows = min(kCI_NB, m - r0);
+    for (int e = tid; e < kCI_NB * kCI_NB; e += blockDim.x) {
+      const int r = e / kCI_NB, c = e % kCI_NB;
+      Dl[r * (kCI_NB + 1) + c] = (r < rows && c <= r) ? L[(long long)(r0 + r) * ldl + r0 + c] : 0.0;
+    }
+    __syncthreads();
+    // inverse of the diagonal block: thread c owns column c (forward substitution)
+    if (tid < rows) {
+      const int c = tid;
+      Dinv[c * (kCI_NB + 1) + c] = 1.0 / Dl[c * (kCI_NB + 1) + c];
+      for (int r = 0; r < c; ++r) Dinv[r * (kCI_NB + 1) + c] = 0.0;
+      for (int r = c + 1; r < rows; ++r) {
+        double sacc = 0.0;
+        for (int k = c; k < r; ++k) sacc = fma(Dl[r * (kCI_NB + 1) + k], Dinv[k * (kCI_NB + 1) + c], sacc);
+        Dinv[r * (kCI_NB + 1) + c] = -sacc / Dl[r * (kCI_NB + 1) + r];
+      }
+    }
+    // Z[r][c] = −Σ_{k<r0} L[r0+r][k] X[k][c], c < r0   (warp = row r, lanes = c)
+    if (warp < rows) {
+      const double* lrow = L + (long long)(r0 + warp) * ldl;
+      for (int cb = 0; cb < r0; cb += 32) {
+        const int c = cb + lane;
+        if (c < r0) {
+          double sacc = 0.0;
+#pragma unroll 8
+          for (int k = cb; k < r0; ++k) sacc = fma(lrow[k], Xs[(long long)k * ldx + c], sacc);
+          Z[warp * m + c] = -sacc;
+        }
+      }
+    }
+    __syncthreads();
+    // X[r0 + r][c] = Σ_j Dinv[r][j] Z[j][c] (c < r0);  X_ii = Dinv; zero above
+    for (int e = tid; e < rows * m; e += blockDim.x) {
+      const int r = e / m, c = e % m;
+      double v;
+      if (c < r0) {
+        v = 0.0;
+        for (int j = 0; j <= r; ++j) v = fma(Dinv[r * (kCI_NB + 1) + j], Z[j * m + c], v);
+      } else if (c < r0 + rows) {
+        v = (c - r0 <= r) ? Dinv[r * (kCI_NB + 1) + (c - r0)] : 0.0;
+      } else {
+        v = 0.0;
+      }
+      Xs[(long long)(r0 + r) * ldx + c] = v;
+      Rinv[(long long)c * ldr + r0 + r] = v;
+    }
+    __syncthreads();
+  }
+}
+
+size_t chol_inv_smem(int m) {
+  const size_t chol = (size_t)m * kCI_LD * sizeof(double);
+  const size_t inv = ((size_t)2 * kCI_NB * (kCI_NB + 1) + (size_t)kCI_NB * m) * sizeof(double);
+  return std::max(chol, inv);
+}
+
+int chol_inv(const double* G, long long ldg, int m, double shift, double* L, long long ldl,
+             double* Rinv, long long ldr, double* Xs, double* status, cudaStream_t st) {
+  const size_t smem = chol_inv_smem(m);
+  if (smem > device_info().max_smem - 2048) return -1;
+  static size_t attr[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem > attr[dev]) {
+    if (cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return -1;
+    attr[dev] = smem;
+  }
+  chol_inv_kernel<<<1, 1024, smem, st>>>(G, ldg, m, shift, L, ldl, Rinv, ldr, Xs, m, status);
+  count_launch();
+  return 0;
+}
+
+}  // namespace psd

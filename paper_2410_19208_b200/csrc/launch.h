@@ -84,6 +84,10 @@ int cholesky_lower(double* a, long long lda, int m, int* info, double* ws, size_
 // rinv = (Lᵀ)⁻¹ (upper triangular), from lower-triangular L.
 void tri_inv_upper_from_lower(const double* l, long long ldl, int m, double* rinv,
                               long long ldr, cudaStream_t st);
+// One launch: L = chol(G + shift I) and (when no pivot failed) Rinv = L⁻ᵀ;
+// status = {info, trace(G), min L_ii, max L_ii}.
+int chol_inv(const double* G, long long ldg, int m, double shift, double* L, long long ldl,
+             double* Rinv, long long ldr, double* Xs, double* status, cudaStream_t st);
 // rdiag[i] *= L[i][i]
 void accumulate_diag(const double* l, long long ldl, int m, double* rdiag, cudaStream_t st);
 // Symmetric eigensolver (block Jacobi).  a (m×m, destroyed), values[m], v (m×m).
