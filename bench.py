@@ -205,7 +205,7 @@ def fp64_peak(torch, dev):
 
 
 def load_traffic():
-    path = os.path.join(REPO, "profiles", "gemm_traffic.json")
+    path = os.path.join(REPO, "profiles", "gemm_traffic.json")  # from the committed ncu --set full capture
     try:
         with open(path) as fh:
             return json.load(fh)
@@ -301,7 +301,7 @@ def run_ours(a):
         "roofline": {
             "bound": "tensor", "achieved": gemm_tf, "peak": peak_tf, "unit": "TFLOP/s",
             "frac": gemm_tf / peak_tf, "traffic": traffic.get("bytes_per_launch") if traffic else None,
-            "kernel": "gemm_f64_kernel<64x288 DMMA, A row-major, B row-major> — op(X)·P "
+            "kernel": "gemm_tma_kernel<TMA-fed, warp-specialised DMMA, 64x272 tiles> — op(X)·P "
                       f"(n×n·n×w), {2 * n * n * params.width / 1e9:.0f} GFLOP per launch, "
                       f"{gemm_ms:.2f} ms avg over {g_cnt} launches (CUDA events, timed region)",
             "peak_source": "cuBLAS DGEMM 8192³ burst measured in this run (MEASURED_PEAKS.json has "
