@@ -151,6 +151,35 @@ int psd_gemm_f64(int32_t a_layout, int32_t b_layout, const double* a, int64_t ld
                  int32_t epilogue, double alpha, const double* s, int64_t lds, double* ws,
                  int64_t ws_elems, void* stream);
 
+/* One CholeskyQR factor step on an m x m Gram matrix (m <= ~600):
+ * L = chol(G + shift I) and, when no pivot failed, rinv = L^-T (upper).
+ * status (DEVICE, 4 doubles) = {first failing pivot + 1 or 0, trace(G),
+ * min L_ii, max L_ii}.  g is not modified. */
+int psd_chol_inv(const double* g, int32_t m, int64_t ldg, double shift, double* l, int64_t ldl,
+                 double* rinv, int64_t ldr, double* scratch, double* status, void* stream);
+
+/* out[i][j] = w[i][j] * d[j] (i < rows, j < cols): the (w_kept * d_kept) of
+ * projection.py:77. */
+int psd_scale_columns(const double* w, int64_t ldw, const double* d, double* out, int64_t ldo,
+                      int64_t rows, int32_t cols, void* stream);
+
+/* out[0] = max |x_ij| over a rows x cols block (one HBM pass). */
+int psd_max_abs(const double* x, int64_t rows, int64_t cols, int64_t ldx, double* out,
+                void* stream);
+
+/* Rows [r0, r1) of the exactly symmetric n x n matrix S = lowtri-mirror(A·B^T)
+ * (A, B: n x k, 16-byte aligned, even ld): every value is computed once on a
+ * lower tile and stored at (i,j) and (j,i), so row blocks produced by
+ * different ranks assemble into a bitwise-symmetric matrix.  out: (r1-r0) x n. */
+int psd_syrk_window(const double* a, int64_t lda, const double* b, int64_t ldb, int64_t n,
+                    int32_t k, int64_t r0, int64_t r1, double* out, int64_t ldo, void* stream);
+
+/* out[i - r0][j] = beta·out[i - r0][j] + scale·z(min(i,j), max(i,j)) for rows
+ * [r0, r0+rows), j < n: rows of a symmetric N(0,1) matrix keyed on (seed,
+ * unordered index pair) — identical on every rank that generates them. */
+int psd_fill_sym_gaussian(double* out, int64_t ldo, int64_t r0, int64_t rows, int64_t n,
+                          uint64_t seed, double scale, double beta, void* stream);
+
 /* Device-side N(0,1) fill (Philox4x32-10 + Box-Muller) for callers that do
  * not need the reference's numpy stream (benchmarks, solver loops). */
 int psd_fill_gaussian(double* out, int64_t rows, int32_t cols, int64_t ld, uint64_t seed,

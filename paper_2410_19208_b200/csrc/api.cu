@@ -872,6 +872,72 @@ int psd_gemm_f64(int32_t a_layout, int32_t b_layout, const double* a, int64_t ld
   return PSD_OK;
 }
 
+int psd_chol_inv(const double* g, int32_t m, int64_t ldg, double shift, double* l, int64_t ldl,
+                 double* rinv, int64_t ldr, double* scratch, double* status, void* stream) {
+  if (!g || !l || !rinv || !scratch || !status || m < 1)
+    return fail(PSD_ERR_INVALID_PARAMS, "bad chol_inv arguments");
+  if (psd::chol_inv(g, ldg, m, shift, l, ldl, rinv, ldr, scratch, status,
+                    static_cast<cudaStream_t>(stream)) != 0)
+    return fail(PSD_ERR_INVALID_PARAMS, "size %d too large for the CholeskyQR kernel", m);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "chol_inv");
+  return PSD_OK;
+}
+
+int psd_scale_columns(const double* w, int64_t ldw, const double* d, double* out, int64_t ldo,
+                      int64_t rows, int32_t cols, void* stream) {
+  if (!w || !d || !out || rows < 0 || cols < 0) return fail(PSD_ERR_INVALID_PARAMS, "bad scale_columns");
+  psd::scale_columns(w, ldw, d, out, ldo, rows, cols, static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "scale_columns");
+  return PSD_OK;
+}
+
+int psd_max_abs(const double* x, int64_t rows, int64_t cols, int64_t ldx, double* out,
+                void* stream) {
+  if (!x || !out || rows < 0 || cols < 0) return fail(PSD_ERR_INVALID_PARAMS, "bad max_abs");
+  psd::max_abs(x, rows, cols, ldx, out, static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "max_abs");
+  return PSD_OK;
+}
+
+int psd_syrk_window(const double* a, int64_t lda, const double* b, int64_t ldb, int64_t n,
+                    int32_t k, int64_t r0, int64_t r1, double* out, int64_t ldo, void* stream) {
+  if (!a || !b || !out || n < 1 || k < 1 || r0 < 0 || r1 > n || r0 >= r1)
+    return fail(PSD_ERR_INVALID_PARAMS, "bad syrk_window arguments");
+  psd::GemmOp op;
+  op.a_layout = psd::A_MK;
+  op.b_layout = psd::B_NK;
+  op.A = a;
+  op.lda = lda;
+  op.B = b;
+  op.ldb = ldb;
+  op.C = out;
+  op.ldc = ldo;
+  op.M = (int)n;
+  op.N = (int)n;
+  op.K = k;
+  op.epi = psd::EPI_MIRROR;
+  op.max_splits = 1;
+  op.win0 = (int)r0;
+  op.win1 = (int)r1;
+  const int r = psd::gemm_f64(op, nullptr, 0, static_cast<cudaStream_t>(stream));
+  if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "syrk_window needs 16-byte aligned operands");
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "syrk_window");
+  return PSD_OK;
+}
+
+int psd_fill_sym_gaussian(double* out, int64_t ldo, int64_t r0, int64_t rows, int64_t n,
+                          uint64_t seed, double scale, double beta, void* stream) {
+  if (!out || rows < 0 || n < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad sym gaussian fill");
+  psd::sym_gaussian_rows(out, ldo, r0, rows, n, seed, scale, beta, static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "sym gaussian");
+  return PSD_OK;
+}
+
 int psd_fill_gaussian(double* out, int64_t rows, int32_t cols, int64_t ld, uint64_t seed,
                       uint64_t offset, void* stream) {
   if (!out || rows < 1 || cols < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad gaussian fill");

@@ -152,6 +152,8 @@ int gemm_f64(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st) {
     const int r = gemm_f64_tma(op, ws, ws_elems, st);
     if (r != -2) return r;
   }
+  if (op.epi == EPI_MIRROR && (op.win0 != 0 || (op.win1 != 0 && op.win1 != op.M)))
+    return -3;  // row-windowed mirror store needs the TMA path (16-byte aligned operands)
   if (op.a_layout == A_MK && op.b_layout == B_KN) return launch_cfg<CfgPanelNN>(op, ws, ws_elems, st);
   if (op.a_layout == A_KM && op.b_layout == B_KN) return launch_cfg<CfgPanelTN>(op, ws, ws_elems, st);
   if (op.a_layout == A_MK && op.b_layout == B_NK) return launch_cfg<CfgSquareNT>(op, ws, ws_elems, st);

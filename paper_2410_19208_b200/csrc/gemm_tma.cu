@@ -86,6 +86,8 @@ int launch(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st) {
   p.S = op.S;
   p.lds = op.lds;
   p.partials = op.partials;
+  p.win0 = op.win0;
+  p.win1 = op.win1 > 0 ? op.win1 : op.M;
   p.m_tiles = (op.M + Cfg::BM - 1) / Cfg::BM;
   p.n_tiles = (op.N + Cfg::BN - 1) / Cfg::BN;
   const int sms = device_info().sms;

@@ -59,6 +59,7 @@ struct TmaParams {
   long long split_stride;
   int m_tiles, n_tiles, splits;
   int units;
+  int win0, win1;  // EPI_MIRROR: only rows [win0, win1) of the symmetric result, stored at C + (row − win0)·ldc
   int epi;
   double alpha;
   const double* S;
@@ -157,6 +158,16 @@ struct Unit {
   int m0, n0, kbeg, nk, split;
 };
 
+// EPI_MIRROR with a row window: a lower tile contributes iff its rows or its
+// (mirrored) columns intersect [win0, win1).
+template <class Cfg>
+PSD_DEVINL bool unit_active(const TmaParams& p, const Unit& u) {
+  if (p.epi != EPI_MIRROR) return true;
+  const bool rows = u.m0 < p.win1 && u.m0 + Cfg::BM > p.win0;
+  const bool cols = u.n0 < p.win1 && u.n0 + Cfg::BN > p.win0;
+  return rows || cols;
+}
+
 template <class Cfg>
 PSD_DEVINL Unit decode_unit(const TmaParams& p, int u) {
   Unit r;
@@ -212,6 +223,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
       int it = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const Unit un = decode_unit<Cfg>(p, u);
+        if (!unit_active<Cfg>(p, un)) continue;
         for (int kt = 0; kt < un.nk; ++kt, ++it) {
           const int s = it % STAGES;
           const int use = it / STAGES;
@@ -254,6 +266,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
   int it = 0;
   for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
     const Unit un = decode_unit<Cfg>(p, u);
+    if (!unit_active<Cfg>(p, un)) continue;
     double acc[M8W][N8W][2];
 #pragma unroll
     for (int i = 0; i < M8W; ++i)
@@ -310,8 +323,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
             case EPI_SUB: C[(long long)m * p.ldc + n] = p.S[(long long)m * p.lds + n] - v; break;
             case EPI_MIRROR:
               if (m >= n) {
-                C[(long long)m * p.ldc + n] = v;
-                C[(long long)n * p.ldc + m] = v;
+                if (m >= p.win0 && m < p.win1) C[(long long)(m - p.win0) * p.ldc + n] = v;
+                if (n >= p.win0 && n < p.win1) C[(long long)(n - p.win0) * p.ldc + m] = v;
               }
               break;
             case EPI_RESID: {

@@ -176,6 +176,42 @@ __global__ void philox_normal_kernel(double* out, long long rows, int cols, long
   if (e1 < total) out[(e1 / cols) * ld + (e1 % cols)] = r * s;
 }
 
+__global__ void sym_gaussian_kernel(double* out, long long ldo, long long r0, long long rows,
+                                    long long n, uint64_t seed, double scale, double beta) {
+  const long long total = rows * n;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = r0 + idx / n, j = idx % n;
+    const long long lo = i < j ? i : j, hi = i < j ? j : i;
+    const unsigned long long key = (unsigned long long)lo * (unsigned long long)n + (unsigned long long)hi;
+    uint32_t c0 = (uint32_t)key, c1 = (uint32_t)(key >> 32), c2 = 0x53594d4du, c3 = 0x45u;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      philox_round(c0, c1, c2, c3, k0, k1);
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const double two53 = 1.0 / 9007199254740992.0;
+    const uint64_t b1 = ((uint64_t)c0 << 21) | (uint64_t)(c1 >> 11);
+    const uint64_t b2 = ((uint64_t)c2 << 21) | (uint64_t)(c3 >> 11);
+    const double u1 = ((double)b1 + 0.5) * two53;
+    const double u2 = (double)b2 * two53;
+    const double z = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+    double* o = out + (idx / n) * ldo + j;
+    *o = (beta != 0.0 ? beta * *o : 0.0) + scale * z;
+  }
+}
+
+void sym_gaussian_rows(double* out, long long ldo, long long r0, long long rows, long long n,
+                       uint64_t seed, double scale, double beta, cudaStream_t st) {
+  const long long total = rows * n;
+  if (total == 0) return;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)device_info().sms * 32);
+  sym_gaussian_kernel<<<blocks, 256, 0, st>>>(out, ldo, r0, rows, n, seed, scale, beta);
+  count_launch();
+}
+
 void philox_normal(double* out, long long rows, int cols, long long ld, uint64_t seed,
                    uint64_t offset, cudaStream_t st) {
   const long long pairs = (rows * (long long)cols + 1) / 2;
@@ -435,6 +471,34 @@ void gather_columns(const double* src, long long lds, const int* idx, int ncols,
   if (total == 0) return;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
   gather_columns_kernel<<<blocks, 256, 0, st>>>(src, lds, idx, ncols, dst, ldd, rows);
+  count_launch();
+}
+
+__global__ void __launch_bounds__(256) max_abs_kernel(const double* __restrict__ x, long long rows,
+                                                      long long cols, long long ldx, double* out) {
+  double m = 0.0;
+  const long long total = rows * cols;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(x[(i / cols) * ldx + (i % cols)]));
+  m = warp_max(m);
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t = fmax(t, red[w]);
+    if (t > 0.0) atomic_max_nonneg(out, t);
+  }
+}
+
+void max_abs(const double* x, long long rows, long long cols, long long ldx, double* out,
+             cudaStream_t st) {
+  cudaMemsetAsync(out, 0, sizeof(double), st);
+  const long long total = rows * cols;
+  if (total == 0) return;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)device_info().sms * 8);
+  max_abs_kernel<<<blocks, 256, 0, st>>>(x, rows, cols, ldx, out);
   count_launch();
 }
 

@@ -34,6 +34,7 @@ struct GemmOp {
   long long lds = 0;
   double* partials = nullptr;  // EPI_RESID: one double per CTA
   int max_splits = 256;        // 1 forces a single pass (required for SUB/MIRROR/RESID)
+  int win0 = 0, win1 = 0;      // EPI_MIRROR row window (win1 = 0 → all rows); TMA path only
 };
 // Launches the DMMA GEMM, splitting K when that shortens the critical path.
 // `ws` must hold ws_elems doubles for split-K partials.  Returns the number
@@ -53,6 +54,9 @@ void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaS
 void symmetrize_small(double* x, int m, long long ld, cudaStream_t st);
 void philox_normal(double* out, long long rows, int cols, long long ld, uint64_t seed,
                    uint64_t offset, cudaStream_t st);
+// rows [r0, r0+rows) of a symmetric N(0,1) matrix keyed on (seed, min(i,j), max(i,j))
+void sym_gaussian_rows(double* out, long long ldo, long long r0, long long rows, long long n,
+                       uint64_t seed, double scale, double beta, cudaStream_t st);
 // y = (X − shift·I)·v ; partials[b] = Σ_{rows of block b} y²; returns #blocks.
 int gemv_shift(const double* x, long long n, long long ldx, const double* v, double shift,
                double* y, double* partials, cudaStream_t st);
@@ -74,6 +78,9 @@ void scale_columns(const double* w, long long ldw, const double* d, double* out,
 void gather_columns(const double* src, long long lds, const int* idx, int ncols, double* dst,
                     long long ldd, long long rows, cudaStream_t st);
 void add_diag(double* a, long long ld, int m, double s, cudaStream_t st);
+// out[0] = max |x| over a rows×cols block (deterministic: non-negative u64 max)
+void max_abs(const double* x, long long rows, long long cols, long long ldx, double* out,
+             cudaStream_t st);
 void set_identity(double* a, long long ld, int m, cudaStream_t st);
 
 // ---- small dense (w×w) kernels ---------------------------------------------

@@ -54,3 +54,31 @@ def c1_device(n=1000, seed=0, device="cuda"):
     x = (v * lam) @ v.T
     _symmetrize_inplace(x)
     return x
+
+
+def c4_rows(n, r0, r1, seed=0, rank=200, device="cuda", chunk_rows=None):
+    """Rows [r0, r1) of BASELINE config 4's X (same form as config 3) generated
+    independently on each rank yet bitwise symmetric as a whole:
+    X = mirror(lower([U·s, −W·t]·[U, W]ᵀ)) + 1e-3·E with E keyed on
+    (seed, min(i,j), max(i,j)); U, W orthonormal n×rank from a seed shared by
+    all ranks."""
+    lib = _native.load_library()
+    g = torch.Generator(device=device).manual_seed(int(seed) + 104729)
+    u = torch.linalg.qr(torch.randn(n, rank, dtype=torch.float64, device=device, generator=g))[0]
+    w = torch.linalg.qr(torch.randn(n, rank, dtype=torch.float64, device=device, generator=g))[0]
+    s = torch.logspace(3.0, 0.0, rank, dtype=torch.float64, device=device)
+    t = 10.0 * torch.rand(rank, dtype=torch.float64, device=device, generator=g)
+    a = torch.cat([u * s, -(w * t)], 1).contiguous()
+    b = torch.cat([u, w], 1).contiguous()
+    x = torch.empty((r1 - r0, n), dtype=torch.float64, device=device)
+    st = _native.stream_handle(torch.device(device))
+    step = chunk_rows or (r1 - r0)
+    for c0 in range(r0, r1, step):
+        c1 = min(r1, c0 + step)
+        view = x[c0 - r0:c1 - r0]
+        _native.check(lib.psd_syrk_window(_native.ptr(a), a.stride(0), _native.ptr(b), b.stride(0),
+                                          n, a.shape[1], c0, c1, _native.ptr(view), view.stride(0), st))
+    _native.check(lib.psd_fill_sym_gaussian(_native.ptr(x), x.stride(0), r0, r1 - r0, n,
+                                            int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                            1e-3 / math.sqrt(2.0 * n), 1.0, st))
+    return x

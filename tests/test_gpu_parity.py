@@ -185,3 +185,32 @@ def test_exact_projection(ours):
     assert _rel(rep.result, ref) <= 1e-10
     rep2 = ours.project(x, ours.ProjectorConfig(method="polar"))
     assert _rel(rep2.result, ref) <= 1e-8
+
+
+@pytest.mark.parametrize("n,k,l,q,alpha", [(1024, 40, 8, 1, 0.0), (777, 30, 9, 2, 0.0), (900, 24, 8, 1, 0.6)])
+def test_sharded_single_rank_kernel_ops(ours, n, k, l, q, alpha):
+    """The row-sharded driver on one rank with the real kernels."""
+    import torch
+    from paper_2410_19208_b200.sharded import KernelOps, sharded_ran_proj
+    x = orc.wigner(n, seed=21)
+    om = np.random.default_rng(22).standard_normal((n, k + l))
+    rep = sharded_ran_proj(torch.from_numpy(x).cuda(), 0, n, torch.from_numpy(om).cuda(),
+                           ours.RangeParams(k=k, l=l, q=q), alpha=alpha, ops=KernelOps("cuda"))
+    ref = orc.ran_proj_scal(x, k, l, q, alpha, omega=om) if alpha > 0 else orc.ran_proj(x, k, l, q, omega=om)
+    assert rep.effective_rank == ref.effective_rank
+    res = rep.result_rows.cpu().numpy()
+    assert np.array_equal(res, res.T)
+    assert _rel(res, ref.result) <= TOL
+
+
+def test_c4_row_blocks_assemble_symmetric(ours):
+    """Config-4 generator: row blocks built independently are bitwise symmetric together."""
+    import torch
+    from paper_2410_19208_b200 import workloads
+    n = 2048
+    a = workloads.c4_rows(n, 0, 1000, seed=3)
+    b = workloads.c4_rows(n, 1000, n, seed=3, chunk_rows=300)
+    x = torch.cat([a, b], 0)
+    assert torch.equal(x, x.T)
+    full = workloads.c4_rows(n, 0, n, seed=3)
+    assert torch.equal(full, x)
