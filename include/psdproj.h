@@ -180,6 +180,23 @@ int psd_syrk_window(const double* a, int64_t lda, const double* b, int64_t ldb, 
 int psd_fill_sym_gaussian(double* out, int64_t ldo, int64_t r0, int64_t rows, int64_t n,
                           uint64_t seed, double scale, double beta, void* stream);
 
+/* ---- solver loop (sdls.py:76-89, :221-245; BASELINE config 5) ---------- */
+/* x = cr + Σ_i y_i A_i: x ← copy(cr) (n x n, the C/ρ term), then for every
+ * distinct stored position p: x[pos[p]] += Σ_{t ∈ [ptr[p], ptr[p+1])}
+ * y[econ[t]]·evals[t] in stored order (assemble_dual_matrix, sdls.py:83-89). */
+int psd_sdls_assemble(const double* cr, int64_t n, const int64_t* pos, const int32_t* ptr,
+                      const int32_t* econ, const double* evals, const double* y, int32_t npos,
+                      double* x, void* stream);
+/* t_i = Tr(A_i X₊) with X₊ = sym((W·D)·Wᵀ) evaluated on A_i's stored entries
+ * (rows/cols/vals grouped by constraint, cptr[m+1]); wd = W·diag(d), n x r
+ * (constraint_traces, sdls.py:76-80, on the factored projection). */
+int psd_sdls_traces(const double* wd, const double* w, int64_t ldw, int32_t r, const int32_t* rows,
+                    const int32_t* cols, const double* vals, const int32_t* cptr, int32_t m,
+                    double* t, void* stream);
+/* grad = b − t; out[0] = ‖grad‖; if out[0] > eps: y += beta·grad (sdls.py:236-245). */
+int psd_sdls_step(const double* b, const double* t, double* y, double* grad, int32_t m,
+                  double beta, double eps, double* out, void* stream);
+
 /* Device-side N(0,1) fill (Philox4x32-10 + Box-Muller) for callers that do
  * not need the reference's numpy stream (benchmarks, solver loops). */
 int psd_fill_gaussian(double* out, int64_t rows, int32_t cols, int64_t ld, uint64_t seed,

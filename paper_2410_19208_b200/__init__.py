@@ -17,6 +17,7 @@ from .sketch import (RangeParams, min_eig_magnitude, orthonormality_defect, powe
                      range_finder)
 from .symmetric import (EigenDecomposition, eigh, exact_psd_projection, frobenius_norm,
                         gaussian_matrix, require_symmetric, rng_from_seed, symmetrize)
+from .sdls import SolveReport, SparseSdlsProblem, TrajectoryPoint, solve
 from .install import install, uninstall
 from . import workloads  # noqa: E402  (seeded HBM generators for the BASELINE configs)
 
@@ -29,5 +30,5 @@ __all__ = [
     "ran_proj_scal", "RangeParams", "min_eig_magnitude", "orthonormality_defect",
     "power_iteration", "range_finder", "EigenDecomposition", "eigh", "exact_psd_projection",
     "frobenius_norm", "gaussian_matrix", "require_symmetric", "rng_from_seed", "symmetrize",
-    "install", "uninstall",
+    "install", "uninstall", "solve", "SparseSdlsProblem", "SolveReport", "TrajectoryPoint",
 ]

@@ -938,6 +938,40 @@ int psd_fill_sym_gaussian(double* out, int64_t ldo, int64_t r0, int64_t rows, in
   return PSD_OK;
 }
 
+int psd_sdls_assemble(const double* cr, int64_t n, const int64_t* pos, const int32_t* ptr,
+                      const int32_t* econ, const double* evals, const double* y, int32_t npos,
+                      double* x, void* stream) {
+  if (!cr || !x || n < 1 || npos < 0) return fail(PSD_ERR_INVALID_PARAMS, "bad sdls_assemble");
+  psd::sdls_assemble(cr, n, reinterpret_cast<const long long*>(pos), ptr, econ, evals, y, npos, x,
+                     static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "sdls_assemble");
+  return PSD_OK;
+}
+
+int psd_sdls_traces(const double* wd, const double* w, int64_t ldw, int32_t r, const int32_t* rows,
+                    const int32_t* cols, const double* vals, const int32_t* cptr, int32_t m,
+                    double* t, void* stream) {
+  if (!t || m < 0 || r < 0) return fail(PSD_ERR_INVALID_PARAMS, "bad sdls_traces");
+  if (r == 0) {
+    cudaMemsetAsync(t, 0, (size_t)m * sizeof(double), static_cast<cudaStream_t>(stream));
+    return PSD_OK;
+  }
+  psd::sdls_traces(wd, w, ldw, r, rows, cols, vals, cptr, m, t, static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "sdls_traces");
+  return PSD_OK;
+}
+
+int psd_sdls_step(const double* b, const double* t, double* y, double* grad, int32_t m,
+                  double beta, double eps, double* out, void* stream) {
+  if (!b || !t || !y || !grad || !out || m < 0) return fail(PSD_ERR_INVALID_PARAMS, "bad sdls_step");
+  psd::sdls_step(b, t, y, grad, m, beta, eps, out, static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "sdls_step");
+  return PSD_OK;
+}
+
 int psd_fill_gaussian(double* out, int64_t rows, int32_t cols, int64_t ld, uint64_t seed,
                       uint64_t offset, void* stream) {
   if (!out || rows < 1 || cols < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad gaussian fill");

@@ -108,4 +108,14 @@ void sort_eigs(const double* vals, const double* vecs, long long ldv, int m, dou
                double* vals_out, double* vecs_out, long long ldo, int* npos, int* perm,
                cudaStream_t st);
 
+// ---- solver loop (sdls_kernels.cu) -------------------------------------------
+void sdls_assemble(const double* cr, long long n, const long long* pos, const int* ptr,
+                   const int* econ, const double* evals, const double* y, int npos, double* x,
+                   cudaStream_t st);
+void sdls_traces(const double* wd, const double* w, long long ldw, int r, const int* rows,
+                 const int* cols, const double* vals, const int* cptr, int m, double* t,
+                 cudaStream_t st);
+void sdls_step(const double* b, const double* t, double* y, double* grad, int m, double beta,
+               double eps, double* out, cudaStream_t st);
+
 }  // namespace psd

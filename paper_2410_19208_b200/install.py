@@ -40,6 +40,8 @@ _TARGETS = {
     ("psdcone.sdls", "project"): "project",
     ("psdcone.sdls", "min_eig_magnitude"): "min_eig_magnitude",
     ("psdcone.sdls", "exact_psd_projection"): "exact_psd_projection",
+    ("psdcone", "solve"): "solve",
+    ("psdcone.sdls", "solve"): "solve",
     ("psdcone.experiments", "ran_proj"): "ran_proj",
     ("psdcone.experiments", "ran_proj_scal"): "ran_proj_scal",
 }

@@ -183,5 +183,29 @@ def main():
           effective_rank=rep.effective_rank, basis_width=rep.basis_width)
 
 
+def solver_cases():
+    """Reference solve() (sdls.py:164-265) on small dense SDLS instances."""
+    from oracle import sdls_oracle as so
+    for name, method, n, m, k, l, q, refresh in (
+        ("sdls_randomized", "randomized", 40, 12, 8, 4, 1, 1),
+        ("sdls_scaled", "scaled_randomized", 36, 10, 6, 4, 1, 3),
+    ):
+        sp = so.config5_instance(n, m, nnz_per=4, seed=123 + n)
+        dense = np.zeros((m, n, n))
+        np.add.at(dense, (sp.con, sp.rows, sp.cols), sp.vals)
+        beta = so.lipschitz_beta(sp)
+        problem = psdcone.SdlsProblem(sp.c, 1.0, list(zip(dense, sp.b)))
+        cfg = ProjectorConfig(method=method, params=RangeParams(k=k, l=l, q=q), power_N=10)
+        rep = psdcone.solve(problem, cfg, beta=beta, epsilon=1e-14, max_iter=25, rng=7,
+                            alpha_refresh=refresh, keep_trajectory=True)
+        _save(name, c=sp.c, con=sp.con, rows=sp.rows, cols=sp.cols, vals=sp.vals, b=sp.b,
+              n=n, m=m, k=k, l=l, q=q, beta=beta, seed=7, alpha_refresh=refresh,
+              method=method, y_final=rep.y_final,
+              grad_norms=np.array([t.grad_norm for t in rep.trajectory]),
+              x_solution=rep.x_solution, objective=rep.objective,
+              iterations=rep.iterations, exact_residual=rep.exact_feasibility_residual)
+
+
 if __name__ == "__main__":
     main()
+    solver_cases()

@@ -214,3 +214,21 @@ def test_c4_row_blocks_assemble_symmetric(ours):
     assert torch.equal(x, x.T)
     full = workloads.c4_rows(n, 0, n, seed=3)
     assert torch.equal(full, x)
+
+
+@pytest.mark.parametrize("name", ["sdls_randomized", "sdls_scaled"])
+def test_solver_loop_matches_reference(ours, name):
+    """Alg. 6 (sdls.py:164-265) on the device vs the reference's own trajectory."""
+    d = gio.load(name)
+    prob = ours.SparseSdlsProblem(d["c"], 1.0, d["con"], d["rows"], d["cols"], d["vals"], d["b"])
+    cfg = ours.ProjectorConfig(method=str(d["method"]),
+                               params=ours.RangeParams(k=int(d["k"]), l=int(d["l"]), q=int(d["q"])),
+                               power_N=10)
+    rep = ours.solve(prob, cfg, beta=float(d["beta"]), epsilon=1e-14, max_iter=25,
+                     rng=int(d["seed"]), alpha_refresh=int(d["alpha_refresh"]), keep_trajectory=True)
+    assert rep.iterations == int(d["iterations"])
+    np.testing.assert_allclose([t.grad_norm for t in rep.trajectory], d["grad_norms"], rtol=1e-8)
+    np.testing.assert_allclose(rep.y_final, d["y_final"], rtol=1e-8, atol=1e-11)
+    assert _rel(rep.x_solution, d["x_solution"]) <= 1e-9
+    assert rep.objective == pytest.approx(float(d["objective"]), rel=1e-8)
+    assert rep.exact_feasibility_residual == pytest.approx(float(d["exact_residual"]), rel=1e-6)

@@ -1,0 +1,44 @@
+"""The solver-loop oracle (oracle/sdls_oracle.py) against the reference's own
+solve() trajectories (tests/golden/sdls_*.npz), for the dense stack and for the
+sparse-COO rebinding used at config-5 scale."""
+
+import numpy as np
+import pytest
+
+from oracle import sdls_oracle as so
+from tests import golden_io as gio
+
+
+def _problems(d):
+    n, m = int(d["n"]), int(d["m"])
+    sp = so.SparseProblem(d["c"], 1.0, d["con"], d["rows"], d["cols"], d["vals"], d["b"])
+    dense = np.zeros((m, n, n))
+    np.add.at(dense, (d["con"], d["rows"], d["cols"]), d["vals"])
+    return so.DenseProblem(d["c"], 1.0, dense, d["b"]), sp
+
+
+@pytest.mark.parametrize("name", ["sdls_randomized", "sdls_scaled"])
+@pytest.mark.parametrize("kind", ["dense", "sparse"])
+def test_solver_oracle_matches_reference(name, kind):
+    d = gio.load(name)
+    dense, sparse = _problems(d)
+    prob = dense if kind == "dense" else sparse
+    rep = so.solve(prob, str(d["method"]), int(d["k"]), int(d["l"]), int(d["q"]),
+                   beta=float(d["beta"]), epsilon=1e-14, max_iter=25, rng=int(d["seed"]),
+                   alpha_refresh=int(d["alpha_refresh"]))
+    assert rep.iterations == int(d["iterations"])
+    np.testing.assert_allclose(rep.trajectory, d["grad_norms"], rtol=1e-9)
+    np.testing.assert_allclose(rep.y_final, d["y_final"], rtol=1e-9, atol=1e-12)
+    err = np.linalg.norm(rep.x_solution - d["x_solution"]) / np.linalg.norm(d["x_solution"])
+    assert err < 1e-9
+    assert rep.objective == pytest.approx(float(d["objective"]), rel=1e-9)
+    assert rep.exact_feasibility_residual == pytest.approx(float(d["exact_residual"]), rel=1e-8)
+
+
+def test_config5_instance_shapes():
+    p = so.config5_instance(64, 30, seed=1)
+    assert p.con.size == 30 * 8 and p.b.shape == (30,)
+    x = p.assemble(np.ones(30))
+    np.testing.assert_array_equal(x, x.T)
+    beta = so.lipschitz_beta(p)
+    assert 0 < beta < 1
