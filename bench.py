@@ -35,6 +35,15 @@ METRIC = "rand-PSD projections/s at n=32768,k=256 fp64; % of FP64 tensor-core ro
 UNIT = "projections/s"
 CPU_SAMPLE_N = 8192
 
+# BASELINE.json configs; c3 is the headline (metric) workload.
+CONFIGS = {
+    "c1": dict(n=1000, k=40, p=10, q=2, desc="config 1: Haar basis, 30 geometric + uniform[-1,0] spectrum"),
+    "c2": dict(n=8192, k=128, p=16, q=2, desc="config 2: Wigner (G+Gᵀ)/(2√n)"),
+    "c3": dict(n=32768, k=256, p=16, q=1, desc="config 3: U diag(s)Uᵀ − W diag(t)Wᵀ + 1e-3 E"),
+    "c4": dict(n=131072, k=512, p=32, q=2, desc="config 4: config-3 form, row-sharded over ranks"),
+    "c5": dict(n=4096, k=64, p=10, q=1, m=20000, desc="config 5: SDLS dual ascent, sparse constraints"),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -42,21 +51,27 @@ def parse():
     ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=32768)
-    ap.add_argument("--k", type=int, default=256)
-    ap.add_argument("--p", type=int, default=16)
-    ap.add_argument("--q", type=int, default=1)
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--p", type=int, default=None)
+    ap.add_argument("--q", type=int, default=None)
     ap.add_argument("--pool", type=int, default=4, help="distinct X matrices cycled per rank")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    cfg = CONFIGS[a.config]
+    for key in ("n", "k", "p", "q"):
+        if getattr(a, key) is None:
+            setattr(a, key, cfg[key])
+    return a
 
 
 def workload_config(a, n_gpus):
     return {
-        "workload": f"BASELINE config 3: ran_proj (Alg. 2) n={a.n}, k={a.k}, p={a.p}, q={a.q}, fp64, "
-                    f"{a.steps} sequential projections per rank",
+        "workload": f"BASELINE {CONFIGS[a.config]['desc']}: ran_proj (Alg. 2) n={a.n}, k={a.k}, "
+                    f"p={a.p}, q={a.q}, fp64, {a.steps} sequential projections per rank",
         "n": a.n, "k": a.k, "p": a.p, "q": a.q, "width": a.k + a.p,
         "x_pool": a.pool,
         "l2": "inputs larger than L2 (each X is 8·n² bytes ≫ 126 MB)",
@@ -83,7 +98,8 @@ def cpu_sample(a, reps=1):
 
     from oracle import psd_oracle as orc
     ns = min(CPU_SAMPLE_N, a.n)
-    x = orc.c3_matrix(ns, seed=11)
+    x = {"c1": lambda: orc.c1_matrix(seed=11, n=ns), "c2": lambda: orc.wigner(ns, seed=11),
+         "c3": lambda: orc.c3_matrix(ns, seed=11)}[a.config]()
     best = 1e300
     for r in range(reps):
         om = np.random.default_rng(100 + r).standard_normal((ns, a.k + a.p))
@@ -108,8 +124,9 @@ def run_reference(a):
         secs.append(s)
     value = a.steps / sum(s / ((ns / a.n) ** 2) for s in secs)
     cores = cpu_cores()
-    sample = (f"oracle port of psdcone.ran_proj (numpy/OpenBLAS, {cores} threads) on a C3 matrix at "
-              f"n={CPU_SAMPLE_N}, k={a.k}, p={a.p}, q={a.q}; time × (n/{CPU_SAMPLE_N})² per step")
+    ns = min(CPU_SAMPLE_N, a.n)
+    sample = (f"oracle port of psdcone.ran_proj (numpy/OpenBLAS, {cores} threads) on a {a.config} matrix at "
+              f"n={ns}, k={a.k}, p={a.p}, q={a.q}; time × (n/{ns})² per step")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": n_gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 / value,
@@ -233,7 +250,12 @@ def run_ours(a):
     peak = fp64_peak(torch, dev) if rank == 0 else None
     nominal = 148 * 128 * 1.965  # GFLOP/s: 148 SMs × 64 DMMA FMA/clk × 2 × 1965 MHz
 
-    pool = [workloads.c3_device(n, seed=1000 * rank + i, device=dev) for i in range(a.pool)]
+    gen = {"c1": lambda sd: workloads.c1_device(n, seed=sd, device=dev),
+           "c2": lambda sd: workloads.wigner_device(n, seed=sd, device=dev),
+           "c3": lambda sd: workloads.c3_device(n, seed=sd, device=dev)}[a.config]
+    pool = [gen(1000 * rank + i) for i in range(a.pool)]
+    # inputs smaller than L2 (config 1: 8 MB) → flush L2 between steps with a 256 MB write
+    flush = torch.empty(32 << 20, dtype=torch.float64, device=dev) if 8 * n * n < (256 << 20) else None
     rng = psd.DeviceRng(seed=4242 + rank)
     plan = psd._native.get_plan(n, params.width, dev)
 
@@ -252,6 +274,8 @@ def run_ours(a):
     ranks = []
     e0.record()
     for i in range(a.steps):
+        if flush is not None:
+            flush.zero_()
         rep = psd.ran_proj(pool[i % a.pool], params, rng)
         launches += rep.device_info["gpu_launches"]
         ranks.append(rep.effective_rank)
@@ -284,7 +308,7 @@ def run_ours(a):
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         v, s, ns = cpu_sample(a, reps=1)
         cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-               "sample": f"1 projection of a C3 matrix at n={ns} (k={a.k}, p={a.p}, q={a.q}) "
+               "sample": f"1 projection of a {a.config} matrix at n={ns} (k={a.k}, p={a.p}, q={a.q}) "
                          f"by the oracle port of psdcone.ran_proj on host cores in {s:.2f} s, "
                          f"scaled by ({ns}/{a.n})²"}
     if world > 1:
@@ -292,11 +316,13 @@ def run_ours(a):
     if rank != 0:
         return
     peak_tf = peak if peak else nominal / 1000.0
+    metric = METRIC if a.config == "c3" else (
+        f"rand-PSD projections/s at n={n},k={a.k} fp64 ({a.config})")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE config-3 matrices generated in HBM)",
+        "data": f"synthetic (seeded BASELINE {a.config} matrices generated in HBM)",
         "config": workload_config(a, world),
         "roofline": {
             "bound": "tensor", "achieved": gemm_tf, "peak": peak_tf, "unit": "TFLOP/s",
@@ -321,6 +347,122 @@ def run_ours(a):
     if e2e:
         line["e2e"] = e2e
     print(json.dumps(line), flush=True)
+
+
+def run_solver(a):
+    """Config 5: `--steps` iterations of the dual gradient ascent (Alg. 6) with a
+    randomized projection each; value = solver iterations/s."""
+    import numpy as np
+
+    from oracle import sdls_oracle as so
+    cfg = CONFIGS["c5"]
+    n, m = a.n, cfg["m"]
+    prob = so.config5_instance(n, m, nnz_per=4, seed=5)
+    beta = so.lipschitz_beta(prob)
+    metric = "SDLS solver iterations/s at n=4096, m=20000, k=64, q=1 (config 5)"
+    conf = {"workload": f"BASELINE config 5: sdls.solve, n={n}, m={m}, k={a.k}, p={a.p}, q={a.q}, "
+                        f"randomized projector, beta=1/L={beta:.4g}, {a.steps} iterations",
+            "n": n, "m": m, "k": a.k, "p": a.p, "q": a.q, "beta": beta}
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    if a.impl == "reference":
+        its = max(1, min(a.steps, 3))
+        t0 = time.perf_counter()
+        so.solve(prob, "randomized", a.k, a.p, a.q, beta=beta, epsilon=1e-300, max_iter=its, rng=1)
+        value = its / (time.perf_counter() - t0)
+        cores = cpu_cores()
+        print(json.dumps({"metric": metric, "value": value, "unit": "iterations/s", "impl": "reference",
+                          "n_gpus": 1, "steps": its, "warmup": 0, "ms_per_step": 1000 / value,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "dtype": "f64", "data": "synthetic (seeded config-5 instance)", "config": conf,
+                          "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": cores,
+                                           "kind": "port", "sample": f"{its} iterations of the oracle "
+                                           "sparse-COO restatement of psdcone.solve"},
+                          "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    import torch
+
+    import paper_2410_19208_b200 as psd
+    dev = torch.device("cuda", 0)
+    sp = psd.SparseSdlsProblem(prob.c, 1.0, prob.con, prob.rows, prob.cols, prob.vals, prob.b)
+    pcfg = psd.ProjectorConfig(method="randomized", params=psd.RangeParams(k=a.k, l=a.p, q=a.q))
+    psd.solve(sp, pcfg, beta=beta, epsilon=1e-300, max_iter=max(a.warmup, 1), rng=1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = psd.solve(sp, pcfg, beta=beta, epsilon=1e-300, max_iter=a.steps, rng=1)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    value = rep.iterations / dt
+    line = {"metric": metric, "value": value, "unit": "iterations/s", "n_gpus": 1, "steps": rep.iterations,
+            "warmup": a.warmup, "ms_per_step": 1000 * dt / rep.iterations, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded config-5 instance)", "config": conf,
+            "final_grad_norm": rep.grad_norm_final,
+            "timing": "wall clock around solve() incl. per-iteration host syncs and the final "
+                      "dense reconstruction (Ω drawn on the host from numpy, as the reference)"}
+    if not a.no_cpu_baseline:
+        t0 = time.perf_counter()
+        so.solve(prob, "randomized", a.k, a.p, a.q, beta=beta, epsilon=1e-300, max_iter=2, rng=1)
+        v = 2 / (time.perf_counter() - t0)
+        line["cpu_baseline"] = {"value": v, "unit": "iterations/s", "cores": cpu_cores(), "kind": "port",
+                                "sample": "2 iterations of the oracle sparse-COO restatement of psdcone.solve"}
+    print(json.dumps(line), flush=True)
+
+
+def run_sharded(a):
+    """Config 4: one row-sharded projection per step over all ranks (NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_19208_b200 as psd
+    from paper_2410_19208_b200 import sharded, workloads
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = a.n
+    params = psd.RangeParams(k=a.k, l=a.p, q=a.q)
+    starts = sharded.row_split(n, world)
+    r0, r1 = starts[rank], starts[rank + 1]
+    x = workloads.c4_rows(n, r0, r1, seed=11, device=dev, chunk_rows=4096)
+    om = psd.DeviceRng(99).normal((n, params.width), dev)      # identical on every rank
+    want = world > 1   # one GPU cannot hold X (137 GB) and the dense result together
+    ops = sharded.KernelOps(dev)
+    comm = sharded.Comm()
+    for _ in range(max(1, a.warmup)):
+        sharded.sharded_ran_proj(x, r0, n, om, params, comm=comm, ops=ops, want_result=want)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        rep = sharded.sharded_ran_proj(x, r0, n, om, params, comm=comm, ops=ops, want_result=want)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    value = a.steps / (ms / 1000.0)
+    flops = 2.0 * n * n * params.width * (2 * params.q + 2) + (float(n) * n * rep.effective_rank if want else 0)
+    print(json.dumps({
+        "metric": f"rand-PSD projections/s at n={n},k={a.k} fp64 (config 4, row-sharded)", "value": value,
+        "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (config-4 rows generated per rank, bitwise symmetric)",
+        "config": {"workload": f"BASELINE config 4: n={n}, k={a.k}, p={a.p}, q={a.q}, row-sharded x{world}",
+                   "result": "dense row blocks" if want else "factored (W, d): X and X₊ do not fit one GPU"},
+        "effective_rank": rep.effective_rank, "tflops": flops * value / 1e12}), flush=True)
 
 
 def run_e2e(a, torch, psd, x_dev, params, dev):
@@ -361,7 +503,11 @@ def run_e2e(a, torch, psd, x_dev, params, dev):
 
 def main():
     a = parse()
-    if a.impl == "reference":
+    if a.config == "c5":
+        run_solver(a)
+    elif a.config == "c4":
+        run_sharded(a)
+    elif a.impl == "reference":
         run_reference(a)
     else:
         run_ours(a)
