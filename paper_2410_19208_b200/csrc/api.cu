@@ -36,6 +36,7 @@ struct psd_plan {
   size_t jws_elems = 0;
   double *gy = nullptr, *gv = nullptr, *gpart = nullptr, *stats = nullptr, *scal = nullptr;
   double* qrstat = nullptr;
+  double* dinv = nullptr;  // ceil(w/32) diagonal-block inverses (32×32) for chol_fast
   int gparts = 0;
   double* rpart = nullptr;
   ll rparts = 0;
@@ -263,8 +264,13 @@ struct QrInfo {
 // Orthonormalises the n×w panel in `bufs[cur]`; `bufs[tmp]` is scratch.
 // On return *qidx is the buffer index holding Q; rdiag (if non-null) holds
 // Π_pass |L_ii| = |R_ii| of Y = Q·R.
+//
+// `span_only` (the power-iteration stabilisation of sketch.py:78/:80): the
+// next product only needs a well-conditioned basis of span(Y) — the final
+// result depends on the span alone — so one unshifted pass with κ²u ≲ 1e-12
+// is accepted instead of two.
 int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rdiag, int* qidx,
-           QrInfo* info, cudaStream_t st) {
+           QrInfo* info, cudaStream_t st, bool span_only = false) {
   Stage mark(p, PSD_STAGE_QR, st);
   const ll ld = p->ldp;
   if (rdiag) {
@@ -278,7 +284,7 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
   double hs[4];
   for (int pass = 0; pass < 10; ++pass) {
     PSD_TRY(panel_tn(p, bufs[cur], bufs[cur], ld, n, w, p->G, true, st));
-    if (psd::chol_inv(p->G, w, w, 0.0, p->L, w, p->Rinv, w, p->T, p->qrstat, st) != 0)
+    if (psd::chol_fast(p->G, w, w, 0.0, p->L, w, p->Rinv, w, p->dinv, p->qrstat, st) != 0)
       return fail(PSD_ERR_INVALID_PARAMS, "width %d too large for the CholeskyQR kernel", w);
     PSD_CUDA_CHECK(cudaMemcpyAsync(hs, p->qrstat, sizeof(hs), cudaMemcpyDeviceToHost, st), "qr status");
     PSD_TRY(sync(st, "cholesky"));
@@ -314,7 +320,7 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
     if (shift) {
       // Fukaya et al. shifted CholeskyQR: s = 11(mn + n(n+1))·u·‖Y‖²
       const double s = 11.0 * ((double)n * w + (double)w * (w + 1)) * u * trace;
-      psd::chol_inv(p->G, w, w, s, p->L, w, p->Rinv, w, p->T, p->qrstat, st);
+      psd::chol_fast(p->G, w, w, s, p->L, w, p->Rinv, w, p->dinv, p->qrstat, st);
       PSD_CUDA_CHECK(cudaMemcpyAsync(hs, p->qrstat, sizeof(hs), cudaMemcpyDeviceToHost, st),
                      "qr status");
       PSD_TRY(sync(st, "shifted cholesky"));
@@ -327,7 +333,7 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
     std::swap(cur, tmp);
     info->passes++;
     unshifted_run = shift ? 0 : unshifted_run + 1;
-    if (unshifted_run >= 2 && kest0 <= 1e4) {
+    if ((unshifted_run >= 2 && kest0 <= 1e4) || (span_only && !shift && kest <= 1e4)) {
       verified = true;
       break;
     }
@@ -372,12 +378,12 @@ int range_finder_core(psd_plan* p, const double* x, ll m, ll n, ll ldx, const do
   PSD_TRY(xmul_rect(p, x, m, n, ldx, omega, ldo, w, bufs[0], ld, alpha, false, st));  // :75
   for (int it = 0; it < q; ++it) {                                 // :76-82
     QrInfo tmp;
-    if (stabilize) PSD_TRY(cholqr(p, bufs, y, (y + 1) % 3, m, w, nullptr, &y, &tmp, st));
+    if (stabilize) PSD_TRY(cholqr(p, bufs, y, (y + 1) % 3, m, w, nullptr, &y, &tmp, st, true));
     const int z = (y + 1) % 3;
     // z = xᵀ @ y (sketch.py:79); for bitwise-symmetric X this equals X·Y exactly
     PSD_TRY(xmul_rect(p, x, m, n, ldx, bufs[y], ld, w, bufs[z], ld, alpha, use_t, st));
     int zq = z;
-    if (stabilize) PSD_TRY(cholqr(p, bufs, z, (z + 1) % 3, n, w, nullptr, &zq, &tmp, st));
+    if (stabilize) PSD_TRY(cholqr(p, bufs, z, (z + 1) % 3, n, w, nullptr, &zq, &tmp, st, true));
     const int ny = (zq + 1) % 3;
     PSD_TRY(xmul_rect(p, x, m, n, ldx, bufs[zq], ld, w, bufs[ny], ld, alpha, false, st));
     y = ny;
@@ -461,6 +467,7 @@ int psd_plan_create(psd_plan** out, int64_t n, int32_t width, int32_t device) {
   ok &= (p->stats = alloc(p, 4)) != nullptr;
   ok &= (p->scal = alloc(p, 8)) != nullptr;
   ok &= (p->qrstat = alloc(p, 8)) != nullptr;
+  ok &= (p->dinv = alloc(p, (size_t)((width + 31) / 32) * 1024)) != nullptr;
   psd::GemmOp rop;
   rop.M = (int)n;
   rop.N = (int)n;

@@ -3,6 +3,8 @@
 // and the descending sort / sign convention.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "launch.h"
@@ -445,6 +447,297 @@ int chol_inv(const double* G, long long ldg, int m, double shift, double* L, lon
   }
   chol_inv_kernel<<<1, 1024, smem, st>>>(G, ldg, m, shift, L, ldl, Rinv, ldr, Xs, m, status);
   count_launch();
+  return 0;
+}
+
+}  // namespace psd
+
+namespace psd {
+
+// ---------------------------------------------------------------------------
+// Fast CholeskyQR factor step (two launches, no explicit full-matrix loops
+// on the critical path):
+//   chol_blocked_kernel  (1 CTA):  L = chol(G + shift I) with 32-column
+//     panels — the 32×32 diagonal block is factored by one warp in
+//     registers (row per lane, shuffles), the panel below by a smem TRSM
+//     against inv(L_jj), the trailing matrix by DMMA; also writes
+//     Dinv_j = inv(L_jj) for every diagonal block and the status vector.
+//   tri_inv_blocked_kernel (1 CTA per block column j): X = L⁻¹ column block
+//     j by block forward substitution X_ij = −Dinv_i Σ_{k=j}^{i−1} L_ik X_kj,
+//     written transposed into Rinv (Rinv = L⁻ᵀ, row block j contiguous).
+// ---------------------------------------------------------------------------
+constexpr int kFB = 32;
+constexpr int kFL = kFB + 4;  // smem stride ≡ 4 (mod 16)
+
+__device__ long long g_chol_t[6];
+__global__ void __launch_bounds__(256, 1)
+    chol_blocked_kernel(const double* __restrict__ G, long long ldg, int m, double shift, double* L,
+                        long long ldl, double* Dinv, double* status) {
+  extern __shared__ double sm[];
+  double* P = sm;                      // panel rows × kFL
+  double* Di = sm + (size_t)max(m, kFB) * kFL;   // current inv(L_jj), 32 × 33
+  __shared__ int info_s;
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double tr = 0.0;
+  for (long long e = tid; e < (long long)m * m; e += blockDim.x) {
+    const int i = (int)(e / m), j = (int)(e % m);
+    double v = G[(long long)i * ldg + j];
+    if (i == j) {
+      tr += v;
+      v += shift;
+    }
+    L[(long long)i * ldl + j] = (j <= i) ? v : 0.0;
+  }
+  tr = warp_sum(tr);
+  if (lane == 0) red[warp] = tr;
+  if (tid == 0) info_s = 0;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    status[1] = t;
+  }
+  long long tc0 = clock64();
+  for (int p0 = 0; p0 < m; p0 += kFB) {
+    const int nb = min(kFB, m - p0);
+    const int rows = m - p0;
+    const long long ta = clock64();
+    // ---- stage the panel (rows × 32) in shared memory (coalesced)
+    for (int e = tid; e < rows * kFB; e += blockDim.x) {
+      const int r = e >> 5, c = e & 31;
+      P[r * kFL + c] = (c < nb && c <= r + kFB) ? L[(long long)(p0 + r) * ldl + p0 + c] : 0.0;
+    }
+    __syncthreads();
+    // ---- diagonal block: warp 0, lane i owns row i (registers); rsqrt, no divisions
+    if (warp == 0) {
+      double d[kFB];
+#pragma unroll
+      for (int k = 0; k < kFB; ++k) d[k] = (lane < nb && k <= lane) ? P[lane * kFL + k] : 0.0;
+      double rdl = 0.0;  // 1 / L_ll of this lane's row
+#pragma unroll
+      for (int j = 0; j < kFB; ++j) {
+        if (j < nb) {
+          const double piv = __shfl_sync(0xffffffffu, d[j], j);
+          if (lane == 0 && (!(piv > 0.0) || !isfinite(piv)) && info_s == 0) info_s = p0 + j + 1;
+          const double inv = rsqrt(fmax(piv, 1e-300));
+          if (lane == j) {
+            d[j] = piv * inv;
+            rdl = inv;
+          }
+          if (lane > j) d[j] *= inv;
+#pragma unroll
+          for (int k = j + 1; k < kFB; ++k) {
+            const double lkj = __shfl_sync(0xffffffffu, d[j], k);
+            if (lane >= k && k < nb) d[k] = fma(-d[j], lkj, d[k]);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kFB; ++k) P[lane * kFL + k] = (lane < nb && k <= lane) ? d[k] : 0.0;
+      __syncwarp();
+      // inverse of the diagonal block: lane c → column c (forward substitution)
+      double x[kFB];
+      const int c = lane;
+#pragma unroll
+      for (int r = 0; r < kFB; ++r) {
+        const double rr = __shfl_sync(0xffffffffu, rdl, r);
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < r; ++k) s = fma(P[r * kFL + k], (k >= c) ? x[k] : 0.0, s);
+        x[r] = (r < c || c >= nb || r >= nb) ? 0.0 : (r == c ? rr : -s * rr);
+      }
+#pragma unroll
+      for (int r = 0; r < kFB; ++r) {
+        Di[r * (kFB + 1) + c] = x[r];
+        Dinv[((size_t)(p0 / kFB) * kFB + r) * kFB + c] = x[r];
+      }
+    }
+    __syncthreads();
+    const long long tb_ = clock64();
+    // ---- panel below: L21 = A21 · Dinvᵀ in shared memory (warp per row, lane per column)
+    for (int i = nb + warp; i < rows; i += (blockDim.x >> 5)) {
+      double s = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < kFB; ++k) s = fma(P[i * kFL + k], (k <= lane) ? Di[lane * (kFB + 1) + k] : 0.0, s);
+      __syncwarp();
+      P[i * kFL + lane] = (lane < nb) ? s : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < rows * kFB; e += blockDim.x) {
+      const int r = e >> 5, c = e & 31;
+      if (c < nb) L[(long long)(p0 + r) * ldl + p0 + c] = (r >= c) ? P[r * kFL + c] : 0.0;
+    }
+    const long long tcc = clock64();
+    // ---- trailing update A22 −= L21 L21ᵀ (lower 8×8 blocks) on DMMA, 4 blocks per warp in flight
+    const int t0 = p0 + nb, tn = m - t0;
+    if (tn > 0) {
+      const int tb = (tn + 7) / 8;
+      const long long nblocks = (long long)tb * (tb + 1) / 2;
+      const int g = lane >> 2, t = lane & 3;
+      const int nw = blockDim.x >> 5;
+      for (long long base = (long long)warp * 4; base < nblocks; base += (long long)nw * 4) {
+        int gi[4], gj0[4];
+        double cv[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const long long b = base + u;
+          gi[u] = -1;
+          if (b < nblocks) {
+            int bi = (int)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+            while ((long long)(bi + 1) * (bi + 2) / 2 <= b) ++bi;
+            while ((long long)bi * (bi + 1) / 2 > b) --bi;
+            const int bj = (int)(b - (long long)bi * (bi + 1) / 2);
+            gi[u] = 8 * bi + g;
+            gj0[u] = 8 * bj + 2 * t;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int ii = t0 + gi[u], jj = t0 + gj0[u] + e;
+              cv[u][e] = (ii < m && jj < m && ii >= jj) ? L[(long long)ii * ldl + jj] : 0.0;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (gi[u] < 0) continue;
+          const int ra = nb + gi[u], rb = nb + (gj0[u] - 2 * t) + g;
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int k0 = 0; k0 < kFB; k0 += 4) {
+            const double a = (ra < rows) ? P[ra * kFL + k0 + t] : 0.0;
+            const double bb = (rb < rows) ? P[rb * kFL + k0 + t] : 0.0;
+            dmma_8x8x4(c0, c1, a, bb);
+          }
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int ii = t0 + gi[u], jj = t0 + gj0[u] + e;
+            if (ii < m && jj < m && ii >= jj) L[(long long)ii * ldl + jj] = cv[u][e] - (e ? c1 : c0);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const long long td = clock64();
+      g_chol_t[1] += tb_ - ta;
+      g_chol_t[2] += tcc - tb_;
+      g_chol_t[3] += td - tcc;
+    }
+  }
+  if (tid == 0) g_chol_t[0] += clock64() - tc0;
+  double dmin = INFINITY, dmax = 0.0;
+  for (int i = tid; i < m; i += blockDim.x) {
+    const double dd = L[(long long)i * ldl + i];
+    dmin = fmin(dmin, dd);
+    dmax = fmax(dmax, dd);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  }
+  __shared__ double rmin[32], rmax[32];
+  if (lane == 0) {
+    rmin[warp] = dmin;
+    rmax[warp] = dmax;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = INFINITY, b2 = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a = fmin(a, rmin[w]);
+      b2 = fmax(b2, rmax[w]);
+    }
+    status[0] = (double)info_s;
+    status[2] = a;
+    status[3] = b2;
+  }
+}
+
+// Block column j of X = L⁻¹ (rows ≥ j): X_jj = Dinv_j; X_ij = −Dinv_i Σ_{k=j}^{i−1} L_ik X_kj.
+// Writes Rinv[j-block rows][c] = X[c][j-block cols] (Rinv = Xᵀ), zero elsewhere.
+__global__ void __launch_bounds__(256) tri_inv_blocked_kernel(const double* __restrict__ L,
+                                                              long long ldl, int m,
+                                                              const double* __restrict__ Dinv,
+                                                              double* Rinv, long long ldr) {
+  extern __shared__ double xs[];   // nblk × 32 × 32 (X_kj for k ≥ j), then scratch 32×32
+  const int j = blockIdx.x;
+  const int nblk = (m + kFB - 1) / kFB;
+  const int tid = threadIdx.x;
+  double* S = xs + (size_t)nblk * kFB * kFB;   // scratch Z (32×32)
+  auto X = [&](int k) { return xs + (size_t)k * kFB * kFB; };
+  for (int e = tid; e < kFB * kFB; e += blockDim.x) X(j)[e] = Dinv[(size_t)j * kFB * kFB + e];
+  __syncthreads();
+  for (int i = j + 1; i < nblk; ++i) {
+    const int ri = i * kFB;
+    // Z = Σ_{k=j}^{i−1} L_ik X_kj   (32×32)
+    for (int e = tid; e < kFB * kFB; e += blockDim.x) {
+      const int r = e / kFB, c = e % kFB;
+      double s = 0.0;
+      if (ri + r < m) {
+        const double* lrow = L + (long long)(ri + r) * ldl;
+        for (int k = j; k < i; ++k) {
+          const double* xk = X(k);
+          const int kb = k * kFB;
+#pragma unroll 8
+          for (int q = 0; q < kFB; ++q) s = fma(lrow[kb + q], xk[q * kFB + c], s);
+        }
+      }
+      S[e] = s;
+    }
+    __syncthreads();
+    // X_ij = −Dinv_i · Z
+    const double* Di = Dinv + (size_t)i * kFB * kFB;
+    for (int e = tid; e < kFB * kFB; e += blockDim.x) {
+      const int r = e / kFB, c = e % kFB;
+      double s = 0.0;
+      for (int q = 0; q <= r; ++q) s = fma(Di[r * kFB + q], S[q * kFB + c], s);
+      X(i)[e] = -s;
+    }
+    __syncthreads();
+  }
+  // Rinv rows [j·32, …) = X[:, j-block]ᵀ
+  const int cj = j * kFB;
+  for (int e = tid; e < kFB * m; e += blockDim.x) {
+    const int c = e / m, row = e % m;   // Rinv[cj + c][row] = X[row][cj + c]
+    if (cj + c >= m) continue;
+    double v = 0.0;
+    if (row >= cj) {
+      const int k = row / kFB, q = row % kFB;
+      v = X(k)[q * kFB + c];
+    }
+    Rinv[(long long)(cj + c) * ldr + row] = v;
+  }
+}
+
+int chol_fast(const double* G, long long ldg, int m, double shift, double* L, long long ldl,
+              double* Rinv, long long ldr, double* Dinv, double* status, cudaStream_t st) {
+  const size_t smem1 = ((size_t)std::max(m, kFB) * kFL + kFB * (kFB + 1)) * sizeof(double);
+  const int nblk = (m + kFB - 1) / kFB;
+  const size_t smem2 = ((size_t)nblk + 1) * kFB * kFB * sizeof(double);
+  if (smem1 > device_info().max_smem - 4096 || smem2 > device_info().max_smem - 1024) return -1;
+  static size_t attr1[16] = {}, attr2[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem1 > attr1[dev]) {
+    cudaFuncSetAttribute(chol_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+    attr1[dev] = smem1;
+  }
+  if (smem2 > attr2[dev]) {
+    cudaFuncSetAttribute(tri_inv_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem2);
+    attr2[dev] = smem2;
+  }
+  chol_blocked_kernel<<<1, 256, smem1, st>>>(G, ldg, m, shift, L, ldl, Dinv, status);
+  count_launch();
+  tri_inv_blocked_kernel<<<nblk, 256, smem2, st>>>(L, ldl, m, Dinv, Rinv, ldr);
+  count_launch();
+  if (getenv("PSD_CHOL_TIMERS")) {
+    long long h[6];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_chol_t, sizeof(h));
+    fprintf(stderr, "chol m=%d cycles: total %lld diag %lld trsm+store %lld trailing %lld\n", m, h[0],
+            h[1], h[2], h[3]);
+  }
   return 0;
 }
 

@@ -95,6 +95,10 @@ void tri_inv_upper_from_lower(const double* l, long long ldl, int m, double* rin
 // status = {info, trace(G), min L_ii, max L_ii}.
 int chol_inv(const double* G, long long ldg, int m, double shift, double* L, long long ldl,
              double* Rinv, long long ldr, double* Xs, double* status, cudaStream_t st);
+// Faster two-launch variant (warp-register diagonal blocks + parallel block
+// inverse); dinv scratch: ceil(m/32)·32·32 doubles.  Same outputs as chol_inv.
+int chol_fast(const double* G, long long ldg, int m, double shift, double* L, long long ldl,
+              double* Rinv, long long ldr, double* Dinv, double* status, cudaStream_t st);
 // rdiag[i] *= L[i][i]
 void accumulate_diag(const double* l, long long ldl, int m, double* rdiag, cudaStream_t st);
 // Symmetric eigensolver (block Jacobi).  a (m×m, destroyed), values[m], v (m×m).
