@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the config-3 FP32 (3xTF32) leg")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     for key in ("n", "k", "p", "q"):
@@ -301,6 +302,10 @@ def run_ours(a):
     traffic = load_traffic()
     stages = {k: round(v[0] / a.steps, 3) for k, v in prof.items() if v[1]}
 
+    fp32 = None
+    if a.config == "c3" and not a.no_fp32:
+        fp32 = run_fp32_leg(a, torch, psd, pool, params, rng, dev, world)
+
     e2e = None
     if rank == 0 and not a.no_e2e:
         e2e = run_e2e(a, torch, psd, pool[0], params, dev)
@@ -346,6 +351,8 @@ def run_ours(a):
         line["cpu_baseline"] = cpu
     if e2e:
         line["e2e"] = e2e
+    if fp32:
+        line["fp32"] = fp32
     print(json.dumps(line), flush=True)
 
 
@@ -463,6 +470,54 @@ def run_sharded(a):
         "config": {"workload": f"BASELINE config 4: n={n}, k={a.k}, p={a.p}, q={a.q}, row-sharded x{world}",
                    "result": "dense row blocks" if want else "factored (W, d): X and X₊ do not fit one GPU"},
         "effective_rank": rep.effective_rank, "tflops": flops * value / 1e12}), flush=True)
+
+
+def run_fp32_leg(a, torch, psd, pool, params, rng, dev, world):
+    """BASELINE config 3 "fp32": the same projections on the fp32-rounded matrices
+    through the FP32 path (3xTF32 tcgen05 GEMMs, FP64 QR/eigh), timed like the
+    FP64 line (CUDA events, max over ranks)."""
+    import torch.distributed as dist
+    n = a.n
+    pool32 = [x.float() for x in pool]
+    plan = psd._native.get_plan(n, params.width, dev)
+    for i in range(max(a.warmup, 2)):
+        psd.ran_proj(pool32[i % len(pool32)], params, rng, dtype="fp32")
+    torch.cuda.synchronize(dev)
+    plan.profile(enable=True, reset=True)
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    e0.record()
+    for i in range(a.steps):
+        rep = psd.ran_proj(pool32[i % len(pool32)], params, rng, dtype="fp32")
+        launches += rep.device_info["gpu_launches"]
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    prof = plan.profile(enable=False, reset=True)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    g_ms, g_cnt = prof["sketch_gemm"]
+    gemm_ms = g_ms / max(g_cnt, 1)
+    eff_tf = 2.0 * n * n * params.width / (gemm_ms / 1000.0) / 1e12
+    del pool32
+    return {
+        "value": world * a.steps / (ms / 1000.0), "unit": UNIT, "ms_per_step": ms / a.steps,
+        "dtype": "f32 (3xTF32 tcgen05, FP32 TMEM accumulation in ≤4096-K chunks, FP64 QR/eigh)",
+        "gpu_launches": launches,
+        "stages_ms_per_projection": {k: round(v[0] / a.steps, 3) for k, v in prof.items() if v[1]},
+        "sketch_gemm": {
+            "ms_per_launch": gemm_ms,
+            "effective_tflops": eff_tf,
+            "tf32_tensor_tflops": 3.0 * eff_tf,
+            "note": "3 tf32 MMAs (lo·hi, hi·lo, hi·hi) per FP32 product; effective = 2n²w/t",
+        },
+        "parity": "≤1e-4 rel. Frobenius vs the FP64 path on the same fp32-rounded X (tests/test_gpu_fp32.py)",
+    }
 
 
 def run_e2e(a, torch, psd, x_dev, params, dev):

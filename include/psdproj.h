@@ -131,6 +131,23 @@ int psd_ran_proj(psd_plan* plan, const double* x, int64_t n, int64_t ldx, const 
                  double* result, int64_t ldr, double* factors_w, int64_t ldw, double* factors_d,
                  psd_report* report, void* stream);
 
+/* FP32 path of ran_proj / ran_proj_scal (BASELINE config 3 "fp32"; no
+ * reference counterpart — the reference casts to float64 at sketch.py:66).
+ * x, omega, result: fp32; every n x n product runs as 3xTF32 on the tcgen05
+ * tensor cores (TMEM accumulators), the power scheme is always
+ * re-orthonormalised, QR / eigh stay FP64.  Same flags and report as
+ * psd_ran_proj (PSD_FLAG_DIAGNOSTICS is ignored: residual_frob = NaN). */
+int psd_ran_proj_f32(psd_plan* plan, const float* x, int64_t n, int64_t ldx, const float* omega,
+                     int64_t ldo, int32_t k, int32_t l, int32_t q, double alpha, uint32_t flags,
+                     float* result, int64_t ldr, double* factors_w, int64_t ldw, double* factors_d,
+                     psd_report* report, void* stream);
+
+/* The 3xTF32 tcgen05 GEMM itself (test entry; allocates its own scratch):
+ * mode 0: C (fp64, m x n) = A · B^T; mode 1: mirrored fp32 C (m == n) from
+ * the lower tiles of A · B^T.  A m x k, B n x k, fp32 row-major. */
+int psd_gemm_tf32x3(int32_t mode, const float* a, int64_t lda, const float* b, int64_t ldb,
+                    int64_t m, int64_t n, int64_t k, void* c, int64_t ldc, void* stream);
+
 /* Dense X = sym(W diag(d) W^T) for W n x r (ld ldw), d[r] — the reconstruction
  * of projection.py:72-78 (and of exact_psd_projection, symmetric.py:109-114):
  * lower tiles on the FP64 tensor cores, each tile stored twice (mirrored). */

@@ -31,7 +31,7 @@ class Operand:
 
 
 def as_device(x, device=None, dtype=torch.float64):
-    """Upload / view ``x`` as a contiguous float64 CUDA tensor (np.asarray(x, float) semantics)."""
+    """Upload / view ``x`` as a contiguous CUDA tensor of ``dtype`` (np.asarray(x, float) semantics)."""
     _native.require_cuda()
     if isinstance(x, torch.Tensor):
         kind = "torch_cuda" if x.is_cuda else "torch_cpu"
@@ -40,7 +40,7 @@ def as_device(x, device=None, dtype=torch.float64):
         if not t.is_contiguous():
             t = t.contiguous()
         return Operand(t, kind, dev)
-    a = np.ascontiguousarray(np.asarray(x, dtype=float))
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float32 if dtype == torch.float32 else float))
     dev = torch.device(device) if device else default_device()
     t = torch.from_numpy(a)
     if t.numel() > (1 << 20):

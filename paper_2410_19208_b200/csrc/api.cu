@@ -8,7 +8,9 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -40,6 +42,10 @@ struct psd_plan {
   int gparts = 0;
   double* rpart = nullptr;
   ll rparts = 0;
+  // FP32 path (ensure_f32)
+  float *xh = nullptr, *xl = nullptr, *f[4] = {}, *ws32 = nullptr;
+  ll ldx32 = 0;
+  size_t ws32_elems = 0;
   std::vector<void*> allocs;
   size_t bytes = 0;
   // stage profiling (psd_plan_profile): CUDA events on the caller's stream
@@ -369,23 +375,26 @@ int symcheck(psd_plan* p, const double* x, ll n, ll ldx, SymInfo* si, cudaStream
 // Range finder core (sketch.py:53-93).  Returns index of the buffer holding
 // the basis (columns compacted to *width_out).  bufs: 3 panel buffers.
 // X is m×n (m == n for the projections); Ω is n×w; the basis is m×w.
-int range_finder_core(psd_plan* p, const double* x, ll m, ll n, ll ldx, const double* omega,
-                      ll ldo, int w, int q, double alpha, bool use_t, bool strict, double** bufs,
-                      int* qidx, int* width_out, QrInfo* qi, cudaStream_t st) {
+// op(X)·P for an n×w panel P: transpose=true asks for Xᵀ·P (sketch.py:79).
+using MulFn = std::function<int(const double* P, ll ldP, int w, double* out, ll ldo, bool transpose)>;
+
+int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* omega, ll ldo, int w,
+                      int q, bool always_stabilize, bool strict, double** bufs, int* qidx,
+                      int* width_out, QrInfo* qi, cudaStream_t st) {
   const ll ld = p->ldp;
-  const bool stabilize = q >= 2;                                   // sketch.py:74
+  const bool stabilize = q >= 2 || always_stabilize;               // sketch.py:74
   int y = 0;
-  PSD_TRY(xmul_rect(p, x, m, n, ldx, omega, ldo, w, bufs[0], ld, alpha, false, st));  // :75
+  PSD_TRY(mul(omega, ldo, w, bufs[0], ld, false));                 // :75
   for (int it = 0; it < q; ++it) {                                 // :76-82
     QrInfo tmp;
     if (stabilize) PSD_TRY(cholqr(p, bufs, y, (y + 1) % 3, m, w, nullptr, &y, &tmp, st, true));
     const int z = (y + 1) % 3;
     // z = xᵀ @ y (sketch.py:79); for bitwise-symmetric X this equals X·Y exactly
-    PSD_TRY(xmul_rect(p, x, m, n, ldx, bufs[y], ld, w, bufs[z], ld, alpha, use_t, st));
+    PSD_TRY(mul(bufs[y], ld, w, bufs[z], ld, true));
     int zq = z;
     if (stabilize) PSD_TRY(cholqr(p, bufs, z, (z + 1) % 3, n, w, nullptr, &zq, &tmp, st, true));
     const int ny = (zq + 1) % 3;
-    PSD_TRY(xmul_rect(p, x, m, n, ldx, bufs[zq], ld, w, bufs[ny], ld, alpha, false, st));
+    PSD_TRY(mul(bufs[zq], ld, w, bufs[ny], ld, false));
     y = ny;
   }
   n = m;  // the final QR and gather act on the m×w sample
@@ -586,7 +595,10 @@ int psd_range_finder(psd_plan* p, const double* x, int64_t m, int64_t n, int64_t
   double* bufs[3] = {p->panel[0], p->panel[1], p->panel[2]};
   int qb = 0, wk = 0;
   QrInfo qi;
-  PSD_TRY(range_finder_core(p, x, m, n, ldx, omega, ldo, width, q, alpha, use_t,
+  const MulFn mul = [&](const double* P, ll ldP, int w, double* out, ll ldo2, bool t) {
+    return xmul_rect(p, x, m, n, ldx, P, ldP, w, out, ldo2, alpha, t && use_t, st);
+  };
+  PSD_TRY(range_finder_core(p, mul, m, n, omega, ldo, width, q, false,
                             (flags & PSD_FLAG_STRICT) != 0, bufs, &qb, &wk, &qi, st));
   if (wk > 0) {
     psd::copy_matrix(bufs[qb], p->ldp, basis, ldb, m, wk, st);
@@ -610,11 +622,92 @@ int psd_eigh(psd_plan* p, double* a, int32_t m, int64_t lda, double* values, dou
   return sync(st, "eigh");
 }
 
-static int ran_proj_impl(psd_plan* p, const double* x, int64_t n, int64_t ldx,
-                         const double* omega, int64_t ldo, int32_t k, int32_t l, int32_t q,
-                         double alpha, uint32_t flags, double* result, int64_t ldr,
-                         double* factors_w, int64_t ldw, double* factors_d, psd_report* rep,
-                         void* stream) {
+}  // extern "C"
+
+namespace {
+
+// FP32 path buffers (allocated on first use): tf32 hi/lo of X, four operand
+// scratch buffers (transposed panels / reconstruction factors), split-K partials.
+int ensure_f32(psd_plan* p, bool need_hi) {
+  if (need_hi && !p->xh) {
+    const size_t xsz = (size_t)p->n * ((p->n + 31) / 32 * 32);
+    p->xh = reinterpret_cast<float*>(alloc(p, (xsz + 1) / 2));
+    if (!p->xh) return fail(PSD_ERR_NO_MEMORY, "device allocation failed for the FP32 hi buffer");
+  }
+  if (p->xl) return PSD_OK;
+  const ll ld = (p->n + 31) / 32 * 32;
+  const ll wp = (p->w + 15) / 16 * 16;
+  const size_t xsz = (size_t)p->n * ld;
+  const size_t fsz = (size_t)std::max(wp * ld, p->n * wp);
+  const size_t wsz = (size_t)psd::tc32_ws_elems(p->n, p->w, 32);
+  auto falloc = [&](size_t elems) { return reinterpret_cast<float*>(alloc(p, (elems + 1) / 2)); };
+  bool ok = (p->xl = falloc(xsz)) != nullptr;
+  for (int i = 0; i < 4; ++i) ok &= (p->f[i] = falloc(fsz)) != nullptr;
+  ok &= (p->ws32 = falloc(wsz)) != nullptr;
+  if (!ok) return fail(PSD_ERR_NO_MEMORY, "device allocation failed for the FP32 buffers (n=%lld)", p->n);
+  p->ldx32 = ld;
+  p->ws32_elems = wsz;
+  return PSD_OK;
+}
+
+// X·P on the 3xTF32 tensor-core path: P (fp64 n×w) → tf32 hi/lo, transposed
+// to the K-major B operand; fp32 partials reduced into the fp64 panel `out`.
+int xmul_tc32(psd_plan* p, ll n, const float* xhi, ll ldhi, const double* P, ll ldP, int w,
+              double* out, ll ldo, double alpha, cudaStream_t st) {
+  Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
+  psd::split_transpose(P, n, w, ldP, p->f[0], p->f[1], p->ldx32, w, st);
+  psd::Tc32Op op;
+  op.a_hi = xhi;
+  op.a_lo = p->xl;
+  op.lda = ldhi;
+  op.lda_lo = p->ldx32;
+  op.b_hi = p->f[0];
+  op.b_lo = p->f[1];
+  op.ldb = p->ldx32;
+  op.M = (int)n;
+  op.N = w;
+  op.K = (int)n;
+  op.mode = 0;
+  op.c64 = out;
+  op.ldc64 = ldo;
+  op.alpha = alpha;
+  op.S = P;
+  op.lds = ldP;
+  op.ws = p->ws32;
+  op.ws_elems = p->ws32_elems;
+  const int r = psd::gemm_tf32x3(op, st);
+  if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "3xTF32 GEMM rejected its operands (%d)", r);
+  return PSD_OK;
+}
+
+// require_symmetric on the fp32 X fused with its tf32 split (one HBM pass);
+// raw: X itself is the hi operand and only lo is written.
+int symcheck32(psd_plan* p, const float* x, ll n, ll ldx, bool raw, SymInfo* si, cudaStream_t st) {
+  {
+    Stage mark(p, PSD_STAGE_SYMCHECK, st);
+    psd::symsplit_f32(x, n, ldx, p->stats, raw ? nullptr : p->xh, p->xl, p->ldx32, st);
+  }
+  double h[3];
+  PSD_CUDA_CHECK(cudaMemcpyAsync(h, p->stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st),
+                 "stats");
+  PSD_TRY(sync(st, "symmetry check"));
+  int flags = 0;
+  std::memcpy(&flags, &h[2], sizeof(int));
+  si->max_abs = h[0];
+  si->defect = h[1];
+  si->bitwise = (flags & 1) == 0;
+  si->nonfinite = (flags & 2) != 0;
+  return PSD_OK;
+}
+
+// x64 (FP64 path) or x32 (FP32 path: 3xTF32 tensor-core GEMMs, FP64 QR/eigh,
+// power-scheme multiplies always re-orthonormalised — SURVEY §7 step 8).
+static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64_t n, int64_t ldx,
+                         const double* omega64, const float* omega32, int64_t ldo, int32_t k,
+                         int32_t l, int32_t q, double alpha, uint32_t flags, double* result64,
+                         float* result32, int64_t ldr, double* factors_w, int64_t ldw,
+                         double* factors_d, psd_report* rep, void* stream) {
+  const bool f32 = x32 != nullptr;
   if (k < 1) return fail(PSD_ERR_INVALID_PARAMS, "target rank k must be >= 1, got %d", k);
   if (l < 0) return fail(PSD_ERR_INVALID_PARAMS, "oversampling l must be >= 0, got %d", l);
   if (q < 0) return fail(PSD_ERR_INVALID_PARAMS, "power exponent q must be >= 0, got %d", q);
@@ -628,15 +721,22 @@ static int ran_proj_impl(psd_plan* p, const double* x, int64_t n, int64_t ldx,
   psd_report r{};
   r.residual_frob = NAN;
   r.alpha_used = alpha;
+  const bool have_result = f32 ? result32 != nullptr : result64 != nullptr;
 
   // require_symmetric (projection.py:100 / :132) + alpha_tol (projection.py:133-137)
   // With PSD_FLAG_SKIP_SYMCHECK the caller has run require_symmetric and the
   // alpha_tol test itself and tells us via PSD_FLAG_ASSUME_SYMMETRIC whether
   // X is bitwise symmetric (then Xᵀ·P == X·P exactly).
   bool use_t = !(flags & PSD_FLAG_ASSUME_SYMMETRIC);
+  // FP32: X itself is the tf32 "hi" operand when its rows are TMA-addressable
+  const bool raw = f32 && ldx % 4 == 0 && (uintptr_t)x32 % 16 == 0 && !getenv("PSD_TF32_RNA");
+  if (f32) PSD_TRY(ensure_f32(p, !raw));
+  const float* xhi = raw ? x32 : p->xh;
+  const ll ldhi = raw ? ldx : p->ldx32;
   if (!(flags & PSD_FLAG_SKIP_SYMCHECK)) {
     SymInfo si;
-    PSD_TRY(symcheck(p, x, n, ldx, &si, st));
+    if (f32) PSD_TRY(symcheck32(p, x32, n, ldx, raw, &si, st));
+    else PSD_TRY(symcheck(p, x64, n, ldx, &si, st));
     r.max_abs = si.max_abs;
     r.sym_defect = si.defect;
     if (si.nonfinite) return fail(PSD_ERR_CONVERGENCE, "matrix has non-finite entries");
@@ -655,21 +755,40 @@ static int ran_proj_impl(psd_plan* p, const double* x, int64_t n, int64_t ldx,
     use_t = use_t && !si.bitwise;
   }
   if (w > n) return fail(PSD_ERR_INVALID_PARAMS, "k+l = %d exceeds min(m, n) = %lld", w, (ll)n);
+  // FP32: Xᵀ·P is taken as X·P — X passed the 1e-10·max|X| symmetry test, far
+  // below the path's 1e-4 tolerance.
+  if (f32) use_t = false;
   r.used_transpose = use_t ? 1 : 0;
 
   const ll ld = p->ldp;
   double* bufs[3] = {p->panel[0], p->panel[1], p->panel[2]};
+  const double* omega = omega64;
+  ll ldo_eff = ldo;
+  if (f32) {
+    if (flags & PSD_FLAG_SKIP_SYMCHECK)
+      psd::split_rows_f32(x32, n, n, ldx, raw ? nullptr : p->xh, p->xl, p->ldx32, n, st);
+    // Ω (fp32) → fp64 panel in the Gram/Cholesky workspace-free buffer panel[3]
+    psd::convert_f32_f64(omega32, ldo, p->panel[3], ld, n, w, st);
+    omega = p->panel[3];
+    ldo_eff = ld;
+  }
+  const MulFn mul = [&](const double* P, ll ldP, int ww, double* out, ll ldo2, bool t) {
+    if (f32) return xmul_tc32(p, n, xhi, ldhi, P, ldP, ww, out, ldo2, alpha, st);
+    return xmul(p, x64, n, ldx, P, ldP, ww, out, ldo2, alpha, t && use_t, st);
+  };
   int qb = 0, wk = 0;
   QrInfo qi;
-  PSD_TRY(range_finder_core(p, x, n, n, ldx, omega, ldo, w, q, alpha, use_t,
-                            (flags & PSD_FLAG_STRICT) != 0, bufs, &qb, &wk, &qi, st));
+  PSD_TRY(range_finder_core(p, mul, n, n, omega, ldo_eff, w, q, f32, (flags & PSD_FLAG_STRICT) != 0,
+                            bufs, &qb, &wk, &qi, st));
   r.qr_passes = qi.passes;
   r.qr_shifted = qi.shifted;
   r.basis_width = wk;
+  auto zero_result = [&]() {
+    if (f32) cudaMemset2DAsync(result32, ldr * sizeof(float), 0, n * sizeof(float), n, st);
+    else psd::fill_zero(result64, ldr, n, n, st);
+  };
   if (wk == 0) {  // _zero_report (projection.py:81-89)
-    if (result) {
-      psd::fill_zero(result, ldr, n, n, st);
-    }
+    if (have_result) zero_result();
     r.effective_rank = 0;
     r.gpu_launches = psd::g_launch_count;
     if (rep) *rep = r;
@@ -681,7 +800,7 @@ static int ran_proj_impl(psd_plan* p, const double* x, int64_t n, int64_t ldx,
   double* WD = p->panel[5];
 
   // compression T = sym(Qᵀ X Q) or sym(Qᵀ B Q)  (projection.py:104 / :143)
-  PSD_TRY(xmul(p, x, n, ldx, Q, ld, wk, C, ld, alpha, false, st));
+  PSD_TRY(mul(Q, ld, wk, C, ld, false));
   {
     Stage mark(p, PSD_STAGE_COMPRESS, st);
     PSD_TRY(panel_tn(p, Q, C, ld, n, wk, p->T, true, st));
@@ -709,7 +828,26 @@ static int ran_proj_impl(psd_plan* p, const double* x, int64_t n, int64_t ldx,
   if (npos > 0) {
     // W = Q·U₊ ; WD = W·diag(d) ; X̂₊ = WD·Wᵀ on lower tiles, mirrored
     PSD_TRY(panel_nn(p, Q, ld, p->U, wk, W, ld, n, wk, npos, st));
-    if (result) {
+    if (have_result && f32) {
+      const int rp = (npos + 15) / 16 * 16;
+      psd::split_rows_f64(W, n, npos, ld, p->dvec, p->f[0], p->f[1], rp, rp, st);
+      psd::split_rows_f64(W, n, npos, ld, nullptr, p->f[2], p->f[3], rp, rp, st);
+      psd::Tc32Op op;
+      op.a_hi = p->f[0];
+      op.a_lo = p->f[1];
+      op.lda = rp;
+      op.b_hi = p->f[2];
+      op.b_lo = p->f[3];
+      op.ldb = rp;
+      op.M = (int)n;
+      op.N = (int)n;
+      op.K = npos;
+      op.mode = 1;
+      op.c32 = result32;
+      op.ldc32 = ldr;
+      const int rr = psd::gemm_tf32x3(op, st);
+      if (rr < 0) return fail(PSD_ERR_INVALID_PARAMS, "3xTF32 reconstruction rejected its operands (%d)", rr);
+    } else if (have_result) {
       psd::scale_columns(W, ld, p->dvec, WD, ld, n, npos, st);
       psd::GemmOp op;
       op.a_layout = psd::A_MK;
@@ -718,7 +856,7 @@ static int ran_proj_impl(psd_plan* p, const double* x, int64_t n, int64_t ldx,
       op.lda = ld;
       op.B = W;
       op.ldb = ld;
-      op.C = result;
+      op.C = result64;
       op.ldc = ldr;
       op.M = (int)n;
       op.N = (int)n;
@@ -735,14 +873,14 @@ static int ran_proj_impl(psd_plan* p, const double* x, int64_t n, int64_t ldx,
                                      cudaMemcpyDeviceToDevice, st),
                      "factors d");
     }
-  } else if (result) {
-    psd::fill_zero(result, ldr, n, n, st);
+  } else if (have_result) {
+    zero_result();
   }
   recon_mark.close();
-  if (flags & PSD_FLAG_DIAGNOSTICS) {
+  if ((flags & PSD_FLAG_DIAGNOSTICS) && !f32) {
     Stage diag_mark(p, PSD_STAGE_DIAG, st);
     // ‖X − Q(QᵀX)‖_F with QᵀX = (XᵀQ)ᵀ (projection.py:110)
-    PSD_TRY(xmul(p, x, n, ldx, Q, ld, wk, C, ld, 0.0, use_t, st));
+    PSD_TRY(xmul(p, x64, n, ldx, Q, ld, wk, C, ld, 0.0, use_t, st));
     psd::GemmOp op;
     op.a_layout = psd::A_MK;
     op.b_layout = psd::B_NK;
@@ -755,7 +893,7 @@ static int ran_proj_impl(psd_plan* p, const double* x, int64_t n, int64_t ldx,
     op.N = (int)n;
     op.K = wk;
     op.epi = psd::EPI_RESID;
-    op.S = x;
+    op.S = x64;
     op.lds = ldx;
     op.partials = p->rpart;
     op.max_splits = 1;
@@ -773,6 +911,10 @@ static int ran_proj_impl(psd_plan* p, const double* x, int64_t n, int64_t ldx,
   return PSD_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
 int psd_ran_proj(psd_plan* p, const double* x, int64_t n, int64_t ldx, const double* omega,
                  int64_t ldo, int32_t k, int32_t l, int32_t q, double alpha, uint32_t flags,
                  double* result, int64_t ldr, double* factors_w, int64_t ldw, double* factors_d,
@@ -783,13 +925,83 @@ int psd_ran_proj(psd_plan* p, const double* x, int64_t n, int64_t ldx, const dou
   int status;
   {
     Stage total(p, PSD_STAGE_TOTAL, st);
-    status = ran_proj_impl(p, x, n, ldx, omega, ldo, k, l, q, alpha, flags, result, ldr,
-                           factors_w, ldw, factors_d, rep, stream);
+    status = ran_proj_impl(p, x, nullptr, n, ldx, omega, nullptr, ldo, k, l, q, alpha, flags, result,
+                           nullptr, ldr, factors_w, ldw, factors_d, rep, stream);
   }
   if (p->prof) {
     cudaStreamSynchronize(st);
     collect_marks(p);
   }
+  return status;
+}
+
+int psd_ran_proj_f32(psd_plan* p, const float* x, int64_t n, int64_t ldx, const float* omega,
+                     int64_t ldo, int32_t k, int32_t l, int32_t q, double alpha, uint32_t flags,
+                     float* result, int64_t ldr, double* factors_w, int64_t ldw, double* factors_d,
+                     psd_report* rep, void* stream) {
+  if (!p || !x || !omega) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  DeviceGuard g(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int status;
+  {
+    Stage total(p, PSD_STAGE_TOTAL, st);
+    status = ran_proj_impl(p, nullptr, x, n, ldx, nullptr, omega, ldo, k, l, q, alpha, flags, nullptr,
+                           result, ldr, factors_w, ldw, factors_d, rep, stream);
+  }
+  if (p->prof) {
+    cudaStreamSynchronize(st);
+    collect_marks(p);
+  }
+  return status;
+}
+
+int psd_gemm_tf32x3(int32_t mode, const float* a, int64_t lda, const float* b, int64_t ldb,
+                    int64_t m, int64_t nn, int64_t kk, void* c, int64_t ldc, void* stream) {
+  if (!a || !b || !c) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  if (m < 1 || nn < 1 || kk < 1 || (mode != 0 && mode != 1) || (mode == 1 && m != nn))
+    return fail(PSD_ERR_INVALID_PARAMS, "bad tf32x3 GEMM shape/mode");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const ll ldk = (kk + 31) / 32 * 32;
+  float *ah = nullptr, *al = nullptr, *bh = nullptr, *bl = nullptr, *ws = nullptr;
+  const size_t wsz = mode == 0 ? (size_t)psd::tc32_ws_elems(m, (int)nn, std::max<int>(8, (int)((kk + 4095) / 4096))) : 0;
+  bool ok = cudaMalloc(&ah, (size_t)m * ldk * 4) == cudaSuccess &&
+            cudaMalloc(&al, (size_t)m * ldk * 4) == cudaSuccess &&
+            cudaMalloc(&bh, (size_t)nn * ldk * 4) == cudaSuccess &&
+            cudaMalloc(&bl, (size_t)nn * ldk * 4) == cudaSuccess &&
+            (wsz == 0 || cudaMalloc(&ws, wsz * 4) == cudaSuccess);
+  int status = PSD_OK;
+  if (!ok) {
+    status = fail(PSD_ERR_NO_MEMORY, "tf32x3 scratch allocation failed");
+  } else {
+    psd::split_rows_f32(a, m, kk, lda, ah, al, ldk, ldk, st);
+    psd::split_rows_f32(b, nn, kk, ldb, bh, bl, ldk, ldk, st);
+    psd::Tc32Op op;
+    op.a_hi = ah;
+    op.a_lo = al;
+    op.lda = ldk;
+    op.b_hi = bh;
+    op.b_lo = bl;
+    op.ldb = ldk;
+    op.M = (int)m;
+    op.N = (int)nn;
+    op.K = (int)kk;
+    op.mode = mode;
+    op.c64 = static_cast<double*>(c);
+    op.ldc64 = ldc;
+    op.c32 = static_cast<float*>(c);
+    op.ldc32 = ldc;
+    op.ws = ws;
+    op.ws_elems = wsz;
+    const int r = psd::gemm_tf32x3(op, st);
+    if (r < 0) status = fail(PSD_ERR_INVALID_PARAMS, "3xTF32 GEMM rejected its operands (%d)", r);
+    if (status == PSD_OK) status = sync(st, "tf32x3 gemm");
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(ah);
+  cudaFree(al);
+  cudaFree(bh);
+  cudaFree(bl);
+  cudaFree(ws);
   return status;
 }
 

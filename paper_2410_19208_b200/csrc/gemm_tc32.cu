@@ -1,0 +1,607 @@
+// 3xTF32 tcgen05 GEMM (see gemm_tc32.cuh) + the tf32 hi/lo split kernels and
+// the split-K reduction that feeds FP64 panels.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+#include "gemm_tc32.cuh"
+#include "launch.h"
+
+namespace psd {
+namespace tc32 {
+
+// ---- tcgen05 / TMEM wrappers ----------------------------------------------
+PSD_DEVINL uint64_t smem_desc(uint32_t saddr) {
+  // K-major, SWIZZLE_64B canonical layout: 8-row atoms of 64-byte rows (512 B),
+  // SBO = stride between atoms, LBO unused for swizzled K-major, version 1 (sm_100).
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((8 * SWZ) >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(SWZ == 128 ? 2 : (SWZ == 64 ? 4 : 6)) << 61;
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = n.
+__host__ __device__ inline uint32_t instr_desc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+PSD_DEVINL void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+PSD_DEVINL void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+               : "memory");
+}
+PSD_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+PSD_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+PSD_DEVINL void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+PSD_DEVINL uint32_t tmem_cols_for(int n) {
+  uint32_t c = 32;
+  while ((int)c < n) c <<= 1;
+  return c;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    tc32_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
+                     const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], acc_bar;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bn_tot = p.bn * p.n_mma;
+  int u = blockIdx.x;
+  const int ng = u % p.n_groups;
+  u /= p.n_groups;
+  const int split = u % p.splits;
+  const int mt = u / p.splits;
+  const int m0 = mt * BM, n0 = ng * bn_tot;
+  // MIRROR keeps only tiles holding some (i, j) with i ≥ j
+  if (p.mode == MIRROR && m0 + BM - 1 < n0) return;
+  const int kb0 = split * p.kb_per_split;
+  const int nkb = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
+
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  const uint32_t a_bytes = BM * SWZ, b_bytes = (uint32_t)bn_tot * SWZ;
+  const uint32_t st_bytes = 2 * a_bytes + 2 * b_bytes;
+  const uint32_t tcols = tmem_cols_for(bn_tot);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    mbar_init(smem_u32(&acc_bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tma_prefetch_desc(&mAh);
+    tma_prefetch_desc(&mAl);
+    tma_prefetch_desc(&mBh);
+    tma_prefetch_desc(&mBl);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "r"(tcols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % p.stages;
+        const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+        mbar_wait(smem_u32(&empty_bar[s]), ph ^ 1u);
+        const uint32_t fb = smem_u32(&full_bar[s]);
+        mbar_expect_tx(fb, st_bytes);
+        const uint32_t sA = sbase + s * st_bytes;
+        const uint32_t sB = sA + 2 * a_bytes;
+        const int kc = (kb0 + i) * BK;
+        tma_load_2d(sA, &mAh, kc, m0, fb);
+        tma_load_2d(sA + a_bytes, &mAl, kc, m0, fb);
+        for (int h = 0; h < p.n_mma; ++h) {
+          const uint32_t off = (uint32_t)h * p.bn * SWZ;
+          tma_load_2d(sB + off, &mBh, kc, n0 + h * p.bn, fb);
+          tma_load_2d(sB + b_bytes + off, &mBl, kc, n0 + h * p.bn, fb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = instr_desc(p.bn);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % p.stages;
+        const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+        mbar_wait(smem_u32(&full_bar[s]), ph);
+        tc_fence_after();
+        const uint32_t sA = sbase + s * st_bytes;
+        const uint32_t sB = sA + 2 * a_bytes;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t ah = smem_desc(sA + kk * 32), al = smem_desc(sA + a_bytes + kk * 32);
+          for (int h = 0; h < p.n_mma; ++h) {
+            const uint32_t off = (uint32_t)h * p.bn * SWZ + kk * 32;
+            const uint64_t bh = smem_desc(sB + off), bl = smem_desc(sB + b_bytes + off);
+            const uint32_t d = tmem + (uint32_t)(h * p.bn);
+            mma_tf32(d, al, bh, idesc, (i | kk) != 0);   // small terms first
+            mma_tf32(d, ah, bl, idesc, 1u);
+            mma_tf32(d, ah, bh, idesc, 1u);
+          }
+        }
+        mma_commit(smem_u32(&empty_bar[s]));   // slot free once these MMAs retire
+      }
+      mma_commit(smem_u32(&acc_bar));          // accumulator complete
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes 32·(w mod 4) …
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int i = m0 + r;
+    mbar_wait(smem_u32(&acc_bar), 0);
+    tc_fence_after();
+    const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
+    if (p.mode == PARTIAL) {
+      for (int c0 = 0; c0 < bn_tot; c0 += 16) {
+        float v[16];
+        tmem_ld16(trow + (uint32_t)c0, v);
+        if (i >= p.M) continue;
+        float4* dst = reinterpret_cast<float4*>(p.out + (long long)split * p.split_stride +
+                                                (long long)i * p.ldo + n0 + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+    } else {
+      // MIRROR: 32×32 blocks; C[j][i] straight from registers (lanes = consecutive i),
+      // C[i][j] through a per-warp smem transpose so each store is one 128-B row.
+      float* tile = reinterpret_cast<float*>(smem_raw + (sbase - sraw) + p.stages * st_bytes) +
+                    (warp - 2) * 32 * 33;
+      const int ib = m0 + quad * 32;
+      for (int c0 = 0; c0 < bn_tot; c0 += 32) {
+        const int j0 = n0 + c0;
+        if (j0 >= p.N || j0 > ib + 31) break;          // block entirely above the diagonal / outside
+        float v[32];
+        tmem_ld16(trow + (uint32_t)c0, *reinterpret_cast<float(*)[16]>(&v[0]));
+        tmem_ld16(trow + (uint32_t)c0 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int j = j0 + e;
+          if (i < p.M && j <= i && j < p.N) p.out[(long long)j * p.ldo + i] = v[e];
+          tile[lane * 33 + e] = v[e];
+        }
+        __syncwarp();
+        const int j = j0 + lane;
+        for (int rr = 0; rr < 32; ++rr) {
+          const int ii = ib + rr;
+          if (ii < p.M && j <= ii && j < p.N) p.out[(long long)ii * p.ldo + j] = tile[rr * 33 + lane];
+        }
+        __syncwarp();
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tcols)
+                 : "memory");
+  }
+}
+
+// ---- split / convert kernels ----------------------------------------------
+PSD_DEVINL float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r & 0xFFFFE000u);
+}
+// raw mode: hi = x itself — kind::tf32 ignores the low 13 mantissa bits, i.e.
+// reads trunc(x) (verified on B200: tools/probe_rawhi.py) — and lo = x − trunc(x),
+// exact in fp32; the hi array then never has to be written.
+PSD_DEVINL void split_f32(float x, bool raw, float& hi, float& lo) {
+  if (raw) {
+    hi = x;
+    lo = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  } else {
+    hi = tf32_rna(x);
+    lo = tf32_rna(x - hi);
+  }
+}
+PSD_DEVINL void split2(double x, float& hi, float& lo) {
+  hi = tf32_rna((float)x);
+  lo = tf32_rna((float)(x - (double)hi));
+}
+
+// hi/lo (rows × cols_pad, ld ldh) of a row-major fp32 matrix; columns ≥ cols zero.
+__global__ void split_rows_f32_kernel(const float* __restrict__ x, long long rows, long long cols,
+                                      long long ldx, float* __restrict__ hi, float* __restrict__ lo,
+                                      long long ldh, long long cols_pad, bool raw) {
+  const long long total = rows * cols_pad;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cols_pad, c = e % cols_pad;
+    const float v = c < cols ? x[r * ldx + c] : 0.f;
+    float h, l;
+    split_f32(v, raw, h, l);
+    if (!raw) hi[r * ldh + c] = h;
+    lo[r * ldh + c] = l;
+  }
+}
+// vectorised variant: cols % 4 == 0 == ldx % 4 == ldh % 4, 16-B aligned
+__global__ void split_rows_f32x4_kernel(const float4* __restrict__ x, long long rows, long long cols4,
+                                        long long ldx4, float4* __restrict__ hi,
+                                        float4* __restrict__ lo, long long ldh4, bool raw) {
+  const long long total = rows * cols4;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cols4, c = e % cols4;
+    const float4 v = x[r * ldx4 + c];
+    float4 h, l;
+    split_f32(v.x, raw, h.x, l.x);
+    split_f32(v.y, raw, h.y, l.y);
+    split_f32(v.z, raw, h.z, l.z);
+    split_f32(v.w, raw, h.w, l.w);
+    if (!raw) hi[r * ldh4 + c] = h;
+    lo[r * ldh4 + c] = l;
+  }
+}
+
+// hi/lo of (x · diag(scale)) for a row-major fp64 rows × cols matrix, padded to cols_pad.
+__global__ void split_rows_f64_kernel(const double* __restrict__ x, long long rows, int cols,
+                                      long long ldx, const double* __restrict__ scale,
+                                      float* __restrict__ hi, float* __restrict__ lo, long long ldh,
+                                      int cols_pad) {
+  const long long total = rows * cols_pad;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cols_pad;
+    const int c = (int)(e % cols_pad);
+    double v = 0.0;
+    if (c < cols) v = x[r * ldx + c] * (scale ? scale[c] : 1.0);
+    float h, l;
+    split2(v, h, l);
+    hi[r * ldh + c] = h;
+    lo[r * ldh + c] = l;
+  }
+}
+
+// Transposed split of an n × w fp64 panel: out[j][i] (j < w_rows; zero rows j ≥ w).
+__global__ void split_transpose_kernel(const double* __restrict__ P, long long n, int w, long long ldp,
+                                       float* __restrict__ hi, float* __restrict__ lo, long long ldt,
+                                       int w_rows) {
+  __shared__ double tile[32][33];
+  const long long i0 = (long long)blockIdx.x * 32;
+  const int j0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 × 8
+  for (int yy = ty; yy < 32; yy += 8) {
+    const long long i = i0 + yy;
+    const int j = j0 + tx;
+    tile[yy][tx] = (i < n && j < w) ? P[i * ldp + j] : 0.0;
+  }
+  __syncthreads();
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int j = j0 + yy;
+    const long long i = i0 + tx;
+    if (j < w_rows && i < n) {
+      float h, l;
+      split2(tile[tx][yy], h, l);
+      hi[(long long)j * ldt + i] = h;
+      lo[(long long)j * ldt + i] = l;
+    }
+  }
+}
+
+// require_symmetric statistics (symmetric.py:39-57) fused with the tf32 hi/lo
+// split of a square fp32 X: one 64×64 tile pair (I ≥ J) per iteration, tile
+// (J, I) staged through shared memory, so X is read from HBM exactly once.
+// stats[0] = max|x|, stats[1] = max|x − xᵀ|, ((int*)(stats+2))[0] bit0: not
+// bitwise symmetric, bit1: non-finite entry.
+constexpr int kSST = 64;
+__global__ void __launch_bounds__(256) symsplit_kernel(const float* __restrict__ x, long long n,
+                                                       long long ldx, long long npairs,
+                                                       double* stats, float* __restrict__ hi,
+                                                       float* __restrict__ lo, long long ldh, bool raw) {
+  __shared__ float tb[kSST][kSST + 1];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  float mabs = 0.f;
+  double mdef = 0.0;
+  int flags = 0;
+  for (long long b = blockIdx.x; b < npairs; b += gridDim.x) {
+    long long ti = (long long)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= b) ++ti;
+    while (ti * (ti + 1) / 2 > b) --ti;
+    const long long tj = b - ti * (ti + 1) / 2;
+    const long long r0 = ti * kSST, c0 = tj * kSST;
+    float a[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = ty + 8 * q;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = tx + 32 * h;
+        const long long ar = r0 + r, ac = c0 + c;   // tile (I, J) → registers
+        a[q][h] = (ar < n && ac < n) ? __ldcs(x + ar * ldx + ac) : 0.f;
+        const long long br = c0 + r, bc = r0 + c;   // tile (J, I) → smem, as stored
+        tb[r][c] = (br < n && bc < n) ? __ldcs(x + br * ldx + bc) : 0.f;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = ty + 8 * q;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = tx + 32 * h;
+        const float av = a[q][h], bt = tb[c][r];    // x[i][j] and x[j][i]
+        if (!isfinite(av) || !isfinite(bt)) flags |= 2;
+        mabs = fmaxf(mabs, fmaxf(fabsf(av), fabsf(bt)));
+        mdef = fmax(mdef, fabs((double)av - (double)bt));   // exact, as after the f64 cast
+        if (av != bt) flags |= 1;
+        const long long ar = r0 + r, ac = c0 + c;
+        if (ar < n && ac < n) {
+          float h1, l1;
+          split_f32(av, raw, h1, l1);
+          if (!raw) __stcs(hi + ar * ldh + ac, h1);
+          __stcs(lo + ar * ldh + ac, l1);
+        }
+        const long long br = c0 + r, bc = r0 + c;
+        if (ti != tj && br < n && bc < n) {
+          float h2, l2;
+          split_f32(tb[r][c], raw, h2, l2);
+          if (!raw) __stcs(hi + br * ldh + bc, h2);
+          __stcs(lo + br * ldh + bc, l2);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  __shared__ float rmax[8];
+  __shared__ double rdef[8];
+  __shared__ int rfl[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mabs = fmaxf(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
+    mdef = fmax(mdef, __shfl_xor_sync(0xffffffffu, mdef, o));
+  }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (tx == 0) {
+    rmax[ty] = mabs;
+    rdef[ty] = mdef;
+    rfl[ty] = flags;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m1 = 0.f;
+    double m2 = 0.0;
+    int f = 0;
+    for (int w = 0; w < 8; ++w) {
+      m1 = fmaxf(m1, rmax[w]);
+      m2 = fmax(m2, rdef[w]);
+      f |= rfl[w];
+    }
+    if (m1 > 0.f) atomic_max_nonneg(&stats[0], (double)m1);
+    if (m2 > 0.0) atomic_max_nonneg(&stats[1], m2);
+    if (f) atomicOr(reinterpret_cast<int*>(stats + 2), f);
+  }
+}
+
+// C (fp64, M × N) = (Σ_s ws[s] + α·S)/α  (α > 0)  or  Σ_s ws[s].
+__global__ void reduce_partials_kernel(const float* __restrict__ ws, int splits, long long stride,
+                                       long long ldw, int M, int N, double* __restrict__ C,
+                                       long long ldc, double alpha, const double* __restrict__ S,
+                                       long long lds) {
+  const long long total = (long long)M * N;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / N;
+    const int j = (int)(e % N);
+    double acc = 0.0;
+    for (int s = 0; s < splits; ++s) acc += (double)ws[s * stride + i * ldw + j];
+    if (alpha > 0.0) acc = (acc + alpha * S[i * lds + j]) / alpha;
+    C[i * ldc + j] = acc;
+  }
+}
+
+}  // namespace tc32
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode32() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool map_f32(CUtensorMap* map, const float* ptr, long long cols, long long rows, long long ld,
+             int box_rows) {
+  auto fn = encode32();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)tc32::BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
+            tc32::SWZ == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int grid_for(long long total, int threads) {
+  const long long b = (total + threads - 1) / threads;
+  return (int)std::min<long long>(std::max<long long>(b, 1), (long long)device_info().sms * 16);
+}
+
+}  // namespace
+
+long long tc32_ws_elems(long long M, int N, int max_splits) {
+  const int bn_tot = (std::min(N, tc32::kMaxN) + 15) / 16 * 16;
+  const int groups = (N + bn_tot - 1) / bn_tot;
+  return (long long)max_splits * M * groups * bn_tot;
+}
+
+int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
+  using namespace tc32;
+  if (op.M < 1 || op.N < 1 || op.K < 1) return 0;
+  if ((op.lda % 4) || (op.ldb % 4) || (op.lda_lo % 4) || ((uintptr_t)op.a_hi % 16) || ((uintptr_t)op.a_lo % 16) ||
+      ((uintptr_t)op.b_hi % 16) || ((uintptr_t)op.b_lo % 16))
+    return -2;
+  Params p{};
+  p.M = op.M;
+  p.N = op.N;
+  p.K = op.K;
+  // N tiling: one group of up to 512 TMEM columns, as ≤ 2 MMAs of ≤ 256
+  int n_tot;
+  if (op.mode == MIRROR) {
+    n_tot = 256;
+  } else {
+    const int groups = (op.N + kMaxN - 1) / kMaxN;
+    n_tot = ((op.N + groups - 1) / groups + 15) / 16 * 16;
+  }
+  p.n_mma = n_tot > 256 ? 2 : 1;
+  p.bn = (n_tot / p.n_mma + 15) / 16 * 16;
+  n_tot = p.bn * p.n_mma;
+  p.n_groups = (op.N + n_tot - 1) / n_tot;
+  p.m_tiles = (op.M + BM - 1) / BM;
+  p.kblocks = (op.K + BK - 1) / BK;
+  const int sms = device_info().sms;
+  int splits = 1;
+  if (op.mode == PARTIAL) {
+    const long long base = (long long)p.m_tiles * p.n_groups;
+    double best = 1e30;
+    // TMEM accumulation is FP32: bound the K length of each split (its error
+    // grows with it); the fp64 reduction over splits adds the chunks exactly.
+    static const int kchunk = [] {
+      const char* e = getenv("PSD_TC32_KCHUNK");
+      return e ? atoi(e) : 4096;
+    }();
+    const int smin = kchunk > 0 ? std::max(1, (op.K + kchunk - 1) / kchunk) : 1;
+    const int smax = std::max(smin, std::min(std::max(op.max_splits, smin), p.kblocks / 8));
+    for (int s = smin; s <= smax; ++s) {
+      const long long units = base * s;
+      const double t = (double)((units + sms - 1) / sms) / s + 0.01 * s;
+      if (t < best - 1e-9) {
+        best = t;
+        splits = s;
+      }
+    }
+    const long long ldw = (long long)p.n_groups * n_tot;
+    while (splits > 1 && (size_t)splits * op.M * ldw > op.ws_elems) --splits;
+    if ((size_t)op.M * ldw > op.ws_elems) return -3;
+    p.out = op.ws;
+    p.ldo = ldw;
+    p.split_stride = (long long)op.M * ldw;
+  } else {
+    if (op.M != op.N) return -2;
+    p.out = op.c32;
+    p.ldo = op.ldc32;
+    p.split_stride = 0;
+  }
+  p.kb_per_split = (p.kblocks + splits - 1) / splits;
+  splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;   // every split non-empty
+  p.splits = splits;
+  p.mode = op.mode;
+  const int sb = stage_bytes(p.bn, p.n_mma);
+  const int epi_bytes = op.mode == MIRROR ? 4 * 32 * 33 * 4 : 0;   // epilogue transpose tiles
+  const int avail = (int)device_info().max_smem - 1024 - 2048 - epi_bytes;
+  p.stages = std::min(8, avail / sb);
+  if (p.stages < 2) return -4;
+  const size_t smem = std::max<size_t>((size_t)p.stages * sb + epi_bytes + 1024, 120 * 1024);
+
+  CUtensorMap mah, mal, mbh, mbl;
+  const long long lda_lo = op.lda_lo ? op.lda_lo : op.lda;
+  bool ok = map_f32(&mah, op.a_hi, op.K, op.M, op.lda, BM) && map_f32(&mal, op.a_lo, op.K, op.M, lda_lo, BM) &&
+            map_f32(&mbh, op.b_hi, op.K, op.N, op.ldb, p.bn) && map_f32(&mbl, op.b_lo, op.K, op.N, op.ldb, p.bn);
+  if (!ok) return -5;
+  static size_t attr[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr[dev] < smem) {
+    cudaFuncSetAttribute(tc32_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[dev] = smem;
+  }
+  const long long units = (long long)p.m_tiles * p.n_groups * p.splits;
+  tc32_gemm_kernel<<<(unsigned)units, kThreads, smem, st>>>(mah, mal, mbh, mbl, p);
+  count_launch();
+  if (op.mode == PARTIAL) {
+    const long long total = (long long)op.M * op.N;
+    reduce_partials_kernel<<<grid_for(total, 256), 256, 0, st>>>(
+        op.ws, p.splits, p.split_stride, p.ldo, op.M, op.N, op.c64, op.ldc64, op.alpha, op.S, op.lds);
+    count_launch();
+  }
+  return p.splits;
+}
+
+void symsplit_f32(const float* x, long long n, long long ldx, double* stats, float* hi, float* lo,
+                  long long ldh, cudaStream_t st) {
+  cudaMemsetAsync(stats, 0, 3 * sizeof(double), st);
+  const long long nt = (n + tc32::kSST - 1) / tc32::kSST;
+  const long long npairs = nt * (nt + 1) / 2;
+  const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * 4);
+  tc32::symsplit_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats, hi, lo, ldh,
+                                                          hi == nullptr);
+  count_launch();
+}
+
+void split_rows_f32(const float* x, long long rows, long long cols, long long ldx, float* hi,
+                    float* lo, long long ldh, long long cols_pad, cudaStream_t st) {
+  const bool vec = cols == cols_pad && cols % 4 == 0 && ldx % 4 == 0 && ldh % 4 == 0 &&
+                   (uintptr_t)x % 16 == 0 && (uintptr_t)hi % 16 == 0 && (uintptr_t)lo % 16 == 0;
+  const bool raw = hi == nullptr;
+  if (vec) {
+    const long long total = rows * (cols / 4);
+    tc32::split_rows_f32x4_kernel<<<grid_for(total, 256), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(x), rows, cols / 4, ldx / 4, reinterpret_cast<float4*>(hi),
+        reinterpret_cast<float4*>(lo), ldh / 4, raw);
+  } else {
+    tc32::split_rows_f32_kernel<<<grid_for(rows * cols_pad, 256), 256, 0, st>>>(x, rows, cols, ldx, hi,
+                                                                                lo, ldh, cols_pad, raw);
+  }
+  count_launch();
+}
+
+void split_rows_f64(const double* x, long long rows, int cols, long long ldx, const double* scale,
+                    float* hi, float* lo, long long ldh, int cols_pad, cudaStream_t st) {
+  tc32::split_rows_f64_kernel<<<grid_for(rows * cols_pad, 256), 256, 0, st>>>(x, rows, cols, ldx, scale,
+                                                                              hi, lo, ldh, cols_pad);
+  count_launch();
+}
+
+void split_transpose(const double* P, long long n, int w, long long ldp, float* hi, float* lo,
+                     long long ldt, int w_rows, cudaStream_t st) {
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((w_rows + 31) / 32));
+  tc32::split_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(P, n, w, ldp, hi, lo, ldt, w_rows);
+  count_launch();
+}
+
+}  // namespace psd

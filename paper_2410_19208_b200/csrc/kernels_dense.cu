@@ -470,6 +470,15 @@ constexpr int kFB = 32;
 constexpr int kFL = kFB + 4;  // smem stride ≡ 4 (mod 16)
 
 __device__ long long g_chol_t[6];
+
+// Element (i, j), i ≥ j, of the matrix being factored at panel step p0:
+// G + shift·I before any update (p0 == 0), the partially updated L after.
+PSD_DEVINL double chol_src(const double* __restrict__ G, long long ldg, const double* L,
+                           long long ldl, bool first, double shift, int i, int j) {
+  if (first) return G[(long long)i * ldg + j] + (i == j ? shift : 0.0);
+  return L[(long long)i * ldl + j];
+}
+
 __global__ void __launch_bounds__(256, 1)
     chol_blocked_kernel(const double* __restrict__ G, long long ldg, int m, double shift, double* L,
                         long long ldl, double* Dinv, double* status) {
@@ -479,34 +488,40 @@ __global__ void __launch_bounds__(256, 1)
   __shared__ int info_s;
   __shared__ double red[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kNT = 256, kNW = 8;
   double tr = 0.0;
-  for (long long e = tid; e < (long long)m * m; e += blockDim.x) {
-    const int i = (int)(e / m), j = (int)(e % m);
-    double v = G[(long long)i * ldg + j];
-    if (i == j) {
-      tr += v;
-      v += shift;
-    }
-    L[(long long)i * ldl + j] = (j <= i) ? v : 0.0;
-  }
+  for (int i = tid; i < m; i += kNT) tr += G[(long long)i * ldg + i];
   tr = warp_sum(tr);
   if (lane == 0) red[warp] = tr;
   if (tid == 0) info_s = 0;
   __syncthreads();
   if (tid == 0) {
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    for (int w = 0; w < kNW; ++w) t += red[w];
     status[1] = t;
   }
   long long tc0 = clock64();
   for (int p0 = 0; p0 < m; p0 += kFB) {
     const int nb = min(kFB, m - p0);
     const int rows = m - p0;
+    const bool first = p0 == 0;
     const long long ta = clock64();
-    // ---- stage the panel (rows × 32) in shared memory (coalesced)
-    for (int e = tid; e < rows * kFB; e += blockDim.x) {
-      const int r = e >> 5, c = e & 31;
-      P[r * kFL + c] = (c < nb && c <= r + kFB) ? L[(long long)(p0 + r) * ldl + p0 + c] : 0.0;
+    // ---- stage the panel (rows × 32) in shared memory: 8 loads in flight per thread
+    {
+      const int tot = rows * kFB;
+      for (int e0 = tid; e0 < tot; e0 += kNT * 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * kNT, r = e >> 5, c = e & 31;
+          v[u] = (e < tot && c < nb && c <= r) ? chol_src(G, ldg, L, ldl, first, shift, p0 + r, p0 + c) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * kNT;
+          if (e < tot) P[(e >> 5) * kFL + (e & 31)] = v[u];
+        }
+      }
     }
     __syncthreads();
     // ---- diagonal block: warp 0, lane i owns row i (registers); rsqrt, no divisions
@@ -536,15 +551,23 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int k = 0; k < kFB; ++k) P[lane * kFL + k] = (lane < nb && k <= lane) ? d[k] : 0.0;
       __syncwarp();
-      // inverse of the diagonal block: lane c → column c (forward substitution)
+      // inverse of the diagonal block: lane c → column c (forward substitution,
+      // four partial sums per row to shorten the dependency chain)
       double x[kFB];
       const int c = lane;
 #pragma unroll
       for (int r = 0; r < kFB; ++r) {
         const double rr = __shfl_sync(0xffffffffu, rdl, r);
-        double s = 0.0;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-        for (int k = 0; k < r; ++k) s = fma(P[r * kFL + k], (k >= c) ? x[k] : 0.0, s);
+        for (int k = 0; k < r; ++k) {
+          const double t = P[r * kFL + k] * ((k >= c) ? x[k] : 0.0);
+          if ((k & 3) == 0) s0 += t;
+          else if ((k & 3) == 1) s1 += t;
+          else if ((k & 3) == 2) s2 += t;
+          else s3 += t;
+        }
+        const double s = (s0 + s1) + (s2 + s3);
         x[r] = (r < c || c >= nb || r >= nb) ? 0.0 : (r == c ? rr : -s * rr);
       }
 #pragma unroll
@@ -556,7 +579,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     const long long tb_ = clock64();
     // ---- panel below: L21 = A21 · Dinvᵀ in shared memory (warp per row, lane per column)
-    for (int i = nb + warp; i < rows; i += (blockDim.x >> 5)) {
+    for (int i = nb + warp; i < rows; i += kNW) {
       double s = 0.0;
 #pragma unroll 8
       for (int k = 0; k < kFB; ++k) s = fma(P[i * kFL + k], (k <= lane) ? Di[lane * (kFB + 1) + k] : 0.0, s);
@@ -564,54 +587,52 @@ __global__ void __launch_bounds__(256, 1)
       P[i * kFL + lane] = (lane < nb) ? s : 0.0;
     }
     __syncthreads();
-    for (int e = tid; e < rows * kFB; e += blockDim.x) {
+    // store the factored panel (zeros above the diagonal of the panel columns)
+    for (int e = tid; e < m * kFB; e += kNT) {
       const int r = e >> 5, c = e & 31;
-      if (c < nb) L[(long long)(p0 + r) * ldl + p0 + c] = (r >= c) ? P[r * kFL + c] : 0.0;
+      if (c < nb) {
+        const int rl = r - p0;
+        L[(long long)r * ldl + p0 + c] = (rl >= c) ? P[rl * kFL + c] : 0.0;
+      }
     }
     const long long tcc = clock64();
-    // ---- trailing update A22 −= L21 L21ᵀ (lower 8×8 blocks) on DMMA, 4 blocks per warp in flight
+    // ---- trailing update A22 −= L21 L21ᵀ (lower 8×8 blocks) on DMMA; block row bi → warp
+    //      bi mod 8, eight blocks per round, all their loads issued before the MMAs
     const int t0 = p0 + nb, tn = m - t0;
     if (tn > 0) {
-      const int tb = (tn + 7) / 8;
-      const long long nblocks = (long long)tb * (tb + 1) / 2;
+      const int tbn = (tn + 7) / 8;
       const int g = lane >> 2, t = lane & 3;
-      const int nw = blockDim.x >> 5;
-      for (long long base = (long long)warp * 4; base < nblocks; base += (long long)nw * 4) {
-        int gi[4], gj0[4];
-        double cv[4][2];
+      for (int bi = warp; bi < tbn; bi += kNW) {
+        const int ii = t0 + 8 * bi + g;
+        const int ra = nb + 8 * bi + g;
+        double afr[kFB / 4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const long long b = base + u;
-          gi[u] = -1;
-          if (b < nblocks) {
-            int bi = (int)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
-            while ((long long)(bi + 1) * (bi + 2) / 2 <= b) ++bi;
-            while ((long long)bi * (bi + 1) / 2 > b) --bi;
-            const int bj = (int)(b - (long long)bi * (bi + 1) / 2);
-            gi[u] = 8 * bi + g;
-            gj0[u] = 8 * bj + 2 * t;
+        for (int k0 = 0; k0 < kFB / 4; ++k0) afr[k0] = (ra < rows) ? P[ra * kFL + 4 * k0 + t] : 0.0;
+        for (int bj0 = 0; bj0 <= bi; bj0 += 8) {
+          double cv[8][2];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int ii = t0 + gi[u], jj = t0 + gj0[u] + e;
-              cv[u][e] = (ii < m && jj < m && ii >= jj) ? L[(long long)ii * ldl + jj] : 0.0;
+              const int jj = t0 + 8 * (bj0 + u) + 2 * t + e;
+              cv[u][e] = (bj0 + u <= bi && ii < m && jj <= ii) ? chol_src(G, ldg, L, ldl, first, shift, ii, jj) : 0.0;
             }
           }
-        }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (gi[u] < 0) continue;
-          const int ra = nb + gi[u], rb = nb + (gj0[u] - 2 * t) + g;
-          double c0 = 0.0, c1 = 0.0;
+          for (int u = 0; u < 8; ++u) {
+            if (bj0 + u > bi) break;
+            const int rb = nb + 8 * (bj0 + u) + g;
+            double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-          for (int k0 = 0; k0 < kFB; k0 += 4) {
-            const double a = (ra < rows) ? P[ra * kFL + k0 + t] : 0.0;
-            const double bb = (rb < rows) ? P[rb * kFL + k0 + t] : 0.0;
-            dmma_8x8x4(c0, c1, a, bb);
-          }
+            for (int k0 = 0; k0 < kFB / 4; ++k0) {
+              const double bb = (rb < rows) ? P[rb * kFL + 4 * k0 + t] : 0.0;
+              dmma_8x8x4(c0, c1, afr[k0], bb);
+            }
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int ii = t0 + gi[u], jj = t0 + gj0[u] + e;
-            if (ii < m && jj < m && ii >= jj) L[(long long)ii * ldl + jj] = cv[u][e] - (e ? c1 : c0);
+            for (int e = 0; e < 2; ++e) {
+              const int jj = t0 + 8 * (bj0 + u) + 2 * t + e;
+              if (ii < m && jj <= ii) L[(long long)ii * ldl + jj] = cv[u][e] - (e ? c1 : c0);
+            }
           }
         }
       }
@@ -626,7 +647,7 @@ __global__ void __launch_bounds__(256, 1)
   }
   if (tid == 0) g_chol_t[0] += clock64() - tc0;
   double dmin = INFINITY, dmax = 0.0;
-  for (int i = tid; i < m; i += blockDim.x) {
+  for (int i = tid; i < m; i += kNT) {
     const double dd = L[(long long)i * ldl + i];
     dmin = fmin(dmin, dd);
     dmax = fmax(dmax, dd);
@@ -643,7 +664,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (tid == 0) {
     double a = INFINITY, b2 = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    for (int w = 0; w < kNW; ++w) {
       a = fmin(a, rmin[w]);
       b2 = fmax(b2, rmax[w]);
     }

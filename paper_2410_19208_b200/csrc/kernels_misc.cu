@@ -18,10 +18,11 @@ constexpr int kSymT = 64;
 // (I ≥ J): tile (J,I) is staged transposed through shared memory, tile (I,J)
 // is read straight into registers, so every element of X is read once
 // (diagonal tiles twice).  One atomic per block per statistic at the end.
-__global__ void __launch_bounds__(256) sym_stats_kernel(const double* __restrict__ x, long long n,
+template <typename T>
+__global__ void __launch_bounds__(256) sym_stats_kernel(const T* __restrict__ x, long long n,
                                                         long long ldx, long long npairs,
                                                         double* stats) {
-  __shared__ double tj[kSymT][kSymT + 1];
+  __shared__ T tj[kSymT][kSymT + 1];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
   double mabs = 0.0, mdef = 0.0;
   int flags = 0;
@@ -31,7 +32,7 @@ __global__ void __launch_bounds__(256) sym_stats_kernel(const double* __restrict
     while (ti * (ti + 1) / 2 > b) --ti;
     const long long tjx = b - ti * (ti + 1) / 2;
     const long long r0 = ti * kSymT, c0 = tjx * kSymT;
-    double a[8][2];
+    T a[8][2];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int r = ty + 8 * q;
@@ -40,9 +41,9 @@ __global__ void __launch_bounds__(256) sym_stats_kernel(const double* __restrict
         const int c = tx + 32 * h;
         // x[c0 + r][r0 + c] → smem (tile (J, I)); x[r0 + r][c0 + c] → registers (tile (I, J))
         const long long gr = c0 + r, gc = r0 + c;
-        tj[r][c] = (gr < n && gc < n) ? __ldcs(x + gr * ldx + gc) : 0.0;
+        tj[r][c] = (gr < n && gc < n) ? __ldcs(x + gr * ldx + gc) : T(0);
         const long long ar = r0 + r, ac = c0 + c;
-        a[q][h] = (ar < n && ac < n) ? __ldcs(x + ar * ldx + ac) : 0.0;
+        a[q][h] = (ar < n && ac < n) ? __ldcs(x + ar * ldx + ac) : T(0);
       }
     }
     __syncthreads();
@@ -52,8 +53,8 @@ __global__ void __launch_bounds__(256) sym_stats_kernel(const double* __restrict
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = tx + 32 * h;
-        const double av = a[q][h];
-        const double bt = tj[c][r];  // x[c0 + c][r0 + r] = x[j][i]
+        const double av = (double)a[q][h];
+        const double bt = (double)tj[c][r];  // x[c0 + c][r0 + r] = x[j][i]
         if (!isfinite(av) || !isfinite(bt)) flags |= 2;
         mabs = fmax(mabs, fmax(fabs(av), fabs(bt)));
         mdef = fmax(mdef, fabs(av - bt));
@@ -87,12 +88,38 @@ __global__ void __launch_bounds__(256) sym_stats_kernel(const double* __restrict
   }
 }
 
-void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st) {
+template <typename T>
+static void sym_stats_t(const T* x, long long n, long long ldx, double* stats, cudaStream_t st) {
   cudaMemsetAsync(stats, 0, 3 * sizeof(double), st);
   const long long nt = (n + kSymT - 1) / kSymT;
   const long long npairs = nt * (nt + 1) / 2;
   const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * 4);
-  sym_stats_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats);
+  sym_stats_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats);
+  count_launch();
+}
+void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st) {
+  sym_stats_t(x, n, ldx, stats, st);
+}
+void sym_stats_f32(const float* x, long long n, long long ldx, double* stats, cudaStream_t st) {
+  sym_stats_t(x, n, ldx, stats, st);
+}
+
+__global__ void convert_f32_f64_kernel(const float* __restrict__ src, long long lds, double* dst,
+                                       long long ldd, long long rows, int cols) {
+  const long long total = rows * cols;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cols;
+    const int c = (int)(e % cols);
+    dst[r * ldd + c] = (double)src[r * lds + c];
+  }
+}
+void convert_f32_f64(const float* src, long long lds, double* dst, long long ldd, long long rows,
+                     int cols, cudaStream_t st) {
+  const long long total = rows * cols;
+  const long long blocks = std::min<long long>((total + 255) / 256, (long long)device_info().sms * 16);
+  convert_f32_f64_kernel<<<(unsigned)std::max<long long>(blocks, 1), 256, 0, st>>>(src, lds, dst, ldd,
+                                                                                  rows, cols);
   count_launch();
 }
 

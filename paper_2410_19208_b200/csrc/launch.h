@@ -46,10 +46,48 @@ long long gemm_resid_ctas(const GemmOp& op);
 int gemm_f64_tma(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st);
 long long gemm_tma_resid_parts(const GemmOp& op);
 
+// ---- 3xTF32 tcgen05 GEMM (gemm_tc32.cu): C = A·Bᵀ, A M×K and B N×K fp32 -------
+// operands given as tf32 hi/lo pairs (K contiguous, ld % 4 == 0, 16-B aligned).
+struct Tc32Op {
+  const float *a_hi = nullptr, *a_lo = nullptr;
+  long long lda = 0;
+  long long lda_lo = 0;       // 0: same as lda
+  const float *b_hi = nullptr, *b_lo = nullptr;
+  long long ldb = 0;
+  int M = 0, N = 0, K = 0;
+  int mode = 0;               // 0: fp64 result c64 (split-K partials in ws), 1: mirrored fp32 c32 (M == N)
+  double* c64 = nullptr;
+  long long ldc64 = 0;
+  double alpha = 0.0;         // mode 0, α > 0: c64 = (acc + α·S)/α
+  const double* S = nullptr;
+  long long lds = 0;
+  float* c32 = nullptr;
+  long long ldc32 = 0;
+  float* ws = nullptr;
+  size_t ws_elems = 0;
+  int max_splits = 8;
+};
+// Returns the K-split count used (≥ 1) or < 0 on error (−2 alignment, −3 workspace).
+int gemm_tf32x3(const Tc32Op& op, cudaStream_t st);
+long long tc32_ws_elems(long long M, int N, int max_splits);
+// require_symmetric statistics of a square fp32 X (as sym_stats) fused with its tf32 hi/lo split;
+// hi == nullptr (also for split_rows_f32): raw mode, X itself serves as hi, only lo is written.
+void symsplit_f32(const float* x, long long n, long long ldx, double* stats, float* hi, float* lo,
+                  long long ldh, cudaStream_t st);
+void split_rows_f32(const float* x, long long rows, long long cols, long long ldx, float* hi,
+                    float* lo, long long ldh, long long cols_pad, cudaStream_t st);
+void split_rows_f64(const double* x, long long rows, int cols, long long ldx, const double* scale,
+                    float* hi, float* lo, long long ldh, int cols_pad, cudaStream_t st);
+void split_transpose(const double* P, long long n, int w, long long ldp, float* hi, float* lo,
+                     long long ldt, int w_rows, cudaStream_t st);
+
 // ---- memory-bound kernels --------------------------------------------------
 // stats[0] = max|x|, stats[1] = max|x - xᵀ|, ((int*)(stats+2))[0] = flags
 // (bit0: not bitwise symmetric, bit1: NaN/Inf present). stats zeroed inside.
 void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st);
+void sym_stats_f32(const float* x, long long n, long long ldx, double* stats, cudaStream_t st);
+void convert_f32_f64(const float* src, long long lds, double* dst, long long ldd, long long rows,
+                     int cols, cudaStream_t st);
 // x ← (x + xᵀ)/2 for a small m×m matrix (in place, exact mirror).
 void symmetrize_small(double* x, int m, long long ld, cudaStream_t st);
 void philox_normal(double* out, long long rows, int cols, long long ld, uint64_t seed,

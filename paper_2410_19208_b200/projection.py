@@ -8,7 +8,9 @@ CholeskyQR, block-Jacobi eigensolver, mirrored SYRK reconstruction); numpy
 inputs are uploaded once and results copied back, torch CUDA inputs stay on
 the device.  Extra keyword-only arguments: ``omega=`` (inject Ω),
 ``assume_symmetric=`` (skip the validation pass for inputs known to be
-bitwise symmetric).
+bitwise symmetric), ``dtype=`` ("fp64" default — the reference's float64
+semantics; "fp32" — the FP32 path: 3xTF32 tcgen05 GEMMs, FP64 QR/eigh,
+fp32 result, parity ≤1e-4 against the FP64 oracle on the fp32-rounded X).
 """
 
 from __future__ import annotations
@@ -40,8 +42,10 @@ class ProjectorConfig:
     scale_factor: float = 1.0
     collect_diagnostics: bool = False
     return_factors: bool = False
+    dtype: str = "fp64"
 
     def __post_init__(self):
+        self.dtype = resolve_dtype(self.dtype)
         if self.method not in METHODS:
             raise errors.error("InvalidParams", f"unknown projection method {self.method!r}")
         if self.method in ("randomized", "scaled_randomized") and self.params is None:
@@ -66,7 +70,25 @@ class ProjectionReport:
     device_info: dict | None = field(default=None, repr=False)
 
 
+def resolve_dtype(dtype):
+    """None / fp64 / float64 → "fp64"; fp32 / float32 → "fp32"."""
+    if dtype is None:
+        return "fp64"
+    name = str(dtype).replace("torch.", "").replace("numpy.", "").lower()
+    if name in ("fp64", "float64", "double", "f64", "<class 'numpy.float64'>"):
+        return "fp64"
+    if name in ("fp32", "float32", "float", "f32", "<class 'numpy.float32'>"):
+        return "fp32"
+    raise errors.error("InvalidParams", f"unsupported dtype {dtype!r} (fp64 or fp32)")
+
+
+def _operand(x, dtype):
+    return as_device(x, dtype=torch.float32 if resolve_dtype(dtype) == "fp32" else torch.float64)
+
+
 def _stats_for(op, assume_symmetric):
+    if op.t.dtype == torch.float32:
+        return None  # the FP32 entry point validates on the device itself
     if assume_symmetric:
         return None
     return check_symmetric_device(op)
@@ -77,19 +99,25 @@ def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, m
     lib = _native.load_library()
     plan = _native.get_plan(n, width, op.device)
     dev = op.device
-    result = torch.empty((n, n), dtype=torch.float64, device=dev)
+    f32 = op.t.dtype == torch.float32
+    result = torch.empty((n, n), dtype=op.t.dtype, device=dev)
     fw = torch.empty((n, width), dtype=torch.float64, device=dev) if return_factors else None
     fd = torch.empty(width, dtype=torch.float64, device=dev) if return_factors else None
-    flags = _native.FLAG_SKIP_SYMCHECK
-    if stats is None or stats.bitwise:
-        flags |= _native.FLAG_ASSUME_SYMMETRIC
+    if f32:
+        flags = 0  # psd_ran_proj_f32 runs require_symmetric / alpha_tol on the fp32 X
+        om = om.to(torch.float32).contiguous()
+    else:
+        flags = _native.FLAG_SKIP_SYMCHECK
+        if stats is None or stats.bitwise:
+            flags |= _native.FLAG_ASSUME_SYMMETRIC
     if collect_diagnostics:
         flags |= _native.FLAG_DIAGNOSTICS
     rep = _native.PsdReport()
-    _native.check(lib.psd_ran_proj(plan.handle, _native.ptr(op.t), n, n, _native.ptr(om),
-                                   om.stride(0), params.k, params.l, params.q, float(alpha), flags,
-                                   _native.ptr(result), n, _native.ptr(fw), width, _native.ptr(fd),
-                                   ctypes.byref(rep), _native.stream_handle(dev)))
+    entry = lib.psd_ran_proj_f32 if f32 else lib.psd_ran_proj
+    _native.check(entry(plan.handle, _native.ptr(op.t), n, n, _native.ptr(om),
+                        om.stride(0), params.k, params.l, params.q, float(alpha), flags,
+                        _native.ptr(result), n, _native.ptr(fw), width, _native.ptr(fd),
+                        ctypes.byref(rep), _native.stream_handle(dev)))
     r = rep.effective_rank
     factors = None
     if return_factors:
@@ -102,7 +130,7 @@ def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, m
         method=method,
         effective_rank=int(r),
         alpha_used=float(alpha) if alpha > 0 else None,
-        residual_frob=float(rep.residual_frob) if collect_diagnostics else None,
+        residual_frob=float(rep.residual_frob) if collect_diagnostics and not f32 else None,
         wall_time=time.perf_counter() - t0,
         factors=factors,
         basis_width=int(rep.basis_width),
@@ -120,10 +148,10 @@ def _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, st
 
 
 def ran_proj(x, params, rng, collect_diagnostics=False, return_factors=False, *, omega=None,
-             assume_symmetric=False):
+             assume_symmetric=False, dtype=None):
     """projection.py:92-119 (Alg. 2): X̂₊ = Q U D₊ Uᵀ Qᵀ."""
     t0 = time.perf_counter()
-    op = as_device(x)
+    op = _operand(x, dtype)
     require_square(op)
     stats = _stats_for(op, assume_symmetric)                   # projection.py:100
     return _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, stats, t0)
@@ -131,14 +159,15 @@ def ran_proj(x, params, rng, collect_diagnostics=False, return_factors=False, *,
 
 def _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factors, omega, stats, t0):
     n = require_square(op)
-    if stats is None:  # assume_symmetric: still need max|x| for alpha_tol (one HBM pass)
-        stats = check_symmetric_device(op)
-    max_abs = stats.max_abs
-    alpha_tol = ALPHA_TOL_FACTOR * max(1.0, max_abs)            # projection.py:133
-    if alpha <= alpha_tol:
-        raise errors.error(
-            "AlphaTooSmall",
-            f"alpha = {alpha:.3e} is at or below tolerance {alpha_tol:.3e}; input is numerically PSD")
+    if op.t.dtype != torch.float32:  # FP32: alpha_tol is tested inside psd_ran_proj_f32
+        if stats is None:  # assume_symmetric: still need max|x| for alpha_tol (one HBM pass)
+            stats = check_symmetric_device(op)
+        max_abs = stats.max_abs
+        alpha_tol = ALPHA_TOL_FACTOR * max(1.0, max_abs)            # projection.py:133
+        if alpha <= alpha_tol:
+            raise errors.error(
+                "AlphaTooSmall",
+                f"alpha = {alpha:.3e} is at or below tolerance {alpha_tol:.3e}; input is numerically PSD")
     width = params.width
     if width > n:
         raise errors.error("InvalidParams", f"k+l = {width} exceeds min(m, n) = {n}")
@@ -148,10 +177,10 @@ def _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factor
 
 
 def ran_proj_scal(x, params, alpha, rng, collect_diagnostics=False, return_factors=False, *,
-                  omega=None, assume_symmetric=False):
+                  omega=None, assume_symmetric=False, dtype=None):
     """projection.py:122-159 (Alg. 3) through B = (X + αI)/α (fused in the GEMM epilogues)."""
     t0 = time.perf_counter()
-    op = as_device(x)
+    op = _operand(x, dtype)
     require_square(op)
     stats = _stats_for(op, assume_symmetric)
     return _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factors, omega,
@@ -180,10 +209,16 @@ def _exact_report(op, method, t0):
 def project(x, cfg, rng=None, *, omega=None, assume_symmetric=False):
     """projection.py:180-223: dispatcher with the scaled → unscaled AlphaTooSmall fallback."""
     t0 = time.perf_counter()
-    op = as_device(x)
+    op = _operand(x, cfg.dtype)
     require_square(op)
     stats = _stats_for(op, assume_symmetric)                   # projection.py:189
     if cfg.method in ("exact", "polar"):
+        if op.t.dtype == torch.float32:  # dense eigh stays FP64; result handed back as fp32
+            op64 = type(op)(op.t.double(), op.kind, op.device)
+            check_symmetric_device(op64)
+            rep = _exact_report(op64, cfg.method, t0)
+            rep.result = op.give_back(torch.as_tensor(rep.result, device=op.device).to(torch.float32))
+            return rep
         return _exact_report(op, cfg.method, t0)
 
     rng = rng_from_seed(rng if rng is not None else (cfg.params.seed if cfg.params else None))
@@ -195,6 +230,8 @@ def project(x, cfg, rng=None, *, omega=None, assume_symmetric=False):
 
     if cfg.alpha_override is not None:
         alpha = float(cfg.alpha_override)
+    elif op.t.dtype == torch.float32:  # α estimate on the fp32 values, in FP64
+        alpha = min_eig_magnitude_device(type(op)(op.t.double(), op.kind, op.device), cfg.power_N, rng)
     else:
         alpha = min_eig_magnitude_device(op, cfg.power_N, rng)   # projection.py:206
     alpha *= cfg.scale_factor
@@ -215,5 +252,5 @@ def flops(n, params, effective_rank):
     return 2.0 * n * n * params.width * (2 * params.q + 2) + float(n) * n * effective_rank
 
 
-__all__ = ["METHODS", "ProjectorConfig", "ProjectionReport", "ran_proj", "ran_proj_scal",
+__all__ = ["METHODS", "resolve_dtype", "ProjectorConfig", "ProjectionReport", "ran_proj", "ran_proj_scal",
            "project", "flops"]

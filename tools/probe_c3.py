@@ -19,6 +19,7 @@ def main():
     k = int(sys.argv[2]) if len(sys.argv) > 2 else 256
     p = int(sys.argv[3]) if len(sys.argv) > 3 else 16
     q = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+    dtype = sys.argv[5] if len(sys.argv) > 5 else "fp64"
     dev = torch.device("cuda", 0)
     print(torch.cuda.get_device_name(0), flush=True)
     # cuBLAS DGEMM context number
@@ -40,17 +41,19 @@ def main():
     t0 = time.time()
     x = psd.workloads.c3_device(n, seed=0, device=dev)
     torch.cuda.synchronize()
-    print(f"generated X in {time.time() - t0:.1f}s", flush=True)
+    if dtype == "fp32":
+        x = x.float()
+    print(f"generated X ({dtype}) in {time.time() - t0:.1f}s", flush=True)
     params = psd.RangeParams(k=k, l=p, q=q)
     rng = psd.DeviceRng(1)
-    rep = psd.ran_proj(x, params, rng, assume_symmetric=False)
+    rep = psd.ran_proj(x, params, rng, assume_symmetric=False, dtype=dtype)
     plan = psd._native.get_plan(n, params.width, dev)
     plan.profile(enable=True, reset=True)
     for it in range(3):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        rep = psd.ran_proj(x, params, rng, assume_symmetric=False)
+        rep = psd.ran_proj(x, params, rng, assume_symmetric=False, dtype=dtype)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
