@@ -487,6 +487,7 @@ __global__ void __launch_bounds__(256, 1)
   double* Di = sm + (size_t)max(m, kFB) * kFL;   // current inv(L_jj), 32 × 33
   __shared__ int info_s;
   __shared__ double red[32];
+  __shared__ __align__(16) double colb[kFB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kNT = 256, kNW = 8;
   double tr = 0.0;
@@ -524,69 +525,98 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
     __syncthreads();
-    // ---- diagonal block: warp 0, lane i owns row i (registers); rsqrt, no divisions
+    // ---- diagonal block: warp 0, lane i owns row i in registers.  The block
+    //      is padded to 32×32 with the identity so no step needs a predicate;
+    //      column j is broadcast through shared memory (one LDS per two
+    //      entries) — compact code: the whole phase stays in the i-cache.
     if (warp == 0) {
       double d[kFB];
 #pragma unroll
-      for (int k = 0; k < kFB; ++k) d[k] = (lane < nb && k <= lane) ? P[lane * kFL + k] : 0.0;
+      for (int k = 0; k < kFB; ++k)
+        d[k] = (lane < nb && k < nb) ? (k <= lane ? P[lane * kFL + k] : 0.0) : (lane == k ? 1.0 : 0.0);
       double rdl = 0.0;  // 1 / L_ll of this lane's row
 #pragma unroll
       for (int j = 0; j < kFB; ++j) {
-        if (j < nb) {
-          const double piv = __shfl_sync(0xffffffffu, d[j], j);
-          if (lane == 0 && (!(piv > 0.0) || !isfinite(piv)) && info_s == 0) info_s = p0 + j + 1;
-          const double inv = rsqrt(fmax(piv, 1e-300));
-          if (lane == j) {
-            d[j] = piv * inv;
-            rdl = inv;
-          }
-          if (lane > j) d[j] *= inv;
+        const double piv = __shfl_sync(0xffffffffu, d[j], j);
+        if (lane == 0 && (!(piv > 0.0) || !isfinite(piv)) && info_s == 0 && j < nb) info_s = p0 + j + 1;
+        const double inv = rsqrt(fmax(piv, 1e-300));
+        d[j] = (lane == j) ? piv * inv : d[j] * inv;
+        if (lane == j) rdl = inv;
+        colb[lane] = d[j];
+        __syncwarp();
 #pragma unroll
-          for (int k = j + 1; k < kFB; ++k) {
-            const double lkj = __shfl_sync(0xffffffffu, d[j], k);
-            if (lane >= k && k < nb) d[k] = fma(-d[j], lkj, d[k]);
-          }
-        }
+        for (int k = j + 1; k < kFB; ++k) d[k] = fma(-d[j], colb[k], d[k]);   // upper entries: don't-care
+        __syncwarp();
       }
 #pragma unroll
       for (int k = 0; k < kFB; ++k) P[lane * kFL + k] = (lane < nb && k <= lane) ? d[k] : 0.0;
+      colb[lane] = rdl;
       __syncwarp();
-      // inverse of the diagonal block: lane c → column c (forward substitution,
-      // four partial sums per row to shorten the dependency chain)
+      // inverse of the (padded) diagonal block: lane c → column c,
+      // x_r = (δ_rc − Σ_{k<r} L_rk x_k) / L_rr ; x_r = 0 for r < c falls out.
       double x[kFB];
       const int c = lane;
 #pragma unroll
       for (int r = 0; r < kFB; ++r) {
-        const double rr = __shfl_sync(0xffffffffu, rdl, r);
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        double s0 = (r == c) ? 1.0 : 0.0, s1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < r; ++k) {
-          const double t = P[r * kFL + k] * ((k >= c) ? x[k] : 0.0);
-          if ((k & 3) == 0) s0 += t;
-          else if ((k & 3) == 1) s1 += t;
-          else if ((k & 3) == 2) s2 += t;
-          else s3 += t;
+        for (int k = 0; k + 1 < r; k += 2) {
+          s0 = fma(-P[r * kFL + k], x[k], s0);
+          s1 = fma(-P[r * kFL + k + 1], x[k + 1], s1);
         }
-        const double s = (s0 + s1) + (s2 + s3);
-        x[r] = (r < c || c >= nb || r >= nb) ? 0.0 : (r == c ? rr : -s * rr);
+        if (r & 1) s0 = fma(-P[r * kFL + r - 1], x[r - 1], s0);
+        x[r] = (s0 + s1) * colb[r];
       }
 #pragma unroll
       for (int r = 0; r < kFB; ++r) {
-        Di[r * (kFB + 1) + c] = x[r];
-        Dinv[((size_t)(p0 / kFB) * kFB + r) * kFB + c] = x[r];
+        const double v = (r < nb && c < nb) ? x[r] : 0.0;
+        Di[r * (kFB + 1) + c] = v;
+        Dinv[((size_t)(p0 / kFB) * kFB + r) * kFB + c] = v;
       }
     }
     __syncthreads();
     const long long tb_ = clock64();
-    // ---- panel below: L21 = A21 · Dinvᵀ in shared memory (warp per row, lane per column)
-    for (int i = nb + warp; i < rows; i += kNW) {
-      double s = 0.0;
-#pragma unroll 8
-      for (int k = 0; k < kFB; ++k) s = fma(P[i * kFL + k], (k <= lane) ? Di[lane * (kFB + 1) + k] : 0.0, s);
-      __syncwarp();
-      P[i * kFL + lane] = (lane < nb) ? s : 0.0;
+    // ---- panel below: L21 = A21 · Dinvᵀ on DMMA (8×8 output blocks).  Rows are
+    //      independent, so waves of 16 row-blocks are computed into registers,
+    //      then written back in place after a barrier.
+    {
+      const int rb_n = (rows - nb + 7) / 8;   // 8-row blocks below the diagonal block
+      const int g = lane >> 2, t = lane & 3;
+      constexpr int kU = 8;                   // blocks per warp per wave
+      const int nblk = rb_n * 4;
+      for (int base = 0; base < nblk; base += kNW * kU) {
+        double o[kU][2];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int bidx = base + warp + u * kNW;
+          double c0 = 0.0, c1 = 0.0;
+          if (bidx < nblk) {
+            const int ra = nb + 8 * (bidx >> 2) + g, cb = bidx & 3;
+#pragma unroll
+            for (int k0 = 0; k0 < kFB; k0 += 4) {
+              const double av = (ra < rows) ? P[ra * kFL + k0 + t] : 0.0;
+              const double bv = Di[(8 * cb + g) * (kFB + 1) + k0 + t];   // (Dinvᵀ)[k][n] = Dinv[n][k]
+              dmma_8x8x4(c0, c1, av, bv);
+            }
+          }
+          o[u][0] = c0;
+          o[u][1] = c1;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int bidx = base + warp + u * kNW;
+          if (bidx < nblk) {
+            const int ra = nb + 8 * (bidx >> 2) + g, col = 8 * (bidx & 3) + 2 * t;
+            if (ra < rows) {
+              P[ra * kFL + col] = (col < nb) ? o[u][0] : 0.0;
+              P[ra * kFL + col + 1] = (col + 1 < nb) ? o[u][1] : 0.0;
+            }
+          }
+        }
+        __syncthreads();
+      }
     }
-    __syncthreads();
     // store the factored panel (zeros above the diagonal of the panel columns)
     for (int e = tid; e < m * kFB; e += kNT) {
       const int r = e >> 5, c = e & 31;
@@ -675,57 +705,80 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // Block column j of X = L⁻¹ (rows ≥ j): X_jj = Dinv_j; X_ij = −Dinv_i Σ_{k=j}^{i−1} L_ik X_kj.
-// Writes Rinv[j-block rows][c] = X[c][j-block cols] (Rinv = Xᵀ), zero elsewhere.
+// Both products on DMMA (8 warps × two 8×8 output blocks); L_i,[j..i) is
+// streamed through shared memory in 128-column chunks.  Writes
+// Rinv[j-block rows][c] = X[c][j-block cols] (Rinv = Xᵀ), zero elsewhere.
+constexpr int kTiChunk = 128;
+constexpr int kTiLdL = kTiChunk + 4;
+constexpr int kTiLdX = kFB + 4;
 __global__ void __launch_bounds__(256) tri_inv_blocked_kernel(const double* __restrict__ L,
                                                               long long ldl, int m,
                                                               const double* __restrict__ Dinv,
                                                               double* Rinv, long long ldr) {
-  extern __shared__ double xs[];   // nblk × 32 × 32 (X_kj for k ≥ j), then scratch 32×32
+  extern __shared__ double xs[];
   const int j = blockIdx.x;
   const int nblk = (m + kFB - 1) / kFB;
-  const int tid = threadIdx.x;
-  double* S = xs + (size_t)nblk * kFB * kFB;   // scratch Z (32×32)
-  auto X = [&](int k) { return xs + (size_t)k * kFB * kFB; };
-  for (int e = tid; e < kFB * kFB; e += blockDim.x) X(j)[e] = Dinv[(size_t)j * kFB * kFB + e];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nk = nblk - j;                              // block rows j..nblk-1 of column block j
+  double* X = xs;                                       // nk·32 rows × kTiLdX (row r ↔ global row 32j + r)
+  double* Lb = X + (size_t)nk * kFB * kTiLdX;           // 32 × kTiLdL chunk of L_i,[j..i)
+  double* Zs = Lb + (size_t)kFB * kTiLdL;               // 32 × kTiLdX
+  double* Ds = Zs + (size_t)kFB * kTiLdX;               // 32 × kTiLdX (Dinv_i)
+  for (int e = tid; e < kFB * kFB; e += blockDim.x)
+    X[(e >> 5) * kTiLdX + (e & 31)] = Dinv[(size_t)j * kFB * kFB + e];
+  const int br = warp >> 1, bc0 = 2 * (warp & 1);       // this warp's output blocks: (br, bc0), (br, bc0+1)
   __syncthreads();
   for (int i = j + 1; i < nblk; ++i) {
     const int ri = i * kFB;
-    // Z = Σ_{k=j}^{i−1} L_ik X_kj   (32×32)
-    for (int e = tid; e < kFB * kFB; e += blockDim.x) {
-      const int r = e / kFB, c = e % kFB;
-      double s = 0.0;
-      if (ri + r < m) {
-        const double* lrow = L + (long long)(ri + r) * ldl;
-        for (int k = j; k < i; ++k) {
-          const double* xk = X(k);
-          const int kb = k * kFB;
-#pragma unroll 8
-          for (int q = 0; q < kFB; ++q) s = fma(lrow[kb + q], xk[q * kFB + c], s);
-        }
+    const int K = (i - j) * kFB;                        // columns 32j .. 32i of L's row block i
+    double z0[2] = {0.0, 0.0}, z1[2] = {0.0, 0.0};
+    for (int e = tid; e < kFB * kFB; e += blockDim.x)
+      Ds[(e >> 5) * kTiLdX + (e & 31)] = Dinv[(size_t)i * kFB * kFB + e];
+    for (int k0 = 0; k0 < K; k0 += kTiChunk) {
+      const int kc = min(kTiChunk, K - k0);
+      for (int e = tid; e < kFB * kTiChunk; e += blockDim.x) {
+        const int r = e / kTiChunk, c = e % kTiChunk;
+        Lb[r * kTiLdL + c] = (c < kc && ri + r < m) ? L[(long long)(ri + r) * ldl + j * kFB + k0 + c] : 0.0;
       }
-      S[e] = s;
+      __syncthreads();
+      for (int kk = 0; kk < kc; kk += 4) {
+        const double av = Lb[(8 * br + g) * kTiLdL + kk + t];
+        const double b0 = X[(k0 + kk + t) * kTiLdX + 8 * bc0 + g];
+        const double b1 = X[(k0 + kk + t) * kTiLdX + 8 * (bc0 + 1) + g];
+        dmma_8x8x4(z0[0], z0[1], av, b0);
+        dmma_8x8x4(z1[0], z1[1], av, b1);
+      }
+      __syncthreads();
     }
+    Zs[(8 * br + g) * kTiLdX + 8 * bc0 + 2 * t] = z0[0];
+    Zs[(8 * br + g) * kTiLdX + 8 * bc0 + 2 * t + 1] = z0[1];
+    Zs[(8 * br + g) * kTiLdX + 8 * (bc0 + 1) + 2 * t] = z1[0];
+    Zs[(8 * br + g) * kTiLdX + 8 * (bc0 + 1) + 2 * t + 1] = z1[1];
     __syncthreads();
     // X_ij = −Dinv_i · Z
-    const double* Di = Dinv + (size_t)i * kFB * kFB;
-    for (int e = tid; e < kFB * kFB; e += blockDim.x) {
-      const int r = e / kFB, c = e % kFB;
-      double s = 0.0;
-      for (int q = 0; q <= r; ++q) s = fma(Di[r * kFB + q], S[q * kFB + c], s);
-      X(i)[e] = -s;
+    double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+#pragma unroll
+    for (int kk = 0; kk < kFB; kk += 4) {
+      const double av = Ds[(8 * br + g) * kTiLdX + kk + t];
+      const double b0 = Zs[(kk + t) * kTiLdX + 8 * bc0 + g];
+      const double b1 = Zs[(kk + t) * kTiLdX + 8 * (bc0 + 1) + g];
+      dmma_8x8x4(w0[0], w0[1], av, b0);
+      dmma_8x8x4(w1[0], w1[1], av, b1);
     }
+    double* Xi = X + (size_t)(i - j) * kFB * kTiLdX;
+    Xi[(8 * br + g) * kTiLdX + 8 * bc0 + 2 * t] = -w0[0];
+    Xi[(8 * br + g) * kTiLdX + 8 * bc0 + 2 * t + 1] = -w0[1];
+    Xi[(8 * br + g) * kTiLdX + 8 * (bc0 + 1) + 2 * t] = -w1[0];
+    Xi[(8 * br + g) * kTiLdX + 8 * (bc0 + 1) + 2 * t + 1] = -w1[1];
     __syncthreads();
   }
-  // Rinv rows [j·32, …) = X[:, j-block]ᵀ
+  // Rinv rows [32j, 32j+32) = X[:, j-block]ᵀ  (row < 32j → 0)
   const int cj = j * kFB;
   for (int e = tid; e < kFB * m; e += blockDim.x) {
     const int c = e / m, row = e % m;   // Rinv[cj + c][row] = X[row][cj + c]
     if (cj + c >= m) continue;
-    double v = 0.0;
-    if (row >= cj) {
-      const int k = row / kFB, q = row % kFB;
-      v = X(k)[q * kFB + c];
-    }
+    const double v = (row >= cj) ? X[(row - cj) * kTiLdX + c] : 0.0;
     Rinv[(long long)(cj + c) * ldr + row] = v;
   }
 }
@@ -734,7 +787,7 @@ int chol_fast(const double* G, long long ldg, int m, double shift, double* L, lo
               double* Rinv, long long ldr, double* Dinv, double* status, cudaStream_t st) {
   const size_t smem1 = ((size_t)std::max(m, kFB) * kFL + kFB * (kFB + 1)) * sizeof(double);
   const int nblk = (m + kFB - 1) / kFB;
-  const size_t smem2 = ((size_t)nblk + 1) * kFB * kFB * sizeof(double);
+  const size_t smem2 = ((size_t)nblk * kFB * kTiLdX + kFB * kTiLdL + 2 * kFB * kTiLdX) * sizeof(double);
   if (smem1 > device_info().max_smem - 4096 || smem2 > device_info().max_smem - 1024) return -1;
   static size_t attr1[16] = {}, attr2[16] = {};
   int dev = 0;
@@ -748,11 +801,16 @@ int chol_fast(const double* G, long long ldg, int m, double shift, double* L, lo
                          (int)smem2);
     attr2[dev] = smem2;
   }
+  static const bool timers = getenv("PSD_CHOL_TIMERS") != nullptr;
+  if (timers) {
+    const long long z[6] = {0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbolAsync(g_chol_t, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+  }
   chol_blocked_kernel<<<1, 256, smem1, st>>>(G, ldg, m, shift, L, ldl, Dinv, status);
   count_launch();
   tri_inv_blocked_kernel<<<nblk, 256, smem2, st>>>(L, ldl, m, Dinv, Rinv, ldr);
   count_launch();
-  if (getenv("PSD_CHOL_TIMERS")) {
+  if (timers) {
     long long h[6];
     cudaStreamSynchronize(st);
     cudaMemcpyFromSymbol(h, g_chol_t, sizeof(h));
