@@ -43,7 +43,7 @@ struct JacobiArgs {
   double* jbuf;     // P × kJS²
   double* sbuf;     // P × kJS²
   int* counters;    // per-sweep rotation counts (zeroed)
-  unsigned* barrier;  // grid barrier counter (zeroed)
+  int* flags;       // dataflow flags: sflag[P], aflag[P²], vflag[P·vch], jread[2P] (zeroed)
   double* norm;     // [0] = ‖A‖_F
   int* out;         // [0] = sweeps (or −1), [1] = 1 if result is in b
   int m, nblk, max_sweeps;
@@ -191,6 +191,38 @@ PSD_DEVINL void mm32_coord(int j, int e, int& row, int& col) {
   col = (warp >> 2) * 16 + 8 * j + 2 * (lane & 3) + e;
 }
 
+// ---- dataflow synchronisation (no grid-wide barrier) -----------------------
+PSD_DEVINL void flag_wait(const int* f, int target) {
+  int v;
+  unsigned spins = 0;
+  do {
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+    if (++spins > (1u << 26)) __trap();   // a dependency that never resolves: fail loudly
+  } while (v < target);
+}
+PSD_DEVINL void flag_set(int* f, int v) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(f), "r"(v) : "memory");
+}
+
+// pair index of block x in round R (inverse of circle_pair)
+PSD_DEVINL int pair_of(int nblk, int R, int x) {
+  const int M = nblk - 1, r = R % M;
+  if (x == M) return 0;
+  if (x == r) return 0;
+  // x = (r + i) mod M  or  x = (r − i) mod M  for i ∈ [1, P)
+  const int i1 = (x - r + M) % M;   // x = r + i1
+  return i1 < (nblk / 2) ? i1 : M - i1;
+}
+
+// One persistent cooperative kernel; every round R = sweep·rounds + r is a set
+// of tasks — P pair solves, P² A-items (J_aᵀ A_ab J_b), P·⌈m/64⌉ V-items
+// (V ← V·J) — spread over the CTAs.  Instead of grid barriers each task
+// waits only on the flags of the tasks it reads from:
+//   solve p (R):   the R−1 A-items holding its four blocks;
+//   A-item (a,b):  solves a, b of round R + the four R−1 A-items of its blocks;
+//   V-item (c,b):  solve b + the two R−1 V-items of its columns;
+// and a solve first waits until every reader of its J/S slot (R−2) is done.
 __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
   __shared__ __align__(16) double sm[5 * kJTile];
   double* S0 = sm;
@@ -201,89 +233,135 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
   __shared__ int ia[kJS], ib[kJS];
   __shared__ int stop_flag;
   const int m = A.m, nblk = A.nblk, P = nblk / 2, rounds = nblk - 1;
+  const int vch = (m + 2 * kJS - 1) / (2 * kJS);       // 64-row V chunks
+  const int ntask = P + P * P + P * vch;
+  const int readers = (2 * P - 1) + vch;               // tasks reading J_p per round
   const double abs_tol = 1e-15 * A.norm[0];
-  unsigned gen = 0;
-  double* cur = A.a;
-  long long ldcur = A.lda;
-  double* nxt = A.b;
-  long long ldnxt = m;
-  int in_b = 0;
+  double* buf[2] = {A.a, A.b};
+  const long long ldb[2] = {A.lda, (long long)m};
+  int* sflag = A.flags;
+  int* aflag = sflag + P;
+  int* vflag = aflag + P * P;
+  int* jread = vflag + P * vch;                        // [2][P]
+  const int tid = threadIdx.x;
   int sweeps_done = -1;
   for (int sweep = 0; sweep < A.max_sweeps; ++sweep) {
     for (int r = 0; r < rounds; ++r) {
-      const long long t0 = clock64();
-      // ------------------------------------------------------------- solve
-      if ((int)blockIdx.x < P) {
-        const int pair = blockIdx.x;
-        if (threadIdx.x < kJS) ia[threadIdx.x] = sub_index(nblk, r, pair, threadIdx.x);
-        __syncthreads();
-        for (int e = threadIdx.x; e < kJS * kJS; e += kJT) {
-          const int i = e / kJS, j = e % kJS;
-          const int gi = ia[i], gj = ia[j];
-          S0[i * kJLd + j] = (gi < m && gj < m) ? cur[(long long)gi * ldcur + gj] : 0.0;
-          V0[i * kJLd + j] = (i == j) ? 1.0 : 0.0;
-        }
-        __syncthreads();
-        int rots = 0;
-        const bool full = (r == 0) || (P == 1);
-        const int inner_sweeps = (P == 1) ? 40 : 1;
-        double *Sc = S0, *Vc = V0, *Sn = S1, *Vn = V1;
-        for (int isw = 0; isw < inner_sweeps; ++isw) {
-          int srot = 0;
-          const int nsteps = full ? kJS - 1 : kJB;
-          for (int ir = 0; ir < nsteps; ++ir) {
-            const int nr = jacobi_step(Sc, Vc, Sn, Vn, full, ir, abs_tol);
-            if (nr) {
-              double* tp = Sc;
-              Sc = Sn;
-              Sn = tp;
-              tp = Vc;
-              Vc = Vn;
-              Vn = tp;
+      const int R = sweep * rounds + r;
+      const double* cur = buf[R & 1];
+      const long long ldc = ldb[R & 1];
+      double* nxt = buf[(R + 1) & 1];
+      const long long ldn = ldb[(R + 1) & 1];
+      double* Jslot = A.jbuf + (size_t)(R & 1) * P * kJS * kJS;
+      double* Sslot = A.sbuf + (size_t)(R & 1) * P * kJS * kJS;
+      for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
+        if (task < P) {
+          // ------------------------------------------------------- solve
+          const int pair = task;
+          const long long tw0 = clock64();
+          if (tid == 0) {
+            if (R >= 2) flag_wait(&jread[(R & 1) * P + pair], (R / 2) * readers);
+            if (R >= 1) {
+              int ba, bb;
+              circle_pair(nblk, r, pair, ba, bb);
+              const int pa = pair_of(nblk, R - 1, ba), pb = pair_of(nblk, R - 1, bb);
+              flag_wait(&aflag[pa * P + pa], R);
+              flag_wait(&aflag[pa * P + pb], R);
+              flag_wait(&aflag[pb * P + pa], R);
+              flag_wait(&aflag[pb * P + pb], R);
             }
-            srot += nr;
           }
-          rots += srot;
-          if (srot == 0) break;
-        }
-        double* J = A.jbuf + (size_t)pair * kJS * kJS;
-        double* So = A.sbuf + (size_t)pair * kJS * kJS;
-        for (int e = threadIdx.x; e < kJS * kJS; e += kJT) {
-          J[e] = Vc[(e / kJS) * kJLd + e % kJS];
-          So[e] = Sc[(e / kJS) * kJLd + e % kJS];
-        }
-        if (threadIdx.x == 0 && rots > 0) atomicAdd(&A.counters[sweep], rots);
-      }
-      const long long t1 = clock64();
-      grid_barrier(A.barrier, gen);
-      const long long t2 = clock64();
-      // ------------------------------------------------------------- apply
-      const int vchunks = (m + kJS - 1) / kJS;
-      const int items = P * P + P * vchunks;
-      for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        double c[2][2];
-        if (it < P * P) {
-          const int pa = it / P, pb = it % P;
-          if (threadIdx.x < kJS) {
-            ia[threadIdx.x] = sub_index(nblk, r, pa, threadIdx.x);
-            ib[threadIdx.x] = sub_index(nblk, r, pb, threadIdx.x);
+          if (tid < kJS) ia[tid] = sub_index(nblk, r, pair, tid);
+          __syncthreads();
+          const long long tw1 = clock64();
+          for (int e = tid; e < kJS * kJS; e += kJT) {
+            const int i = e / kJS, j = e % kJS;
+            const int gi = ia[i], gj = ia[j];
+            S0[i * kJLd + j] = (gi < m && gj < m) ? __ldcg(cur + (long long)gi * ldc + gj) : 0.0;
+            V0[i * kJLd + j] = (i == j) ? 1.0 : 0.0;
           }
           __syncthreads();
+          const long long tw2 = clock64();
+          int rots = 0;
+          const bool full = (r == 0) || (P == 1);
+          const int inner_sweeps = (P == 1) ? 40 : 1;
+          double *Sc = S0, *Vc = V0, *Sn = S1, *Vn = V1;
+          for (int isw = 0; isw < inner_sweeps; ++isw) {
+            int srot = 0;
+            const int nsteps = full ? kJS - 1 : kJB;
+            for (int ir = 0; ir < nsteps; ++ir) {
+              const int nr = jacobi_step(Sc, Vc, Sn, Vn, full, ir, abs_tol);
+              if (nr) {
+                double* tp = Sc;
+                Sc = Sn;
+                Sn = tp;
+                tp = Vc;
+                Vc = Vn;
+                Vn = tp;
+              }
+              srot += nr;
+            }
+            rots += srot;
+            if (srot == 0) break;
+          }
+          double* J = Jslot + (size_t)pair * kJS * kJS;
+          double* So = Sslot + (size_t)pair * kJS * kJS;
+          for (int e = tid; e < kJS * kJS; e += kJT) {
+            J[e] = Vc[(e / kJS) * kJLd + e % kJS];
+            So[e] = Sc[(e / kJS) * kJLd + e % kJS];
+          }
+          __syncthreads();
+          if (tid == 0) {
+            if (rots > 0) atomicAdd(&A.counters[sweep], rots);
+            flag_set(&sflag[pair], R + 1);
+            if (A.timers && pair == 0) {
+              A.timers[0] += tw1 - tw0;
+              A.timers[1] += tw2 - tw1;
+              A.timers[2] += clock64() - tw2;
+            }
+          }
+        } else if (task < P + P * P) {
+          // ------------------------------------------------------- A-item
+          const int it = task - P;
+          const int pa = it / P, pb = it % P;
+          const long long tw0 = clock64();
+          if (tid < kJS) {
+            ia[tid] = sub_index(nblk, r, pa, tid);
+            ib[tid] = sub_index(nblk, r, pb, tid);
+          }
+          if (tid == 0) {
+            flag_wait(&sflag[pa], R + 1);
+            flag_wait(&sflag[pb], R + 1);
+            if (R >= 1) {
+              int a0, a1, b0, b1;
+              circle_pair(nblk, r, pa, a0, a1);
+              circle_pair(nblk, r, pb, b0, b1);
+              const int qa0 = pair_of(nblk, R - 1, a0), qa1 = pair_of(nblk, R - 1, a1);
+              const int qb0 = pair_of(nblk, R - 1, b0), qb1 = pair_of(nblk, R - 1, b1);
+              flag_wait(&aflag[qa0 * P + qb0], R);
+              flag_wait(&aflag[qa0 * P + qb1], R);
+              flag_wait(&aflag[qa1 * P + qb0], R);
+              flag_wait(&aflag[qa1 * P + qb1], R);
+            }
+          }
+          __syncthreads();
+          const long long tw1 = clock64();
+          double c[2][2];
           if (pa == pb) {
-            const double* Sp = A.sbuf + (size_t)pa * kJS * kJS;
-            for (int e = threadIdx.x; e < kJS * kJS; e += kJT) {
+            const double* Sp = Sslot + (size_t)pa * kJS * kJS;
+            for (int e = tid; e < kJS * kJS; e += kJT) {
               const int gi = ia[e / kJS], gj = ib[e % kJS];
-              if (gi < m && gj < m) nxt[(long long)gi * ldnxt + gj] = Sp[e];
+              if (gi < m && gj < m) nxt[(long long)gi * ldn + gj] = __ldcg(Sp + e);
             }
           } else {
-            const double* Ja = A.jbuf + (size_t)pa * kJS * kJS;
-            const double* Jb = A.jbuf + (size_t)pb * kJS * kJS;
-            for (int e = threadIdx.x; e < kJS * kJS; e += kJT) {
+            const double* Ja = Jslot + (size_t)pa * kJS * kJS;
+            const double* Jb = Jslot + (size_t)pb * kJS * kJS;
+            for (int e = tid; e < kJS * kJS; e += kJT) {
               const int i = e / kJS, j = e % kJS;
               const int gi = ia[i], gj = ib[j];
-              S0[i * kJLd + j] = (gi < m && gj < m) ? cur[(long long)gi * ldcur + gj] : 0.0;
-              V0[i * kJLd + j] = Ja[e];
-              X[i * kJLd + j] = Jb[e];
+              S0[i * kJLd + j] = (gi < m && gj < m) ? __ldcg(cur + (long long)gi * ldc + gj) : 0.0;
+              V0[i * kJLd + j] = __ldcg(Ja + e);
+              X[i * kJLd + j] = __ldcg(Jb + e);
             }
             __syncthreads();
             mm32_dmma(V0, true, S0, c);  // J_aᵀ T
@@ -304,62 +382,83 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
                 int row, col;
                 mm32_coord(j, e, row, col);
                 const int gi = ia[row], gj = ib[col];
-                if (gi < m && gj < m) nxt[(long long)gi * ldnxt + gj] = c[j][e];
+                if (gi < m && gj < m) nxt[(long long)gi * ldn + gj] = c[j][e];
               }
           }
-        } else {
-          const int vb = it - P * P;
-          const int pb = vb % P;
-          const int r0 = (vb / P) * kJS;
-          if (threadIdx.x < kJS) ib[threadIdx.x] = sub_index(nblk, r, pb, threadIdx.x);
           __syncthreads();
-          const double* Jb = A.jbuf + (size_t)pb * kJS * kJS;
-          for (int e = threadIdx.x; e < kJS * kJS; e += kJT) {
-            const int i = e / kJS, j = e % kJS;
-            const int gr = r0 + i, gj = ib[j];
-            S0[i * kJLd + j] = (gr < m && gj < m) ? A.v[(long long)gr * A.ldv + gj] : 0.0;
-            X[i * kJLd + j] = Jb[e];
+          if (tid == 0) {
+            __threadfence();
+            atomicAdd(&jread[(R & 1) * P + pa], 1);
+            if (pb != pa) atomicAdd(&jread[(R & 1) * P + pb], 1);
+            flag_set(&aflag[pa * P + pb], R + 1);
+            if (A.timers && it == 1) {
+              A.timers[3] += tw1 - tw0;
+              A.timers[4] += clock64() - tw1;
+            }
+          }
+        } else {
+          // ------------------------------------------------------- V-item
+          const int vb = task - P - P * P;
+          const int pb = vb % P, vc = vb / P;
+          if (tid < kJS) ib[tid] = sub_index(nblk, r, pb, tid);
+          if (tid == 0) {
+            flag_wait(&sflag[pb], R + 1);
+            if (R >= 1) {
+              int b0, b1;
+              circle_pair(nblk, r, pb, b0, b1);
+              flag_wait(&vflag[vc * P + pair_of(nblk, R - 1, b0)], R);
+              flag_wait(&vflag[vc * P + pair_of(nblk, R - 1, b1)], R);
+            }
           }
           __syncthreads();
-          mm32_dmma(S0, false, X, c);
-#pragma unroll
-          for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              int row, col;
-              mm32_coord(j, e, row, col);
-              const int gr = r0 + row, gj = ib[col];
-              if (gr < m && gj < m) A.v[(long long)gr * A.ldv + gj] = c[j][e];
+          const double* Jb = Jslot + (size_t)pb * kJS * kJS;
+          for (int e = tid; e < kJS * kJS; e += kJT) X[(e / kJS) * kJLd + e % kJS] = __ldcg(Jb + e);
+          for (int h = 0; h < 2; ++h) {
+            const int r0 = vc * 2 * kJS + h * kJS;
+            if (r0 >= m) break;
+            double c[2][2];
+            for (int e = tid; e < kJS * kJS; e += kJT) {
+              const int i = e / kJS, j = e % kJS;
+              const int gr = r0 + i, gj = ib[j];
+              S0[i * kJLd + j] = (gr < m && gj < m) ? __ldcg(A.v + (long long)gr * A.ldv + gj) : 0.0;
             }
+            __syncthreads();
+            mm32_dmma(S0, false, X, c);
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                int row, col;
+                mm32_coord(j, e, row, col);
+                const int gr = r0 + row, gj = ib[col];
+                if (gr < m && gj < m) A.v[(long long)gr * A.ldv + gj] = c[j][e];
+              }
+            __syncthreads();
+          }
+          if (tid == 0) {
+            __threadfence();
+            atomicAdd(&jread[(R & 1) * P + pb], 1);
+            flag_set(&vflag[vc * P + pb], R + 1);
+          }
         }
         __syncthreads();
       }
-      const long long t3 = clock64();
-      grid_barrier(A.barrier, gen);
-      if (A.timers && blockIdx.x == 0 && threadIdx.x == 0) {
-        A.timers[0] += t1 - t0;
-        A.timers[1] += t2 - t1;
-        A.timers[2] += t3 - t2;
-        A.timers[3] += clock64() - t3;
-      }
-      double* tp = cur;
-      cur = nxt;
-      nxt = tp;
-      const long long tl = ldcur;
-      ldcur = ldnxt;
-      ldnxt = tl;
-      in_b ^= 1;
     }
-    if (threadIdx.x == 0) stop_flag = (*((volatile int*)&A.counters[sweep]) == 0);
+    // convergence: every solve of this sweep is done once its last round's flags are up
+    const int Rlast = sweep * rounds + rounds - 1;
+    if (tid == 0) {
+      for (int p = 0; p < P; ++p) flag_wait(&sflag[p], Rlast + 1);
+      stop_flag = (*((volatile int*)&A.counters[sweep]) == 0);
+    }
     __syncthreads();
     if (stop_flag) {
       sweeps_done = sweep + 1;
       break;
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && tid == 0) {
     A.out[0] = sweeps_done;
-    A.out[1] = in_b;
+    A.out[1] = sweeps_done > 0 ? ((sweeps_done * rounds) & 1) : 0;
   }
 }
 
@@ -395,10 +494,16 @@ static void jacobi_geometry(int m, int& nblk, int& P) {
   P = nblk / 2;
 }
 
+static int jacobi_nflags(int m, int P) {
+  const int vch = (m + 2 * kJS - 1) / (2 * kJS);
+  return P + P * P + P * vch + 2 * P;
+}
+
 size_t jacobi_ws_elems(int m) {
   int nblk, P;
   jacobi_geometry(m, nblk, P);
-  return (size_t)m * m + (size_t)2 * P * kJS * kJS + 8 + kJacobiMaxSweeps + 8;
+  return (size_t)m * m + (size_t)4 * P * kJS * kJS + 8 + kJacobiMaxSweeps + 8 +
+         (size_t)(jacobi_nflags(m, P) + 1) / 2 + 8;
 }
 
 int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long long ldv,
@@ -418,24 +523,25 @@ int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long
   A.b = ws;
   A.v = v;
   A.ldv = ldv;
-  A.jbuf = ws + (size_t)m * m;
-  A.sbuf = A.jbuf + (size_t)P * kJS * kJS;
-  A.norm = A.sbuf + (size_t)P * kJS * kJS;
+  A.jbuf = ws + (size_t)m * m;                    // [2 slots][P] rotation products
+  A.sbuf = A.jbuf + (size_t)2 * P * kJS * kJS;     // [2 slots][P] rotated subproblems
+  A.norm = A.sbuf + (size_t)2 * P * kJS * kJS;
   int* ints = reinterpret_cast<int*>(A.norm + 8);
   A.counters = ints;
-  A.barrier = reinterpret_cast<unsigned*>(ints + kJacobiMaxSweeps);
   A.out = ints + kJacobiMaxSweeps + 2;
+  A.flags = ints + kJacobiMaxSweeps + 8;
+  const int nflags = jacobi_nflags(m, P);
   A.m = m;
   A.nblk = nblk;
   A.max_sweeps = kJacobiMaxSweeps;
   A.timers = nullptr;
   static long long* dtimers = nullptr;
   if (getenv("PSD_JACOBI_TIMERS")) {
-    if (!dtimers) cudaMalloc(&dtimers, 4 * sizeof(long long));
-    cudaMemsetAsync(dtimers, 0, 4 * sizeof(long long), st);
+    if (!dtimers) cudaMalloc(&dtimers, 6 * sizeof(long long));
+    cudaMemsetAsync(dtimers, 0, 6 * sizeof(long long), st);
     A.timers = dtimers;
   }
-  cudaMemsetAsync(ints, 0, (kJacobiMaxSweeps + 4) * sizeof(int), st);
+  cudaMemsetAsync(ints, 0, (kJacobiMaxSweeps + 8 + nflags) * sizeof(int), st);
   set_identity(v, ldv, m, st);
   jacobi_norm_kernel<<<1, 1024, 0, st>>>(a, lda, m, A.norm);
   count_launch();
@@ -448,9 +554,9 @@ int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_persistent_kernel, kJT, 0);
     max_blocks[dev] = std::max(1, per_sm) * device_info().sms;
   }
-  const int vchunks = (m + kJS - 1) / kJS;
-  const int items = P * P + P * vchunks;
-  const int grid = std::max(P, std::min({items, max_blocks[dev], device_info().sms}));
+  const int vch = (m + 2 * kJS - 1) / (2 * kJS);
+  const int tasks = P + P * P + P * vch;
+  const int grid = std::max(1, std::min({tasks, max_blocks[dev], device_info().sms}));
   void* args[] = {&A};
   if (cudaLaunchCooperativeKernel((const void*)jacobi_persistent_kernel, dim3(grid), dim3(kJT),
                                   args, 0, st) != cudaSuccess)
@@ -463,10 +569,11 @@ int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long
   count_launch();
   if (out[1]) copy_matrix(ws, m, a, lda, m, m, st);
   if (A.timers) {
-    long long h[4];
+    long long h[6];
     cudaMemcpy(h, A.timers, sizeof(h), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "jacobi m=%d sweeps=%d grid=%d cycles: solve %lld bar1 %lld apply %lld bar2 %lld\n",
-            m, out[0], grid, h[0], h[1], h[2], h[3]);
+    fprintf(stderr,
+            "jacobi m=%d sweeps=%d grid=%d cycles: solve0 wait %lld load %lld compute %lld | item(0,1) wait %lld work %lld\n",
+            m, out[0], grid, h[0], h[1], h[2], h[3], h[4]);
   }
   return out[0];
 }
