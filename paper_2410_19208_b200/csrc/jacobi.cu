@@ -47,6 +47,7 @@ struct JacobiArgs {
   double* norm;     // [0] = ‖A‖_F
   int* out;         // [0] = sweeps (or −1), [1] = 1 if result is in b
   int m, nblk, max_sweeps;
+  int inner;        // inner sweeps per pair solve
   long long* timers;  // optional: block 0 clock64 per phase [solve, bar1, apply, bar2]
 };
 
@@ -200,8 +201,9 @@ PSD_DEVINL void flag_wait(const int* f, int target) {
     if (++spins > (1u << 26)) __trap();   // a dependency that never resolves: fail loudly
   } while (v < target);
 }
+// Called by thread 0 after a __syncthreads that orders the CTA's data writes
+// before it; st.release is cumulative over them (PTX memory model).
 PSD_DEVINL void flag_set(int* f, int v) {
-  __threadfence();
   asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(f), "r"(v) : "memory");
 }
 
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
           const long long tw2 = clock64();
           int rots = 0;
           const bool full = (r == 0) || (P == 1);
-          const int inner_sweeps = (P == 1) ? 40 : 1;
+          const int inner_sweeps = (P == 1) ? 40 : A.inner;
           double *Sc = S0, *Vc = V0, *Sn = S1, *Vn = V1;
           for (int isw = 0; isw < inner_sweeps; ++isw) {
             int srot = 0;
@@ -387,7 +389,6 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
           }
           __syncthreads();
           if (tid == 0) {
-            __threadfence();
             atomicAdd(&jread[(R & 1) * P + pa], 1);
             if (pb != pa) atomicAdd(&jread[(R & 1) * P + pb], 1);
             flag_set(&aflag[pa * P + pb], R + 1);
@@ -436,7 +437,6 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
             __syncthreads();
           }
           if (tid == 0) {
-            __threadfence();
             atomicAdd(&jread[(R & 1) * P + pb], 1);
             flag_set(&vflag[vc * P + pb], R + 1);
           }
@@ -534,6 +534,10 @@ int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long
   A.m = m;
   A.nblk = nblk;
   A.max_sweeps = kJacobiMaxSweeps;
+  {
+    const char* e = getenv("PSD_JACOBI_INNER");
+    A.inner = e ? std::max(1, atoi(e)) : 1;
+  }
   A.timers = nullptr;
   static long long* dtimers = nullptr;
   if (getenv("PSD_JACOBI_TIMERS")) {
