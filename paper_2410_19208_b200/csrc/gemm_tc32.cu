@@ -55,6 +55,21 @@ PSD_DEVINL void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// mbarrier wait that traps instead of hanging if a phase never completes
+// (a mis-programmed pipeline fails loudly rather than wedging the GPU).
+PSD_DEVINL void mbar_wait_t(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0, spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (++spins > (1u << 24)) __trap();
+  }
+}
+
 PSD_DEVINL uint32_t tmem_cols_for(int n) {
   uint32_t c = 32;
   while ((int)c < n) c <<= 1;
@@ -117,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < nkb; ++i) {
         const int s = i % p.stages;
         const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
-        mbar_wait(smem_u32(&empty_bar[s]), ph ^ 1u);
+        mbar_wait_t(smem_u32(&empty_bar[s]), ph ^ 1u);
         const uint32_t fb = smem_u32(&full_bar[s]);
         mbar_expect_tx(fb, st_bytes);
         const uint32_t sA = sbase + s * st_bytes;
@@ -138,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < nkb; ++i) {
         const int s = i % p.stages;
         const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
-        mbar_wait(smem_u32(&full_bar[s]), ph);
+        mbar_wait_t(smem_u32(&full_bar[s]), ph);
         tc_fence_after();
         const uint32_t sA = sbase + s * st_bytes;
         const uint32_t sB = sA + 2 * a_bytes;
@@ -163,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     const int i = m0 + r;
-    mbar_wait(smem_u32(&acc_bar), 0);
+    mbar_wait_t(smem_u32(&acc_bar), 0);
     tc_fence_after();
     const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
     if (p.mode == PARTIAL) {
@@ -209,6 +224,169 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tcols)
+                 : "memory");
+  }
+}
+
+// ---- CTA-pair variant (cta_group::2) for the PARTIAL (panel) mode ----------
+// A pair of CTAs on one TPC computes a 256 × n_tot tile: each CTA streams its
+// own 128 rows of A and HALF of every B box (bn/2 rows), the leader issues
+// tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' shared memory, and
+// each CTA's TMEM receives its 128 rows.  Per SM this halves the B bytes
+// streamed and read per MMA.
+PSD_DEVINL uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+PSD_DEVINL uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+PSD_DEVINL void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+PSD_DEVINL void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+PSD_DEVINL void mma_tf32_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+PSD_DEVINL void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    tc32_gemm2_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
+                      const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], acc_bar;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int bn_tot = p.bn * p.n_mma;
+  const int hb = p.bn / 2;                       // B rows per CTA per MMA
+  int u = blockIdx.x >> 1;
+  const int ng = u % p.n_groups;
+  u /= p.n_groups;
+  const int split = u % p.splits;
+  const int mp = u / p.splits;
+  const int m0 = mp * 2 * BM + (int)rank * BM, n0 = ng * bn_tot;
+  const int kb0 = split * p.kb_per_split;
+  const int nkb = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
+
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  const uint32_t a_bytes = BM * SWZ, b_bytes = (uint32_t)p.n_mma * hb * SWZ;
+  const uint32_t st_bytes = 2 * a_bytes + 2 * b_bytes;
+  const uint32_t tcols = tmem_cols_for(bn_tot);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    mbar_init(smem_u32(&acc_bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tma_prefetch_desc(&mAh);
+    tma_prefetch_desc(&mAl);
+    tma_prefetch_desc(&mBh);
+    tma_prefetch_desc(&mBl);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "r"(tcols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % p.stages;
+        const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+        mbar_wait_t(smem_u32(&empty_bar[s]), ph ^ 1u);
+        const uint32_t fb_local = smem_u32(&full_bar[s]);
+        const uint32_t fb = map_to_rank(fb_local, 0);          // the leader's barrier
+        if (rank == 0) mbar_expect_tx(fb_local, 2 * st_bytes);  // both CTAs' bytes
+        const uint32_t sA = sbase + s * st_bytes;
+        const uint32_t sB = sA + 2 * a_bytes;
+        const int kc = (kb0 + i) * BK;
+        tma_load_2d_pair(sA, &mAh, kc, m0, fb);
+        tma_load_2d_pair(sA + a_bytes, &mAl, kc, m0, fb);
+        for (int h = 0; h < p.n_mma; ++h) {
+          const uint32_t off = (uint32_t)h * hb * SWZ;
+          const int nrow = n0 + h * p.bn + (int)rank * hb;
+          tma_load_2d_pair(sB + off, &mBh, kc, nrow, fb);
+          tma_load_2d_pair(sB + b_bytes + off, &mBl, kc, nrow, fb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.bn >> 3) << 17) |
+                             ((uint32_t)(2 * BM >> 4) << 24);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % p.stages;
+        const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+        mbar_wait_t(smem_u32(&full_bar[s]), ph);
+        tc_fence_after();
+        const uint32_t sA = sbase + s * st_bytes;
+        const uint32_t sB = sA + 2 * a_bytes;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t ah = smem_desc(sA + kk * 32), al = smem_desc(sA + a_bytes + kk * 32);
+          for (int h = 0; h < p.n_mma; ++h) {
+            const uint32_t off = (uint32_t)h * hb * SWZ + kk * 32;
+            const uint64_t bh = smem_desc(sB + off), bl = smem_desc(sB + b_bytes + off);
+            const uint32_t d = tmem + (uint32_t)(h * p.bn);
+            if (p.nprod >= 3) mma_tf32_pair(d, al, bh, idesc, (i | kk) != 0);
+            if (p.nprod >= 2) mma_tf32_pair(d, ah, bl, idesc, (p.nprod >= 3) || (i | kk) != 0);
+            mma_tf32_pair(d, ah, bh, idesc, (p.nprod >= 2) || (i | kk) != 0);
+          }
+        }
+        mma_commit_pair(smem_u32(&empty_bar[s]));   // frees slot s in both CTAs
+      }
+      mma_commit_pair(smem_u32(&acc_bar));          // both CTAs' accumulators complete
+    }
+  } else {
+    const int quad = warp & 3;
+    const int i = m0 + quad * 32 + lane;
+    mbar_wait_t(smem_u32(&acc_bar), 0);
+    tc_fence_after();
+    const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
+    for (int c0 = 0; c0 < bn_tot; c0 += 16) {
+      float v[16];
+      tmem_ld16(trow + (uint32_t)c0, v);
+      if (i >= p.M) continue;
+      float4* dst = reinterpret_cast<float4*>(p.out + (long long)split * p.split_stride +
+                                              (long long)i * p.ldo + n0 + c0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tcols)
                  : "memory");
   }
 }
@@ -495,9 +673,16 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
   p.m_tiles = (op.M + BM - 1) / BM;
   p.kblocks = (op.K + BK - 1) / BK;
   const int sms = device_info().sms;
+  // CTA pairs (cta_group::2) for the panel products unless disabled
+  static const bool pair_ok = [] {
+    const char* e = getenv("PSD_TC32_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  const bool pair = op.mode == PARTIAL && pair_ok;
   int splits = 1;
   if (op.mode == PARTIAL) {
-    const long long base = (long long)p.m_tiles * p.n_groups;
+    const long long base = (long long)(pair ? (op.M + 2 * BM - 1) / (2 * BM) : p.m_tiles) * p.n_groups;
+    const int slots = pair ? sms / 2 : sms;
     double best = 1e30;
     // TMEM accumulation is FP32: bound the K length of each split (its error
     // grows with it); the fp64 reduction over splits adds the chunks exactly.
@@ -509,7 +694,7 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     const int smax = std::max(smin, std::min(std::max(op.max_splits, smin), p.kblocks / 8));
     for (int s = smin; s <= smax; ++s) {
       const long long units = base * s;
-      const double t = (double)((units + sms - 1) / sms) / s + 0.01 * s;
+      const double t = (double)((units + slots - 1) / slots) / s + 0.01 * s;
       if (t < best - 1e-9) {
         best = t;
         splits = s;
@@ -531,7 +716,11 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
   splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;   // every split non-empty
   p.splits = splits;
   p.mode = op.mode;
-  const int sb = stage_bytes(p.bn, p.n_mma);
+  {
+    const char* e = getenv("PSD_TC32_NPROD");   // experiment knob: tf32 products per k-step
+    p.nprod = e ? std::max(1, std::min(3, atoi(e))) : 3;
+  }
+  const int sb = pair ? 2 * BM * SWZ + p.bn * p.n_mma * SWZ : stage_bytes(p.bn, p.n_mma);
   const int epi_bytes = op.mode == MIRROR ? 4 * 32 * 33 * 4 : 0;   // epilogue transpose tiles
   const int avail = (int)device_info().max_smem - 1024 - 2048 - epi_bytes;
   p.stages = std::min(8, avail / sb);
@@ -540,18 +729,41 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
 
   CUtensorMap mah, mal, mbh, mbl;
   const long long lda_lo = op.lda_lo ? op.lda_lo : op.lda;
+  const int brows = pair ? p.bn / 2 : p.bn;
   bool ok = map_f32(&mah, op.a_hi, op.K, op.M, op.lda, BM) && map_f32(&mal, op.a_lo, op.K, op.M, lda_lo, BM) &&
-            map_f32(&mbh, op.b_hi, op.K, op.N, op.ldb, p.bn) && map_f32(&mbl, op.b_lo, op.K, op.N, op.ldb, p.bn);
+            map_f32(&mbh, op.b_hi, op.K, op.N, op.ldb, brows) && map_f32(&mbl, op.b_lo, op.K, op.N, op.ldb, brows);
   if (!ok) return -5;
-  static size_t attr[16] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (attr[dev] < smem) {
-    cudaFuncSetAttribute(tc32_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[dev] = smem;
+  if (pair) {
+    static size_t attr2[16] = {};
+    if (attr2[dev] < smem) {
+      cudaFuncSetAttribute(tc32_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr2[dev] = smem;
+    }
+    const long long units = (long long)((op.M + 2 * BM - 1) / (2 * BM)) * p.n_groups * p.splits;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * units));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, tc32_gemm2_kernel, mah, mal, mbh, mbl, p) != cudaSuccess) return -6;
+  } else {
+    static size_t attr1[16] = {};
+    if (attr1[dev] < smem) {
+      cudaFuncSetAttribute(tc32_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr1[dev] = smem;
+    }
+    const long long units = (long long)p.m_tiles * p.n_groups * p.splits;
+    tc32_gemm_kernel<<<(unsigned)units, kThreads, smem, st>>>(mah, mal, mbh, mbl, p);
   }
-  const long long units = (long long)p.m_tiles * p.n_groups * p.splits;
-  tc32_gemm_kernel<<<(unsigned)units, kThreads, smem, st>>>(mah, mal, mbh, mbl, p);
   count_launch();
   if (op.mode == PARTIAL) {
     const long long total = (long long)op.M * op.N;

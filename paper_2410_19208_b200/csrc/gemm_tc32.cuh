@@ -24,7 +24,7 @@ namespace psd {
 namespace tc32 {
 
 constexpr int BM = 128;
-constexpr int SWZ = 64;          // smem row bytes = TMA/UMMA swizzle span
+constexpr int SWZ = 128;         // smem row bytes = TMA/UMMA swizzle span
 constexpr int BK = SWZ / 4;      // fp32 K elements per k-block
 constexpr int kThreads = 192;
 constexpr int kMaxN = 512;       // TMEM columns
@@ -38,6 +38,7 @@ struct Params {
   int m_tiles, n_groups, splits;
   int stages;
   int mode;
+  int nprod;            // tf32 products per k-step (3 = 3xTF32; fewer only for experiments)
   float* out;           // PARTIAL: out[split·split_stride + row·ldo + col]; MIRROR: C
   long long ldo, split_stride;
 };

@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 300 python tools/probe_c3.py 32768 256 16 1 fp32 > gpurun_out/probe_fp32b.log 2>&1 || { echo "probe failed"; tail gpurun_out/probe_fp32b.log; exit 1; }
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:tc32_gemm_kernel -s 2 -c 1 -o gpurun_out/tc32_sketch python tools/probe_c3.py 32768 256 16 1 fp32 > gpurun_out/ncu_tc32.log 2>&1; echo "ncu rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:tc32_gemm2_kernel -s 2 -c 1 -o gpurun_out/tc32_pair python tools/probe_c3.py 32768 256 16 1 fp32 > gpurun_out/ncu_tc32.log 2>&1; echo "ncu rc=$?"
 tail -3 gpurun_out/ncu_tc32.log
