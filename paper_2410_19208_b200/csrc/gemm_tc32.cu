@@ -13,14 +13,15 @@ namespace psd {
 namespace tc32 {
 
 // ---- tcgen05 / TMEM wrappers ----------------------------------------------
+template <int SW = SWZ>
 PSD_DEVINL uint64_t smem_desc(uint32_t saddr) {
-  // K-major, SWIZZLE_64B canonical layout: 8-row atoms of 64-byte rows (512 B),
-  // SBO = stride between atoms, LBO unused for swizzled K-major, version 1 (sm_100).
+  // K-major swizzled canonical layout: 8-row atoms of SW-byte rows, SBO =
+  // stride between atoms, LBO unused for swizzled K-major, version 1 (sm_100).
   uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
   d |= (uint64_t)1 << 16;
-  d |= (uint64_t)((8 * SWZ) >> 4) << 32;
+  d |= (uint64_t)((8 * SW) >> 4) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)(SWZ == 128 ? 2 : (SWZ == 64 ? 4 : 6)) << 61;
+  d |= (uint64_t)(SW == 128 ? 2 : (SW == 64 ? 4 : 6)) << 61;
   return d;
 }
 
@@ -76,10 +77,12 @@ PSD_DEVINL uint32_t tmem_cols_for(int n) {
   return c;
 }
 
+template <int SW>
 __global__ void __launch_bounds__(kThreads, 1)
     tc32_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
                      const Params p) {
+  constexpr int BKk = SW / 4;   // K elements per k-block for this swizzle
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], acc_bar;
   __shared__ uint32_t tmem_slot;
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t sbase = (sraw + 1023u) & ~1023u;
-  const uint32_t a_bytes = BM * SWZ, b_bytes = (uint32_t)bn_tot * SWZ;
+  const uint32_t a_bytes = BM * SW, b_bytes = (uint32_t)bn_tot * SW;
   const uint32_t st_bytes = 2 * a_bytes + 2 * b_bytes;
   const uint32_t tcols = tmem_cols_for(bn_tot);
 
@@ -137,11 +140,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(fb, st_bytes);
         const uint32_t sA = sbase + s * st_bytes;
         const uint32_t sB = sA + 2 * a_bytes;
-        const int kc = (kb0 + i) * BK;
+        const int kc = (kb0 + i) * BKk;
         tma_load_2d(sA, &mAh, kc, m0, fb);
         tma_load_2d(sA + a_bytes, &mAl, kc, m0, fb);
         for (int h = 0; h < p.n_mma; ++h) {
-          const uint32_t off = (uint32_t)h * p.bn * SWZ;
+          const uint32_t off = (uint32_t)h * p.bn * SW;
           tma_load_2d(sB + off, &mBh, kc, n0 + h * p.bn, fb);
           tma_load_2d(sB + b_bytes + off, &mBl, kc, n0 + h * p.bn, fb);
         }
@@ -158,11 +161,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sA = sbase + s * st_bytes;
         const uint32_t sB = sA + 2 * a_bytes;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t ah = smem_desc(sA + kk * 32), al = smem_desc(sA + a_bytes + kk * 32);
+        for (int kk = 0; kk < BKk / 8; ++kk) {
+          const uint64_t ah = smem_desc<SW>(sA + kk * 32), al = smem_desc<SW>(sA + a_bytes + kk * 32);
           for (int h = 0; h < p.n_mma; ++h) {
-            const uint32_t off = (uint32_t)h * p.bn * SWZ + kk * 32;
-            const uint64_t bh = smem_desc(sB + off), bl = smem_desc(sB + b_bytes + off);
+            const uint32_t off = (uint32_t)h * p.bn * SW + kk * 32;
+            const uint64_t bh = smem_desc<SW>(sB + off), bl = smem_desc<SW>(sB + b_bytes + off);
             const uint32_t d = tmem + (uint32_t)(h * p.bn);
             mma_tf32(d, al, bh, idesc, (i | kk) != 0);   // small terms first
             mma_tf32(d, ah, bl, idesc, 1u);
@@ -225,6 +228,169 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tcols)
                  : "memory");
+  }
+}
+
+// ---- persistent mirrored reconstruction ----------------------------------
+// C = sym(A·Bᵀ) written from the lower 128×256 tiles only (each element to
+// (i,j) and (j,i)).  One CTA per SM walks the lower tiles; the TMEM holds two
+// 256-column accumulators so the epilogue of tile t (4 warps, TMEM → 2×
+// coalesced stores) overlaps the MMAs of tile t+1, and the producer streams
+// operands across tile boundaries.
+PSD_DEVINL void lower_tile(int t, int m_tiles, int& mt, int& nt) {
+  // tiles of block-column nt: mt ∈ [2·nt, m_tiles)
+  nt = 0;
+  while (true) {
+    const int cnt = m_tiles - 2 * nt;
+    if (t < cnt) break;
+    t -= cnt;
+    ++nt;
+  }
+  mt = 2 * nt + t;
+}
+
+template <int SW>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc32_mirror_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                       const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
+                       const Params p, int ntiles) {
+  constexpr int BKk = SW / 4;
+  constexpr int BN = 256;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], accf_bar[2], acce_bar[2];
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  const uint32_t a_bytes = BM * SW, b_bytes = (uint32_t)BN * SW;
+  const uint32_t st_bytes = 2 * a_bytes + 2 * b_bytes;
+  const int nkb = p.kblocks;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&accf_bar[b]), 1);
+      mbar_init(smem_u32(&acce_bar[b]), 4);   // one arrival per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tma_prefetch_desc(&mAh);
+    tma_prefetch_desc(&mAl);
+    tma_prefetch_desc(&mBh);
+    tma_prefetch_desc(&mBl);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;   // global k-block counter across tiles
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int mt, nt;
+        lower_tile(t, p.m_tiles, mt, nt);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % p.stages;
+          const uint32_t ph = (uint32_t)(it / p.stages) & 1u;
+          mbar_wait_t(smem_u32(&empty_bar[s]), ph ^ 1u);
+          const uint32_t fb = smem_u32(&full_bar[s]);
+          mbar_expect_tx(fb, st_bytes);
+          const uint32_t sA = sbase + s * st_bytes;
+          const uint32_t sB = sA + 2 * a_bytes;
+          const int kc = kb * BKk;
+          tma_load_2d(sA, &mAh, kc, mt * BM, fb);
+          tma_load_2d(sA + a_bytes, &mAl, kc, mt * BM, fb);
+          tma_load_2d(sB, &mBh, kc, nt * BN, fb);
+          tma_load_2d(sB + b_bytes, &mBl, kc, nt * BN, fb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(BM >> 4) << 24);
+      int it = 0, j = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+        const int b = j & 1;
+        // wait until the epilogue drained this accumulator (its previous use: tile j−2)
+        mbar_wait_t(smem_u32(&acce_bar[b]), (((uint32_t)j >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(b * BN);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % p.stages;
+          const uint32_t ph = (uint32_t)(it / p.stages) & 1u;
+          mbar_wait_t(smem_u32(&full_bar[s]), ph);
+          tc_fence_after();
+          const uint32_t sA = sbase + s * st_bytes;
+          const uint32_t sB = sA + 2 * a_bytes;
+#pragma unroll
+          for (int kk = 0; kk < BKk / 8; ++kk) {
+            const uint64_t ah = smem_desc<SW>(sA + kk * 32), al = smem_desc<SW>(sA + a_bytes + kk * 32);
+            const uint64_t bh = smem_desc<SW>(sB + kk * 32), bl = smem_desc<SW>(sB + b_bytes + kk * 32);
+            mma_tf32(d, al, bh, idesc, (kb | kk) != 0);
+            mma_tf32(d, ah, bl, idesc, 1u);
+            mma_tf32(d, ah, bh, idesc, 1u);
+          }
+          mma_commit(smem_u32(&empty_bar[s]));
+        }
+        mma_commit(smem_u32(&accf_bar[b]));
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    float* tile = reinterpret_cast<float*>(smem_raw + (sbase - sraw) + p.stages * st_bytes) +
+                  (warp - 2) * 32 * 33;
+    const uint32_t tq = (uint32_t)(quad * 32) << 16;
+    int j = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+      int mt, nt;
+      lower_tile(t, p.m_tiles, mt, nt);
+      const int b = j & 1;
+      mbar_wait_t(smem_u32(&accf_bar[b]), ((uint32_t)j >> 1) & 1u);
+      tc_fence_after();
+      const int ib = mt * BM + quad * 32;
+      const int i = ib + lane;
+      const int n0 = nt * BN;
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        const int j0 = n0 + c0;
+        if (j0 >= p.N || j0 > ib + 31) break;          // block above the diagonal / outside
+        float v[32];
+        tmem_ld16(tmem + tq + (uint32_t)(b * BN + c0), *reinterpret_cast<float(*)[16]>(&v[0]));
+        tmem_ld16(tmem + tq + (uint32_t)(b * BN + c0 + 16), *reinterpret_cast<float(*)[16]>(&v[16]));
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int jj = j0 + e;
+          if (i < p.M && jj <= i && jj < p.N) p.out[(long long)jj * p.ldo + i] = v[e];
+          tile[lane * 33 + e] = v[e];
+        }
+        __syncwarp();
+        const int jj = j0 + lane;
+        for (int rr = 0; rr < 32; ++rr) {
+          const int ii = ib + rr;
+          if (ii < p.M && jj <= ii && jj < p.N) p.out[(long long)ii * p.ldo + jj] = tile[rr * 33 + lane];
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&acce_bar[b]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512) : "memory");
   }
 }
 
@@ -622,16 +788,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode32() {
 }
 
 bool map_f32(CUtensorMap* map, const float* ptr, long long cols, long long rows, long long ld,
-             int box_rows) {
+             int box_rows, int swz = tc32::SWZ) {
   auto fn = encode32();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
-  cuuint32_t box[2] = {(cuuint32_t)tc32::BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)(swz / 4), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE,
-            tc32::SWZ == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -671,7 +837,6 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
   n_tot = p.bn * p.n_mma;
   p.n_groups = (op.N + n_tot - 1) / n_tot;
   p.m_tiles = (op.M + BM - 1) / BM;
-  p.kblocks = (op.K + BK - 1) / BK;
   const int sms = device_info().sms;
   // CTA pairs (cta_group::2) for the panel products unless disabled
   static const bool pair_ok = [] {
@@ -679,6 +844,11 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     return !(e && e[0] == '0');
   }();
   const bool pair = op.mode == PARTIAL && pair_ok;
+  // the reconstruction (short K, store-bound) keeps 64-byte rows and 4 stages;
+  // the panel products stream 128-byte rows
+  const int sw = op.mode == MIRROR ? 64 : 128;
+  const int bk = sw / 4;
+  p.kblocks = (op.K + bk - 1) / bk;
   int splits = 1;
   if (op.mode == PARTIAL) {
     const long long base = (long long)(pair ? (op.M + 2 * BM - 1) / (2 * BM) : p.m_tiles) * p.n_groups;
@@ -720,7 +890,7 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     const char* e = getenv("PSD_TC32_NPROD");   // experiment knob: tf32 products per k-step
     p.nprod = e ? std::max(1, std::min(3, atoi(e))) : 3;
   }
-  const int sb = pair ? 2 * BM * SWZ + p.bn * p.n_mma * SWZ : stage_bytes(p.bn, p.n_mma);
+  const int sb = pair ? 2 * BM * sw + p.bn * p.n_mma * sw : 2 * BM * sw + 2 * p.bn * p.n_mma * sw;
   const int epi_bytes = op.mode == MIRROR ? 4 * 32 * 33 * 4 : 0;   // epilogue transpose tiles
   const int avail = (int)device_info().max_smem - 1024 - 2048 - epi_bytes;
   p.stages = std::min(8, avail / sb);
@@ -730,12 +900,22 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
   CUtensorMap mah, mal, mbh, mbl;
   const long long lda_lo = op.lda_lo ? op.lda_lo : op.lda;
   const int brows = pair ? p.bn / 2 : p.bn;
-  bool ok = map_f32(&mah, op.a_hi, op.K, op.M, op.lda, BM) && map_f32(&mal, op.a_lo, op.K, op.M, lda_lo, BM) &&
-            map_f32(&mbh, op.b_hi, op.K, op.N, op.ldb, brows) && map_f32(&mbl, op.b_lo, op.K, op.N, op.ldb, brows);
+  bool ok = map_f32(&mah, op.a_hi, op.K, op.M, op.lda, BM, sw) && map_f32(&mal, op.a_lo, op.K, op.M, lda_lo, BM, sw) &&
+            map_f32(&mbh, op.b_hi, op.K, op.N, op.ldb, brows, sw) && map_f32(&mbl, op.b_lo, op.K, op.N, op.ldb, brows, sw);
   if (!ok) return -5;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (pair) {
+  if (op.mode == MIRROR) {
+    static size_t attrm[16] = {};
+    if (attrm[dev] < smem) {
+      cudaFuncSetAttribute(tc32_mirror_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attrm[dev] = smem;
+    }
+    long long ntiles = 0;
+    for (int nt = 0; 2 * nt < p.m_tiles; ++nt) ntiles += p.m_tiles - 2 * nt;
+    const int grid = (int)std::min<long long>(ntiles, sms);
+    tc32_mirror_kernel<64><<<grid, kThreads, smem, st>>>(mah, mal, mbh, mbl, p, (int)ntiles);
+  } else if (pair) {
     static size_t attr2[16] = {};
     if (attr2[dev] < smem) {
       cudaFuncSetAttribute(tc32_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -756,13 +936,18 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, tc32_gemm2_kernel, mah, mal, mbh, mbl, p) != cudaSuccess) return -6;
   } else {
-    static size_t attr1[16] = {};
+    static size_t attr64[16] = {}, attr128[16] = {};
+    size_t* attr1 = sw == 64 ? attr64 : attr128;
     if (attr1[dev] < smem) {
-      cudaFuncSetAttribute(tc32_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(sw == 64 ? tc32_gemm_kernel<64> : tc32_gemm_kernel<128>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr1[dev] = smem;
     }
     const long long units = (long long)p.m_tiles * p.n_groups * p.splits;
-    tc32_gemm_kernel<<<(unsigned)units, kThreads, smem, st>>>(mah, mal, mbh, mbl, p);
+    if (sw == 64)
+      tc32_gemm_kernel<64><<<(unsigned)units, kThreads, smem, st>>>(mah, mal, mbh, mbl, p);
+    else
+      tc32_gemm_kernel<128><<<(unsigned)units, kThreads, smem, st>>>(mah, mal, mbh, mbl, p);
   }
   count_launch();
   if (op.mode == PARTIAL) {

@@ -24,8 +24,8 @@ namespace psd {
 namespace tc32 {
 
 constexpr int BM = 128;
-constexpr int SWZ = 128;         // smem row bytes = TMA/UMMA swizzle span
-constexpr int BK = SWZ / 4;      // fp32 K elements per k-block
+constexpr int SWZ = 128;         // smem row bytes (TMA/UMMA swizzle span) of the pair kernel
+constexpr int BK = SWZ / 4;      // fp32 K elements per k-block of the pair kernel
 constexpr int kThreads = 192;
 constexpr int kMaxN = 512;       // TMEM columns
 
@@ -43,7 +43,6 @@ struct Params {
   long long ldo, split_stride;
 };
 
-inline int stage_bytes(int bn, int n_mma) { return 2 * BM * SWZ + 2 * bn * n_mma * SWZ; }
 
 }  // namespace tc32
 }  // namespace psd
