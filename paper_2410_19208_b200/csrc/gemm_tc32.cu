@@ -249,8 +249,10 @@ PSD_DEVINL void lower_tile(int t, int m_tiles, int& mt, int& nt) {
   mt = 2 * nt + t;
 }
 
+constexpr int kMirrorEpi = 8;                       // epilogue warps (2 per TMEM lane quadrant)
+constexpr int kMirrorThreads = (2 + kMirrorEpi) * 32;
 template <int SW>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kMirrorThreads, 1)
     tc32_mirror_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                        const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
                        const Params p, int ntiles) {
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&accf_bar[b]), 1);
-      mbar_init(smem_u32(&acce_bar[b]), 4);   // one arrival per epilogue warp
+      mbar_init(smem_u32(&acce_bar[b]), kMirrorEpi);   // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tma_prefetch_desc(&mAh);
@@ -348,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quad = warp & 3;
+    const int half = (warp - 2) / 4;            // column half of the tile this warp stores
     float* tile = reinterpret_cast<float*>(smem_raw + (sbase - sraw) + p.stages * st_bytes) +
                   (warp - 2) * 32 * 33;
     const uint32_t tq = (uint32_t)(quad * 32) << 16;
@@ -361,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ib = mt * BM + quad * 32;
       const int i = ib + lane;
       const int n0 = nt * BN;
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
         const int j0 = n0 + c0;
         if (j0 >= p.N || j0 > ib + 31) break;          // block above the diagonal / outside
         float v[32];
@@ -891,7 +894,7 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     p.nprod = e ? std::max(1, std::min(3, atoi(e))) : 3;
   }
   const int sb = pair ? 2 * BM * sw + p.bn * p.n_mma * sw : 2 * BM * sw + 2 * p.bn * p.n_mma * sw;
-  const int epi_bytes = op.mode == MIRROR ? 4 * 32 * 33 * 4 : 0;   // epilogue transpose tiles
+  const int epi_bytes = op.mode == MIRROR ? kMirrorEpi * 32 * 33 * 4 : 0;   // epilogue transpose tiles
   const int avail = (int)device_info().max_smem - 1024 - 2048 - epi_bytes;
   p.stages = std::min(8, avail / sb);
   if (p.stages < 2) return -4;
@@ -914,7 +917,7 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     long long ntiles = 0;
     for (int nt = 0; 2 * nt < p.m_tiles; ++nt) ntiles += p.m_tiles - 2 * nt;
     const int grid = (int)std::min<long long>(ntiles, sms);
-    tc32_mirror_kernel<64><<<grid, kThreads, smem, st>>>(mah, mal, mbh, mbl, p, (int)ntiles);
+    tc32_mirror_kernel<64><<<grid, kMirrorThreads, smem, st>>>(mah, mal, mbh, mbl, p, (int)ntiles);
   } else if (pair) {
     static size_t attr2[16] = {};
     if (attr2[dev] < smem) {
