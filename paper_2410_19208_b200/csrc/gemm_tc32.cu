@@ -249,7 +249,7 @@ PSD_DEVINL void lower_tile(int t, int m_tiles, int& mt, int& nt) {
   mt = 2 * nt + t;
 }
 
-constexpr int kMirrorEpi = 8;                       // epilogue warps (2 per TMEM lane quadrant)
+constexpr int kMirrorEpi = 16;                      // epilogue warps (4 per TMEM lane quadrant)
 constexpr int kMirrorThreads = (2 + kMirrorEpi) * 32;
 template <int SW>
 __global__ void __launch_bounds__(kMirrorThreads, 1)
@@ -350,7 +350,8 @@ __global__ void __launch_bounds__(kMirrorThreads, 1)
     }
   } else {
     const int quad = warp & 3;
-    const int half = (warp - 2) / 4;            // column half of the tile this warp stores
+    const int half = (warp - 2) / 4;            // column slice of the tile this warp stores
+    constexpr int kSlice = BN / (kMirrorEpi / 4);
     float* tile = reinterpret_cast<float*>(smem_raw + (sbase - sraw) + p.stages * st_bytes) +
                   (warp - 2) * 32 * 33;
     const uint32_t tq = (uint32_t)(quad * 32) << 16;
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(kMirrorThreads, 1)
       const int ib = mt * BM + quad * 32;
       const int i = ib + lane;
       const int n0 = nt * BN;
-      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+      for (int c0 = half * kSlice; c0 < (half + 1) * kSlice; c0 += 32) {
         const int j0 = n0 + c0;
         if (j0 >= p.N || j0 > ib + 31) break;          // block above the diagonal / outside
         float v[32];
