@@ -489,13 +489,17 @@ def run_fp32_leg(a, torch, psd, pool, params, rng, dev, world):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     launches = 0
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
     e0.record()
     for i in range(a.steps):
+        marks[i].record()
         rep = psd.ran_proj(pool32[i % len(pool32)], params, rng, dtype="fp32")
         launches += rep.device_info["gpu_launches"]
+    marks[a.steps].record()
     e1.record()
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
+    per_step = sorted(marks[i].elapsed_time(marks[i + 1]) for i in range(a.steps))
     prof = plan.profile(enable=False, reset=True)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -507,6 +511,7 @@ def run_fp32_leg(a, torch, psd, pool, params, rng, dev, world):
     del pool32
     return {
         "value": world * a.steps / (ms / 1000.0), "unit": UNIT, "ms_per_step": ms / a.steps,
+        "step_ms_min_median_max": [per_step[0], per_step[len(per_step) // 2], per_step[-1]],
         "dtype": "f32 (3xTF32 tcgen05, FP32 TMEM accumulation in ≤4096-K chunks, FP64 QR/eigh)",
         "gpu_launches": launches,
         "stages_ms_per_projection": {k: round(v[0] / a.steps, 3) for k, v in prof.items() if v[1]},

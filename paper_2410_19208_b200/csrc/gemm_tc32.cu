@@ -669,7 +669,7 @@ __global__ void split_transpose_kernel(const double* __restrict__ P, long long n
 // stats[0] = max|x|, stats[1] = max|x − xᵀ|, ((int*)(stats+2))[0] bit0: not
 // bitwise symmetric, bit1: non-finite entry.
 constexpr int kSST = 64;
-__global__ void __launch_bounds__(256) symsplit_kernel(const float* __restrict__ x, long long n,
+__global__ void __launch_bounds__(256, 4) symsplit_kernel(const float* __restrict__ x, long long n,
                                                        long long ldx, long long npairs,
                                                        double* stats, float* __restrict__ hi,
                                                        float* __restrict__ lo, long long ldh, bool raw) {
@@ -968,7 +968,11 @@ void symsplit_f32(const float* x, long long n, long long ldx, double* stats, flo
   cudaMemsetAsync(stats, 0, 3 * sizeof(double), st);
   const long long nt = (n + tc32::kSST - 1) / tc32::kSST;
   const long long npairs = nt * (nt + 1) / 2;
-  const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * 4);
+  static const int per_sm = [] {
+    const char* e = getenv("PSD_SYMSPLIT_BPS");
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
+  const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * per_sm);
   tc32::symsplit_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats, hi, lo, ldh,
                                                           hi == nullptr);
   count_launch();

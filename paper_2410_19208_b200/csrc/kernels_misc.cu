@@ -19,7 +19,7 @@ constexpr int kSymT = 64;
 // is read straight into registers, so every element of X is read once
 // (diagonal tiles twice).  One atomic per block per statistic at the end.
 template <typename T>
-__global__ void __launch_bounds__(256) sym_stats_kernel(const T* __restrict__ x, long long n,
+__global__ void __launch_bounds__(256, 4) sym_stats_kernel(const T* __restrict__ x, long long n,
                                                         long long ldx, long long npairs,
                                                         double* stats) {
   __shared__ T tj[kSymT][kSymT + 1];
@@ -93,7 +93,7 @@ static void sym_stats_t(const T* x, long long n, long long ldx, double* stats, c
   cudaMemsetAsync(stats, 0, 3 * sizeof(double), st);
   const long long nt = (n + kSymT - 1) / kSymT;
   const long long npairs = nt * (nt + 1) / 2;
-  const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * 4);
+  const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * 6);
   sym_stats_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats);
   count_launch();
 }

@@ -1,6 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 120 python tools/probe_tc32.py 4096 2>&1 | grep -E "ALL OK|FAIL"
-for pf in 0 4 8 16; do
-PSD_TC32_PF=$pf timeout 300 python tools/probe_c3.py 32768 256 16 1 fp32 2>&1 | grep -E "sketch_gemm " | sed "s/^/pf=$pf /"
-done
-PSD_TC32_PF=8 PSD_TC32_NPROD=1 timeout 300 python tools/probe_c3.py 32768 256 16 1 fp32 2>&1 | grep -E "sketch_gemm " | sed "s/^/pf=8 nprod1 /"
+timeout 300 python bench.py --no-e2e --no-cpu-baseline --steps 8 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['fp32']['value'], d['fp32']['ms_per_step'], d['fp32']['step_ms_min_median_max'], d['fp32']['stages_ms_per_projection'])"
