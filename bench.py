@@ -521,8 +521,34 @@ def run_fp32_leg(a, torch, psd, pool, params, rng, dev, world):
             "tf32_tensor_tflops": 3.0 * eff_tf,
             "note": "3 tf32 MMAs (lo·hi, hi·lo, hi·hi) per FP32 product; effective = 2n²w/t",
         },
+        "roofline": fp32_roofline(3.0 * eff_tf),
         "parity": "≤1e-4 rel. Frobenius vs the FP64 path on the same fp32-rounded X (tests/test_gpu_fp32.py)",
     }
+
+
+def fp32_roofline(tf32_tflops):
+    """tf32 issue rate of the 3xTF32 sketch GEMM against the tf32 tensor peak:
+    MEASURED_PEAKS.json's bf16 burst / 2 (kind::tf32 runs the tcgen05 datapath
+    at half the f16 rate — 1.1 vs 2.25 PFLOP/s nominal in B200_PROFILING.md)."""
+    peak, src = None, None
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            peak = float(json.load(fh)["bf16_tflops"]) / 2.0
+            src = "MEASURED_PEAKS.json bf16_tflops (burst) / 2"
+    except Exception:
+        peak, src = 1100.0, "B200_PROFILING.md nominal tf32 dense 1.1 PFLOP/s (no MEASURED_PEAKS.json)"
+    return {"bound": "tensor", "achieved": tf32_tflops, "peak": peak, "unit": "TFLOP/s",
+            "frac": tf32_tflops / peak, "traffic": load_traffic32(),
+            "kernel": "tc32_gemm2_kernel (tcgen05.mma.cta_group::2.kind::tf32, TMA SW128, TMEM accumulators)",
+            "peak_source": src}
+
+
+def load_traffic32():
+    try:
+        with open(os.path.join(REPO, "profiles", "tc32_traffic.json")) as fh:
+            return json.load(fh).get("bytes_per_launch")
+    except Exception:
+        return None
 
 
 def run_e2e(a, torch, psd, x_dev, params, dev):
