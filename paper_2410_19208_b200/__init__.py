@@ -20,10 +20,13 @@ from .symmetric import (EigenDecomposition, eigh, exact_psd_projection, frobeniu
 from .sdls import SolveReport, SparseSdlsProblem, TrajectoryPoint, solve
 from .install import install, uninstall
 from . import workloads  # noqa: E402  (seeded HBM generators for the BASELINE configs)
+from . import experiments  # noqa: E402  (Monte-Carlo projection-error harness, §8 f3)
+from .experiments import projection_error_sweep  # noqa: E402
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "experiments", "projection_error_sweep",
     "AlphaTooSmall", "AsymmetricMatrixError", "ConvergenceFailure", "DeviceError",
     "DimensionMismatch", "InvalidParams", "NonSquareError", "PsdconeError", "RankDeficientSample",
     "DeviceRng", "METHODS", "ProjectionReport", "ProjectorConfig", "flops", "project", "ran_proj",

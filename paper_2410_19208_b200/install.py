@@ -44,6 +44,8 @@ _TARGETS = {
     ("psdcone.sdls", "solve"): "solve",
     ("psdcone.experiments", "ran_proj"): "ran_proj",
     ("psdcone.experiments", "ran_proj_scal"): "ran_proj_scal",
+    ("psdcone.experiments", "projection_error_sweep"): "projection_error_sweep",
+    ("psdcone", "projection_error_sweep"): "projection_error_sweep",
 }
 
 

@@ -206,6 +206,42 @@ def solver_cases():
               iterations=rep.iterations, exact_residual=rep.exact_feasibility_residual)
 
 
+def sweep_cases():
+    """Reference projection_error_sweep (experiments.py:78-137) and bounds (bounds.py)."""
+    from psdcone import bounds as rb
+    from psdcone import experiments as rx
+    codes = {"randomized": 0, "scaled_randomized": 1}
+    for name, n, l, q, k_grid, trials, seed in (
+        ("sweep_fourblock_q0", 64, 4, 0, (4, 8, 16), 2, 5),
+        ("sweep_fourblock_q1", 64, 4, 1, (8, 12), 2, 9),
+    ):
+        rows = rx.projection_error_sweep(n, rx.FOUR_BLOCK_BETAS, l, q, k_grid, trials, seed)
+        x = rx.four_block_matrix(n, rx.FOUR_BLOCK_BETAS, np.random.default_rng(seed))
+        _save(name, n=n, l=l, q=q, k_grid=np.array(k_grid), trials=trials, seed=seed, x=x,
+              k=np.array([r.k for r in rows]), method=np.array([codes[r.method] for r in rows]),
+              mean_frob=np.array([r.mean_frob_error for r in rows]),
+              mean_spec=np.array([r.mean_spectral_error for r in rows]),
+              frob_bound=np.array([np.nan if r.frob_bound is None else r.frob_bound for r in rows]),
+              spec_bound=np.array([r.spectral_bound for r in rows]))
+    # bounds on a generic spectrum (descending, mixed signs)
+    ev = np.sort(np.random.default_rng(3).standard_normal(40) * np.geomspace(10, 0.01, 40))[::-1]
+    spec = rb.SpectrumSummary.from_eigenvalues(ev)
+    vals = []
+    for k, l, q, alpha in ((3, 2, 0, 0.5), (10, 5, 0, 2.0), (10, 5, 1, 2.0), (20, 8, 2, 0.1)):
+        p = rb.BoundParams(k=k, l=l, q=q)
+        vals.append([k, l, q, alpha, rb.eps1(spec.sigmas, k, l), rb.eps2(spec.sigmas[k], k, l, q, 40),
+                     rb.frob_bound_unscaled(spec, p) if q == 0 else np.nan,
+                     rb.spectral_bound_unscaled(spec, p),
+                     rb.frob_bound_scaled(spec, p, alpha) if q == 0 else np.nan,
+                     rb.spectral_bound_scaled(spec, p, alpha)])
+    _save("bounds_generic", eigenvalues=ev, table=np.array(vals))
+
+
 if __name__ == "__main__":
-    main()
-    solver_cases()
+    import sys as _sys
+    if "--sweep-only" in _sys.argv:
+        sweep_cases()
+    else:
+        main()
+        solver_cases()
+        sweep_cases()
