@@ -3,6 +3,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm_tma.cuh"
@@ -18,6 +19,8 @@ template <int N8W, int ST>
 using TmaTN = TmaCfg<A_KM, B_KN, 64, 4, 2, 2, N8W, ST>;
 // (W·D)·Wᵀ mirrored SYRK, residual, Cholesky trailing update (A row-major, Bᵀ stored)
 using TmaNT = TmaCfg<A_MK, B_NK, 128, 4, 2, 4, 8, 6>;
+// mirrored SYRK with the smem-staged epilogue stored by the producer warpgroup
+using TmaNTs = TmaCfg<A_MK, B_NK, 128, 4, 2, 4, 8, 2, true>;
 
 namespace {
 
@@ -166,7 +169,14 @@ int gemm_f64_tma(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st)
   if (!tma_ok(op.A, op.lda) || !tma_ok(op.B, op.ldb)) return -2;
   if (op.a_layout == A_MK && op.b_layout == B_KN) return launch_panel<TmaNN>(op, ws, ws_elems, st);
   if (op.a_layout == A_KM && op.b_layout == B_KN) return launch_panel<TmaTN>(op, ws, ws_elems, st);
-  if (op.a_layout == A_MK && op.b_layout == B_NK) return launch<TmaNT>(op, ws, ws_elems, st);
+  if (op.a_layout == A_MK && op.b_layout == B_NK) {
+    static const bool staged = [] {
+      const char* e = getenv("PSD_STAGED_EPI");
+      return !(e && e[0] == '0');
+    }();
+    if (op.epi == EPI_MIRROR && staged) return launch<TmaNTs>(op, ws, ws_elems, st);
+    return launch<TmaNT>(op, ws, ws_elems, st);
+  }
   return -1;
 }
 

@@ -29,10 +29,15 @@
 
 namespace psd {
 
-template <int AL_, int BL_, int BM_, int WARPS_M_, int WARPS_N_, int M8W_, int N8W_, int STAGES_>
+template <int AL_, int BL_, int BM_, int WARPS_M_, int WARPS_N_, int M8W_, int N8W_, int STAGES_,
+          bool STAGED_EPI_ = false>
 struct TmaCfg {
   static constexpr int AL = AL_, BL = BL_, BM = BM_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
   static constexpr int M8W = M8W_, N8W = N8W_, STAGES = STAGES_;
+  // EPI_MIRROR through shared memory: consumers park the tile in smem and the
+  // three otherwise idle producer-warpgroup warps store it (both orientations,
+  // 256-byte rows) while the consumers run the next tile's MMAs.
+  static constexpr bool STAGED_EPI = STAGED_EPI_;
   static constexpr int BK = 16;
   static constexpr int BN = WARPS_N * N8W * 8;
   static constexpr int kConsumers = WARPS_M * WARPS_N;
@@ -43,7 +48,9 @@ struct TmaCfg {
   static constexpr int A_BYTES = BM * BK * 8;
   static constexpr int B_BYTES = BN * BK * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr size_t kSmem = (size_t)STAGES * STAGE_BYTES + 1024;
+  static constexpr int C_LD = BN + 1;  // staged tile row stride (doubles)
+  static constexpr size_t C_BYTES = STAGED_EPI ? (size_t)BM * C_LD * 8 : 0;
+  static constexpr size_t kSmem = (size_t)STAGES * STAGE_BYTES + C_BYTES + 1024;
   static_assert(BM == WARPS_M * M8W * 8, "BM must equal WARPS_M*M8W*8");
   static_assert(kConsumers % 4 == 0, "consumers form whole warpgroups");
   static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "swizzle atoms are 1 KiB");
@@ -201,15 +208,22 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[Cfg::STAGES];
   __shared__ __align__(8) uint64_t empty_bar[Cfg::STAGES];
+  __shared__ __align__(8) uint64_t cfull_bar, cfree_bar;   // staged mirror epilogue
   constexpr int STAGES = Cfg::STAGES, M8W = Cfg::M8W, N8W = Cfg::N8W;
+  constexpr int kStoreWarps = 3;
   const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool staged = Cfg::STAGED_EPI && p.epi == EPI_MIRROR;
+  double* Cs = reinterpret_cast<double*>(smem_raw + (smem_base - smem_u32(smem_raw)) +
+                                         (size_t)STAGES * Cfg::STAGE_BYTES);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(&full_bar[s]), 1);
       mbar_init(smem_u32(&empty_bar[s]), Cfg::kConsumers);
     }
+    mbar_init(smem_u32(&cfull_bar), Cfg::kConsumers);
+    mbar_init(smem_u32(&cfree_bar), kStoreWarps);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -247,6 +261,39 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
           }
         }
       }
+    } else if (staged && warp > Cfg::kConsumers) {
+      // ------------------------------------------------------ store warps
+      const int sw = warp - Cfg::kConsumers - 1;   // 0 .. kStoreWarps-1
+      int j = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const Unit un = decode_unit<Cfg>(p, u);
+        if (!unit_active<Cfg>(p, un)) continue;
+        mbar_wait(smem_u32(&cfull_bar), (uint32_t)j & 1u);
+        // (m, n) = (m0 + r, n0 + c), m ≥ n: C[m][n] (row m) and C[n][m] (row n)
+        for (int r = sw; r < Cfg::BM; r += kStoreWarps) {
+          const int m = un.m0 + r;
+          if (m >= p.M || m < p.win0 || m >= p.win1) continue;
+          double* crow = p.C + (long long)(m - p.win0) * p.ldc;
+#pragma unroll
+          for (int c = lane; c < Cfg::BN; c += 32) {
+            const int n = un.n0 + c;
+            if (n < p.N && n <= m) crow[n] = Cs[r * Cfg::C_LD + c];
+          }
+        }
+        for (int c = sw; c < Cfg::BN; c += kStoreWarps) {
+          const int n = un.n0 + c;
+          if (n >= p.N || n < p.win0 || n >= p.win1) continue;
+          double* crow = p.C + (long long)(n - p.win0) * p.ldc;
+#pragma unroll
+          for (int r = lane; r < Cfg::BM; r += 32) {
+            const int m = un.m0 + r;
+            if (m < p.M && m > n) crow[m] = Cs[r * Cfg::C_LD + c];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&cfree_bar));
+        ++j;
+      }
     }
     return;
   }
@@ -264,6 +311,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
   for (int j = 0; j < N8W; ++j) boff[j] = Cfg::A_BYTES + b_off<Cfg>(t, b_col<Cfg>(wn * N8W + j, g));
   double resid = 0.0;
   int it = 0;
+  int stage_j = 0;
   for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
     const Unit un = decode_unit<Cfg>(p, u);
     if (!unit_active<Cfg>(p, un)) continue;
@@ -303,6 +351,21 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
     }
 
     // ------------------------------------------------------------- epilogue
+    if (staged) {
+      mbar_wait(smem_u32(&cfree_bar), ((uint32_t)stage_j & 1u) ^ 1u);   // previous tile stored
+#pragma unroll
+      for (int i = 0; i < M8W; ++i) {
+        const int r = a_row<Cfg>(wm * M8W + i, g);
+#pragma unroll
+        for (int j = 0; j < N8W; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) Cs[r * Cfg::C_LD + b_col<Cfg>(wn * N8W + j, 2 * t + e)] = acc[i][j][e];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&cfull_bar));
+      ++stage_j;
+      continue;
+    }
     double* C = p.C + (long long)un.split * p.split_stride;
 #pragma unroll
     for (int i = 0; i < M8W; ++i) {

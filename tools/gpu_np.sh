@@ -1,2 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 300 python bench.py --no-e2e --no-cpu-baseline --steps 8 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['fp32']['value'], d['fp32']['ms_per_step'], d['fp32']['step_ms_min_median_max'], d['fp32']['stages_ms_per_projection'])"
+timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -x > /tmp/pt.log 2>&1; echo "pytest rc=$?"; tail -2 /tmp/pt.log
+for st in 1 0; do
+PSD_STAGED_EPI=$st timeout 300 python tools/probe_c3.py 32768 256 16 1 > /tmp/o.log 2>&1; grep -E "recon|total" /tmp/o.log | sed "s/^/staged=$st /"
+done
