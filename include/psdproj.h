@@ -144,7 +144,9 @@ int psd_ran_proj_f32(psd_plan* plan, const float* x, int64_t n, int64_t ldx, con
 
 /* The 3xTF32 tcgen05 GEMM itself (test entry; allocates its own scratch):
  * mode 0: C (fp64, m x n) = A · B^T; mode 1: mirrored fp32 C (m == n) from
- * the lower tiles of A · B^T.  A m x k, B n x k, fp32 row-major. */
+ * the lower tiles of A · B^T; mode 2: as mode 0 with `a` given transposed
+ * (k x m, ld lda — the M-contiguous operand path the FP32 projection uses).
+ * A m x k, B n x k, fp32 row-major. */
 int psd_gemm_tf32x3(int32_t mode, const float* a, int64_t lda, const float* b, int64_t ldb,
                     int64_t m, int64_t n, int64_t k, void* c, int64_t ldc, void* stream);
 

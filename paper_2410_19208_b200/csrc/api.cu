@@ -661,6 +661,7 @@ int xmul_tc32(psd_plan* p, ll n, const float* xhi, ll ldhi, const double* P, ll 
   op.a_lo = p->xl;
   op.lda = ldhi;
   op.lda_lo = p->ldx32;
+  op.a_mn = true;   // X symmetric: read it as Xᵀ, M-contiguous (512-byte DRAM runs per row)
   op.b_hi = p->f[0];
   op.b_lo = p->f[1];
   op.ldb = p->ldx32;
@@ -958,14 +959,18 @@ int psd_ran_proj_f32(psd_plan* p, const float* x, int64_t n, int64_t ldx, const 
 int psd_gemm_tf32x3(int32_t mode, const float* a, int64_t lda, const float* b, int64_t ldb,
                     int64_t m, int64_t nn, int64_t kk, void* c, int64_t ldc, void* stream) {
   if (!a || !b || !c) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
-  if (m < 1 || nn < 1 || kk < 1 || (mode != 0 && mode != 1) || (mode == 1 && m != nn))
+  if (m < 1 || nn < 1 || kk < 1 || mode < 0 || mode > 2 || (mode == 1 && m != nn))
     return fail(PSD_ERR_INVALID_PARAMS, "bad tf32x3 GEMM shape/mode");
+  const bool amn = mode == 2;   // a is given transposed (k x m, ld lda)
+  if (amn) mode = 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const ll ldk = (kk + 31) / 32 * 32;
+  const ll ldm = (m + 31) / 32 * 32;
   float *ah = nullptr, *al = nullptr, *bh = nullptr, *bl = nullptr, *ws = nullptr;
   const size_t wsz = mode == 0 ? (size_t)psd::tc32_ws_elems(m, (int)nn, std::max<int>(8, (int)((kk + 4095) / 4096))) : 0;
-  bool ok = cudaMalloc(&ah, (size_t)m * ldk * 4) == cudaSuccess &&
-            cudaMalloc(&al, (size_t)m * ldk * 4) == cudaSuccess &&
+  const size_t asz = amn ? (size_t)kk * ldm : (size_t)m * ldk;
+  bool ok = cudaMalloc(&ah, asz * 4) == cudaSuccess &&
+            cudaMalloc(&al, asz * 4) == cudaSuccess &&
             cudaMalloc(&bh, (size_t)nn * ldk * 4) == cudaSuccess &&
             cudaMalloc(&bl, (size_t)nn * ldk * 4) == cudaSuccess &&
             (wsz == 0 || cudaMalloc(&ws, wsz * 4) == cudaSuccess);
@@ -973,12 +978,14 @@ int psd_gemm_tf32x3(int32_t mode, const float* a, int64_t lda, const float* b, i
   if (!ok) {
     status = fail(PSD_ERR_NO_MEMORY, "tf32x3 scratch allocation failed");
   } else {
-    psd::split_rows_f32(a, m, kk, lda, ah, al, ldk, ldk, st);
+    if (amn) psd::split_rows_f32(a, kk, m, lda, ah, al, ldm, ldm, st);
+    else psd::split_rows_f32(a, m, kk, lda, ah, al, ldk, ldk, st);
     psd::split_rows_f32(b, nn, kk, ldb, bh, bl, ldk, ldk, st);
     psd::Tc32Op op;
     op.a_hi = ah;
     op.a_lo = al;
-    op.lda = ldk;
+    op.lda = amn ? ldm : ldk;
+    op.a_mn = amn;
     op.b_hi = bh;
     op.b_lo = bl;
     op.ldb = ldk;

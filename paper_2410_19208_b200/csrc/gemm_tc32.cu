@@ -25,6 +25,22 @@ PSD_DEVINL uint64_t smem_desc(uint32_t saddr) {
   return d;
 }
 
+// MN-major tf32 operand (A read M-contiguous): the 32-bit MN-major canonical
+// layout SWIZZLE_128B_BASE32B (layout type 1; TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B):
+// 128-byte M rows, swizzled in 32-byte granules over 4-row (512 B) atoms;
+// LBO = 4 KB between 32-element M chunks (one TMA box each), SBO = 512 B
+// between 4-row K groups.  One tf32 MMA (K = 8) spans two groups: +1 KB per
+// K step.  (Plain SWIZZLE_128B MN-major is not a valid tf32 operand layout:
+// measured, the MMA returns zeros.)
+PSD_DEVINL uint64_t smem_desc_mn(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)(4096 >> 4) << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;
+  return d;
+}
+
 // kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = n.
 __host__ __device__ inline uint32_t instr_desc(int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -436,6 +452,10 @@ PSD_DEVINL void mma_commit_pair(uint32_t bar) {
       : "memory");
 }
 
+// AMN: A is read M-contiguous ("MN-major"): A = Sᵀ for a row-major S, so every
+// TMA box row is 128 contiguous bytes of S and the four M-chunks of a stage
+// give 512-byte runs per row of S (DRAM-friendly); used with symmetric X.
+template <bool AMN>
 __global__ void __launch_bounds__(kThreads, 1)
     tc32_gemm2_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                       const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
@@ -499,8 +519,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sA = sbase + s * st_bytes;
         const uint32_t sB = sA + 2 * a_bytes;
         const int kc = (kb0 + i) * BK;
-        tma_load_2d_pair(sA, &mAh, kc, m0, fb);
-        tma_load_2d_pair(sA + a_bytes, &mAl, kc, m0, fb);
+        if constexpr (AMN) {
+          // box = 32 M × BK K-rows (4 KB); M-chunk c at +4 KB
+#pragma unroll
+          for (int c = 0; c < BM / 32; ++c) {
+            tma_load_2d_pair(sA + c * 4096, &mAh, m0 + 32 * c, kc, fb);
+            tma_load_2d_pair(sA + a_bytes + c * 4096, &mAl, m0 + 32 * c, kc, fb);
+          }
+        } else {
+          tma_load_2d_pair(sA, &mAh, kc, m0, fb);
+          tma_load_2d_pair(sA + a_bytes, &mAl, kc, m0, fb);
+        }
         for (int h = 0; h < p.n_mma; ++h) {
           const uint32_t off = (uint32_t)h * hb * SWZ;
           const int nrow = n0 + h * p.bn + (int)rank * hb;
@@ -511,8 +540,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.bn >> 3) << 17) |
-                             ((uint32_t)(2 * BM >> 4) << 24);
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((AMN ? 1u : 0u) << 15) |
+                             ((uint32_t)(p.bn >> 3) << 17) | ((uint32_t)(2 * BM >> 4) << 24);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % p.stages;
         const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
@@ -522,7 +551,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sB = sA + 2 * a_bytes;
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t ah = smem_desc(sA + kk * 32), al = smem_desc(sA + a_bytes + kk * 32);
+          uint64_t ah, al;
+          if constexpr (AMN) {   // next 8 K-rows = next 1 KB swizzle atom row group
+            ah = smem_desc_mn(sA + kk * 1024);
+            al = smem_desc_mn(sA + a_bytes + kk * 1024);
+          } else {
+            ah = smem_desc(sA + kk * 32);
+            al = smem_desc(sA + a_bytes + kk * 32);
+          }
           for (int h = 0; h < p.n_mma; ++h) {
             const uint32_t off = (uint32_t)h * hb * SWZ + kk * 32;
             const uint64_t bh = smem_desc(sB + off), bl = smem_desc(sB + b_bytes + off);
@@ -805,6 +841,20 @@ bool map_f32(CUtensorMap* map, const float* ptr, long long cols, long long rows,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 2-D fp32 map for the MN-major operand: box = 32 elements (128 B) × box_rows, 32-byte-atom 128B swizzle
+bool map_f32_box(CUtensorMap* map, const float* ptr, long long cols, long long rows, long long ld,
+                 int box_cols, int box_rows) {
+  auto fn = encode32();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int grid_for(long long total, int threads) {
   const long long b = (total + threads - 1) / threads;
   return (int)std::min<long long>(std::max<long long>(b, 1), (long long)device_info().sms * 16);
@@ -904,8 +954,15 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
   CUtensorMap mah, mal, mbh, mbl;
   const long long lda_lo = op.lda_lo ? op.lda_lo : op.lda;
   const int brows = pair ? p.bn / 2 : p.bn;
-  bool ok = map_f32(&mah, op.a_hi, op.K, op.M, op.lda, BM, sw) && map_f32(&mal, op.a_lo, op.K, op.M, lda_lo, BM, sw) &&
-            map_f32(&mbh, op.b_hi, op.K, op.N, op.ldb, brows, sw) && map_f32(&mbl, op.b_lo, op.K, op.N, op.ldb, brows, sw);
+  const bool amn = pair && op.a_mn;
+  bool ok;
+  if (amn) {   // A stored K×M row-major (Aᵀ): box = 32 M-columns × BK K-rows
+    ok = map_f32_box(&mah, op.a_hi, op.M, op.K, op.lda, 32, BK) &&
+         map_f32_box(&mal, op.a_lo, op.M, op.K, lda_lo, 32, BK);
+  } else {
+    ok = map_f32(&mah, op.a_hi, op.K, op.M, op.lda, BM, sw) && map_f32(&mal, op.a_lo, op.K, op.M, lda_lo, BM, sw);
+  }
+  ok = ok && map_f32(&mbh, op.b_hi, op.K, op.N, op.ldb, brows, sw) && map_f32(&mbl, op.b_lo, op.K, op.N, op.ldb, brows, sw);
   if (!ok) return -5;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -920,10 +977,11 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     const int grid = (int)std::min<long long>(ntiles, sms);
     tc32_mirror_kernel<64><<<grid, kMirrorThreads, smem, st>>>(mah, mal, mbh, mbl, p, (int)ntiles);
   } else if (pair) {
-    static size_t attr2[16] = {};
-    if (attr2[dev] < smem) {
-      cudaFuncSetAttribute(tc32_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr2[dev] = smem;
+    static size_t attr2[2][16] = {};
+    if (attr2[amn][dev] < smem) {
+      cudaFuncSetAttribute(amn ? tc32_gemm2_kernel<true> : tc32_gemm2_kernel<false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr2[amn][dev] = smem;
     }
     const long long units = (long long)((op.M + 2 * BM - 1) / (2 * BM)) * p.n_groups * p.splits;
     cudaLaunchConfig_t cfg = {};
@@ -938,7 +996,9 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, tc32_gemm2_kernel, mah, mal, mbh, mbl, p) != cudaSuccess) return -6;
+    const cudaError_t le = amn ? cudaLaunchKernelEx(&cfg, tc32_gemm2_kernel<true>, mah, mal, mbh, mbl, p)
+                               : cudaLaunchKernelEx(&cfg, tc32_gemm2_kernel<false>, mah, mal, mbh, mbl, p);
+    if (le != cudaSuccess) return -6;
   } else {
     static size_t attr64[16] = {}, attr128[16] = {};
     size_t* attr1 = sw == 64 ? attr64 : attr128;

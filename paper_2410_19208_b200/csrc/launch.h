@@ -66,6 +66,7 @@ struct Tc32Op {
   float* ws = nullptr;
   size_t ws_elems = 0;
   int max_splits = 8;
+  bool a_mn = false;          // A given as Aᵀ (K×M row-major, ld lda): M-contiguous TMA loads
 };
 // Returns the K-split count used (≥ 1) or < 0 on error (−2 alignment, −3 workspace).
 int gemm_tf32x3(const Tc32Op& op, cudaStream_t st);

@@ -55,6 +55,23 @@ def test_tf32x3_gemm_matches_fp64(ours, m, n, k):
     assert err <= 2e-7 * max(1.0, np.sqrt(k)), err
 
 
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (256, 48, 64), (1000, 272, 4096), (300, 520, 1000),
+                                   (513, 17, 7), (2048, 272, 32768)])
+def test_tf32x3_gemm_a_transposed(ours, m, n, k):
+    """mode 2: A handed over as Aᵀ (k×m) — the M-contiguous operand path of the FP32 projection."""
+    g = torch.Generator(device="cuda").manual_seed(m + 5 * n + 11 * k)
+    at = torch.randn(k, m, device="cuda", generator=g)
+    b = torch.randn(n, k, device="cuda", generator=g)
+    c = torch.full((m, n), float("nan"), device="cuda", dtype=torch.float64)
+    lib = ours._native.load_library()
+    ours._native.check(lib.psd_gemm_tf32x3(2, ours._native.ptr(at), at.stride(0), ours._native.ptr(b),
+                                           b.stride(0), m, n, k, ours._native.ptr(c), c.stride(0),
+                                           ours._native.stream_handle(at.device)))
+    ref = at.double().T @ b.double().T
+    err = ((c - ref).norm() / ref.norm()).item()
+    assert err <= 2e-7 * max(1.0, np.sqrt(k)), err
+
+
 @pytest.mark.parametrize("n,k", [(1, 1), (129, 5), (512, 40), (1000, 64), (777, 256)])
 def test_tf32x3_mirrored_store(ours, n, k):
     g = torch.Generator(device="cuda").manual_seed(n + k)
