@@ -420,6 +420,11 @@ __global__ void __launch_bounds__(kMirrorThreads, 1)
 // tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' shared memory, and
 // each CTA's TMEM receives its 128 rows.  Per SM this halves the B bytes
 // streamed and read per MMA.
+PSD_DEVINL bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(pred));
+  return pred != 0;
+}
 PSD_DEVINL uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
@@ -507,12 +512,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
 
+  // Producer and MMA warps run their loops warp-uniformly and elect one lane
+  // to issue: the descriptors then live in uniform registers (no per-MMA
+  // R2UR round trips on the single issuing thread).
   if (warp == 0) {
-    if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % p.stages;
-        const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
-        mbar_wait_t(smem_u32(&empty_bar[s]), ph ^ 1u);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % p.stages;
+      const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+      mbar_wait_t(smem_u32(&empty_bar[s]), ph ^ 1u);
+      if (elect_one()) {
         const uint32_t fb_local = smem_u32(&full_bar[s]);
         const uint32_t fb = map_to_rank(fb_local, 0);          // the leader's barrier
         if (rank == 0) mbar_expect_tx(fb_local, 2 * st_bytes);  // both CTAs' bytes
@@ -537,40 +545,47 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d_pair(sB + b_bytes + off, &mBl, kc, nrow, fb);
         }
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((AMN ? 1u : 0u) << 15) |
                              ((uint32_t)(p.bn >> 3) << 17) | ((uint32_t)(2 * BM >> 4) << 24);
+      // stage-0 descriptors; stage s / step kk / half h only move the 14-bit start-address field
+      const uint64_t dah = AMN ? smem_desc_mn(sbase) : smem_desc(sbase);
+      const uint64_t dal = AMN ? smem_desc_mn(sbase + a_bytes) : smem_desc(sbase + a_bytes);
+      const uint64_t dbh = smem_desc(sbase + 2 * a_bytes);
+      const uint64_t dbl = smem_desc(sbase + 2 * a_bytes + b_bytes);
+      constexpr uint32_t a_kstep = (AMN ? 1024u : 32u) >> 4, b_kstep = 32u >> 4;
+      const uint32_t b_half = (uint32_t)(hb * SWZ) >> 4;
+      const bool two = p.n_mma > 1;
       for (int i = 0; i < nkb; ++i) {
         const int s = i % p.stages;
         const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
         mbar_wait_t(smem_u32(&full_bar[s]), ph);
         tc_fence_after();
-        const uint32_t sA = sbase + s * st_bytes;
-        const uint32_t sB = sA + 2 * a_bytes;
+        if (elect_one()) {
+          const uint32_t so = (uint32_t)(s * st_bytes) >> 4;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          uint64_t ah, al;
-          if constexpr (AMN) {   // next 8 K-rows = next 1 KB swizzle atom row group
-            ah = smem_desc_mn(sA + kk * 1024);
-            al = smem_desc_mn(sA + a_bytes + kk * 1024);
-          } else {
-            ah = smem_desc(sA + kk * 32);
-            al = smem_desc(sA + a_bytes + kk * 32);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t ah = dah + so + kk * a_kstep, al = dal + so + kk * a_kstep;
+            const uint64_t bh0 = dbh + so + kk * b_kstep, bl0 = dbl + so + kk * b_kstep;
+            const uint32_t acc0 = (i | kk) != 0;
+            mma_tf32_pair(tmem, al, bh0, idesc, acc0);
+            mma_tf32_pair(tmem, ah, bl0, idesc, 1u);
+            mma_tf32_pair(tmem, ah, bh0, idesc, 1u);
+            if (two) {
+              const uint32_t d1 = tmem + (uint32_t)p.bn;
+              mma_tf32_pair(d1, al, bh0 + b_half, idesc, acc0);
+              mma_tf32_pair(d1, ah, bl0 + b_half, idesc, 1u);
+              mma_tf32_pair(d1, ah, bh0 + b_half, idesc, 1u);
+            }
           }
-          for (int h = 0; h < p.n_mma; ++h) {
-            const uint32_t off = (uint32_t)h * hb * SWZ + kk * 32;
-            const uint64_t bh = smem_desc(sB + off), bl = smem_desc(sB + b_bytes + off);
-            const uint32_t d = tmem + (uint32_t)(h * p.bn);
-            if (p.nprod >= 3) mma_tf32_pair(d, al, bh, idesc, (i | kk) != 0);
-            if (p.nprod >= 2) mma_tf32_pair(d, ah, bl, idesc, (p.nprod >= 3) || (i | kk) != 0);
-            mma_tf32_pair(d, ah, bh, idesc, (p.nprod >= 2) || (i | kk) != 0);
-          }
+          mma_commit_pair(smem_u32(&empty_bar[s]));   // frees slot s in both CTAs
+          if (i == nkb - 1) mma_commit_pair(smem_u32(&acc_bar));   // accumulators complete
         }
-        mma_commit_pair(smem_u32(&empty_bar[s]));   // frees slot s in both CTAs
+        __syncwarp();
       }
-      mma_commit_pair(smem_u32(&acc_bar));          // both CTAs' accumulators complete
     }
   } else {
     const int quad = warp & 3;
