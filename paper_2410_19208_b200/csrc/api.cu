@@ -661,7 +661,6 @@ int xmul_tc32(psd_plan* p, ll n, const float* xhi, ll ldhi, const double* P, ll 
   op.a_lo = p->xl;
   op.lda = ldhi;
   op.lda_lo = p->ldx32;
-  op.a_mn = true;   // X symmetric: read it as Xᵀ, M-contiguous (512-byte DRAM runs per row)
   op.b_hi = p->f[0];
   op.b_lo = p->f[1];
   op.ldb = p->ldx32;

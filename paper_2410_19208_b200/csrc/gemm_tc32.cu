@@ -612,6 +612,158 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---- CTA-pair variant with A staged in TMEM (tcgen05.cp + MMA "TS") -------
+// Experiment (opt-in, PSD_TC32_TS=1): in the SS kernel A is read from shared
+// memory by 6 MMAs per K step.  Here each stage's A hi/lo (128 rows × 32 K per CTA)
+// is copied once into TMEM with tcgen05.cp and every MMA takes A from TMEM;
+// shared memory only feeds B.  The N range is split 256 + n1 (n1 a multiple
+// of 32: TS MMAs need N % 32 == 0), e.g. w = 272 → 256 + 32.
+PSD_DEVINL void tmem_cp_pair(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;\n" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+PSD_DEVINL void mma_tf32_pair_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                 uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum));
+}
+
+struct Ts2Maps {
+  CUtensorMap ah, al, bh0, bl0, bh1, bl1;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    tc32_gemm2ts_kernel(const __grid_constant__ Ts2Maps mp, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], acc_bar;
+  __shared__ uint32_t tmem_slot;
+  constexpr int kAcol = 320;                     // TMEM column of the two A buffers (64 cols each)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int bn1 = p.bn;                          // second N piece (first is 256)
+  const int hb0 = 128, hb1 = bn1 / 2;            // B rows per CTA per piece
+  const int bn_tot = 256 + bn1;
+  int u = blockIdx.x >> 1;
+  const int ng = u % p.n_groups;
+  u /= p.n_groups;
+  const int split = u % p.splits;
+  const int mpair = u / p.splits;
+  const int m0 = mpair * 2 * BM + (int)rank * BM, n0 = ng * bn_tot;
+  const int kb0 = split * p.kb_per_split;
+  const int nkb = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
+
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  const uint32_t a_bytes = BM * SWZ, b_bytes = (uint32_t)(hb0 + hb1) * SWZ;
+  const uint32_t st_bytes = 2 * a_bytes + 2 * b_bytes;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    mbar_init(smem_u32(&acc_bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % p.stages;
+      const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+      mbar_wait_t(smem_u32(&empty_bar[s]), ph ^ 1u);
+      if (elect_one()) {
+        const uint32_t fb_local = smem_u32(&full_bar[s]);
+        const uint32_t fb = map_to_rank(fb_local, 0);
+        if (rank == 0) mbar_expect_tx(fb_local, 2 * st_bytes);
+        const uint32_t sA = sbase + s * st_bytes;
+        const uint32_t sB = sA + 2 * a_bytes;
+        const int kc = (kb0 + i) * BK;
+        tma_load_2d_pair(sA, &mp.ah, kc, m0, fb);
+        tma_load_2d_pair(sA + a_bytes, &mp.al, kc, m0, fb);
+        tma_load_2d_pair(sB, &mp.bh0, kc, n0 + (int)rank * hb0, fb);
+        tma_load_2d_pair(sB + hb0 * SWZ, &mp.bh1, kc, n0 + 256 + (int)rank * hb1, fb);
+        tma_load_2d_pair(sB + b_bytes, &mp.bl0, kc, n0 + (int)rank * hb0, fb);
+        tma_load_2d_pair(sB + b_bytes + hb0 * SWZ, &mp.bl1, kc, n0 + 256 + (int)rank * hb1, fb);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      const uint32_t id0 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                           ((uint32_t)(2 * BM >> 4) << 24);
+      const uint32_t id1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(bn1 >> 3) << 17) |
+                           ((uint32_t)(2 * BM >> 4) << 24);
+      const uint64_t dah = smem_desc(sbase), dal = smem_desc(sbase + a_bytes);
+      const uint64_t dbh = smem_desc(sbase + 2 * a_bytes), dbl = smem_desc(sbase + 2 * a_bytes + b_bytes);
+      const uint32_t b1off = (uint32_t)(hb0 * SWZ) >> 4;
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % p.stages;
+        const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+        mbar_wait_t(smem_u32(&full_bar[s]), ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t so = (uint32_t)(s * st_bytes) >> 4;
+          const uint32_t abuf = tmem + (uint32_t)(kAcol + (i & 1) * 64);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {   // A hi → cols [0,32), A lo → [32,64) of the buffer
+            tmem_cp_pair(abuf + kk * 8, dah + so + kk * 2);
+            tmem_cp_pair(abuf + 32 + kk * 8, dal + so + kk * 2);
+          }
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t ah = abuf + kk * 8, al = abuf + 32 + kk * 8;
+            const uint64_t bh = dbh + so + kk * 2, bl = dbl + so + kk * 2;
+            const uint32_t acc0 = (i | kk) != 0;
+            mma_tf32_pair_ts(tmem, al, bh, id0, acc0);
+            mma_tf32_pair_ts(tmem, ah, bl, id0, 1u);
+            mma_tf32_pair_ts(tmem, ah, bh, id0, 1u);
+            const uint32_t d1 = tmem + 256u;
+            mma_tf32_pair_ts(d1, al, bh + b1off, id1, acc0);
+            mma_tf32_pair_ts(d1, ah, bl + b1off, id1, 1u);
+            mma_tf32_pair_ts(d1, ah, bh + b1off, id1, 1u);
+          }
+          mma_commit_pair(smem_u32(&empty_bar[s]));
+          if (i == nkb - 1) mma_commit_pair(smem_u32(&acc_bar));
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    const int i = m0 + quad * 32 + lane;
+    mbar_wait_t(smem_u32(&acc_bar), 0);
+    tc_fence_after();
+    const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
+    for (int c0 = 0; c0 < bn_tot; c0 += 16) {
+      float v[16];
+      tmem_ld16(trow + (uint32_t)c0, v);
+      if (i >= p.M) continue;
+      float4* dst = reinterpret_cast<float4*>(p.out + (long long)split * p.split_stride +
+                                              (long long)i * p.ldo + n0 + c0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
 // ---- split / convert kernels ----------------------------------------------
 PSD_DEVINL float tf32_rna(float x) {
   uint32_t r;
@@ -901,9 +1053,23 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     const int groups = (op.N + kMaxN - 1) / kMaxN;
     n_tot = ((op.N + groups - 1) / groups + 15) / 16 * 16;
   }
-  p.n_mma = n_tot > 256 ? 2 : 1;
-  p.bn = (n_tot / p.n_mma + 15) / 16 * 16;
-  n_tot = p.bn * p.n_mma;
+  // A staged in TMEM (TS MMAs, N pieces 256 + n1 with n1 % 32 == 0): correct but measured
+  // slower than the SS pair kernel at C3 (2.73 vs 2.50 ms) — opt-in via PSD_TC32_TS=1
+  static const bool ts_ok = [] {
+    const char* e = getenv("PSD_TC32_TS");
+    return e && e[0] == '1';
+  }();
+  const bool ts = op.mode == PARTIAL && ts_ok && !op.a_mn && n_tot > 256 && n_tot <= 512 &&
+                  !(getenv("PSD_TC32_PAIR") && getenv("PSD_TC32_PAIR")[0] == '0');
+  if (ts) {
+    p.n_mma = 2;
+    p.bn = (n_tot - 256 + 31) / 32 * 32;   // second piece
+    n_tot = 256 + p.bn;
+  } else {
+    p.n_mma = n_tot > 256 ? 2 : 1;
+    p.bn = (n_tot / p.n_mma + 15) / 16 * 16;
+    n_tot = p.bn * p.n_mma;
+  }
   p.n_groups = (op.N + n_tot - 1) / n_tot;
   p.m_tiles = (op.M + BM - 1) / BM;
   const int sms = device_info().sms;
@@ -959,7 +1125,8 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     const char* e = getenv("PSD_TC32_NPROD");   // experiment knob: tf32 products per k-step
     p.nprod = e ? std::max(1, std::min(3, atoi(e))) : 3;
   }
-  const int sb = pair ? 2 * BM * sw + p.bn * p.n_mma * sw : 2 * BM * sw + 2 * p.bn * p.n_mma * sw;
+  const int sb = ts ? 2 * BM * sw + (256 + p.bn) * sw
+                    : (pair ? 2 * BM * sw + p.bn * p.n_mma * sw : 2 * BM * sw + 2 * p.bn * p.n_mma * sw);
   const int epi_bytes = op.mode == MIRROR ? kMirrorEpi * 32 * 33 * 4 : 0;   // epilogue transpose tiles
   const int avail = (int)device_info().max_smem - 1024 - 2048 - epi_bytes;
   p.stages = std::min(8, avail / sb);
@@ -969,7 +1136,7 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
   CUtensorMap mah, mal, mbh, mbl;
   const long long lda_lo = op.lda_lo ? op.lda_lo : op.lda;
   const int brows = pair ? p.bn / 2 : p.bn;
-  const bool amn = pair && op.a_mn;
+  const bool amn = pair && op.a_mn && !ts;
   bool ok;
   if (amn) {   // A stored K×M row-major (Aᵀ): box = 32 M-columns × BK K-rows
     ok = map_f32_box(&mah, op.a_hi, op.M, op.K, op.lda, 32, BK) &&
@@ -981,7 +1148,33 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
   if (!ok) return -5;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (op.mode == MIRROR) {
+  if (ts) {
+    Ts2Maps mp;
+    ok = map_f32(&mp.ah, op.a_hi, op.K, op.M, op.lda, BM, sw) && map_f32(&mp.al, op.a_lo, op.K, op.M, lda_lo, BM, sw) &&
+         map_f32(&mp.bh0, op.b_hi, op.K, op.N, op.ldb, 128, sw) && map_f32(&mp.bl0, op.b_lo, op.K, op.N, op.ldb, 128, sw) &&
+         map_f32(&mp.bh1, op.b_hi, op.K, op.N, op.ldb, p.bn / 2, sw) &&
+         map_f32(&mp.bl1, op.b_lo, op.K, op.N, op.ldb, p.bn / 2, sw);
+    if (!ok) return -5;
+    static size_t attrts[16] = {};
+    if (attrts[dev] < smem) {
+      cudaFuncSetAttribute(tc32_gemm2ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attrts[dev] = smem;
+    }
+    const long long units = (long long)((op.M + 2 * BM - 1) / (2 * BM)) * p.n_groups * p.splits;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * units));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, tc32_gemm2ts_kernel, mp, p) != cudaSuccess) return -6;
+  } else if (op.mode == MIRROR) {
     static size_t attrm[16] = {};
     if (attrm[dev] < smem) {
       cudaFuncSetAttribute(tc32_mirror_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
