@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _native, errors
-from ._tensors import Operand, default_device, draw_gaussian
+from ._tensors import DeviceRng, Operand, default_device, draw_gaussian
 from .projection import ALPHA_TOL_FACTOR, ProjectorConfig
 from .sketch import min_eig_magnitude_device
 from .symmetric import exact_psd_projection_device, reconstruct_device, rng_from_seed
@@ -196,10 +196,13 @@ def solve(problem, proj=None, *, beta=0.5, epsilon=1e-8, max_iter=100, y0=None, 
                            0.5 * float((misfit * misfit).sum().item()), proj.method, True,
                            time.perf_counter() - t0)
 
-    y_host = rng.standard_normal(m) if y0 is None else np.asarray(y0, dtype=float).ravel()  # :212
-    if y_host.size != m:
-        raise errors.error("DimensionMismatch", f"y has length {y_host.size}, expected m = {m}")
-    y = torch.from_numpy(y_host.copy()).to(dev)
+    if y0 is None and isinstance(rng, DeviceRng):      # perf mode: device Philox stream
+        y = rng.normal(m, dev).clone()
+    else:
+        y_host = rng.standard_normal(m) if y0 is None else np.asarray(y0, dtype=float).ravel()  # :212
+        if y_host.size != m:
+            raise errors.error("DimensionMismatch", f"y has length {y_host.size}, expected m = {m}")
+        y = torch.from_numpy(y_host.copy()).to(dev)
     trajectory = [] if keep_trajectory else None
     y_trajectory = [] if keep_trajectory else None
     iterations, converged, r = 0, False, 0
