@@ -190,7 +190,7 @@ int xmul_rect(psd_plan* p, const double* x, ll rows, ll cols, ll ldx, const doub
   op.alpha = alpha;
   op.S = P;
   op.lds = ldP;
-  op.max_splits = 4;
+  op.max_splits = 16;   // wave quantisation at small n (config 2: 128 tiles on 148 SMs)
   const int r = psd::gemm_f64(op, p->ws, p->ws_elems, st);
   if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "unsupported GEMM layout");
   return PSD_OK;
@@ -306,14 +306,11 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
     if (!std::isfinite(trace)) return fail(PSD_ERR_CONVERGENCE, "non-finite Gram matrix in QR");
     if (unshifted_run >= 2) {
       // verification Gram of an ill-conditioned input: accept if ‖QᵀQ − I‖_max small
-      std::vector<double> hg((size_t)w * w);
-      PSD_CUDA_CHECK(cudaMemcpyAsync(hg.data(), p->G, hg.size() * sizeof(double),
-                                     cudaMemcpyDeviceToHost, st),
-                     "gram copy");
-      PSD_TRY(sync(st, "gram copy"));
+      psd::identity_defect(p->G, w, w, p->scal + 3, st);
       double dev = 0.0;
-      for (int i = 0; i < w; ++i)
-        for (int j = 0; j < w; ++j) dev = std::max(dev, std::fabs(hg[(size_t)i * w + j] - (i == j)));
+      PSD_CUDA_CHECK(cudaMemcpyAsync(&dev, p->scal + 3, sizeof(double), cudaMemcpyDeviceToHost, st),
+                     "orthogonality defect");
+      PSD_TRY(sync(st, "orthogonality defect"));
       if (dev <= 1e-13 * std::max(1, w)) {
         verified = true;
         break;
@@ -465,6 +462,7 @@ int psd_plan_create(psd_plan** out, int64_t n, int32_t width, int32_t device) {
   ok &= (p->dvec = alloc(p, width)) != nullptr;
   ok &= (p->ints = reinterpret_cast<int*>(alloc(p, width + 8))) != nullptr;
   p->ws_elems = std::max<size_t>((size_t)4 * n * p->ldp, (size_t)256 * width * p->ldp);
+  p->ws_elems = std::max<size_t>(p->ws_elems, std::min<size_t>((size_t)16 * n * p->ldp, (size_t)64 << 20));
   p->ws_elems = std::max<size_t>(p->ws_elems, 1 << 20);
   ok &= (p->ws = alloc(p, p->ws_elems)) != nullptr;
   p->jws_elems = psd::jacobi_ws_elems(width);

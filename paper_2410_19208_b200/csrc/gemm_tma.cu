@@ -170,11 +170,11 @@ int gemm_f64_tma(const GemmOp& op, double* ws, size_t ws_elems, cudaStream_t st)
   if (op.a_layout == A_MK && op.b_layout == B_KN) return launch_panel<TmaNN>(op, ws, ws_elems, st);
   if (op.a_layout == A_KM && op.b_layout == B_KN) return launch_panel<TmaTN>(op, ws, ws_elems, st);
   if (op.a_layout == A_MK && op.b_layout == B_NK) {
-    static const bool staged = [] {
+    static const int staged = [] {
       const char* e = getenv("PSD_STAGED_EPI");
-      return !(e && e[0] == '0');
+      return e ? atoi(e) : 1;
     }();
-    if (op.epi == EPI_MIRROR && staged) return launch<TmaNTs>(op, ws, ws_elems, st);
+    if (op.epi == EPI_MIRROR && staged == 1) return launch<TmaNTs>(op, ws, ws_elems, st);
     return launch<TmaNT>(op, ws, ws_elems, st);
   }
   return -1;

@@ -102,6 +102,13 @@ PSD_DEVINL void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+// named CTA barriers between warp roles (id 0 is __syncthreads)
+PSD_DEVINL void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+PSD_DEVINL void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
 PSD_DEVINL void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -208,7 +215,11 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[Cfg::STAGES];
   __shared__ __align__(8) uint64_t empty_bar[Cfg::STAGES];
-  __shared__ __align__(8) uint64_t cfull_bar, cfree_bar;   // staged mirror epilogue
+  // staged mirror epilogue handshake: named barrier 1 = tile parked in smem
+  // (consumers arrive, store warps sync), 2 = tile stored (the reverse).
+  // (An mbarrier arrive/wait pair here lost generic-proxy smem writes under
+  // load — measured: ~10% of reconstructions had stale rows.)
+  constexpr int kEpiBarCount = (Cfg::kConsumers + 3) * 32;
   constexpr int STAGES = Cfg::STAGES, M8W = Cfg::M8W, N8W = Cfg::N8W;
   constexpr int kStoreWarps = 3;
   const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -222,8 +233,6 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
       mbar_init(smem_u32(&full_bar[s]), 1);
       mbar_init(smem_u32(&empty_bar[s]), Cfg::kConsumers);
     }
-    mbar_init(smem_u32(&cfull_bar), Cfg::kConsumers);
-    mbar_init(smem_u32(&cfree_bar), kStoreWarps);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -268,7 +277,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const Unit un = decode_unit<Cfg>(p, u);
         if (!unit_active<Cfg>(p, un)) continue;
-        mbar_wait(smem_u32(&cfull_bar), (uint32_t)j & 1u);
+        named_sync(1, kEpiBarCount);
         // (m, n) = (m0 + r, n0 + c), m ≥ n: C[m][n] (row m) and C[n][m] (row n)
         for (int r = sw; r < Cfg::BM; r += kStoreWarps) {
           const int m = un.m0 + r;
@@ -290,8 +299,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
             if (m < p.M && m > n) crow[m] = Cs[r * Cfg::C_LD + c];
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&cfree_bar));
+        named_arrive(2, kEpiBarCount);
         ++j;
       }
     }
@@ -352,7 +360,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
 
     // ------------------------------------------------------------- epilogue
     if (staged) {
-      mbar_wait(smem_u32(&cfree_bar), ((uint32_t)stage_j & 1u) ^ 1u);   // previous tile stored
+      if (stage_j > 0) named_sync(2, kEpiBarCount);   // previous tile stored
 #pragma unroll
       for (int i = 0; i < M8W; ++i) {
         const int r = a_row<Cfg>(wm * M8W + i, g);
@@ -361,8 +369,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
 #pragma unroll
           for (int e = 0; e < 2; ++e) Cs[r * Cfg::C_LD + b_col<Cfg>(wn * N8W + j, 2 * t + e)] = acc[i][j][e];
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&cfull_bar));
+      named_arrive(1, kEpiBarCount);
       ++stage_j;
       continue;
     }
@@ -404,6 +411,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
       resid = 0.0;
     }
   }
+  // consume the store warps' arrival for the last parked tile
+  if (staged && stage_j > 0) named_sync(2, kEpiBarCount);
 }
 
 }  // namespace psd

@@ -97,6 +97,28 @@ static void sym_stats_t(const T* x, long long n, long long ldx, double* stats, c
   sym_stats_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats);
   count_launch();
 }
+// out[0] = max_ij |G_ij − δ_ij| for a w×w Gram (orthogonality defect of Q).
+__global__ void identity_defect_kernel(const double* __restrict__ g, int w, long long ldg, double* out) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (long long e = threadIdx.x; e < (long long)w * w; e += blockDim.x) {
+    const int i = (int)(e / w), j = (int)(e % w);
+    m = fmax(m, fabs(g[(long long)i * ldg + j] - (i == j ? 1.0 : 0.0)));
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t = fmax(t, red[k]);
+    out[0] = t;
+  }
+}
+void identity_defect(const double* g, int w, long long ldg, double* out, cudaStream_t st) {
+  identity_defect_kernel<<<1, 1024, 0, st>>>(g, w, ldg, out);
+  count_launch();
+}
+
 void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st) {
   sym_stats_t(x, n, ldx, stats, st);
 }

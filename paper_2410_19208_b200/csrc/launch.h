@@ -86,6 +86,8 @@ void split_transpose(const double* P, long long n, int w, long long ldp, float* 
 // stats[0] = max|x|, stats[1] = max|x - xᵀ|, ((int*)(stats+2))[0] = flags
 // (bit0: not bitwise symmetric, bit1: NaN/Inf present). stats zeroed inside.
 void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st);
+// out[0] = max |G − I| over a w×w Gram (single block)
+void identity_defect(const double* g, int w, long long ldg, double* out, cudaStream_t st);
 void sym_stats_f32(const float* x, long long n, long long ldx, double* stats, cudaStream_t st);
 void convert_f32_f64(const float* src, long long lds, double* dst, long long ldd, long long rows,
                      int cols, cudaStream_t st);

@@ -141,3 +141,30 @@ def test_require_symmetric_stats(env):
     st = psd.symmetric.check_symmetric_device(op)
     assert not st.bitwise and st.defect == pytest.approx(abs(c[5, 7] - c[7, 5]))
     assert st.max_abs == np.abs(c).max()
+
+
+def test_mirrored_syrk_deterministic_tma_path():
+    """The staged-epilogue SYRK (TMA path: even leading dimension) must be
+    bitwise reproducible and bitwise symmetric over repeated launches (a
+    consumer/store-warp handshake race once produced stale rows)."""
+    import torch
+    import paper_2410_19208_b200 as psd
+    n, r = 1536, 159
+    g = torch.Generator(device="cuda").manual_seed(3)
+    w = torch.randn(n, r + 1, dtype=torch.float64, device="cuda", generator=g)[:, :r]
+    d = torch.rand(r, dtype=torch.float64, device="cuda", generator=g)
+    lib = psd._native.load_library()
+    plan = psd._native.get_plan(n, r, torch.device("cuda"))
+
+    def recon():
+        out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        psd._native.check(lib.psd_reconstruct(plan.handle, psd._native.ptr(w), n, w.stride(0),
+                                              psd._native.ptr(d), r, psd._native.ptr(out), n,
+                                              psd._native.stream_handle(torch.device("cuda"))))
+        return out
+    ref = recon()
+    exact = (w * d) @ w.T
+    assert torch.equal(ref, ref.T)
+    assert float((ref - exact).abs().max() / exact.abs().max()) < 1e-13
+    for _ in range(30):
+        assert torch.equal(recon(), ref)
