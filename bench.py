@@ -273,15 +273,19 @@ def run_ours(a):
     e1 = torch.cuda.Event(enable_timing=True)
     launches = 0
     ranks = []
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
     e0.record()
     for i in range(a.steps):
+        marks[i].record()
         if flush is not None:
             flush.zero_()
         rep = psd.ran_proj(pool[i % a.pool], params, rng)
         launches += rep.device_info["gpu_launches"]
         ranks.append(rep.effective_rank)
+    marks[a.steps].record()
     e1.record()
     torch.cuda.synchronize(dev)
+    per_step = sorted(marks[i].elapsed_time(marks[i + 1]) for i in range(a.steps))
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -326,6 +330,7 @@ def run_ours(a):
     line = {
         "metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+        "step_ms_min_median_max": [per_step[0], per_step[len(per_step) // 2], per_step[-1]],
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded BASELINE {a.config} matrices generated in HBM)",
         "config": workload_config(a, world),
