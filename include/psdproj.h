@@ -142,6 +142,12 @@ int psd_ran_proj_f32(psd_plan* plan, const float* x, int64_t n, int64_t ldx, con
                      float* result, int64_t ldr, double* factors_w, int64_t ldw, double* factors_d,
                      psd_report* report, void* stream);
 
+/* FP64 GEMM emulated on the INT8 tensor cores (Ozaki scheme II, 16 moduli;
+ * test entry, allocates its own scratch): C (fp64, m x n) = A (m x k) · P (k x n),
+ * all row-major, n <= 512. */
+int psd_gemm_f64_ozaki(const double* a, int64_t lda, const double* p, int64_t ldp, int64_t m,
+                       int64_t n, int64_t k, double* c, int64_t ldc, void* stream);
+
 /* The 3xTF32 tcgen05 GEMM itself (test entry; allocates its own scratch):
  * mode 0: C (fp64, m x n) = A · B^T; mode 1: mirrored fp32 C (m == n) from
  * the lower tiles of A · B^T; mode 2: as mode 0 with `a` given transposed

@@ -44,6 +44,12 @@ struct psd_plan {
   ll rparts = 0;
   // FP32 path (ensure_f32)
   float *xh = nullptr, *xl = nullptr, *f[4] = {}, *ws32 = nullptr;
+  // FP64-on-INT8 (Ozaki II) path (ensure_oz): X residues, panel residues, exponents, partials
+  int8_t *oz_ar = nullptr, *oz_br = nullptr;
+  int *oz_e = nullptr, *oz_f = nullptr;
+  uint8_t* oz_res = nullptr;
+  ll oz_ldk = 0;
+  size_t oz_res_elems = 0;
   ll ldx32 = 0;
   size_t ws32_elems = 0;
   std::vector<void*> allocs;
@@ -648,6 +654,58 @@ int ensure_f32(psd_plan* p, bool need_hi) {
   return PSD_OK;
 }
 
+// Ozaki-II buffers (allocated on first use): 16 int8 residue planes of X
+// (n × ldk each), panel residues, exponents, per-split residue partials.
+int ensure_oz(psd_plan* p) {
+  if (p->oz_ar) return PSD_OK;
+  const int L = psd::oz_num_moduli();
+  const ll ldk = (p->n + 127) / 128 * 128;
+  const ll wpad = (p->w + 15) / 16 * 16;
+  auto balloc = [&](size_t bytes) -> void* {
+    return static_cast<void*>(alloc(p, (bytes + 7) / 8));
+  };
+  p->oz_ar = static_cast<int8_t*>(balloc((size_t)L * p->n * ldk));
+  p->oz_br = static_cast<int8_t*>(balloc((size_t)L * wpad * ldk));
+  p->oz_e = static_cast<int*>(balloc((size_t)p->n * sizeof(int)));
+  p->oz_f = static_cast<int*>(balloc((size_t)wpad * sizeof(int)));
+  p->oz_res_elems = (size_t)L * 8 * p->n * wpad;
+  p->oz_res = static_cast<uint8_t*>(balloc(p->oz_res_elems));
+  if (!p->oz_ar || !p->oz_br || !p->oz_e || !p->oz_f || !p->oz_res)
+    return fail(PSD_ERR_NO_MEMORY, "device allocation failed for the INT8-emulation buffers");
+  p->oz_ldk = ldk;
+  cudaMemset(p->oz_ar, 0, (size_t)L * p->n * ldk);   // K padding stays zero
+  cudaMemset(p->oz_br, 0, (size_t)L * wpad * ldk);
+  return PSD_OK;
+}
+
+// X·P (X bitwise symmetric, residues prepared) as 16 INT8 GEMMs + CRT.
+int xmul_oz(psd_plan* p, ll n, const double* P, ll ldP, int w, double* out, ll ldo, double alpha,
+            cudaStream_t st) {
+  Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
+  psd::OzOp op;
+  op.ar = p->oz_ar;
+  op.ldar = p->oz_ldk;
+  op.e = p->oz_e;
+  op.P = P;
+  op.ldp = ldP;
+  op.M = (int)n;
+  op.N = w;
+  op.K = (int)n;
+  op.br = p->oz_br;
+  op.ldbr = p->oz_ldk;
+  op.f = p->oz_f;
+  op.res = p->oz_res;
+  op.res_elems = p->oz_res_elems;
+  op.C = out;
+  op.ldc = ldo;
+  op.alpha = alpha;
+  op.S = P;
+  op.lds = ldP;
+  const int r = psd::oz_gemm(op, st);
+  if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "INT8-emulated GEMM rejected its operands (%d)", r);
+  return PSD_OK;
+}
+
 // X·P on the 3xTF32 tensor-core path: P (fp64 n×w) → tf32 hi/lo, transposed
 // to the K-major B operand; fp32 partials reduced into the fp64 panel `out`.
 int xmul_tc32(psd_plan* p, ll n, const float* xhi, ll ldhi, const double* P, ll ldP, int w,
@@ -770,8 +828,21 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     omega = p->panel[3];
     ldo_eff = ld;
   }
+  // FP64 n×n products on the INT8 tensor cores (Ozaki II) when X is bitwise
+  // symmetric (Xᵀ·P = X·P, the residues of X's rows serve both) — opt-in
+  static const bool oz_on = [] {
+    const char* e = getenv("PSD_FP64_OZAKI");
+    return e && e[0] == '1';
+  }();
+  const bool oz = !f32 && oz_on && !use_t && w <= 512;
+  if (oz) {
+    PSD_TRY(ensure_oz(p));
+    Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
+    psd::oz_prepare_rows(x64, n, n, ldx, p->oz_e, p->oz_ar, p->oz_ldk, st);
+  }
   const MulFn mul = [&](const double* P, ll ldP, int ww, double* out, ll ldo2, bool t) {
     if (f32) return xmul_tc32(p, n, xhi, ldhi, P, ldP, ww, out, ldo2, alpha, st);
+    if (oz) return xmul_oz(p, n, P, ldP, ww, out, ldo2, alpha, st);
     return xmul(p, x64, n, ldx, P, ldP, ww, out, ldo2, alpha, t && use_t, st);
   };
   int qb = 0, wk = 0;
@@ -950,6 +1021,59 @@ int psd_ran_proj_f32(psd_plan* p, const float* x, int64_t n, int64_t ldx, const 
     cudaStreamSynchronize(st);
     collect_marks(p);
   }
+  return status;
+}
+
+int psd_gemm_f64_ozaki(const double* a, int64_t lda, const double* pp, int64_t ldp, int64_t m,
+                       int64_t nn, int64_t kk, double* c, int64_t ldc, void* stream) {
+  if (!a || !pp || !c) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  if (m < 1 || nn < 1 || nn > 512 || kk < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad ozaki GEMM shape");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int L = psd::oz_num_moduli();
+  const ll ldk = (kk + 127) / 128 * 128;
+  const ll wpad = (nn + 15) / 16 * 16;
+  int8_t *ar = nullptr, *br = nullptr;
+  int *e = nullptr, *f = nullptr;
+  uint8_t* res = nullptr;
+  const size_t res_elems = (size_t)L * 8 * m * wpad;
+  bool ok = cudaMalloc(&ar, (size_t)L * m * ldk) == cudaSuccess &&
+            cudaMalloc(&br, (size_t)L * wpad * ldk) == cudaSuccess &&
+            cudaMalloc(&e, (size_t)m * sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&f, (size_t)nn * sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&res, res_elems) == cudaSuccess;
+  int status = PSD_OK;
+  if (!ok) {
+    status = fail(PSD_ERR_NO_MEMORY, "ozaki scratch allocation failed");
+  } else {
+    cudaMemsetAsync(ar, 0, (size_t)L * m * ldk, st);
+    cudaMemsetAsync(br, 0, (size_t)L * wpad * ldk, st);
+    psd::oz_prepare_rows(a, m, kk, lda, e, ar, ldk, st);
+    psd::OzOp op;
+    op.ar = ar;
+    op.ldar = ldk;
+    op.e = e;
+    op.P = pp;
+    op.ldp = ldp;
+    op.M = (int)m;
+    op.N = (int)nn;
+    op.K = (int)kk;
+    op.br = br;
+    op.ldbr = ldk;
+    op.f = f;
+    op.res = res;
+    op.res_elems = res_elems;
+    op.C = c;
+    op.ldc = ldc;
+    const int r = psd::oz_gemm(op, st);
+    if (r < 0) status = fail(PSD_ERR_INVALID_PARAMS, "ozaki GEMM rejected its operands (%d)", r);
+    if (status == PSD_OK) status = sync(st, "ozaki gemm");
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(ar);
+  cudaFree(br);
+  cudaFree(e);
+  cudaFree(f);
+  cudaFree(res);
   return status;
 }
 

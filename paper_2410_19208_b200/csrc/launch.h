@@ -68,6 +68,30 @@ struct Tc32Op {
   int max_splits = 8;
   bool a_mn = false;          // A given as Aᵀ (K×M row-major, ld lda): M-contiguous TMA loads
 };
+// ---- FP64 GEMM emulated on INT8 tensor cores (ozaki.cu): C (M×N) = A (M×K) · P (K×N) ----
+// A is given as prepared residues (oz_prepare_rows): ar[ℓ][M][ldar] int8 + row exponents e[M].
+struct OzOp {
+  const int8_t* ar = nullptr;
+  long long ldar = 0;
+  const int* e = nullptr;
+  const double* P = nullptr;   // K×N row-major fp64 panel
+  long long ldp = 0;
+  int M = 0, N = 0, K = 0;
+  int8_t* br = nullptr;        // scratch: [16][round16(N)][ldbr] int8
+  long long ldbr = 0;
+  int* f = nullptr;            // scratch: N column exponents
+  uint8_t* res = nullptr;      // scratch: residue partials
+  size_t res_elems = 0;
+  double* C = nullptr;
+  long long ldc = 0;
+  double alpha = 0.0;          // α > 0: C = (acc + α·S)/α
+  const double* S = nullptr;
+  long long lds = 0;
+};
+int oz_num_moduli();
+void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
+                     long long ldr, cudaStream_t st);
+int oz_gemm(const OzOp& op, cudaStream_t st);
 // Returns the K-split count used (≥ 1) or < 0 on error (−2 alignment, −3 workspace).
 int gemm_tf32x3(const Tc32Op& op, cudaStream_t st);
 long long tc32_ws_elems(long long M, int N, int max_splits);

@@ -1,0 +1,499 @@
+// FP64 GEMM emulated on the INT8 tensor cores (Ozaki scheme II: integer
+// scaling + Chinese-remainder reconstruction), for the n×n · n×w products of
+// the projection.
+//
+//   A (M×K, fp64) is scaled per row to 53-bit integers a = rint(x·2^(53−e_i)),
+//   B (K×N, fp64) per column to b = rint(p·2^(53−f_j));
+//   for 16 pairwise-coprime moduli m_ℓ ≤ 256 the symmetric residues a mod m_ℓ,
+//   b mod m_ℓ are int8; each (A mod m_ℓ)·(B mod m_ℓ) runs as an exact INT8
+//   GEMM with INT32 TMEM accumulation (|Σ| ≤ K·2^14 < 2^31), reduced mod m_ℓ;
+//   Garner's mixed-radix CRT recovers the exact integer product
+//   C' = Σ_k a_ik b_kj (|C'| ≤ K·2^106 < M/2, M = Π m_ℓ ≈ 2^125.4) and
+//   C = C'·2^(e_i + f_j − 106).
+//
+// The only rounding is the 53-bit fixed-point truncation of each row / column
+// (≤ 2^-54 of its largest entry) and the final conversion of C' to double —
+// the result is as accurate as an FP64 GEMM.  Cost: 16 INT8 GEMMs (≈ 4.5
+// POPS dense) and one n²-byte residue stream per modulus instead of an FP64
+// DMMA GEMM (≈ 37 TFLOP/s).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+
+#include "gemm_tc32.cuh"
+#include "launch.h"
+
+namespace psd {
+namespace oz {
+
+constexpr int kNumMod = 16;
+constexpr int kMods[kNumMod] = {256, 255, 253, 251, 247, 241, 239, 233,
+                                229, 227, 223, 217, 211, 199, 197, 193};
+__constant__ int c_mod[kNumMod];
+__constant__ double c_rmod[kNumMod];        // 1 / m
+__constant__ int c_inv[kNumMod][kNumMod];   // (m_i)^{-1} mod m_j, i < j
+
+constexpr int BM = 128;
+constexpr int BKB = 128;                    // K bytes (= int8 elements) per stage row (SWIZZLE_128B)
+constexpr int kThreads = 192;
+
+// r = v mod m ∈ [0, m) for |v| < 2^53 (exact: fma residual, one fix-up)
+PSD_DEVINL int mod_pos(double v, int l) {
+  const double m = (double)c_mod[l];
+  const double q = floor(v * c_rmod[l]);
+  double r = fma(-m, q, v);
+  if (r < 0.0) r += m;
+  if (r >= m) r -= m;
+  return (int)r;
+}
+// symmetric residue as int8: [−128, 127] for m = 256, [−(m−1)/2, (m−1)/2] for odd m
+PSD_DEVINL int8_t sym_res(int r, int l) {
+  const int m = c_mod[l];
+  return (int8_t)(r > (m - 1) / 2 ? r - m : r);
+}
+
+// ---- exponents: e[i] with max_k |x_ik| < 2^e[i] (0 for an all-zero row) ----------
+__global__ void row_exp_kernel(const double* __restrict__ x, long long rows, long long cols,
+                               long long ldx, int* __restrict__ e) {
+  const long long i = blockIdx.x;
+  if (i >= rows) return;
+  double m = 0.0;
+  const double* row = x + i * ldx;
+  for (long long k = threadIdx.x; k < cols; k += blockDim.x) m = fmax(m, fabs(__ldcs(row + k)));
+  m = warp_max(m);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+    e[i] = t > 0.0 ? ilogb(t) + 1 : 0;
+  }
+}
+// column exponents of a K×N row-major panel: atomicMax over per-element exponents
+__global__ void col_exp_kernel(const double* __restrict__ p, long long rows, int cols, long long ldp,
+                               int* __restrict__ f) {
+  const int j = blockIdx.y * 32 + (threadIdx.x & 31);
+  if (j >= cols) return;
+  int mx = -100000;
+  for (long long k = blockIdx.x * 8 + (threadIdx.x >> 5); k < rows; k += (long long)gridDim.x * 8) {
+    const double v = fabs(p[k * ldp + j]);
+    if (v > 0.0) mx = max(mx, ilogb(v) + 1);
+  }
+  if (mx > -100000) atomicMax(&f[j], mx);
+}
+
+// ---- residues of a row-scaled matrix: R[ℓ][i][k] (int8), ld ldr bytes ---------------
+__global__ void residues_rows_kernel(const double* __restrict__ x, long long rows, long long cols,
+                                     long long ldx, const int* __restrict__ e, int8_t* __restrict__ r,
+                                     long long ldr, long long plane) {
+  const long long total = rows * cols;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / cols, k = t % cols;
+    const double a = rint(ldexp(__ldcs(x + i * ldx + k), 53 - e[i]));
+    int8_t* out = r + i * ldr + k;
+#pragma unroll
+    for (int l = 0; l < kNumMod; ++l) out[l * plane] = sym_res(mod_pos(a, l), l);
+  }
+}
+// residues of a K×N panel, transposed and column-scaled: R[ℓ][j][k], j < nrows_pad (zero rows j ≥ N)
+__global__ void residues_panel_t_kernel(const double* __restrict__ p, long long K, int N, long long ldp,
+                                        const int* __restrict__ f, int8_t* __restrict__ r, long long ldr,
+                                        long long plane, int nrows_pad) {
+  __shared__ double tile[32][33];
+  const long long k0 = (long long)blockIdx.x * 32;
+  const int j0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 × 8
+  for (int yy = ty; yy < 32; yy += 8) {
+    const long long k = k0 + yy;
+    const int j = j0 + tx;
+    tile[yy][tx] = (k < K && j < N) ? p[k * ldp + j] : 0.0;
+  }
+  __syncthreads();
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int j = j0 + yy;
+    const long long k = k0 + tx;
+    if (j < nrows_pad && k < K) {
+      const double b = (j < N) ? rint(ldexp(tile[tx][yy], 53 - f[j])) : 0.0;
+      int8_t* out = r + (long long)j * ldr + k;
+#pragma unroll
+      for (int l = 0; l < kNumMod; ++l) out[l * plane] = sym_res(mod_pos(b, l), l);
+    }
+  }
+}
+
+// ---- INT8 CTA-pair GEMM: residue products mod m_ℓ -------------------------------------
+struct I8Params {
+  int M, N, K;
+  int bn, n_mma;            // N per MMA (multiple of 16), MMAs per K step (≤ 2)
+  int kblocks, kb_per_split, m_pairs, splits;
+  int stages;
+  uint8_t* out;             // out[((ℓ·splits + split)·M + i)·ldo + col] = (Σ) mod m_ℓ
+  long long ldo;
+};
+
+PSD_DEVINL void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                 uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+PSD_DEVINL void mma_i8_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+PSD_DEVINL uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    i8_gemm2_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
+                    const I8Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], acc_bar;
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc32::cluster_rank();
+  const int bn_tot = p.bn * p.n_mma;
+  const int hb = p.bn / 2;
+  int u = blockIdx.x >> 1;
+  const int split = u % p.splits;
+  u /= p.splits;
+  const int l = u % kNumMod;
+  const int mp = u / kNumMod;
+  const int m0 = mp * 2 * BM + (int)rank * BM;
+  const int kb0 = split * p.kb_per_split;
+  const int nkb = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  const uint32_t a_bytes = BM * BKB, b_bytes = (uint32_t)p.n_mma * hb * BKB;
+  const uint32_t st_bytes = a_bytes + b_bytes;
+  const uint32_t tcols = bn_tot <= 256 ? 256 : 512;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    mbar_init(smem_u32(&acc_bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "r"(tcols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+  }
+  tc32::tc_fence_before();
+  tc32::cluster_sync_all();
+  tc32::tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % p.stages;
+      const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+      tc32::mbar_wait_t(smem_u32(&empty_bar[s]), ph ^ 1u);
+      if (tc32::elect_one()) {
+        const uint32_t fb_local = smem_u32(&full_bar[s]);
+        const uint32_t fb = tc32::map_to_rank(fb_local, 0);
+        if (rank == 0) mbar_expect_tx(fb_local, 2 * st_bytes);
+        const uint32_t sA = sbase + s * st_bytes;
+        const uint32_t sB = sA + a_bytes;
+        const int kc = (kb0 + i) * BKB;
+        tma_load_3d_pair(sA, &mA, kc, m0, l, fb);
+        for (int h = 0; h < p.n_mma; ++h)
+          tma_load_3d_pair(sB + (uint32_t)h * hb * BKB, &mB, kc, h * p.bn + (int)rank * hb, l, fb);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // kind::i8: D s32 (2), A/B signed int8 (1), K-major, M = 256, N = bn
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.bn >> 3) << 17) |
+                             ((uint32_t)(2 * BM >> 4) << 24);
+      const uint64_t da = desc_sw128(sbase), db = desc_sw128(sbase + a_bytes);
+      const uint32_t b_half = (uint32_t)(hb * BKB) >> 4;
+      const bool two = p.n_mma > 1;
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % p.stages;
+        const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+        tc32::mbar_wait_t(smem_u32(&full_bar[s]), ph);
+        tc32::tc_fence_after();
+        if (tc32::elect_one()) {
+          const uint32_t so = (uint32_t)(s * st_bytes) >> 4;
+#pragma unroll
+          for (int kk = 0; kk < BKB / 32; ++kk) {   // 32 int8 K per MMA = 32 bytes
+            const uint64_t a = da + so + kk * 2, b = db + so + kk * 2;
+            const uint32_t acc0 = (i | kk) != 0;
+            mma_i8_pair(tmem, a, b, idesc, acc0);
+            if (two) mma_i8_pair(tmem + (uint32_t)p.bn, a, b + b_half, idesc, acc0);
+          }
+          tc32::mma_commit_pair(smem_u32(&empty_bar[s]));
+          if (i == nkb - 1) tc32::mma_commit_pair(smem_u32(&acc_bar));
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    const int i = m0 + quad * 32 + lane;
+    tc32::mbar_wait_t(smem_u32(&acc_bar), 0);
+    tc32::tc_fence_after();
+    const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
+    const int m = c_mod[l];
+    uint8_t* orow = p.out + (((long long)l * p.splits + split) * p.M + i) * p.ldo;
+    for (int c0 = 0; c0 < bn_tot; c0 += 16) {
+      float v[16];
+      tc32::tmem_ld16(trow + (uint32_t)c0, v);
+      if (i >= p.M) continue;
+      uint32_t w4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t packed = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          int s32 = __float_as_int(v[4 * q + e]) % m;   // |Σ| < 2^31: exact int mod
+          if (s32 < 0) s32 += m;
+          packed |= (uint32_t)s32 << (8 * e);
+        }
+        w4[q] = packed;
+      }
+      *reinterpret_cast<uint4*>(orow + c0) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+  }
+  tc32::tc_fence_before();
+  tc32::cluster_sync_all();
+  if (warp == 1) {
+    tc32::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tcols) : "memory");
+  }
+}
+
+// ---- CRT (Garner) reconstruction + scaling --------------------------------------------
+// C[i][j] = C'·2^(e_i + f_j − 106) with C' from the residues Σ_split out[ℓ][s][i][j] mod m_ℓ;
+// alpha > 0: C = (C + α·S)/α (the shifted sketch of Alg. 3).
+__global__ void crt_kernel(const uint8_t* __restrict__ res, int splits, long long M, int N, long long ldo,
+                           const int* __restrict__ e, const int* __restrict__ f, double* __restrict__ C,
+                           long long ldc, double alpha, const double* __restrict__ S, long long lds) {
+  const long long total = M * N;
+  const long long plane = M * ldo;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / N;
+    const int j = (int)(t % N);
+    int v[kNumMod];
+#pragma unroll
+    for (int l = 0; l < kNumMod; ++l) {
+      int r = 0;
+      for (int s = 0; s < splits; ++s) r += res[((long long)l * splits + s) * plane + i * ldo + j];
+      v[l] = r % c_mod[l];
+    }
+    // Garner: v[j] ← mixed-radix digits, v_j ∈ [0, m_j)
+#pragma unroll
+    for (int jj = 1; jj < kNumMod; ++jj) {
+      int tt = v[jj];
+      const int mj = c_mod[jj];
+#pragma unroll
+      for (int ii = 0; ii < jj; ++ii) {
+        tt = tt - v[ii];
+        if (tt < 0) tt += mj * ((-tt + mj - 1) / mj);
+        tt = (tt * c_inv[ii][jj]) % mj;
+      }
+      v[jj] = tt;
+    }
+    // C' = v_0 + m_0 (v_1 + m_1 (v_2 + …))  in [0, M)
+    unsigned __int128 acc = (unsigned __int128)v[kNumMod - 1];
+#pragma unroll
+    for (int jj = kNumMod - 2; jj >= 0; --jj) acc = acc * (unsigned)c_mod[jj] + (unsigned)v[jj];
+    // symmetric: C' ≥ M/2 → C' − M (M = Π m_ℓ, passed as two halves via the top bit test)
+    bool neg = false;
+    unsigned __int128 mag = acc;
+    {
+      unsigned __int128 Mfull = 1;
+#pragma unroll
+      for (int l = 0; l < kNumMod; ++l) Mfull *= (unsigned)c_mod[l];
+      if (acc > (Mfull >> 1)) {
+        neg = true;
+        mag = Mfull - acc;
+      }
+    }
+    const unsigned long long hi = (unsigned long long)(mag >> 64), lo = (unsigned long long)mag;
+    double val = fma((double)hi, 18446744073709551616.0, (double)lo);
+    if (neg) val = -val;
+    val = ldexp(val, e[i] + f[j] - 106);
+    if (alpha > 0.0) val = (val + alpha * S[i * lds + j]) / alpha;
+    C[i * ldc + j] = val;
+  }
+}
+
+}  // namespace oz
+
+namespace {
+
+void ensure_oz_constants() {
+  static bool done[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done[dev]) return;
+  int mods[oz::kNumMod];
+  double rm[oz::kNumMod];
+  int inv[oz::kNumMod][oz::kNumMod] = {};
+  for (int l = 0; l < oz::kNumMod; ++l) {
+    mods[l] = oz::kMods[l];
+    rm[l] = 1.0 / oz::kMods[l];
+  }
+  for (int i = 0; i < oz::kNumMod; ++i)
+    for (int j = i + 1; j < oz::kNumMod; ++j) {
+      const int a = oz::kMods[i] % oz::kMods[j], m = oz::kMods[j];
+      int x = 1;
+      while ((a * x) % m != 1) ++x;
+      inv[i][j] = x;
+    }
+  cudaMemcpyToSymbol(oz::c_mod, mods, sizeof(mods));
+  cudaMemcpyToSymbol(oz::c_rmod, rm, sizeof(rm));
+  cudaMemcpyToSymbol(oz::c_inv, inv, sizeof(inv));
+  done[dev] = true;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_oz() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult r;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r) == cudaSuccess &&
+        r == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(q);
+  });
+  return fn;
+}
+
+// int8 planes [L][rows][ld]: box = 128 bytes of K × box_rows × 1 plane, SWIZZLE_128B
+bool map_i8_3d(CUtensorMap* map, const int8_t* ptr, long long cols, long long rows, long long ld,
+               long long planes, int box_rows) {
+  auto fn = encode_oz();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)(ld * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)oz::BKB, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int grid_oz(long long total, int threads) {
+  return (int)std::min<long long>(std::max<long long>((total + threads - 1) / threads, 1),
+                                  (long long)device_info().sms * 16);
+}
+
+}  // namespace
+
+int oz_num_moduli() { return oz::kNumMod; }
+
+void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
+                     long long ldr, cudaStream_t st) {
+  ensure_oz_constants();
+  oz::row_exp_kernel<<<(unsigned)rows, 256, 0, st>>>(x, rows, cols, ldx, e);
+  count_launch();
+  oz::residues_rows_kernel<<<grid_oz(rows * cols, 256), 256, 0, st>>>(x, rows, cols, ldx, e, r, ldr,
+                                                                      ldr * rows);
+  count_launch();
+}
+
+int oz_gemm(const OzOp& op, cudaStream_t st) {
+  using namespace oz;
+  ensure_oz_constants();
+  if (op.M < 1 || op.N < 1 || op.K < 1) return 0;
+  const int w_pad = (op.N + 15) / 16 * 16;
+  if (w_pad > 512 || op.ldbr < op.K || op.ldbr % 16 || op.ldar % 16) return -2;
+  // B = the panel: column exponents and transposed residues
+  cudaMemsetAsync(op.f, 0x80, (size_t)op.N * sizeof(int), st);   // very negative → atomicMax
+  {
+    dim3 grid((unsigned)std::min<long long>((op.K + 7) / 8, 256), (unsigned)((op.N + 31) / 32));
+    col_exp_kernel<<<grid, 256, 0, st>>>(op.P, op.K, op.N, op.ldp, op.f);
+    count_launch();
+  }
+  {
+    dim3 grid((unsigned)((op.K + 31) / 32), (unsigned)((w_pad + 31) / 32));
+    residues_panel_t_kernel<<<grid, dim3(32, 8), 0, st>>>(op.P, op.K, op.N, op.ldp, op.f, op.br, op.ldbr,
+                                                          op.ldbr * w_pad, w_pad);
+    count_launch();
+  }
+  I8Params p{};
+  p.M = op.M;
+  p.N = op.N;
+  p.K = op.K;
+  p.n_mma = w_pad > 256 ? 2 : 1;
+  p.bn = (w_pad / p.n_mma + 15) / 16 * 16;
+  const int bn_tot = p.bn * p.n_mma;
+  p.kblocks = (op.K + BKB - 1) / BKB;
+  p.m_pairs = (op.M + 2 * BM - 1) / (2 * BM);
+  const int slots = device_info().sms / 2;
+  const long long base = (long long)p.m_pairs * kNumMod;
+  int splits = 1;
+  double best = 1e30;
+  for (int s = 1; s <= 8 && s <= p.kblocks; ++s) {
+    const double t = (double)((base * s + slots - 1) / slots) / s + 0.01 * s;
+    if (t < best - 1e-9) {
+      best = t;
+      splits = s;
+    }
+  }
+  while (splits > 1 && (size_t)kNumMod * splits * op.M * bn_tot > op.res_elems) --splits;
+  if ((size_t)kNumMod * op.M * bn_tot > op.res_elems) return -3;
+  p.kb_per_split = (p.kblocks + splits - 1) / splits;
+  p.splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;
+  p.out = op.res;
+  p.ldo = bn_tot;
+  const int sb = BM * BKB + bn_tot / 2 * BKB;
+  p.stages = std::min(8, ((int)device_info().max_smem - 3072) / sb);
+  const size_t smem = (size_t)p.stages * sb + 1024;
+  CUtensorMap ma, mb;
+  if (!map_i8_3d(&ma, op.ar, op.K, op.M, op.ldar, kNumMod, BM) ||
+      !map_i8_3d(&mb, op.br, op.K, w_pad, op.ldbr, kNumMod, p.bn / 2))
+    return -5;
+  static size_t attr[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr[dev] < smem) {
+    cudaFuncSetAttribute(i8_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[dev] = smem;
+  }
+  const long long units = base * p.splits;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * units));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr2[1];
+  attr2[0].id = cudaLaunchAttributeClusterDimension;
+  attr2[0].val.clusterDim.x = 2;
+  attr2[0].val.clusterDim.y = 1;
+  attr2[0].val.clusterDim.z = 1;
+  cfg.attrs = attr2;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, i8_gemm2_kernel, ma, mb, p) != cudaSuccess) return -6;
+  count_launch();
+  crt_kernel<<<grid_oz((long long)op.M * op.N, 256), 256, 0, st>>>(op.res, p.splits, op.M, op.N, p.ldo,
+                                                                   op.e, op.f, op.C, op.ldc, op.alpha,
+                                                                   op.S, op.lds);
+  count_launch();
+  return p.splits;
+}
+
+}  // namespace psd

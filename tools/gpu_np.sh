@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
-for i in 1 2 3; do
-timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider > /tmp/pt.log 2>&1; echo "run $i rc=$?"; tail -1 /tmp/pt.log; grep -E "^FAILED" /tmp/pt.log | head -3
-done
-for i in 1 2 3 4 5 6; do timeout 300 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -k "reduced_n" 2>&1 | tail -1; done
+PSD_FP64_OZAKI=1 timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider > /tmp/pt.log 2>&1; echo "pytest(ozaki) rc=$?"; tail -1 /tmp/pt.log; grep -E "^FAILED" /tmp/pt.log | head -8
+PSD_FP64_OZAKI=1 timeout 300 python tools/probe_c3.py 32768 256 16 1 > /tmp/o.log 2>&1; grep -E "proj 2|sketch|qr |eigh|recon|total" /tmp/o.log
+PSD_FP64_OZAKI=1 timeout 600 python tools/flaky.py 4096 10 2>&1 | tail -2
