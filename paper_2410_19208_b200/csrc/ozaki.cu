@@ -34,6 +34,7 @@ constexpr int kMods[kNumMod] = {256, 255, 253, 251, 247, 241, 239, 233,
                                 229, 227, 223, 217, 211, 199, 197, 193};
 __constant__ int c_mod[kNumMod];
 __constant__ double c_rmod[kNumMod];        // 1 / m
+__constant__ float c_rmodf[kNumMod];        // 1 / m (fp32) for small non-negative operands
 __constant__ int c_inv[kNumMod][kNumMod];   // (m_i)^{-1} mod m_j, i < j
 
 constexpr int BM = 128;
@@ -48,6 +49,15 @@ PSD_DEVINL int mod_pos(double v, int l) {
   if (r < 0.0) r += m;
   if (r >= m) r -= m;
   return (int)r;
+}
+// x mod m for 0 ≤ x < 2^22 (fp32 reciprocal, one fix-up each way)
+PSD_DEVINL int mod_small(int x, int l) {
+  const int m = c_mod[l];
+  int q = (int)((float)x * c_rmodf[l]);
+  int r = x - q * m;
+  if (r < 0) r += m;
+  if (r >= m) r -= m;
+  return r;
 }
 // symmetric residue as int8: [−128, 127] for m = 256, [−(m−1)/2, (m−1)/2] for odd m
 PSD_DEVINL int8_t sym_res(int r, int l) {
@@ -90,6 +100,31 @@ __global__ void col_exp_kernel(const double* __restrict__ p, long long rows, int
 __global__ void residues_rows_kernel(const double* __restrict__ x, long long rows, long long cols,
                                      long long ldx, const int* __restrict__ e, int8_t* __restrict__ r,
                                      long long ldr, long long plane) {
+  // 4 consecutive k per thread: one 32-bit store per modulus (cols % 4 == 0 path)
+  const long long c4 = cols / 4;
+  const long long total = rows * c4;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / c4, k = (t % c4) * 4;
+    const int sh = 53 - e[i];
+    const double2 v01 = __ldcs(reinterpret_cast<const double2*>(x + i * ldx + k));
+    const double2 v23 = __ldcs(reinterpret_cast<const double2*>(x + i * ldx + k + 2));
+    const double a[4] = {rint(ldexp(v01.x, sh)), rint(ldexp(v01.y, sh)), rint(ldexp(v23.x, sh)),
+                         rint(ldexp(v23.y, sh))};
+    int8_t* out = r + i * ldr + k;
+#pragma unroll
+    for (int l = 0; l < kNumMod; ++l) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) packed |= (uint32_t)(uint8_t)sym_res(mod_pos(a[q], l), l) << (8 * q);
+      *reinterpret_cast<uint32_t*>(out + l * plane) = packed;
+    }
+  }
+}
+// scalar fallback (cols % 4 != 0)
+__global__ void residues_rows1_kernel(const double* __restrict__ x, long long rows, long long cols,
+                                      long long ldx, const int* __restrict__ e, int8_t* __restrict__ r,
+                                      long long ldr, long long plane) {
   const long long total = rows * cols;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
@@ -168,11 +203,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t rank = tc32::cluster_rank();
   const int bn_tot = p.bn * p.n_mma;
   const int hb = p.bn / 2;
+  // modulus slowest: the concurrently running CTAs share one B residue plane (L2-resident)
   int u = blockIdx.x >> 1;
+  const int mp = u % p.m_pairs;
+  u /= p.m_pairs;
   const int split = u % p.splits;
-  u /= p.splits;
-  const int l = u % kNumMod;
-  const int mp = u / kNumMod;
+  const int l = u / p.splits;
   const int m0 = mp * 2 * BM + (int)rank * BM;
   const int kb0 = split * p.kb_per_split;
   const int nkb = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
@@ -255,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc32::tc_fence_after();
     const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
     const int m = c_mod[l];
+    const int c15 = mod_small(32768, l);   // 2^15 mod m
     uint8_t* orow = p.out + (((long long)l * p.splits + split) * p.M + i) * p.ldo;
     for (int c0 = 0; c0 < bn_tot; c0 += 16) {
       float v[16];
@@ -266,9 +303,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t packed = 0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          int s32 = __float_as_int(v[4 * q + e]) % m;   // |Σ| < 2^31: exact int mod
-          if (s32 < 0) s32 += m;
-          packed |= (uint32_t)s32 << (8 * e);
+          // |Σ| < 2^30: fold the high part first, then a small-operand mod
+          const int sv = __float_as_int(v[4 * q + e]);
+          const int av = sv < 0 ? -sv : sv;
+          int rr = mod_small(mod_small(av >> 15, l) * c15 + (av & 32767), l);
+          if (sv < 0 && rr) rr = m - rr;
+          packed |= (uint32_t)rr << (8 * e);
         }
         w4[q] = packed;
       }
@@ -300,18 +340,16 @@ __global__ void crt_kernel(const uint8_t* __restrict__ res, int splits, long lon
     for (int l = 0; l < kNumMod; ++l) {
       int r = 0;
       for (int s = 0; s < splits; ++s) r += res[((long long)l * splits + s) * plane + i * ldo + j];
-      v[l] = r % c_mod[l];
+      v[l] = mod_small(r, l);
     }
     // Garner: v[j] ← mixed-radix digits, v_j ∈ [0, m_j)
 #pragma unroll
     for (int jj = 1; jj < kNumMod; ++jj) {
       int tt = v[jj];
-      const int mj = c_mod[jj];
 #pragma unroll
       for (int ii = 0; ii < jj; ++ii) {
-        tt = tt - v[ii];
-        if (tt < 0) tt += mj * ((-tt + mj - 1) / mj);
-        tt = (tt * c_inv[ii][jj]) % mj;
+        tt = tt - v[ii] + 2 * c_mod[jj];               // ≥ 0 (v_i < 256 ≤ 2·m_j), ≡ tt − v_i
+        tt = mod_small(tt * c_inv[ii][jj], jj);        // < 2^18
       }
       v[jj] = tt;
     }
@@ -351,10 +389,12 @@ void ensure_oz_constants() {
   if (done[dev]) return;
   int mods[oz::kNumMod];
   double rm[oz::kNumMod];
+  float rmf[oz::kNumMod];
   int inv[oz::kNumMod][oz::kNumMod] = {};
   for (int l = 0; l < oz::kNumMod; ++l) {
     mods[l] = oz::kMods[l];
     rm[l] = 1.0 / oz::kMods[l];
+    rmf[l] = 1.0f / (float)oz::kMods[l];
   }
   for (int i = 0; i < oz::kNumMod; ++i)
     for (int j = i + 1; j < oz::kNumMod; ++j) {
@@ -365,6 +405,7 @@ void ensure_oz_constants() {
     }
   cudaMemcpyToSymbol(oz::c_mod, mods, sizeof(mods));
   cudaMemcpyToSymbol(oz::c_rmod, rm, sizeof(rm));
+  cudaMemcpyToSymbol(oz::c_rmodf, rmf, sizeof(rmf));
   cudaMemcpyToSymbol(oz::c_inv, inv, sizeof(inv));
   done[dev] = true;
 }
@@ -410,8 +451,12 @@ void oz_prepare_rows(const double* x, long long rows, long long cols, long long 
   ensure_oz_constants();
   oz::row_exp_kernel<<<(unsigned)rows, 256, 0, st>>>(x, rows, cols, ldx, e);
   count_launch();
-  oz::residues_rows_kernel<<<grid_oz(rows * cols, 256), 256, 0, st>>>(x, rows, cols, ldx, e, r, ldr,
-                                                                      ldr * rows);
+  if (cols % 4 == 0 && ldx % 2 == 0 && ldr % 4 == 0 && (uintptr_t)x % 16 == 0)
+    oz::residues_rows_kernel<<<grid_oz(rows * cols / 4, 256), 256, 0, st>>>(x, rows, cols, ldx, e, r, ldr,
+                                                                            ldr * rows);
+  else
+    oz::residues_rows1_kernel<<<grid_oz(rows * cols, 256), 256, 0, st>>>(x, rows, cols, ldx, e, r, ldr,
+                                                                          ldr * rows);
   count_launch();
 }
 
