@@ -36,6 +36,24 @@ __constant__ int c_mod[kNumMod];
 __constant__ double c_rmod[kNumMod];        // 1 / m
 __constant__ float c_rmodf[kNumMod];        // 1 / m (fp32) for small non-negative operands
 __constant__ int c_inv[kNumMod][kNumMod];   // (m_i)^{-1} mod m_j, i < j
+__constant__ unsigned long long c_M[2];     // M = Π m_ℓ as (lo, hi)
+__constant__ float c_modf[kNumMod];         // m_ℓ
+__constant__ float c_pow14f[4][kNumMod];    // 2^(14t) mod m_ℓ
+__constant__ float c_wInvf[kNumMod];        // (M/m_ℓ)^{-1} mod m_ℓ
+__constant__ unsigned long long c_W[kNumMod][2];   // M/m_ℓ as (lo, hi)
+
+// fp32 integer tricks.  kMagic = 1.5·2^23: fmaf(s, 1/m, kMagic) − kMagic = rint(s/m)
+// for |s| < 2^22·m; the bits of (r + kMagic) hold the integer r in their low bytes.
+constexpr float kMagic = 12582912.0f;
+PSD_DEVINL float sym_mod_f(float s, float m, float rm) {   // s − m·rint(s/m), |s| < 2^24 exact
+  const float q = fmaf(s, rm, kMagic) - kMagic;
+  return fmaf(-m, q, s);
+}
+PSD_DEVINL uint32_t low_bits(float r) { return __float_as_uint(r + kMagic); }
+PSD_DEVINL float u2f_small(uint32_t u) { return __uint_as_float(u | 0x4B000000u) - 8388608.0f; }   // u < 2^23
+PSD_DEVINL uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {   // low bytes → one word
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
 
 constexpr int BM = 128;
 constexpr int BKB = 128;                    // K bytes (= int8 elements) per stage row (SWIZZLE_128B)
@@ -100,24 +118,46 @@ __global__ void col_exp_kernel(const double* __restrict__ p, long long rows, int
 __global__ void residues_rows_kernel(const double* __restrict__ x, long long rows, long long cols,
                                      long long ldx, const int* __restrict__ e, int8_t* __restrict__ r,
                                      long long ldr, long long plane) {
-  // 4 consecutive k per thread: one 32-bit store per modulus (cols % 4 == 0 path)
+  // 4 consecutive k per thread: one 32-bit store per modulus (cols % 4 == 0 path).
+  // a (signed, |a| < 2^53) = d0 + d1·2^14 + d2·2^28 + d3·2^42 with 14-bit limbs d0..d2 ≥ 0 and
+  // signed d3; a ≡ s = Σ d_t·(2^(14t) mod m)  (|s| < 2^23.1, exact in fp32), then one
+  // fp32 symmetric reduction.  m = 256 is the low byte of a.
   const long long c4 = cols / 4;
   const long long total = rows * c4;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const long long i = t / c4, k = (t % c4) * 4;
     const int sh = 53 - e[i];
+    const double s1 = ldexp(1.0, sh / 2), s2 = ldexp(1.0, sh - sh / 2);
     const double2 v01 = __ldcs(reinterpret_cast<const double2*>(x + i * ldx + k));
     const double2 v23 = __ldcs(reinterpret_cast<const double2*>(x + i * ldx + k + 2));
-    const double a[4] = {rint(ldexp(v01.x, sh)), rint(ldexp(v01.y, sh)), rint(ldexp(v23.x, sh)),
-                         rint(ldexp(v23.y, sh))};
+    const double xv[4] = {v01.x, v01.y, v23.x, v23.y};
+    float f[4][4];
+    uint32_t lowb[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const long long a = __double2ll_rn(xv[q] * s1 * s2);
+      lowb[q] = (uint32_t)a;
+      f[q][0] = u2f_small((uint32_t)a & 16383u);
+      f[q][1] = u2f_small((uint32_t)(a >> 14) & 16383u);
+      f[q][2] = u2f_small((uint32_t)(a >> 28) & 16383u);
+      f[q][3] = u2f_small((uint32_t)((a >> 42) + 2048)) - 2048.0f;
+    }
     int8_t* out = r + i * ldr + k;
+    *reinterpret_cast<uint32_t*>(out) = pack4(lowb[0], lowb[1], lowb[2], lowb[3]);
 #pragma unroll
-    for (int l = 0; l < kNumMod; ++l) {
-      uint32_t packed = 0;
+    for (int l = 1; l < kNumMod; ++l) {
+      const float m = c_modf[l], rm = c_rmodf[l];
+      const float p1 = c_pow14f[1][l], p2 = c_pow14f[2][l], p3 = c_pow14f[3][l];
+      uint32_t b[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) packed |= (uint32_t)(uint8_t)sym_res(mod_pos(a[q], l), l) << (8 * q);
-      *reinterpret_cast<uint32_t*>(out + l * plane) = packed;
+      for (int q = 0; q < 4; ++q) {
+        const float sacc = fmaf(f[q][3], p3, fmaf(f[q][2], p2, fmaf(f[q][1], p1, f[q][0])));
+        float rr = sym_mod_f(sacc, m, rm);     // |rr| ≤ 0.503·m
+        if (l == 1) rr = rr > 127.5f ? rr - m : rr;   // m = 255 can land on +128
+        b[q] = low_bits(rr);
+      }
+      *reinterpret_cast<uint32_t*>(out + l * plane) = pack4(b[0], b[1], b[2], b[3]);
     }
   }
 }
@@ -290,28 +330,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc32::mbar_wait_t(smem_u32(&acc_bar), 0);
     tc32::tc_fence_after();
     const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
-    const int m = c_mod[l];
-    const int c15 = mod_small(32768, l);   // 2^15 mod m
+    // |Σ| ≤ K_split·2^14 ≤ 2^29: Σ = hi·2^15 + lo, s = hi·(2^15 mod m) + lo (|s| < 2^23),
+    // stored as a signed int8 representative of Σ mod m (m = 256: the low byte).
+    const float m = c_modf[l], rm = c_rmodf[l];
+    const float c15 = (float)(32768 % c_mod[l]);
     uint8_t* orow = p.out + (((long long)l * p.splits + split) * p.M + i) * p.ldo;
     for (int c0 = 0; c0 < bn_tot; c0 += 16) {
       float v[16];
       tc32::tmem_ld16(trow + (uint32_t)c0, v);
       if (i >= p.M) continue;
+      uint32_t b[16];
+      if (l == 0) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) b[e] = __float_as_uint(v[e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int sv = __float_as_int(v[e]);
+          const float hf = u2f_small((uint32_t)((sv >> 15) + 32768)) - 32768.0f;
+          const float lf = u2f_small((uint32_t)sv & 32767u);
+          float rr = sym_mod_f(fmaf(hf, c15, lf), m, rm);
+          rr = rr > 127.5f ? rr - m : rr;
+          b[e] = low_bits(rr);
+        }
+      }
       uint32_t w4[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t packed = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          // |Σ| < 2^30: fold the high part first, then a small-operand mod
-          const int sv = __float_as_int(v[4 * q + e]);
-          const int av = sv < 0 ? -sv : sv;
-          int rr = mod_small(mod_small(av >> 15, l) * c15 + (av & 32767), l);
-          if (sv < 0 && rr) rr = m - rr;
-          packed |= (uint32_t)rr << (8 * e);
-        }
-        w4[q] = packed;
-      }
+      for (int q = 0; q < 4; ++q) w4[q] = pack4(b[4 * q], b[4 * q + 1], b[4 * q + 2], b[4 * q + 3]);
       *reinterpret_cast<uint4*>(orow + c0) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
     }
   }
@@ -323,58 +368,61 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// ---- CRT (Garner) reconstruction + scaling --------------------------------------------
-// C[i][j] = C'·2^(e_i + f_j − 106) with C' from the residues Σ_split out[ℓ][s][i][j] mod m_ℓ;
+// ---- CRT reconstruction + scaling ----------------------------------------------------
+// C[i][j] = C'·2^(e_i + f_j − 106), C' the symmetric residue of the product mod M:
+//   y_ℓ = (Σ_split out[ℓ][s][i][j])·(M/m_ℓ)^{-1} mod m_ℓ,   S = Σ_ℓ y_ℓ·(M/m_ℓ),
+//   S/M = Σ_ℓ y_ℓ/m_ℓ  →  k = rint(Σ_ℓ y_ℓ/m_ℓ) (fp32: |C'|/M ≤ 2^-3, far from ½),
+//   C' = S − k·M evaluated mod 2^128 (|C'| < 2^127, so the wrapped value is exact).
+// Four columns per thread (ldo % 4 == 0; columns ≥ N are padding and not stored).
 // alpha > 0: C = (C + α·S)/α (the shifted sketch of Alg. 3).
 __global__ void crt_kernel(const uint8_t* __restrict__ res, int splits, long long M, int N, long long ldo,
                            const int* __restrict__ e, const int* __restrict__ f, double* __restrict__ C,
                            long long ldc, double alpha, const double* __restrict__ S, long long lds) {
-  const long long total = M * N;
+  const int n4 = (N + 3) / 4;
+  const long long total = M * n4;
   const long long plane = M * ldo;
+  const unsigned __int128 Mfull = ((unsigned __int128)c_M[1] << 64) | c_M[0];
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
-    const long long i = t / N;
-    const int j = (int)(t % N);
-    int v[kNumMod];
+    const long long i = t / n4;
+    const int j0 = (int)(t % n4) * 4;
+    const uint8_t* base = res + i * ldo + j0;
+    float ks[4] = {0.f, 0.f, 0.f, 0.f};
+    unsigned __int128 acc[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int l = 0; l < kNumMod; ++l) {
-      int r = 0;
-      for (int s = 0; s < splits; ++s) r += res[((long long)l * splits + s) * plane + i * ldo + j];
-      v[l] = mod_small(r, l);
-    }
-    // Garner: v[j] ← mixed-radix digits, v_j ∈ [0, m_j)
+      int sum[4] = {0, 0, 0, 0};
+      for (int sp = 0; sp < splits; ++sp) {
+        const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(base + ((long long)l * splits + sp) * plane));
 #pragma unroll
-    for (int jj = 1; jj < kNumMod; ++jj) {
-      int tt = v[jj];
-#pragma unroll
-      for (int ii = 0; ii < jj; ++ii) {
-        tt = tt - v[ii] + 2 * c_mod[jj];               // ≥ 0 (v_i < 256 ≤ 2·m_j), ≡ tt − v_i
-        tt = mod_small(tt * c_inv[ii][jj], jj);        // < 2^18
+        for (int q = 0; q < 4; ++q) sum[q] += (int)(int8_t)(w >> (8 * q));
       }
-      v[jj] = tt;
-    }
-    // C' = v_0 + m_0 (v_1 + m_1 (v_2 + …))  in [0, M)
-    unsigned __int128 acc = (unsigned __int128)v[kNumMod - 1];
+      const float m = c_modf[l], rm = c_rmodf[l], winv = c_wInvf[l];
+      const unsigned __int128 W = ((unsigned __int128)c_W[l][1] << 64) | c_W[l][0];
 #pragma unroll
-    for (int jj = kNumMod - 2; jj >= 0; --jj) acc = acc * (unsigned)c_mod[jj] + (unsigned)v[jj];
-    // symmetric: C' ≥ M/2 → C' − M (M = Π m_ℓ, passed as two halves via the top bit test)
-    bool neg = false;
-    unsigned __int128 mag = acc;
-    {
-      unsigned __int128 Mfull = 1;
-#pragma unroll
-      for (int l = 0; l < kNumMod; ++l) Mfull *= (unsigned)c_mod[l];
-      if (acc > (Mfull >> 1)) {
-        neg = true;
-        mag = Mfull - acc;
+      for (int q = 0; q < 4; ++q) {
+        float y = sym_mod_f((float)sum[q] * winv, m, rm);   // |sum·winv| < 2^19: exact
+        y = y < 0.f ? y + m : y;                             // y ∈ [0, m]
+        ks[q] = fmaf(y, rm, ks[q]);
+        const uint32_t yi = __float_as_uint(y + kMagic) - 0x4B400000u;
+        acc[q] += W * yi;
       }
     }
-    const unsigned long long hi = (unsigned long long)(mag >> 64), lo = (unsigned long long)mag;
-    double val = fma((double)hi, 18446744073709551616.0, (double)lo);
-    if (neg) val = -val;
-    val = ldexp(val, e[i] + f[j] - 106);
-    if (alpha > 0.0) val = (val + alpha * S[i * lds + j]) / alpha;
-    C[i * ldc + j] = val;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q;
+      if (j >= N) break;
+      const unsigned __int128 kM = Mfull * (unsigned)(int)rintf(ks[q]);
+      const unsigned __int128 cs = acc[q] - kM;           // two's complement of C'
+      const bool neg = (long long)(cs >> 64) < 0;
+      const unsigned __int128 mag = neg ? (unsigned __int128)0 - cs : cs;
+      const unsigned long long hi = (unsigned long long)(mag >> 64), lo = (unsigned long long)mag;
+      double val = fma((double)hi, 18446744073709551616.0, (double)lo);
+      if (neg) val = -val;
+      val = ldexp(val, e[i] + f[j] - 106);
+      if (alpha > 0.0) val = (val + alpha * S[i * lds + j]) / alpha;
+      C[i * ldc + j] = val;
+    }
   }
 }
 
@@ -407,6 +455,32 @@ void ensure_oz_constants() {
   cudaMemcpyToSymbol(oz::c_rmod, rm, sizeof(rm));
   cudaMemcpyToSymbol(oz::c_rmodf, rmf, sizeof(rmf));
   cudaMemcpyToSymbol(oz::c_inv, inv, sizeof(inv));
+  unsigned __int128 M = 1;
+  for (int l = 0; l < oz::kNumMod; ++l) M *= (unsigned)oz::kMods[l];
+  const unsigned long long Mh[2] = {(unsigned long long)M, (unsigned long long)(M >> 64)};
+  cudaMemcpyToSymbol(oz::c_M, Mh, sizeof(Mh));
+  float modf[oz::kNumMod], pw[4][oz::kNumMod], winv[oz::kNumMod];
+  unsigned long long W[oz::kNumMod][2];
+  for (int l = 0; l < oz::kNumMod; ++l) {
+    const int m = oz::kMods[l];
+    modf[l] = (float)m;
+    long long v = 1;
+    for (int t = 0; t < 4; ++t) {
+      pw[t][l] = (float)(v % m);
+      v = (v * 16384) % m;
+    }
+    const unsigned __int128 w = M / (unsigned)m;
+    W[l][0] = (unsigned long long)w;
+    W[l][1] = (unsigned long long)(w >> 64);
+    const int wm = (int)(w % (unsigned)m);
+    int x = 1;
+    while ((wm * x) % m != 1) ++x;
+    winv[l] = (float)x;
+  }
+  cudaMemcpyToSymbol(oz::c_modf, modf, sizeof(modf));
+  cudaMemcpyToSymbol(oz::c_pow14f, pw, sizeof(pw));
+  cudaMemcpyToSymbol(oz::c_wInvf, winv, sizeof(winv));
+  cudaMemcpyToSymbol(oz::c_W, W, sizeof(W));
   done[dev] = true;
 }
 
@@ -490,10 +564,13 @@ int oz_gemm(const OzOp& op, cudaStream_t st) {
   p.m_pairs = (op.M + 2 * BM - 1) / (2 * BM);
   const int slots = device_info().sms / 2;
   const long long base = (long long)p.m_pairs * kNumMod;
-  int splits = 1;
+  // unit time ≈ T/s + c (setup, pipeline fill, epilogue; c ≈ 2% of a full-K unit at K = 32k);
+  // the epilogue bound |Σ| ≤ 2^29 needs K per split ≤ 32768.
+  const int min_splits = (p.kblocks + 255) / 256;
+  int splits = min_splits;
   double best = 1e30;
-  for (int s = 1; s <= 8 && s <= p.kblocks; ++s) {
-    const double t = (double)((base * s + slots - 1) / slots) / s + 0.01 * s;
+  for (int s = min_splits; s <= std::max(8, min_splits) && s <= p.kblocks; ++s) {
+    const double t = (double)((base * s + slots - 1) / slots) * (p.kblocks / 256.0 / s + 0.02);
     if (t < best - 1e-9) {
       best = t;
       splits = s;
@@ -534,7 +611,7 @@ int oz_gemm(const OzOp& op, cudaStream_t st) {
   cfg.numAttrs = 1;
   if (cudaLaunchKernelEx(&cfg, i8_gemm2_kernel, ma, mb, p) != cudaSuccess) return -6;
   count_launch();
-  crt_kernel<<<grid_oz((long long)op.M * op.N, 256), 256, 0, st>>>(op.res, p.splits, op.M, op.N, p.ldo,
+  crt_kernel<<<grid_oz((long long)op.M * ((op.N + 3) / 4), 256), 256, 0, st>>>(op.res, p.splits, op.M, op.N, p.ldo,
                                                                    op.e, op.f, op.C, op.ldc, op.alpha,
                                                                    op.S, op.lds);
   count_launch();
