@@ -7,7 +7,10 @@
 One step = one projection (``ran_proj``, Alg. 2) of a seeded C3 matrix that is
 already resident in HBM; the K timed steps cycle through a pool of distinct
 matrices (8.6 GB each ≫ 126 MB L2, so no L2 flush is needed).  Ω is drawn on
-the device each step (Philox).  Multi-GPU: independent replicas, one process
+the device each step (Philox).  The FP64 n×n sketch products run by default on
+the INT8 tensor cores as an exact FP64 emulation (Ozaki scheme II, csrc/ozaki.cu;
+same ≤1e-10 parity as the DMMA path); ``--fp64-engine dmma`` keeps them on the
+FP64 DMMA kernel.  Multi-GPU: independent replicas, one process
 per GPU (the C3 projections are independent), value
 = all ranks' projections / max-over-ranks device time.
 
@@ -61,6 +64,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the config-3 FP32 (3xTF32) leg")
+    ap.add_argument("--fp64-engine", choices=["int8", "dmma"], default="int8",
+                    help="FP64 sketch products: exact emulation on the INT8 tensor cores (default) or DMMA")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     for key in ("n", "k", "p", "q"):
@@ -222,8 +227,45 @@ def fp64_peak(torch, dev):
     return 2 * 8192 ** 3 / best / 1e9
 
 
-def load_traffic():
-    path = os.path.join(REPO, "profiles", "gemm_traffic.json")  # from the committed ncu --set full capture
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def int8_roofline(n, w, i8_ms, i8_cnt, traffic):
+    """HBM roofline of i8_gemm2_kernel (one emulated FP64 sketch product)."""
+    L = 16
+    ldk = (n + 127) // 128 * 128
+    wpad = (w + 15) // 16 * 16
+    bn_tot = wpad if wpad <= 256 else 2 * ((wpad // 2 + 15) // 16 * 16)
+    algo = L * n * ldk + L * wpad * ldk + L * n * bn_tot      # A planes + panel planes + outputs
+    pk = measured_peaks()
+    hbm = pk.get("hbm_gbs") or 7700.0
+    achieved = algo / (i8_ms / 1000.0) / 1e9
+    int8_ops = 2.0 * L * n * n * w
+    tops = int8_ops / (i8_ms / 1000.0) / 1e12
+    int8_peak = 2.0 * (pk.get("bf16_tflops") or 2250.0)
+    return {
+        "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+        "traffic": traffic.get("bytes_per_launch") if traffic else None,
+        "algorithmic_bytes_per_launch": algo,
+        "kernel": f"i8_gemm2_kernel<tcgen05.mma.cta_group::2.kind::i8, TMEM, TMA> — the 16 residue "
+                  f"products of X·P mod m_l for one FP64 sketch product; {algo / 1e9:.2f} GB "
+                  f"algorithmic per launch, {i8_ms:.3f} ms avg over {i8_cnt} launches (CUDA events "
+                  f"on the launching stream, timed region)",
+        "peak_source": ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if pk.get("hbm_gbs")
+                        else "B200_PROFILING.md fallback"),
+        "tensor_view": {"achieved_tops": tops, "int8_peak_tops": int8_peak, "frac": tops / int8_peak,
+                        "peak_source": "2 x MEASURED_PEAKS bf16_tflops (dense int8 = 2x bf16 on B200)"},
+        "traffic_source": traffic.get("source") if traffic else None,
+    }
+
+
+def load_traffic(name="gemm_traffic.json"):
+    path = os.path.join(REPO, "profiles", name)  # from the committed ncu --set full capture
     try:
         with open(path) as fh:
             return json.load(fh)
@@ -247,6 +289,7 @@ def run_ours(a):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     n, params = a.n, psd.RangeParams(k=a.k, l=a.p, q=a.q)
+    psd.set_fp64_engine(a.fp64_engine)
 
     peak = fp64_peak(torch, dev) if rank == 0 else None
     nominal = 148 * 128 * 1.965  # GFLOP/s: 148 SMs × 64 DMMA FMA/clk × 2 × 1965 MHz
@@ -273,6 +316,7 @@ def run_ours(a):
     e1 = torch.cuda.Event(enable_timing=True)
     launches = 0
     ranks = []
+    engine = 0
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
     e0.record()
     for i in range(a.steps):
@@ -282,6 +326,7 @@ def run_ours(a):
         rep = psd.ran_proj(pool[i % a.pool], params, rng)
         launches += rep.device_info["gpu_launches"]
         ranks.append(rep.effective_rank)
+        engine = rep.device_info["sketch_engine"]
     marks[a.steps].record()
     e1.record()
     torch.cuda.synchronize(dev)
@@ -297,13 +342,17 @@ def run_ours(a):
         ms = float(t.item())
     value = world * a.steps / (ms / 1000.0)
 
-    # FP64 roofline of the dominant kernel: the op(X)·P DMMA GEMM (2n²w flops per launch)
+    # roofline of the dominant kernel.  DMMA engine: the op(X)·P FP64 GEMM (2n²w flops
+    # per launch).  INT8 engine: the residue GEMM i8_gemm2_kernel, HBM-bound — per
+    # launch it streams the 16 int8 residue planes of X (16·n·ld_k bytes) plus the
+    # panel residues and the per-modulus outputs.
     g_ms, g_cnt = prof["sketch_gemm"]
     gemm_ms = g_ms / max(g_cnt, 1)
     gemm_tf = 2.0 * n * n * params.width / (gemm_ms / 1000.0) / 1e12
+    i8_ms, i8_cnt = prof.get("int8_gemm", (0.0, 0))
     r_plus = statistics.median(ranks) if ranks else 0
     flops = psd.flops(n, params, r_plus)
-    traffic = load_traffic()
+    traffic = load_traffic("oz_traffic.json" if engine == 1 else "gemm_traffic.json")
     stages = {k: round(v[0] / a.steps, 3) for k, v in prof.items() if v[1]}
 
     fp32 = None
@@ -334,7 +383,8 @@ def run_ours(a):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded BASELINE {a.config} matrices generated in HBM)",
         "config": workload_config(a, world),
-        "roofline": {
+        "roofline": (int8_roofline(n, params.width, i8_ms / max(i8_cnt, 1), i8_cnt, traffic)
+                     if engine == 1 and i8_cnt else {
             "bound": "tensor", "achieved": gemm_tf, "peak": peak_tf, "unit": "TFLOP/s",
             "frac": gemm_tf / peak_tf, "traffic": traffic.get("bytes_per_launch") if traffic else None,
             "kernel": "gemm_tma_kernel<TMA-fed, warp-specialised DMMA, 64x272 tiles> — op(X)·P "
@@ -343,7 +393,11 @@ def run_ours(a):
             "peak_source": "cuBLAS DGEMM 8192³ burst measured in this run (MEASURED_PEAKS.json has "
                            f"no FP64 entry); nominal DMMA peak at 1965 MHz = {nominal / 1000:.1f}",
             "traffic_source": traffic.get("source") if traffic else None,
-        },
+        }),
+        "sketch_engine": {0: "fp64-dmma", 1: "int8-ozaki2 (exact FP64 emulation)", 2: "3xtf32"}[engine],
+        "sketch_product_fp64_equiv_tflops": gemm_tf,
+        "sketch_product_ms": gemm_ms,
+        "fp64_dmma_peak_tflops": peak_tf,
         "projection_tflops": flops * value / world / 1e12,
         "projection_roofline_frac": flops * value / world / 1e12 / peak_tf,
         "flops_per_projection": flops,

@@ -40,6 +40,7 @@ enum psd_status {
 #define PSD_FLAG_STRICT 2u        /* RankDeficientSample instead of truncation (sketch.py:86-92) */
 #define PSD_FLAG_SKIP_SYMCHECK 4u /* caller already ran psd_require_symmetric on X */
 #define PSD_FLAG_ASSUME_SYMMETRIC 8u /* X is bitwise symmetric: X^T·P computed as X·P */
+#define PSD_FLAG_FP64_DMMA 16u     /* keep the FP64 n x n products on the DMMA kernel (no INT8 emulation) */
 
 typedef struct psd_plan psd_plan;
 
@@ -53,7 +54,8 @@ enum psd_stage {
   PSD_STAGE_RECON = 5,       /* W = Q U, mirrored SYRK reconstruction        */
   PSD_STAGE_DIAG = 6,        /* residual diagnostics                         */
   PSD_STAGE_TOTAL = 7,       /* whole psd_ran_proj call                      */
-  PSD_NUM_STAGES = 8
+  PSD_STAGE_INT8_GEMM = 8,   /* INT8 tensor-core kernel inside an emulated FP64 sketch product */
+  PSD_NUM_STAGES = 9
 };
 
 typedef struct psd_report {
@@ -64,7 +66,7 @@ typedef struct psd_report {
   int32_t qr_shifted;      /* 1 if a shifted CholeskyQR pass was needed */
   int32_t eig_sweeps;      /* block-Jacobi sweeps of the k x k eigensolve */
   int32_t gpu_launches;    /* kernels this call launched */
-  int32_t reserved;
+  int32_t sketch_engine;   /* n x n products ran on: 0 FP64 DMMA, 1 INT8-emulated FP64 (Ozaki II), 2 3xTF32 */
   double residual_frob;    /* PSD_FLAG_DIAGNOSTICS only, else NaN */
   double max_abs;          /* max|x_ij| (symmetric.py:51) */
   double sym_defect;       /* max|x_ij - x_ji| (symmetric.py:52) */

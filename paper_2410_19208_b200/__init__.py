@@ -12,7 +12,7 @@ from .errors import (AlphaTooSmall, AsymmetricMatrixError, ConvergenceFailure, D
                      RankDeficientSample)
 from ._tensors import DeviceRng
 from .projection import (METHODS, ProjectionReport, ProjectorConfig, flops, project, ran_proj,
-                         ran_proj_scal)
+                         ran_proj_scal, set_fp64_engine)
 from .sketch import (RangeParams, min_eig_magnitude, orthonormality_defect, power_iteration,
                      range_finder)
 from .symmetric import (EigenDecomposition, eigh, exact_psd_projection, frobenius_norm,
@@ -30,7 +30,7 @@ __all__ = [
     "AlphaTooSmall", "AsymmetricMatrixError", "ConvergenceFailure", "DeviceError",
     "DimensionMismatch", "InvalidParams", "NonSquareError", "PsdconeError", "RankDeficientSample",
     "DeviceRng", "METHODS", "ProjectionReport", "ProjectorConfig", "flops", "project", "ran_proj",
-    "ran_proj_scal", "RangeParams", "min_eig_magnitude", "orthonormality_defect",
+    "ran_proj_scal", "set_fp64_engine", "RangeParams", "min_eig_magnitude", "orthonormality_defect",
     "power_iteration", "range_finder", "EigenDecomposition", "eigh", "exact_psd_projection",
     "frobenius_norm", "gaussian_matrix", "require_symmetric", "rng_from_seed", "symmetrize",
     "install", "uninstall", "solve", "SparseSdlsProblem", "SolveReport", "TrajectoryPoint",

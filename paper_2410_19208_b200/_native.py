@@ -32,7 +32,7 @@ class PsdReport(ctypes.Structure):
         ("qr_shifted", ctypes.c_int32),
         ("eig_sweeps", ctypes.c_int32),
         ("gpu_launches", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("sketch_engine", ctypes.c_int32),
         ("residual_frob", ctypes.c_double),
         ("max_abs", ctypes.c_double),
         ("sym_defect", ctypes.c_double),
@@ -40,15 +40,16 @@ class PsdReport(ctypes.Structure):
     ]
 
     def as_dict(self):
-        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+        return {name: getattr(self, name) for name, _ in self._fields_}
 
 
-STAGES = ("symcheck", "sketch_gemm", "qr", "compress", "eigh", "recon", "diag", "total")
+STAGES = ("symcheck", "sketch_gemm", "qr", "compress", "eigh", "recon", "diag", "total", "int8_gemm")
 
 FLAG_DIAGNOSTICS = 1
 FLAG_STRICT = 2
 FLAG_SKIP_SYMCHECK = 4
 FLAG_ASSUME_SYMMETRIC = 8
+FLAG_FP64_DMMA = 16
 
 # name → (restype, argtypes); the full exported surface of include/psdproj.h
 SIGNATURES = {

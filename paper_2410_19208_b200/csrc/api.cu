@@ -49,6 +49,7 @@ struct psd_plan {
   int *oz_e = nullptr, *oz_f = nullptr;
   uint8_t* oz_res = nullptr;
   ll oz_ldk = 0;
+  bool oz_failed = false;
   size_t oz_res_elems = 0;
   ll ldx32 = 0;
   size_t ws32_elems = 0;
@@ -657,7 +658,8 @@ int ensure_f32(psd_plan* p, bool need_hi) {
 // Ozaki-II buffers (allocated on first use): 16 int8 residue planes of X
 // (n × ldk each), panel residues, exponents, per-split residue partials.
 int ensure_oz(psd_plan* p) {
-  if (p->oz_ar) return PSD_OK;
+  if (p->oz_ldk) return PSD_OK;
+  if (p->oz_failed) return PSD_ERR_NO_MEMORY;
   const int L = psd::oz_num_moduli();
   const ll ldk = (p->n + 127) / 128 * 128;
   const ll wpad = (p->w + 15) / 16 * 16;
@@ -670,8 +672,10 @@ int ensure_oz(psd_plan* p) {
   p->oz_f = static_cast<int*>(balloc((size_t)wpad * sizeof(int)));
   p->oz_res_elems = (size_t)L * 8 * p->n * wpad;
   p->oz_res = static_cast<uint8_t*>(balloc(p->oz_res_elems));
-  if (!p->oz_ar || !p->oz_br || !p->oz_e || !p->oz_f || !p->oz_res)
+  if (!p->oz_ar || !p->oz_br || !p->oz_e || !p->oz_f || !p->oz_res) {
+    p->oz_failed = true;
     return fail(PSD_ERR_NO_MEMORY, "device allocation failed for the INT8-emulation buffers");
+  }
   p->oz_ldk = ldk;
   cudaMemset(p->oz_ar, 0, (size_t)L * p->n * ldk);   // K padding stays zero
   cudaMemset(p->oz_br, 0, (size_t)L * wpad * ldk);
@@ -701,8 +705,13 @@ int xmul_oz(psd_plan* p, ll n, const double* P, ll ldP, int w, double* out, ll l
   op.alpha = alpha;
   op.S = P;
   op.lds = ldP;
+  if (p->prof) {
+    op.ev_gemm[0] = take_event(p);
+    op.ev_gemm[1] = take_event(p);
+  }
   const int r = psd::oz_gemm(op, st);
   if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "INT8-emulated GEMM rejected its operands (%d)", r);
+  if (p->prof) p->marks.push_back({PSD_STAGE_INT8_GEMM, {op.ev_gemm[0], op.ev_gemm[1]}});
   return PSD_OK;
 }
 
@@ -829,14 +838,19 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     ldo_eff = ld;
   }
   // FP64 n×n products on the INT8 tensor cores (Ozaki II) when X is bitwise
-  // symmetric (Xᵀ·P = X·P, the residues of X's rows serve both) — opt-in
+  // symmetric (Xᵀ·P = X·P, the residues of X's rows serve both); PSD_FP64_OZAKI=0
+  // keeps them on the FP64 DMMA kernel.
   static const bool oz_on = [] {
     const char* e = getenv("PSD_FP64_OZAKI");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
-  const bool oz = !f32 && oz_on && !use_t && w <= 512;
+  bool oz = !f32 && oz_on && !(flags & PSD_FLAG_FP64_DMMA) && !use_t && w <= 512;
+  if (oz && ensure_oz(p) != PSD_OK) {   // no room for the residue planes: DMMA products
+    cudaGetLastError();
+    oz = false;
+  }
+  r.sketch_engine = f32 ? 2 : (oz ? 1 : 0);
   if (oz) {
-    PSD_TRY(ensure_oz(p));
     Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
     psd::oz_prepare_rows(x64, n, n, ldx, p->oz_e, p->oz_ar, p->oz_ldk, st);
   }
@@ -1035,7 +1049,7 @@ int psd_gemm_f64_ozaki(const double* a, int64_t lda, const double* pp, int64_t l
   int8_t *ar = nullptr, *br = nullptr;
   int *e = nullptr, *f = nullptr;
   uint8_t* res = nullptr;
-  const size_t res_elems = (size_t)L * 8 * m * wpad;
+  const size_t res_elems = (size_t)L * std::max<ll>(8, (kk + 32767) / 32768 + 1) * m * (wpad + 16);
   bool ok = cudaMalloc(&ar, (size_t)L * m * ldk) == cudaSuccess &&
             cudaMalloc(&br, (size_t)L * wpad * ldk) == cudaSuccess &&
             cudaMalloc(&e, (size_t)m * sizeof(int)) == cudaSuccess &&

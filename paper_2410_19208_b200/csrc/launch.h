@@ -87,6 +87,7 @@ struct OzOp {
   double alpha = 0.0;          // α > 0: C = (acc + α·S)/α
   const double* S = nullptr;
   long long lds = 0;
+  cudaEvent_t ev_gemm[2] = {nullptr, nullptr};   // optional: recorded around the INT8 kernel
 };
 int oz_num_moduli();
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,

@@ -576,8 +576,8 @@ int oz_gemm(const OzOp& op, cudaStream_t st) {
       splits = s;
     }
   }
-  while (splits > 1 && (size_t)kNumMod * splits * op.M * bn_tot > op.res_elems) --splits;
-  if ((size_t)kNumMod * op.M * bn_tot > op.res_elems) return -3;
+  while (splits > min_splits && (size_t)kNumMod * splits * op.M * bn_tot > op.res_elems) --splits;
+  if ((size_t)kNumMod * splits * op.M * bn_tot > op.res_elems) return -3;
   p.kb_per_split = (p.kblocks + splits - 1) / splits;
   p.splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;
   p.out = op.res;
@@ -609,7 +609,9 @@ int oz_gemm(const OzOp& op, cudaStream_t st) {
   attr2[0].val.clusterDim.z = 1;
   cfg.attrs = attr2;
   cfg.numAttrs = 1;
+  if (op.ev_gemm[0]) cudaEventRecord(op.ev_gemm[0], st);
   if (cudaLaunchKernelEx(&cfg, i8_gemm2_kernel, ma, mb, p) != cudaSuccess) return -6;
+  if (op.ev_gemm[1]) cudaEventRecord(op.ev_gemm[1], st);
   count_launch();
   crt_kernel<<<grid_oz((long long)op.M * ((op.N + 3) / 4), 256), 256, 0, st>>>(op.res, p.splits, op.M, op.N, p.ldo,
                                                                    op.e, op.f, op.C, op.ldc, op.alpha,

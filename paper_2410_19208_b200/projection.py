@@ -82,6 +82,20 @@ def resolve_dtype(dtype):
     raise errors.error("InvalidParams", f"unsupported dtype {dtype!r} (fp64 or fp32)")
 
 
+_FP64_ENGINE = "int8"
+
+
+def set_fp64_engine(engine):
+    """Tensor-core engine of the FP64 n×n sketch products: "int8" (default; FP64
+    emulated exactly on the INT8 tensor cores, Ozaki scheme II, when X is bitwise
+    symmetric) or "dmma" (the FP64 DMMA kernel).  Returns the previous setting."""
+    global _FP64_ENGINE
+    if engine not in ("int8", "dmma"):
+        raise errors.error("InvalidParams", f"unknown FP64 engine {engine!r} (int8 or dmma)")
+    prev, _FP64_ENGINE = _FP64_ENGINE, engine
+    return prev
+
+
 def _operand(x, dtype):
     return as_device(x, dtype=torch.float32 if resolve_dtype(dtype) == "fp32" else torch.float64)
 
@@ -110,6 +124,8 @@ def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, m
         flags = _native.FLAG_SKIP_SYMCHECK
         if stats is None or stats.bitwise:
             flags |= _native.FLAG_ASSUME_SYMMETRIC
+        if _FP64_ENGINE == "dmma":
+            flags |= _native.FLAG_FP64_DMMA
     if collect_diagnostics:
         flags |= _native.FLAG_DIAGNOSTICS
     rep = _native.PsdReport()
@@ -253,4 +269,4 @@ def flops(n, params, effective_rank):
 
 
 __all__ = ["METHODS", "resolve_dtype", "ProjectorConfig", "ProjectionReport", "ran_proj", "ran_proj_scal",
-           "project", "flops"]
+           "project", "flops", "set_fp64_engine"]

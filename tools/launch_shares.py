@@ -6,7 +6,7 @@ import sys
 
 path = sys.argv[1]
 title = sys.argv[2] if len(sys.argv) > 2 else path
-OURS = ("psd::", "tc32::", "<unnamed>::")   # kernels of libpsdproj.so (workload generators excluded)
+OURS = ("psd::", "tc32::", "oz::", "<unnamed>::")   # kernels of libpsdproj.so (workload generators excluded)
 with open(path) as f:
     lines = [l for l in f if l.startswith('"')]
 agg = collections.OrderedDict()
