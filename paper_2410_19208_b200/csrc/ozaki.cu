@@ -38,7 +38,7 @@ __constant__ float c_rmodf[kNumMod];        // 1 / m (fp32) for small non-negati
 __constant__ int c_inv[kNumMod][kNumMod];   // (m_i)^{-1} mod m_j, i < j
 __constant__ unsigned long long c_M[2];     // M = Π m_ℓ as (lo, hi)
 __constant__ float c_modf[kNumMod];         // m_ℓ
-__constant__ float c_pow14f[4][kNumMod];    // 2^(14t) mod m_ℓ
+__constant__ float c_pow13f[4][kNumMod];    // 2^(13t) mod m_ℓ in (−m/2, m/2]
 __constant__ float c_wInvf[kNumMod];        // (M/m_ℓ)^{-1} mod m_ℓ
 __constant__ unsigned long long c_W[kNumMod][2];   // M/m_ℓ as (lo, hi)
 
@@ -115,49 +115,75 @@ __global__ void col_exp_kernel(const double* __restrict__ p, long long rows, int
 }
 
 // ---- residues of a row-scaled matrix: R[ℓ][i][k] (int8), ld ldr bytes ---------------
-__global__ void residues_rows_kernel(const double* __restrict__ x, long long rows, long long cols,
-                                     long long ldx, const int* __restrict__ e, int8_t* __restrict__ r,
-                                     long long ldr, long long plane) {
-  // 4 consecutive k per thread: one 32-bit store per modulus (cols % 4 == 0 path).
-  // a (signed, |a| < 2^53) = d0 + d1·2^14 + d2·2^28 + d3·2^42 with 14-bit limbs d0..d2 ≥ 0 and
-  // signed d3; a ≡ s = Σ d_t·(2^(14t) mod m)  (|s| < 2^23.1, exact in fp32), then one
-  // fp32 symmetric reduction.  m = 256 is the low byte of a.
+__global__ void __launch_bounds__(256) residues_rows_kernel(const double* __restrict__ x, long long rows,
+                                                          long long cols, long long ldx, int* __restrict__ e,
+                                                          int8_t* __restrict__ r, long long ldr,
+                                                          long long plane) {
+  // One block per row (grid-stride): pass 1 takes the row's max exponent (the row
+  // then sits in L2 for pass 2), pass 2 writes the 16 residues of 4 consecutive k
+  // per thread, one 32-bit store per modulus (cols % 4 == 0 path).
+  // a (signed, |a| < 2^53) = d0 + d1·2^13 + d2·2^26 + d3·2^39 with 13-bit limbs d0..d2 ≥ 0 and
+  // signed d3 (|d3| ≤ 2^14); a ≡ s = Σ d_t·p_t, p_t = 2^(13t) mod m taken in (−m/2, m/2], so
+  // |s| < 2^22 and s, s + kMagic are exact in fp32.  With q = rint(s/m) from one fma, the
+  // residue byte is (bits(s + kMagic) − m·bits(q + kMagic)) mod 256 — one IMAD (the kMagic
+  // bit patterns cancel in the low byte).  m = 256 is the low byte of a.
+  __shared__ double red[8];
   const long long c4 = cols / 4;
-  const long long total = rows * c4;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long i = t / c4, k = (t % c4) * 4;
-    const int sh = 53 - e[i];
-    const double s1 = ldexp(1.0, sh / 2), s2 = ldexp(1.0, sh - sh / 2);
-    const double2 v01 = __ldcs(reinterpret_cast<const double2*>(x + i * ldx + k));
-    const double2 v23 = __ldcs(reinterpret_cast<const double2*>(x + i * ldx + k + 2));
-    const double xv[4] = {v01.x, v01.y, v23.x, v23.y};
-    float f[4][4];
-    uint32_t lowb[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const long long a = __double2ll_rn(xv[q] * s1 * s2);
-      lowb[q] = (uint32_t)a;
-      f[q][0] = u2f_small((uint32_t)a & 16383u);
-      f[q][1] = u2f_small((uint32_t)(a >> 14) & 16383u);
-      f[q][2] = u2f_small((uint32_t)(a >> 28) & 16383u);
-      f[q][3] = u2f_small((uint32_t)((a >> 42) + 2048)) - 2048.0f;
+  for (long long i = blockIdx.x; i < rows; i += gridDim.x) {
+    const double* row = x + i * ldx;
+    double mx = 0.0;
+    for (long long k4 = threadIdx.x; k4 < c4; k4 += blockDim.x) {
+      const double2 v01 = reinterpret_cast<const double2*>(row)[2 * k4];
+      const double2 v23 = reinterpret_cast<const double2*>(row)[2 * k4 + 1];
+      mx = fmax(mx, fmax(fmax(fabs(v01.x), fabs(v01.y)), fmax(fabs(v23.x), fabs(v23.y))));
     }
-    int8_t* out = r + i * ldr + k;
-    *reinterpret_cast<uint32_t*>(out) = pack4(lowb[0], lowb[1], lowb[2], lowb[3]);
-#pragma unroll
-    for (int l = 1; l < kNumMod; ++l) {
-      const float m = c_modf[l], rm = c_rmodf[l];
-      const float p1 = c_pow14f[1][l], p2 = c_pow14f[2][l], p3 = c_pow14f[3][l];
-      uint32_t b[4];
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    double t = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+    __syncthreads();
+    const int ei = t > 0.0 ? ilogb(t) + 1 : 0;
+    if (threadIdx.x == 0) e[i] = ei;
+    const int sh = 53 - ei;
+    const double s1 = ldexp(1.0, sh / 2), s2 = ldexp(1.0, sh - sh / 2);
+    int8_t* orow = r + i * ldr;
+    for (long long k4 = threadIdx.x; k4 < c4; k4 += blockDim.x) {
+      const double2 v01 = __ldcs(reinterpret_cast<const double2*>(row) + 2 * k4);
+      const double2 v23 = __ldcs(reinterpret_cast<const double2*>(row) + 2 * k4 + 1);
+      const double xv[4] = {v01.x, v01.y, v23.x, v23.y};
+      float f[4][4];
+      uint32_t lowb[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const float sacc = fmaf(f[q][3], p3, fmaf(f[q][2], p2, fmaf(f[q][1], p1, f[q][0])));
-        float rr = sym_mod_f(sacc, m, rm);     // |rr| ≤ 0.503·m
-        if (l == 1) rr = rr > 127.5f ? rr - m : rr;   // m = 255 can land on +128
-        b[q] = low_bits(rr);
+        const long long a = __double2ll_rn(xv[q] * s1 * s2);
+        lowb[q] = (uint32_t)a;
+        f[q][0] = u2f_small((uint32_t)a & 8191u);
+        f[q][1] = u2f_small((uint32_t)(a >> 13) & 8191u);
+        f[q][2] = u2f_small((uint32_t)(a >> 26) & 8191u);
+        f[q][3] = u2f_small((uint32_t)((a >> 39) + 16384)) - 16384.0f;
       }
-      *reinterpret_cast<uint32_t*>(out + l * plane) = pack4(b[0], b[1], b[2], b[3]);
+      int8_t* out = orow + 4 * k4;
+      *reinterpret_cast<uint32_t*>(out) = pack4(lowb[0], lowb[1], lowb[2], lowb[3]);
+#pragma unroll
+      for (int l = 1; l < kNumMod; ++l) {
+        const float m = c_modf[l], rm = c_rmodf[l];
+        const float p1 = c_pow13f[1][l], p2 = c_pow13f[2][l], p3 = c_pow13f[3][l];
+        const uint32_t mi = (uint32_t)c_mod[l];
+        uint32_t b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float sacc = fmaf(f[q][3], p3, fmaf(f[q][2], p2, fmaf(f[q][1], p1, f[q][0])));
+          if (l == 1) {   // m = 255: |r| can reach 128 — fold into int8 range
+            float rr = sym_mod_f(sacc, m, rm);
+            rr = rr > 127.5f ? rr - m : rr;
+            b[q] = low_bits(rr);
+          } else {        // |r| ≤ 0.503·m ≤ 127
+            b[q] = __float_as_uint(sacc + kMagic) - mi * __float_as_uint(fmaf(sacc, rm, kMagic));
+          }
+        }
+        *reinterpret_cast<uint32_t*>(out + l * plane) = pack4(b[0], b[1], b[2], b[3]);
+      }
     }
   }
 }
@@ -466,8 +492,9 @@ void ensure_oz_constants() {
     modf[l] = (float)m;
     long long v = 1;
     for (int t = 0; t < 4; ++t) {
-      pw[t][l] = (float)(v % m);
-      v = (v * 16384) % m;
+      const long long r = v % m;
+      pw[t][l] = (float)(r > m / 2 ? r - m : r);
+      v = (v * 8192) % m;
     }
     const unsigned __int128 w = M / (unsigned)m;
     W[l][0] = (unsigned long long)w;
@@ -478,7 +505,7 @@ void ensure_oz_constants() {
     winv[l] = (float)x;
   }
   cudaMemcpyToSymbol(oz::c_modf, modf, sizeof(modf));
-  cudaMemcpyToSymbol(oz::c_pow14f, pw, sizeof(pw));
+  cudaMemcpyToSymbol(oz::c_pow13f, pw, sizeof(pw));
   cudaMemcpyToSymbol(oz::c_wInvf, winv, sizeof(winv));
   cudaMemcpyToSymbol(oz::c_W, W, sizeof(W));
   done[dev] = true;
@@ -523,15 +550,18 @@ int oz_num_moduli() { return oz::kNumMod; }
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
                      long long ldr, cudaStream_t st) {
   ensure_oz_constants();
-  oz::row_exp_kernel<<<(unsigned)rows, 256, 0, st>>>(x, rows, cols, ldx, e);
-  count_launch();
-  if (cols % 4 == 0 && ldx % 2 == 0 && ldr % 4 == 0 && (uintptr_t)x % 16 == 0)
-    oz::residues_rows_kernel<<<grid_oz(rows * cols / 4, 256), 256, 0, st>>>(x, rows, cols, ldx, e, r, ldr,
-                                                                            ldr * rows);
-  else
+  if (cols % 4 == 0 && ldx % 2 == 0 && ldr % 4 == 0 && (uintptr_t)x % 16 == 0) {
+    // row exponents fused: one block per row
+    oz::residues_rows_kernel<<<(unsigned)std::min<long long>(rows, (long long)device_info().sms * 8), 256, 0,
+                               st>>>(x, rows, cols, ldx, e, r, ldr, ldr * rows);
+    count_launch();
+  } else {
+    oz::row_exp_kernel<<<(unsigned)rows, 256, 0, st>>>(x, rows, cols, ldx, e);
+    count_launch();
     oz::residues_rows1_kernel<<<grid_oz(rows * cols, 256), 256, 0, st>>>(x, rows, cols, ldx, e, r, ldr,
                                                                           ldr * rows);
-  count_launch();
+    count_launch();
+  }
 }
 
 int oz_gemm(const OzOp& op, cudaStream_t st) {
