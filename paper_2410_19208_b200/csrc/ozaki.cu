@@ -38,6 +38,7 @@ __constant__ float c_rmodf[kNumMod];        // 1 / m (fp32) for small non-negati
 __constant__ int c_inv[kNumMod][kNumMod];   // (m_i)^{-1} mod m_j, i < j
 __constant__ unsigned long long c_M[2];     // M = Π m_ℓ as (lo, hi)
 __constant__ float c_modf[kNumMod];         // m_ℓ
+__constant__ uint32_t c_nmod[kNumMod];      // −m_ℓ mod 2^32
 __constant__ float c_pow13f[4][kNumMod];    // 2^(13t) mod m_ℓ in (−m/2, m/2]
 __constant__ float c_wInvf[kNumMod];        // (M/m_ℓ)^{-1} mod m_ℓ
 __constant__ unsigned long long c_W[kNumMod][2];   // M/m_ℓ as (lo, hi)
@@ -120,8 +121,8 @@ __global__ void __launch_bounds__(256) residues_rows_kernel(const double* __rest
                                                           int8_t* __restrict__ r, long long ldr,
                                                           long long plane) {
   // One block per row (grid-stride): pass 1 takes the row's max exponent (the row
-  // then sits in L2 for pass 2), pass 2 writes the 16 residues of 4 consecutive k
-  // per thread, one 32-bit store per modulus (cols % 4 == 0 path).
+  // then sits in L2 for pass 2), pass 2 writes the 16 residues of 8 consecutive k
+  // per thread, one 64-bit store per modulus (cols % 8 == 0 path).
   // a (signed, |a| < 2^53) = d0 + d1·2^13 + d2·2^26 + d3·2^39 with 13-bit limbs d0..d2 ≥ 0 and
   // signed d3 (|d3| ≤ 2^14); a ≡ s = Σ d_t·p_t, p_t = 2^(13t) mod m taken in (−m/2, m/2], so
   // |s| < 2^22 and s, s + kMagic are exact in fp32.  With q = rint(s/m) from one fma, the
@@ -148,41 +149,47 @@ __global__ void __launch_bounds__(256) residues_rows_kernel(const double* __rest
     const int sh = 53 - ei;
     const double s1 = ldexp(1.0, sh / 2), s2 = ldexp(1.0, sh - sh / 2);
     int8_t* orow = r + i * ldr;
-    for (long long k4 = threadIdx.x; k4 < c4; k4 += blockDim.x) {
-      const double2 v01 = __ldcs(reinterpret_cast<const double2*>(row) + 2 * k4);
-      const double2 v23 = __ldcs(reinterpret_cast<const double2*>(row) + 2 * k4 + 1);
-      const double xv[4] = {v01.x, v01.y, v23.x, v23.y};
-      float f[4][4];
-      uint32_t lowb[4];
+    // 8 consecutive k per thread (two 32-bit words per modulus → one 64-bit store)
+    for (long long k8 = threadIdx.x; k8 < c4 / 2; k8 += blockDim.x) {
+      const double2* src = reinterpret_cast<const double2*>(row) + 4 * k8;
+      float f[8][4];
+      uint32_t lowb[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const long long a = __double2ll_rn(xv[q] * s1 * s2);
-        lowb[q] = (uint32_t)a;
-        f[q][0] = u2f_small((uint32_t)a & 8191u);
-        f[q][1] = u2f_small((uint32_t)(a >> 13) & 8191u);
-        f[q][2] = u2f_small((uint32_t)(a >> 26) & 8191u);
-        f[q][3] = u2f_small((uint32_t)((a >> 39) + 16384)) - 16384.0f;
+      for (int h = 0; h < 4; ++h) {
+        const double2 v = __ldcs(src + h);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int q = 2 * h + u;
+          const long long a = __double2ll_rn((u ? v.y : v.x) * s1 * s2);
+          lowb[q] = (uint32_t)a;
+          f[q][0] = u2f_small((uint32_t)a & 8191u);
+          f[q][1] = u2f_small((uint32_t)(a >> 13) & 8191u);
+          f[q][2] = u2f_small((uint32_t)(a >> 26) & 8191u);
+          f[q][3] = u2f_small((uint32_t)((a >> 39) + 16384)) - 16384.0f;
+        }
       }
-      int8_t* out = orow + 4 * k4;
-      *reinterpret_cast<uint32_t*>(out) = pack4(lowb[0], lowb[1], lowb[2], lowb[3]);
+      int8_t* out = orow + 8 * k8;
+      *reinterpret_cast<uint2*>(out) =
+          make_uint2(pack4(lowb[0], lowb[1], lowb[2], lowb[3]), pack4(lowb[4], lowb[5], lowb[6], lowb[7]));
 #pragma unroll
       for (int l = 1; l < kNumMod; ++l) {
+        out += plane;
         const float m = c_modf[l], rm = c_rmodf[l];
         const float p1 = c_pow13f[1][l], p2 = c_pow13f[2][l], p3 = c_pow13f[3][l];
-        const uint32_t mi = (uint32_t)c_mod[l];
-        uint32_t b[4];
+        const uint32_t nmi = c_nmod[l];   // −m (mod 2^32)
+        uint32_t b[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 8; ++q) {
           const float sacc = fmaf(f[q][3], p3, fmaf(f[q][2], p2, fmaf(f[q][1], p1, f[q][0])));
           if (l == 1) {   // m = 255: |r| can reach 128 — fold into int8 range
             float rr = sym_mod_f(sacc, m, rm);
             rr = rr > 127.5f ? rr - m : rr;
             b[q] = low_bits(rr);
           } else {        // |r| ≤ 0.503·m ≤ 127
-            b[q] = __float_as_uint(sacc + kMagic) - mi * __float_as_uint(fmaf(sacc, rm, kMagic));
+            b[q] = __float_as_uint(fmaf(sacc, rm, kMagic)) * nmi + __float_as_uint(sacc + kMagic);
           }
         }
-        *reinterpret_cast<uint32_t*>(out + l * plane) = pack4(b[0], b[1], b[2], b[3]);
+        *reinterpret_cast<uint2*>(out) = make_uint2(pack4(b[0], b[1], b[2], b[3]), pack4(b[4], b[5], b[6], b[7]));
       }
     }
   }
@@ -505,6 +512,9 @@ void ensure_oz_constants() {
     winv[l] = (float)x;
   }
   cudaMemcpyToSymbol(oz::c_modf, modf, sizeof(modf));
+  uint32_t nmod[oz::kNumMod];
+  for (int l = 0; l < oz::kNumMod; ++l) nmod[l] = 0u - (uint32_t)oz::kMods[l];
+  cudaMemcpyToSymbol(oz::c_nmod, nmod, sizeof(nmod));
   cudaMemcpyToSymbol(oz::c_pow13f, pw, sizeof(pw));
   cudaMemcpyToSymbol(oz::c_wInvf, winv, sizeof(winv));
   cudaMemcpyToSymbol(oz::c_W, W, sizeof(W));
@@ -550,7 +560,7 @@ int oz_num_moduli() { return oz::kNumMod; }
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
                      long long ldr, cudaStream_t st) {
   ensure_oz_constants();
-  if (cols % 4 == 0 && ldx % 2 == 0 && ldr % 4 == 0 && (uintptr_t)x % 16 == 0) {
+  if (cols % 8 == 0 && ldx % 2 == 0 && ldr % 8 == 0 && (uintptr_t)x % 16 == 0) {
     // row exponents fused: one block per row
     oz::residues_rows_kernel<<<(unsigned)std::min<long long>(rows, (long long)device_info().sms * 8), 256, 0,
                                st>>>(x, rows, cols, ldx, e, r, ldr, ldr * rows);
