@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--p", type=int, default=None)
     ap.add_argument("--q", type=int, default=None)
     ap.add_argument("--pool", type=int, default=4, help="distinct X matrices cycled per rank")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the config-3 FP32 (3xTF32) leg")
@@ -149,18 +149,57 @@ def run_reference(a):
 # ------------------------------------------------------------------ clocks ---
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks, power and clock-event (throttle) reasons sampled during the
+    timed region — in-process NVML polling every 20 ms (no child process: forking
+    a process that maps tens of GB of pinned memory stalls the timed steps);
+    nvidia-smi only if NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.lines = []
+        self.samples = []
+        self.nvml = None
+        self.stop_flag = threading.Event()
+
+    def _handle(self, nv):
+        count = nv.nvmlDeviceGetCount()
+        if count == 1:
+            return nv.nvmlDeviceGetHandleByIndex(0)
+        try:   # match the CUDA device to its NVML handle by UUID
+            import torch
+            want = str(torch.cuda.get_device_properties(self.index).uuid).lower()
+            for i in range(count):
+                h = nv.nvmlDeviceGetHandleByIndex(i)
+                u = nv.nvmlDeviceGetUUID(h)
+                u = (u.decode() if isinstance(u, bytes) else u).lower()
+                if want in u:
+                    return h
+        except Exception:
+            pass
+        return nv.nvmlDeviceGetHandleByIndex(self.index)
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.h = self._handle(nv)
+            self.nvml = nv
+            self.bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            self.smax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -171,11 +210,33 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop_flag.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                util = nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                self.samples.append((sm, pw, rs, util))
+            except Exception:
+                pass
+            self.stop_flag.wait(0.02)
+
     def _read(self):
         for ln in self.proc.stdout:
             self.lines.append(ln.strip())
 
     def stop(self):
+        if self.nvml is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=5)
+            busy = [s for s in self.samples if s[3] > 0] or self.samples
+            sm = [s[0] for s in busy]
+            reasons = sorted({nm for s in busy for nm, bit in self.bits.items() if s[2] & bit})
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax,
+                    "power_w_max": max(s[1] for s in busy) if busy else None,
+                    "samples": len(sm), "source": "NVML, 20 ms polling", "reasons": reasons}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -184,7 +245,6 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         sm, smax, reasons, power = [], [], set(), []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
@@ -195,13 +255,13 @@ class ClockSampler:
                 power.append(float(parts[2]))
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[4:8]):
+            for nm, val in zip(self.NAMES, parts[4:8]):
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
                 "power_w_max": max(power) if power else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "source": "nvidia-smi -lms 200", "reasons": sorted(reasons)}
 
 
 # ------------------------------------------------------------------- ours ---
@@ -613,39 +673,36 @@ def load_traffic32():
 
 
 def run_e2e(a, torch, psd, x_dev, params, dev):
-    """Same metric through the public API with HOST buffers: pinned X → HBM,
-    projection, result → pinned host, all inside the timed region."""
+    """Same metric through the public API with HOST buffers: every step uploads
+    its X from pinned host memory and downloads its X̂₊ into pinned host memory,
+    all inside the timed region.  ``psd.ran_proj_many`` overlaps the upload of
+    X_{i+1} and the download of X̂₊_{i−1} with the projection of X_i (two copy
+    streams, double-buffered device X / result)."""
     n = a.n
     try:
         hx = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        hr = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        hr = [torch.empty((n, n), dtype=torch.float64, pin_memory=True) for _ in range(2)]
     except Exception as exc:  # pragma: no cover - host RAM
         return {"value": None, "unit": UNIT, "error": f"pinned alloc failed: {exc}"}
     hx.copy_(x_dev.cpu())
-    dx = torch.empty((n, n), dtype=torch.float64, device=dev)
     rng = psd.DeviceRng(seed=777)
     steps = max(1, a.e2e_steps)
-
-    def one():
-        dx.copy_(hx, non_blocking=True)
-        rep = psd.ran_proj(dx, params, rng)
-        hr.copy_(rep.result, non_blocking=True)
-        return rep
-
-    one()
+    psd.ran_proj_many([hx], params, rng, out=[hr[0]])      # warm-up (buffers, plan)
     torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(steps):
-        one()
+    reps = psd.ran_proj_many([hx] * steps, params, rng, out=[hr[i % 2] for i in range(steps)])
     e1.record()
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
-    del dx
+    wall = time.perf_counter() - t0
+    ok = all(r.effective_rank > 0 for r in reps)
     return {"value": steps / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": 8 * n * n,
-            "d2h_bytes_per_step": 8 * n * n, "steps": steps,
-            "path": "pinned host X → cudaMemcpyAsync → paper_2410_19208_b200.ran_proj → pinned host result"}
+            "d2h_bytes_per_step": 8 * n * n, "steps": steps, "wall_s": wall, "results_ok": ok,
+            "path": "pinned host X → paper_2410_19208_b200.ran_proj_many (H2D / projection / D2H "
+                    "overlapped on three streams) → pinned host X̂₊"}
 
 
 def main():

@@ -17,6 +17,7 @@ from .sketch import (RangeParams, min_eig_magnitude, orthonormality_defect, powe
                      range_finder)
 from .symmetric import (EigenDecomposition, eigh, exact_psd_projection, frobenius_norm,
                         gaussian_matrix, require_symmetric, rng_from_seed, symmetrize)
+from .pipeline import ran_proj_many
 from .sdls import SolveReport, SparseSdlsProblem, TrajectoryPoint, solve
 from .install import install, uninstall
 from . import workloads  # noqa: E402  (seeded HBM generators for the BASELINE configs)
@@ -30,7 +31,7 @@ __all__ = [
     "AlphaTooSmall", "AsymmetricMatrixError", "ConvergenceFailure", "DeviceError",
     "DimensionMismatch", "InvalidParams", "NonSquareError", "PsdconeError", "RankDeficientSample",
     "DeviceRng", "METHODS", "ProjectionReport", "ProjectorConfig", "flops", "project", "ran_proj",
-    "ran_proj_scal", "set_fp64_engine", "RangeParams", "min_eig_magnitude", "orthonormality_defect",
+    "ran_proj_scal", "ran_proj_many", "set_fp64_engine", "RangeParams", "min_eig_magnitude", "orthonormality_defect",
     "power_iteration", "range_finder", "EigenDecomposition", "eigh", "exact_psd_projection",
     "frobenius_norm", "gaussian_matrix", "require_symmetric", "rng_from_seed", "symmetrize",
     "install", "uninstall", "solve", "SparseSdlsProblem", "SolveReport", "TrajectoryPoint",

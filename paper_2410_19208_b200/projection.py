@@ -108,13 +108,23 @@ def _stats_for(op, assume_symmetric):
     return check_symmetric_device(op)
 
 
-def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, method, t0):
+def _result_buffer(out, n, op):
+    """``out=`` of ran_proj / ran_proj_scal: a contiguous n×n CUDA tensor of X's dtype."""
+    if out is None:
+        return torch.empty((n, n), dtype=op.t.dtype, device=op.device)
+    if (not isinstance(out, torch.Tensor) or not out.is_cuda or out.device != op.device
+            or out.dtype != op.t.dtype or tuple(out.shape) != (n, n) or not out.is_contiguous()):
+        raise errors.error("InvalidParams", f"out must be a contiguous {n}x{n} {op.t.dtype} tensor on {op.device}")
+    return out
+
+
+def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, method, t0, out=None):
     width = params.width
     lib = _native.load_library()
     plan = _native.get_plan(n, width, op.device)
     dev = op.device
     f32 = op.t.dtype == torch.float32
-    result = torch.empty((n, n), dtype=op.t.dtype, device=dev)
+    result = _result_buffer(out, n, op)
     fw = torch.empty((n, width), dtype=torch.float64, device=dev) if return_factors else None
     fd = torch.empty(width, dtype=torch.float64, device=dev) if return_factors else None
     if f32:
@@ -154,26 +164,28 @@ def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, m
     )
 
 
-def _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, stats, t0):
+def _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, stats, t0, out=None):
     n = require_square(op)
     width = params.width
     if width > n:                                               # sketch.py:67-69
         raise errors.error("InvalidParams", f"k+l = {width} exceeds min(m, n) = {n}")
     om = as_device(omega, op.device).t if omega is not None else draw_gaussian(rng, (n, width), op.device)
-    return _run(op, n, params, om, 0.0, stats, collect_diagnostics, return_factors, "randomized", t0)
+    return _run(op, n, params, om, 0.0, stats, collect_diagnostics, return_factors, "randomized", t0,
+                out)
 
 
 def ran_proj(x, params, rng, collect_diagnostics=False, return_factors=False, *, omega=None,
-             assume_symmetric=False, dtype=None):
+             assume_symmetric=False, dtype=None, out=None):
     """projection.py:92-119 (Alg. 2): X̂₊ = Q U D₊ Uᵀ Qᵀ."""
     t0 = time.perf_counter()
     op = _operand(x, dtype)
     require_square(op)
     stats = _stats_for(op, assume_symmetric)                   # projection.py:100
-    return _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, stats, t0)
+    return _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, stats, t0, out)
 
 
-def _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factors, omega, stats, t0):
+def _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factors, omega, stats, t0,
+                      out=None):
     n = require_square(op)
     if op.t.dtype != torch.float32:  # FP32: alpha_tol is tested inside psd_ran_proj_f32
         if stats is None:  # assume_symmetric: still need max|x| for alpha_tol (one HBM pass)
@@ -189,18 +201,18 @@ def _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factor
         raise errors.error("InvalidParams", f"k+l = {width} exceeds min(m, n) = {n}")
     om = as_device(omega, op.device).t if omega is not None else draw_gaussian(rng, (n, width), op.device)
     return _run(op, n, params, om, float(alpha), stats, collect_diagnostics, return_factors,
-                "scaled_randomized", t0)
+                "scaled_randomized", t0, out)
 
 
 def ran_proj_scal(x, params, alpha, rng, collect_diagnostics=False, return_factors=False, *,
-                  omega=None, assume_symmetric=False, dtype=None):
+                  omega=None, assume_symmetric=False, dtype=None, out=None):
     """projection.py:122-159 (Alg. 3) through B = (X + αI)/α (fused in the GEMM epilogues)."""
     t0 = time.perf_counter()
     op = _operand(x, dtype)
     require_square(op)
     stats = _stats_for(op, assume_symmetric)
     return _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factors, omega,
-                             stats, t0)
+                             stats, t0, out)
 
 
 def _exact_report(op, method, t0):
