@@ -276,11 +276,21 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
           if (tid < kJS) ia[tid] = sub_index(nblk, r, pair, tid);
           __syncthreads();
           const long long tw1 = clock64();
-          for (int e = tid; e < kJS * kJS; e += kJT) {
-            const int i = e / kJS, j = e % kJS;
-            const int gi = ia[i], gj = ia[j];
-            S0[i * kJLd + j] = (gi < m && gj < m) ? __ldcg(cur + (long long)gi * ldc + gj) : 0.0;
-            V0[i * kJLd + j] = (i == j) ? 1.0 : 0.0;
+          {
+            // all loads of this thread in flight at once (register staging)
+            constexpr int NS = kJS * kJS / kJT;
+            double vs[NS];
+#pragma unroll
+            for (int u = 0; u < NS; ++u) {
+              const int e = tid + u * kJT, gi = ia[e / kJS], gj = ia[e % kJS];
+              vs[u] = (gi < m && gj < m) ? __ldcg(cur + (long long)gi * ldc + gj) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < NS; ++u) {
+              const int e = tid + u * kJT, i = e / kJS, j = e % kJS;
+              S0[i * kJLd + j] = vs[u];
+              V0[i * kJLd + j] = (i == j) ? 1.0 : 0.0;
+            }
           }
           __syncthreads();
           const long long tw2 = clock64();
@@ -351,19 +361,35 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
           double c[2][2];
           if (pa == pb) {
             const double* Sp = Sslot + (size_t)pa * kJS * kJS;
-            for (int e = tid; e < kJS * kJS; e += kJT) {
-              const int gi = ia[e / kJS], gj = ib[e % kJS];
-              if (gi < m && gj < m) nxt[(long long)gi * ldn + gj] = __ldcg(Sp + e);
+            constexpr int NS = kJS * kJS / kJT;
+            double vs[NS];
+#pragma unroll
+            for (int u = 0; u < NS; ++u) vs[u] = __ldcg(Sp + tid + u * kJT);
+#pragma unroll
+            for (int u = 0; u < NS; ++u) {
+              const int e = tid + u * kJT, gi = ia[e / kJS], gj = ib[e % kJS];
+              if (gi < m && gj < m) nxt[(long long)gi * ldn + gj] = vs[u];
             }
           } else {
             const double* Ja = Jslot + (size_t)pa * kJS * kJS;
             const double* Jb = Jslot + (size_t)pb * kJS * kJS;
-            for (int e = tid; e < kJS * kJS; e += kJT) {
-              const int i = e / kJS, j = e % kJS;
-              const int gi = ia[i], gj = ib[j];
-              S0[i * kJLd + j] = (gi < m && gj < m) ? __ldcg(cur + (long long)gi * ldc + gj) : 0.0;
-              V0[i * kJLd + j] = __ldcg(Ja + e);
-              X[i * kJLd + j] = __ldcg(Jb + e);
+            {
+              constexpr int NS = kJS * kJS / kJT;
+              double vs[NS], va[NS], vb[NS];
+#pragma unroll
+              for (int u = 0; u < NS; ++u) {
+                const int e = tid + u * kJT, gi = ia[e / kJS], gj = ib[e % kJS];
+                vs[u] = (gi < m && gj < m) ? __ldcg(cur + (long long)gi * ldc + gj) : 0.0;
+                va[u] = __ldcg(Ja + e);
+                vb[u] = __ldcg(Jb + e);
+              }
+#pragma unroll
+              for (int u = 0; u < NS; ++u) {
+                const int e = tid + u * kJT, i = e / kJS, j = e % kJS;
+                S0[i * kJLd + j] = vs[u];
+                V0[i * kJLd + j] = va[u];
+                X[i * kJLd + j] = vb[u];
+              }
             }
             __syncthreads();
             mm32_dmma(V0, true, S0, c);  // J_aᵀ T
@@ -413,15 +439,31 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
           }
           __syncthreads();
           const double* Jb = Jslot + (size_t)pb * kJS * kJS;
-          for (int e = tid; e < kJS * kJS; e += kJT) X[(e / kJS) * kJLd + e % kJS] = __ldcg(Jb + e);
+          constexpr int NS = kJS * kJS / kJT;
+          {
+            double vb[NS];
+#pragma unroll
+            for (int u = 0; u < NS; ++u) vb[u] = __ldcg(Jb + tid + u * kJT);
+#pragma unroll
+            for (int u = 0; u < NS; ++u) {
+              const int e = tid + u * kJT;
+              X[(e / kJS) * kJLd + e % kJS] = vb[u];
+            }
+          }
           for (int h = 0; h < 2; ++h) {
             const int r0 = vc * 2 * kJS + h * kJS;
             if (r0 >= m) break;
             double c[2][2];
-            for (int e = tid; e < kJS * kJS; e += kJT) {
-              const int i = e / kJS, j = e % kJS;
-              const int gr = r0 + i, gj = ib[j];
-              S0[i * kJLd + j] = (gr < m && gj < m) ? __ldcg(A.v + (long long)gr * A.ldv + gj) : 0.0;
+            double vs[NS];
+#pragma unroll
+            for (int u = 0; u < NS; ++u) {
+              const int e = tid + u * kJT, gr = r0 + e / kJS, gj = ib[e % kJS];
+              vs[u] = (gr < m && gj < m) ? __ldcg(A.v + (long long)gr * A.ldv + gj) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < NS; ++u) {
+              const int e = tid + u * kJT;
+              S0[(e / kJS) * kJLd + e % kJS] = vs[u];
             }
             __syncthreads();
             mm32_dmma(S0, false, X, c);
