@@ -22,12 +22,14 @@ from .sdls import SolveReport, SparseSdlsProblem, TrajectoryPoint, solve
 from .install import install, uninstall
 from . import workloads  # noqa: E402  (seeded HBM generators for the BASELINE configs)
 from . import experiments  # noqa: E402  (Monte-Carlo projection-error harness, §8 f3)
+from . import matrix_io  # noqa: E402  (Matrix Market / JSON problem files, §8 f4)
+from .matrix_io import read_matrix_market, write_matrix_market  # noqa: E402
 from .experiments import projection_error_sweep  # noqa: E402
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "experiments", "projection_error_sweep",
+    "experiments", "projection_error_sweep", "matrix_io", "read_matrix_market", "write_matrix_market",
     "AlphaTooSmall", "AsymmetricMatrixError", "ConvergenceFailure", "DeviceError",
     "DimensionMismatch", "InvalidParams", "NonSquareError", "PsdconeError", "RankDeficientSample",
     "DeviceRng", "METHODS", "ProjectionReport", "ProjectorConfig", "flops", "project", "ran_proj",
