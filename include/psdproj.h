@@ -150,6 +150,17 @@ int psd_ran_proj_f32(psd_plan* plan, const float* x, int64_t n, int64_t ldx, con
 int psd_gemm_f64_ozaki(const double* a, int64_t lda, const double* p, int64_t ldp, int64_t m,
                        int64_t n, int64_t k, double* c, int64_t ldc, void* stream);
 
+/* The same emulated FP64 GEMM for a general A streamed in row chunks, with a
+ * caller-owned device workspace (replaces the DGEMM of sketch.py:75/:82 and
+ * projection.py:104 for a row block X_g of a sharded X):
+ * C = A·P, or C = (A·P + alpha·S)/alpha when alpha > 0 (B = (X+αI)/α with S the
+ * rows of P matching the rows of A).  chunk_rows <= 0 picks 8192.
+ * psd_gemm_f64_int8_ws_bytes reports the workspace size for (m, n, k, chunk_rows). */
+int psd_gemm_f64_int8_ws_bytes(int64_t m, int64_t n, int64_t k, int64_t chunk_rows, int64_t* bytes);
+int psd_gemm_f64_int8(const double* a, int64_t lda, const double* p, int64_t ldp, int64_t m, int64_t n,
+                      int64_t k, double* c, int64_t ldc, double alpha, const double* s, int64_t lds,
+                      void* ws, int64_t ws_bytes, int64_t chunk_rows, void* stream);
+
 /* The 3xTF32 tcgen05 GEMM itself (test entry; allocates its own scratch):
  * mode 0: C (fp64, m x n) = A · B^T; mode 1: mirrored fp32 C (m == n) from
  * the lower tiles of A · B^T; mode 2: as mode 0 with `a` given transposed

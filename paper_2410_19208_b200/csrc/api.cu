@@ -1043,52 +1043,42 @@ int psd_gemm_f64_ozaki(const double* a, int64_t lda, const double* pp, int64_t l
   if (!a || !pp || !c) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
   if (m < 1 || nn < 1 || nn > 512 || kk < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad ozaki GEMM shape");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int L = psd::oz_num_moduli();
-  const ll ldk = (kk + 127) / 128 * 128;
-  const ll wpad = (nn + 15) / 16 * 16;
-  int8_t *ar = nullptr, *br = nullptr;
-  int *e = nullptr, *f = nullptr;
-  uint8_t* res = nullptr;
-  const size_t res_elems = (size_t)L * std::max<ll>(8, (kk + 32767) / 32768 + 1) * m * (wpad + 16);
-  bool ok = cudaMalloc(&ar, (size_t)L * m * ldk) == cudaSuccess &&
-            cudaMalloc(&br, (size_t)L * wpad * ldk) == cudaSuccess &&
-            cudaMalloc(&e, (size_t)m * sizeof(int)) == cudaSuccess &&
-            cudaMalloc(&f, (size_t)nn * sizeof(int)) == cudaSuccess &&
-            cudaMalloc(&res, res_elems) == cudaSuccess;
-  int status = PSD_OK;
-  if (!ok) {
-    status = fail(PSD_ERR_NO_MEMORY, "ozaki scratch allocation failed");
-  } else {
-    cudaMemsetAsync(ar, 0, (size_t)L * m * ldk, st);
-    cudaMemsetAsync(br, 0, (size_t)L * wpad * ldk, st);
-    psd::oz_prepare_rows(a, m, kk, lda, e, ar, ldk, st);
-    psd::OzOp op;
-    op.ar = ar;
-    op.ldar = ldk;
-    op.e = e;
-    op.P = pp;
-    op.ldp = ldp;
-    op.M = (int)m;
-    op.N = (int)nn;
-    op.K = (int)kk;
-    op.br = br;
-    op.ldbr = ldk;
-    op.f = f;
-    op.res = res;
-    op.res_elems = res_elems;
-    op.C = c;
-    op.ldc = ldc;
-    const int r = psd::oz_gemm(op, st);
-    if (r < 0) status = fail(PSD_ERR_INVALID_PARAMS, "ozaki GEMM rejected its operands (%d)", r);
-    if (status == PSD_OK) status = sync(st, "ozaki gemm");
+  const long long chunk = m;   // whole A at once (test entry)
+  const size_t bytes = psd::oz_stream_ws_bytes(m, nn, kk, chunk);
+  void* ws = nullptr;
+  if (cudaMalloc(&ws, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PSD_ERR_NO_MEMORY, "ozaki scratch allocation failed");
   }
+  int status = PSD_OK;
+  const int r = psd::oz_gemm_stream(a, lda, pp, ldp, m, (int)nn, kk, c, ldc, 0.0, nullptr, 0, ws, bytes,
+                                    chunk, st);
+  if (r < 0) status = fail(PSD_ERR_INVALID_PARAMS, "ozaki GEMM rejected its operands (%d)", r);
+  if (status == PSD_OK) status = sync(st, "ozaki gemm");
   cudaStreamSynchronize(st);
-  cudaFree(ar);
-  cudaFree(br);
-  cudaFree(e);
-  cudaFree(f);
-  cudaFree(res);
+  cudaFree(ws);
   return status;
+}
+
+int psd_gemm_f64_int8_ws_bytes(int64_t m, int64_t n, int64_t k, int64_t chunk_rows, int64_t* bytes) {
+  if (!bytes) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  if (m < 1 || n < 1 || n > 512 || k < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad INT8-emulated GEMM shape");
+  *bytes = (int64_t)psd::oz_stream_ws_bytes(m, n, k, chunk_rows > 0 ? chunk_rows : 8192);
+  return PSD_OK;
+}
+
+int psd_gemm_f64_int8(const double* a, int64_t lda, const double* pp, int64_t ldp, int64_t m, int64_t nn,
+                      int64_t kk, double* c, int64_t ldc, double alpha, const double* s, int64_t lds,
+                      void* ws, int64_t ws_bytes, int64_t chunk_rows, void* stream) {
+  if (!a || !pp || !c || !ws) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  if (m < 1 || nn < 1 || nn > 512 || kk < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad INT8-emulated GEMM shape");
+  if (alpha > 0.0 && !s) return fail(PSD_ERR_INVALID_PARAMS, "alpha > 0 needs the shift source");
+  if (lda < kk || ldp < nn || ldc < nn) return fail(PSD_ERR_INVALID_PARAMS, "leading dimension too small");
+  const int r = psd::oz_gemm_stream(a, lda, pp, ldp, m, (int)nn, kk, c, ldc, alpha, s, lds, ws, (size_t)ws_bytes,
+                                    chunk_rows > 0 ? chunk_rows : 8192, static_cast<cudaStream_t>(stream));
+  if (r == -3) return fail(PSD_ERR_INVALID_PARAMS, "workspace too small (see psd_gemm_f64_int8_ws_bytes)");
+  if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "INT8-emulated GEMM rejected its operands (%d)", r);
+  return PSD_OK;
 }
 
 int psd_gemm_tf32x3(int32_t mode, const float* a, int64_t lda, const float* b, int64_t ldb,

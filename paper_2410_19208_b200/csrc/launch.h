@@ -93,6 +93,12 @@ int oz_num_moduli();
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
                      long long ldr, cudaStream_t st);
 int oz_gemm(const OzOp& op, cudaStream_t st);
+int oz_prepare_panel(const OzOp& op, cudaStream_t st);
+int oz_gemm_prepared(const OzOp& op, cudaStream_t st);
+size_t oz_stream_ws_bytes(long long m, long long n, long long k, long long chunk);
+int oz_gemm_stream(const double* a, long long lda, const double* P, long long ldp, long long m, int n,
+                   long long k, double* c, long long ldc, double alpha, const double* S, long long lds,
+                   void* ws, size_t ws_bytes, long long chunk, cudaStream_t st);
 // Returns the K-split count used (≥ 1) or < 0 on error (−2 alignment, −3 workspace).
 int gemm_tf32x3(const Tc32Op& op, cudaStream_t st);
 long long tc32_ws_elems(long long M, int N, int max_splits);

@@ -237,7 +237,7 @@ __global__ void residues_panel_t_kernel(const double* __restrict__ p, long long 
 // ---- INT8 CTA-pair GEMM: residue products mod m_ℓ -------------------------------------
 struct I8Params {
   int M, N, K;
-  int bn, n_mma;            // N per MMA (multiple of 16), MMAs per K step (≤ 2)
+  int bn, bn2;              // N of the first MMA (≤ 256) and of the second (0: none); multiples of 16
   int kblocks, kb_per_split, m_pairs, splits;
   int stages;
   uint8_t* out;             // out[((ℓ·splits + split)·M + i)·ldo + col] = (Σ) mod m_ℓ
@@ -268,13 +268,13 @@ PSD_DEVINL uint64_t desc_sw128(uint32_t saddr) {
 
 __global__ void __launch_bounds__(kThreads, 1)
     i8_gemm2_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
-                    const I8Params p) {
+                    const __grid_constant__ CUtensorMap mB2, const I8Params p) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], acc_bar;
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc32::cluster_rank();
-  const int bn_tot = p.bn * p.n_mma;
+  const int bn_tot = p.bn + p.bn2;   // = w rounded to 16: no padded MMA columns
   const int hb = p.bn / 2;
   // modulus slowest: the concurrently running CTAs share one B residue plane (L2-resident)
   int u = blockIdx.x >> 1;
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nkb = min(p.kblocks, kb0 + p.kb_per_split) - kb0;
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t sbase = (sraw + 1023u) & ~1023u;
-  const uint32_t a_bytes = BM * BKB, b_bytes = (uint32_t)p.n_mma * hb * BKB;
+  const uint32_t a_bytes = BM * BKB, b_bytes = (uint32_t)(bn_tot / 2) * BKB;
   const uint32_t st_bytes = a_bytes + b_bytes;
   const uint32_t tcols = bn_tot <= 256 ? 256 : 512;
 
@@ -324,8 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sB = sA + a_bytes;
         const int kc = (kb0 + i) * BKB;
         tma_load_3d_pair(sA, &mA, kc, m0, l, fb);
-        for (int h = 0; h < p.n_mma; ++h)
-          tma_load_3d_pair(sB + (uint32_t)h * hb * BKB, &mB, kc, h * p.bn + (int)rank * hb, l, fb);
+        tma_load_3d_pair(sB, &mB, kc, (int)rank * hb, l, fb);
+        if (p.bn2) tma_load_3d_pair(sB + (uint32_t)hb * BKB, &mB2, kc, p.bn + (int)rank * (p.bn2 / 2), l, fb);
       }
       __syncwarp();
     }
@@ -335,8 +335,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.bn >> 3) << 17) |
                              ((uint32_t)(2 * BM >> 4) << 24);
       const uint64_t da = desc_sw128(sbase), db = desc_sw128(sbase + a_bytes);
+      const uint32_t idesc2 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.bn2 >> 3) << 17) |
+                              ((uint32_t)(2 * BM >> 4) << 24);
       const uint32_t b_half = (uint32_t)(hb * BKB) >> 4;
-      const bool two = p.n_mma > 1;
+      const bool two = p.bn2 > 0;
       for (int i = 0; i < nkb; ++i) {
         const int s = i % p.stages;
         const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t a = da + so + kk * 2, b = db + so + kk * 2;
             const uint32_t acc0 = (i | kk) != 0;
             mma_i8_pair(tmem, a, b, idesc, acc0);
-            if (two) mma_i8_pair(tmem + (uint32_t)p.bn, a, b + b_half, idesc, acc0);
+            if (two) mma_i8_pair(tmem + (uint32_t)p.bn, a, b + b_half, idesc2, acc0);
           }
           tc32::mma_commit_pair(smem_u32(&empty_bar[s]));
           if (i == nkb - 1) tc32::mma_commit_pair(smem_u32(&acc_bar));
@@ -574,13 +576,13 @@ void oz_prepare_rows(const double* x, long long rows, long long cols, long long 
   }
 }
 
-int oz_gemm(const OzOp& op, cudaStream_t st) {
+// B = the panel P (K×N): column exponents and transposed residues into op.f / op.br.
+int oz_prepare_panel(const OzOp& op, cudaStream_t st) {
   using namespace oz;
   ensure_oz_constants();
-  if (op.M < 1 || op.N < 1 || op.K < 1) return 0;
+  if (op.N < 1 || op.K < 1) return 0;
   const int w_pad = (op.N + 15) / 16 * 16;
-  if (w_pad > 512 || op.ldbr < op.K || op.ldbr % 16 || op.ldar % 16) return -2;
-  // B = the panel: column exponents and transposed residues
+  if (w_pad > 512 || op.ldbr < op.K || op.ldbr % 16) return -2;
   cudaMemsetAsync(op.f, 0x80, (size_t)op.N * sizeof(int), st);   // very negative → atomicMax
   {
     dim3 grid((unsigned)std::min<long long>((op.K + 7) / 8, 256), (unsigned)((op.N + 31) / 32));
@@ -593,13 +595,28 @@ int oz_gemm(const OzOp& op, cudaStream_t st) {
                                                           op.ldbr * w_pad, w_pad);
     count_launch();
   }
+  return 0;
+}
+
+// The 16 residue GEMMs + CRT for prepared A (op.ar / op.e) and B (op.br / op.f).
+int oz_gemm_prepared(const OzOp& op, cudaStream_t st) {
+  using namespace oz;
+  ensure_oz_constants();
+  if (op.M < 1 || op.N < 1 || op.K < 1) return 0;
+  const int w_pad = (op.N + 15) / 16 * 16;
+  if (w_pad > 512 || op.ldbr < op.K || op.ldbr % 16 || op.ldar % 16) return -2;
   I8Params p{};
   p.M = op.M;
   p.N = op.N;
   p.K = op.K;
-  p.n_mma = w_pad > 256 ? 2 : 1;
-  p.bn = (w_pad / p.n_mma + 15) / 16 * 16;
-  const int bn_tot = p.bn * p.n_mma;
+  // two balanced MMAs when w > 256 (e.g. 272 = 144 + 128): no padded columns, and
+  // a tiny second MMA (256 + 16) measured slower than the pair of ~equal halves
+  static const int nsplit = [] { const char* e = getenv("PSD_OZ_NSPLIT"); return e ? atoi(e) : 1; }();
+  p.bn = w_pad <= 256 ? w_pad : (w_pad / 2 + 15) / 16 * 16;
+  p.bn2 = w_pad - p.bn;
+  if (w_pad > 256 && nsplit == 0) p.bn2 = p.bn;          // padded equal halves (288 for 272)
+  if (w_pad > 256 && nsplit == 2) { p.bn = 256; p.bn2 = w_pad - 256; }
+  const int bn_tot = p.bn + p.bn2;
   p.kblocks = (op.K + BKB - 1) / BKB;
   p.m_pairs = (op.M + 2 * BM - 1) / (2 * BM);
   const int slots = device_info().sms / 2;
@@ -625,9 +642,10 @@ int oz_gemm(const OzOp& op, cudaStream_t st) {
   const int sb = BM * BKB + bn_tot / 2 * BKB;
   p.stages = std::min(8, ((int)device_info().max_smem - 3072) / sb);
   const size_t smem = (size_t)p.stages * sb + 1024;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mb2;
   if (!map_i8_3d(&ma, op.ar, op.K, op.M, op.ldar, kNumMod, BM) ||
-      !map_i8_3d(&mb, op.br, op.K, w_pad, op.ldbr, kNumMod, p.bn / 2))
+      !map_i8_3d(&mb, op.br, op.K, w_pad, op.ldbr, kNumMod, p.bn / 2) ||
+      !map_i8_3d(&mb2, op.br, op.K, w_pad, op.ldbr, kNumMod, std::max(p.bn2, 16) / 2))
     return -5;
   static size_t attr[16] = {};
   int dev = 0;
@@ -650,7 +668,7 @@ int oz_gemm(const OzOp& op, cudaStream_t st) {
   cfg.attrs = attr2;
   cfg.numAttrs = 1;
   if (op.ev_gemm[0]) cudaEventRecord(op.ev_gemm[0], st);
-  if (cudaLaunchKernelEx(&cfg, i8_gemm2_kernel, ma, mb, p) != cudaSuccess) return -6;
+  if (cudaLaunchKernelEx(&cfg, i8_gemm2_kernel, ma, mb, mb2, p) != cudaSuccess) return -6;
   if (op.ev_gemm[1]) cudaEventRecord(op.ev_gemm[1], st);
   count_launch();
   crt_kernel<<<grid_oz((long long)op.M * ((op.N + 3) / 4), 256), 256, 0, st>>>(op.res, p.splits, op.M, op.N, p.ldo,
@@ -658,6 +676,80 @@ int oz_gemm(const OzOp& op, cudaStream_t st) {
                                                                    op.S, op.lds);
   count_launch();
   return p.splits;
+}
+
+int oz_gemm(const OzOp& op, cudaStream_t st) {
+  const int r = oz_prepare_panel(op, st);
+  if (r < 0) return r;
+  return oz_gemm_prepared(op, st);
+}
+
+// Workspace layout of oz_gemm_stream (bytes, 256-aligned pieces).
+struct OzStreamLayout {
+  long long ldk, wpad, chunk;
+  size_t ar, br, e, f, res, total;
+};
+static OzStreamLayout oz_stream_layout(long long m, long long n, long long k, long long chunk) {
+  OzStreamLayout L{};
+  L.ldk = (k + 127) / 128 * 128;
+  L.wpad = (n + 15) / 16 * 16;
+  L.chunk = std::max<long long>(1, std::min(m, chunk));
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const int nm = oz::kNumMod;
+  const long long splits = std::max<long long>(8, (k + 32767) / 32768 + 1);
+  L.ar = al((size_t)nm * L.chunk * L.ldk);
+  L.br = al((size_t)nm * L.wpad * L.ldk);
+  L.e = al((size_t)L.chunk * sizeof(int));
+  L.f = al((size_t)L.wpad * sizeof(int));
+  L.res = al((size_t)nm * splits * L.chunk * L.wpad);
+  L.total = L.ar + L.br + L.e + L.f + L.res;
+  return L;
+}
+
+size_t oz_stream_ws_bytes(long long m, long long n, long long k, long long chunk) {
+  return oz_stream_layout(m, n, k, chunk).total;
+}
+
+// C (M×N) = A·P (A any M×K fp64 matrix, row-major) — or (A·P + α·S)/α — with A
+// streamed in row chunks: residues of a chunk, its 16 GEMMs and CRT, next chunk.
+// The panel is prepared once.
+int oz_gemm_stream(const double* a, long long lda, const double* P, long long ldp, long long m, int n,
+                   long long k, double* c, long long ldc, double alpha, const double* S, long long lds,
+                   void* ws, size_t ws_bytes, long long chunk, cudaStream_t st) {
+  const OzStreamLayout L = oz_stream_layout(m, n, k, chunk);
+  if (ws_bytes < L.total) return -3;
+  if (n > 512) return -2;
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  OzOp op;
+  op.ar = reinterpret_cast<int8_t*>(base);
+  op.br = reinterpret_cast<int8_t*>(base + L.ar);
+  op.e = reinterpret_cast<int*>(base + L.ar + L.br);
+  op.f = reinterpret_cast<int*>(base + L.ar + L.br + L.e);
+  op.res = base + L.ar + L.br + L.e + L.f;
+  op.res_elems = L.res;
+  op.ldar = L.ldk;
+  op.ldbr = L.ldk;
+  op.P = P;
+  op.ldp = ldp;
+  op.N = n;
+  op.K = (int)k;
+  op.alpha = alpha;
+  // K padding of both residue buffers stays zero
+  cudaMemsetAsync(base, 0, L.ar + L.br, st);
+  int r = oz_prepare_panel(op, st);
+  if (r < 0) return r;
+  for (long long r0 = 0; r0 < m; r0 += L.chunk) {
+    const long long rows = std::min(L.chunk, m - r0);
+    oz_prepare_rows(a + r0 * lda, rows, k, lda, const_cast<int*>(op.e), const_cast<int8_t*>(op.ar), L.ldk, st);
+    op.M = (int)rows;
+    op.C = c + r0 * ldc;
+    op.ldc = ldc;
+    op.S = S ? S + r0 * lds : nullptr;
+    op.lds = lds;
+    r = oz_gemm_prepared(op, st);
+    if (r < 0) return r;
+  }
+  return 0;
 }
 
 }  // namespace psd

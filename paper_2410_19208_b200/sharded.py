@@ -86,6 +86,8 @@ class KernelOps:
         self.device = torch.device(device)
         self.lib = _native.load_library()
         self.ws = None
+        self.ws8 = None
+        self.int8_products = 0     # X_g·P products that ran on the INT8 engine
 
     def _stream(self):
         return _native.stream_handle(self.device)
@@ -97,6 +99,33 @@ class KernelOps:
 
     def empty(self, shape):
         return torch.empty(shape, dtype=torch.float64, device=self.device)
+
+    def xmul(self, x_rows, panel, shift_alpha=0.0, shift_src=None):
+        """X_g·P for the n-wide products (sketch.py:75/:79/:82, projection.py:104): on the
+        INT8 tensor cores as an exact FP64 emulation (X_g streamed in row chunks) when the
+        FP64 engine is "int8" and w ≤ 512, else the DMMA GEMM."""
+        from . import projection
+        m, k = x_rows.shape
+        n = panel.shape[1]
+        if (projection._FP64_ENGINE != "int8" or n > 512 or x_rows.stride(1) != 1
+                or panel.stride(1) != 1):
+            return self.matmul(x_rows, panel, shift_alpha=shift_alpha, shift_src=shift_src)
+        out = self.empty((m, n))
+        chunk = 8192
+        nbytes = ctypes.c_int64(0)
+        _native.check(self.lib.psd_gemm_f64_int8_ws_bytes(m, n, k, chunk, ctypes.byref(nbytes)))
+        if self.ws8 is None or self.ws8.numel() < nbytes.value:
+            self.ws8 = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
+        s = shift_src
+        alpha = float(shift_alpha) if shift_alpha > 0.0 else 0.0
+        _native.check(self.lib.psd_gemm_f64_int8(
+            _native.ptr(x_rows), x_rows.stride(0), _native.ptr(panel), panel.stride(0), m, n, k,
+            _native.ptr(out), out.stride(0), alpha,
+            _native.ptr(s) if (s is not None and alpha > 0.0) else ctypes.c_void_p(0),
+            s.stride(0) if (s is not None and alpha > 0.0) else 0,
+            _native.ptr(self.ws8), self.ws8.numel(), chunk, self._stream()))
+        self.int8_products += 1
+        return out
 
     def matmul(self, a, b, a_trans=False, b_trans=False, shift_alpha=0.0, shift_src=None):
         """op(a)·op(b); shift_alpha > 0: (acc + α·shift_src)/α (B = (X+αI)/α fused)."""
@@ -261,9 +290,10 @@ def sharded_ran_proj(x_rows, row_start, n, omega, params, *, alpha=0.0, comm=Non
 
     def xmul(panel_full):
         # (X P)[rows_g] or, scaled, ((X + αI) P / α)[rows_g]
+        mul = getattr(ops, "xmul", None) or ops.matmul
         if alpha > 0.0:
-            return ops.matmul(x_rows, panel_full, shift_alpha=alpha, shift_src=panel_full[r0:r1])
-        return ops.matmul(x_rows, panel_full)
+            return mul(x_rows, panel_full, shift_alpha=alpha, shift_src=panel_full[r0:r1])
+        return mul(x_rows, panel_full)
 
     stabilize = params.q >= 2                                   # sketch.py:74
     y = xmul(omega)                                             # sketch.py:75

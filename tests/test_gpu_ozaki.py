@@ -101,6 +101,57 @@ def test_gemm_long_k_multiple_splits(ours):
     assert bool(((c - ref).abs() <= _bound(a, p) + 1e-15 * ref.abs()).all())
 
 
+def _int8_stream(ours, a, p, alpha=0.0, s=None, chunk=0):
+    import ctypes
+    lib = ours._native.load_library()
+    m, k = a.shape
+    n = p.shape[1]
+    nb = ctypes.c_int64(0)
+    ours._native.check(lib.psd_gemm_f64_int8_ws_bytes(m, n, k, chunk, ctypes.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device=a.device)
+    c = torch.full((m, n), float("nan"), dtype=torch.float64, device=a.device)
+    ours._native.check(lib.psd_gemm_f64_int8(
+        ours._native.ptr(a), a.stride(0), ours._native.ptr(p), p.stride(0), m, n, k, ours._native.ptr(c),
+        c.stride(0), alpha, ours._native.ptr(s) if s is not None else None, s.stride(0) if s is not None else 0,
+        ours._native.ptr(ws), ws.numel(), chunk, ours._native.stream_handle(a.device)))
+    torch.cuda.synchronize()
+    return c
+
+
+@pytest.mark.parametrize("m,n,k,chunk", [(350, 40, 300, 100), (1000, 272, 777, 256), (64, 17, 33000, 0)])
+def test_streamed_general_gemm(ours, m, n, k, chunk):
+    """General (non-symmetric) A streamed in row chunks, panel prepared once."""
+    g = torch.Generator(device="cpu").manual_seed(m + n + k)
+    a = torch.randn(m, k, generator=g, dtype=torch.float64).cuda()
+    p = torch.randn(k, n, generator=g, dtype=torch.float64).cuda()
+    a[::3] *= 1e4
+    c = _int8_stream(ours, a, p, chunk=chunk)
+    ref = a @ p
+    assert bool(((c - ref).abs() <= _bound(a, p) + 1e-15 * ref.abs()).all())
+
+
+def test_streamed_gemm_shift_epilogue(ours):
+    """(A·P + α·S)/α — the B = (X + αI)/α product of Alg. 3 on a row block."""
+    g = torch.Generator(device="cpu").manual_seed(77)
+    a = torch.randn(300, 500, generator=g, dtype=torch.float64).cuda()
+    p = torch.randn(500, 24, generator=g, dtype=torch.float64).cuda()
+    s = p[100:400]
+    c = _int8_stream(ours, a, p, alpha=0.75, s=s, chunk=128)
+    ref = (a @ p + 0.75 * s) / 0.75
+    assert float((c - ref).norm() / ref.norm()) < 1e-14
+
+
+def test_streamed_gemm_workspace_too_small(ours):
+    import ctypes
+    lib = ours._native.load_library()
+    a = torch.randn(64, 64, dtype=torch.float64).cuda()
+    ws = torch.empty(16, dtype=torch.uint8, device="cuda")
+    c = torch.empty(64, 8, dtype=torch.float64, device="cuda")
+    st = lib.psd_gemm_f64_int8(ours._native.ptr(a), 64, ours._native.ptr(a), 64, 64, 8, 64, ours._native.ptr(c), 8,
+                               0.0, None, 0, ours._native.ptr(ws), 16, 0, ours._native.stream_handle(a.device))
+    assert st == 1 and b"workspace" in lib.psd_last_error()
+
+
 def _sym(n, seed):
     x = np.random.default_rng(seed).standard_normal((n, n))
     return (x + x.T) / 2

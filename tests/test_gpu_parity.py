@@ -194,13 +194,20 @@ def test_sharded_single_rank_kernel_ops(ours, n, k, l, q, alpha):
     from paper_2410_19208_b200.sharded import KernelOps, sharded_ran_proj
     x = orc.wigner(n, seed=21)
     om = np.random.default_rng(22).standard_normal((n, k + l))
-    rep = sharded_ran_proj(torch.from_numpy(x).cuda(), 0, n, torch.from_numpy(om).cuda(),
-                           ours.RangeParams(k=k, l=l, q=q), alpha=alpha, ops=KernelOps("cuda"))
     ref = orc.ran_proj_scal(x, k, l, q, alpha, omega=om) if alpha > 0 else orc.ran_proj(x, k, l, q, omega=om)
-    assert rep.effective_rank == ref.effective_rank
-    res = rep.result_rows.cpu().numpy()
-    assert np.array_equal(res, res.T)
-    assert _rel(res, ref.result) <= TOL
+    for engine in ("int8", "dmma"):
+        prev = ours.set_fp64_engine(engine)
+        try:
+            ops = KernelOps("cuda")
+            rep = sharded_ran_proj(torch.from_numpy(x).cuda(), 0, n, torch.from_numpy(om).cuda(),
+                                   ours.RangeParams(k=k, l=l, q=q), alpha=alpha, ops=ops)
+        finally:
+            ours.set_fp64_engine(prev)
+        assert (ops.int8_products > 0) == (engine == "int8")
+        assert rep.effective_rank == ref.effective_rank
+        res = rep.result_rows.cpu().numpy()
+        assert np.array_equal(res, res.T)
+        assert _rel(res, ref.result) <= TOL
 
 
 def test_c4_row_blocks_assemble_symmetric(ours):
