@@ -555,6 +555,7 @@ def run_sharded(a):
         dist.init_process_group("nccl", device_id=dev)
     n = a.n
     params = psd.RangeParams(k=a.k, l=a.p, q=a.q)
+    psd.set_fp64_engine(a.fp64_engine)
     starts = sharded.row_split(n, world)
     r0, r1 = starts[rank], starts[rank + 1]
     x = workloads.c4_rows(n, r0, r1, seed=11, device=dev, chunk_rows=4096)
@@ -590,7 +591,9 @@ def run_sharded(a):
         "data": "synthetic (config-4 rows generated per rank, bitwise symmetric)",
         "config": {"workload": f"BASELINE config 4: n={n}, k={a.k}, p={a.p}, q={a.q}, row-sharded x{world}",
                    "result": "dense row blocks" if want else "factored (W, d): X and X₊ do not fit one GPU"},
-        "effective_rank": rep.effective_rank, "tflops": flops * value / 1e12}), flush=True)
+        "effective_rank": rep.effective_rank, "tflops": flops * value / 1e12,
+        "sketch_engine": "int8-ozaki2 (exact FP64 emulation, X_g streamed in 8192-row chunks)"
+                         if ops.int8_products else "fp64-dmma"}), flush=True)
 
 
 def run_fp32_leg(a, torch, psd, pool, params, rng, dev, world):

@@ -154,7 +154,8 @@ int psd_gemm_f64_ozaki(const double* a, int64_t lda, const double* p, int64_t ld
  * caller-owned device workspace (replaces the DGEMM of sketch.py:75/:82 and
  * projection.py:104 for a row block X_g of a sharded X):
  * C = A·P, or C = (A·P + alpha·S)/alpha when alpha > 0 (B = (X+αI)/α with S the
- * rows of P matching the rows of A).  chunk_rows <= 0 picks 8192.
+ * rows of P matching the rows of A).  chunk_rows <= 0 picks 8192.  Panels wider
+ * than 512 columns run as column groups of <= 512 (TMEM budget).
  * psd_gemm_f64_int8_ws_bytes reports the workspace size for (m, n, k, chunk_rows). */
 int psd_gemm_f64_int8_ws_bytes(int64_t m, int64_t n, int64_t k, int64_t chunk_rows, int64_t* bytes);
 int psd_gemm_f64_int8(const double* a, int64_t lda, const double* p, int64_t ldp, int64_t m, int64_t n,

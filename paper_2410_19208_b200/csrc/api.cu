@@ -1062,7 +1062,7 @@ int psd_gemm_f64_ozaki(const double* a, int64_t lda, const double* pp, int64_t l
 
 int psd_gemm_f64_int8_ws_bytes(int64_t m, int64_t n, int64_t k, int64_t chunk_rows, int64_t* bytes) {
   if (!bytes) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
-  if (m < 1 || n < 1 || n > 512 || k < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad INT8-emulated GEMM shape");
+  if (m < 1 || n < 1 || k < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad INT8-emulated GEMM shape");
   *bytes = (int64_t)psd::oz_stream_ws_bytes(m, n, k, chunk_rows > 0 ? chunk_rows : 8192);
   return PSD_OK;
 }
@@ -1071,7 +1071,7 @@ int psd_gemm_f64_int8(const double* a, int64_t lda, const double* pp, int64_t ld
                       int64_t kk, double* c, int64_t ldc, double alpha, const double* s, int64_t lds,
                       void* ws, int64_t ws_bytes, int64_t chunk_rows, void* stream) {
   if (!a || !pp || !c || !ws) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
-  if (m < 1 || nn < 1 || nn > 512 || kk < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad INT8-emulated GEMM shape");
+  if (m < 1 || nn < 1 || kk < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad INT8-emulated GEMM shape");
   if (alpha > 0.0 && !s) return fail(PSD_ERR_INVALID_PARAMS, "alpha > 0 needs the shift source");
   if (lda < kk || ldp < nn || ldc < nn) return fail(PSD_ERR_INVALID_PARAMS, "leading dimension too small");
   const int r = psd::oz_gemm_stream(a, lda, pp, ldp, m, (int)nn, kk, c, ldc, alpha, s, lds, ws, (size_t)ws_bytes,

@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "gemm_tc32.cuh"
 #include "launch.h"
@@ -684,24 +685,27 @@ int oz_gemm(const OzOp& op, cudaStream_t st) {
   return oz_gemm_prepared(op, st);
 }
 
-// Workspace layout of oz_gemm_stream (bytes, 256-aligned pieces).
+// Workspace layout of oz_gemm_stream (bytes, 256-aligned pieces).  Panels wider
+// than 512 columns (the TMEM budget) are cut into G column groups of ≤ 512.
 struct OzStreamLayout {
-  long long ldk, wpad, chunk;
+  long long ldk, groups, gw, gw_pad, chunk;
   size_t ar, br, e, f, res, total;
 };
 static OzStreamLayout oz_stream_layout(long long m, long long n, long long k, long long chunk) {
   OzStreamLayout L{};
   L.ldk = (k + 127) / 128 * 128;
-  L.wpad = (n + 15) / 16 * 16;
+  L.groups = (n + 511) / 512;
+  L.gw = (n + L.groups - 1) / L.groups;
+  L.gw_pad = (L.gw + 15) / 16 * 16;
   L.chunk = std::max<long long>(1, std::min(m, chunk));
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   const int nm = oz::kNumMod;
   const long long splits = std::max<long long>(8, (k + 32767) / 32768 + 1);
   L.ar = al((size_t)nm * L.chunk * L.ldk);
-  L.br = al((size_t)nm * L.wpad * L.ldk);
+  L.br = al((size_t)nm * L.gw_pad * L.ldk) * L.groups;
   L.e = al((size_t)L.chunk * sizeof(int));
-  L.f = al((size_t)L.wpad * sizeof(int));
-  L.res = al((size_t)nm * splits * L.chunk * L.wpad);
+  L.f = al((size_t)L.gw_pad * sizeof(int)) * L.groups;
+  L.res = al((size_t)nm * splits * L.chunk * L.gw_pad);
   L.total = L.ar + L.br + L.e + L.f + L.res;
   return L;
 }
@@ -711,43 +715,56 @@ size_t oz_stream_ws_bytes(long long m, long long n, long long k, long long chunk
 }
 
 // C (M×N) = A·P (A any M×K fp64 matrix, row-major) — or (A·P + α·S)/α — with A
-// streamed in row chunks: residues of a chunk, its 16 GEMMs and CRT, next chunk.
-// The panel is prepared once.
+// streamed in row chunks: residues of a chunk, then for each ≤512-column group of
+// the panel its 16 GEMMs and CRT; the panel groups are prepared once.
 int oz_gemm_stream(const double* a, long long lda, const double* P, long long ldp, long long m, int n,
                    long long k, double* c, long long ldc, double alpha, const double* S, long long lds,
                    void* ws, size_t ws_bytes, long long chunk, cudaStream_t st) {
   const OzStreamLayout L = oz_stream_layout(m, n, k, chunk);
   if (ws_bytes < L.total) return -3;
-  if (n > 512) return -2;
   uint8_t* base = static_cast<uint8_t*>(ws);
-  OzOp op;
-  op.ar = reinterpret_cast<int8_t*>(base);
-  op.br = reinterpret_cast<int8_t*>(base + L.ar);
-  op.e = reinterpret_cast<int*>(base + L.ar + L.br);
-  op.f = reinterpret_cast<int*>(base + L.ar + L.br + L.e);
-  op.res = base + L.ar + L.br + L.e + L.f;
-  op.res_elems = L.res;
-  op.ldar = L.ldk;
-  op.ldbr = L.ldk;
-  op.P = P;
-  op.ldp = ldp;
-  op.N = n;
-  op.K = (int)k;
-  op.alpha = alpha;
+  int8_t* ar = reinterpret_cast<int8_t*>(base);
+  uint8_t* br0 = base + L.ar;
+  int* e = reinterpret_cast<int*>(base + L.ar + L.br);
+  uint8_t* f0 = base + L.ar + L.br + L.e;
+  uint8_t* res = base + L.ar + L.br + L.e + L.f;
+  const size_t br_g = L.br / L.groups, f_g = L.f / L.groups;
   // K padding of both residue buffers stays zero
   cudaMemsetAsync(base, 0, L.ar + L.br, st);
-  int r = oz_prepare_panel(op, st);
-  if (r < 0) return r;
+  std::vector<OzOp> ops((size_t)L.groups);
+  for (long long g = 0; g < L.groups; ++g) {
+    OzOp& op = ops[(size_t)g];
+    const long long c0 = g * L.gw;
+    op.ar = ar;
+    op.ldar = L.ldk;
+    op.e = e;
+    op.br = reinterpret_cast<int8_t*>(br0 + g * br_g);
+    op.ldbr = L.ldk;
+    op.f = reinterpret_cast<int*>(f0 + g * f_g);
+    op.res = res;
+    op.res_elems = L.res;
+    op.P = P + c0;
+    op.ldp = ldp;
+    op.N = (int)std::min<long long>(L.gw, n - c0);
+    op.K = (int)k;
+    op.alpha = alpha;
+    const int r = oz_prepare_panel(op, st);
+    if (r < 0) return r;
+  }
   for (long long r0 = 0; r0 < m; r0 += L.chunk) {
     const long long rows = std::min(L.chunk, m - r0);
-    oz_prepare_rows(a + r0 * lda, rows, k, lda, const_cast<int*>(op.e), const_cast<int8_t*>(op.ar), L.ldk, st);
-    op.M = (int)rows;
-    op.C = c + r0 * ldc;
-    op.ldc = ldc;
-    op.S = S ? S + r0 * lds : nullptr;
-    op.lds = lds;
-    r = oz_gemm_prepared(op, st);
-    if (r < 0) return r;
+    oz_prepare_rows(a + r0 * lda, rows, k, lda, e, ar, L.ldk, st);
+    for (long long g = 0; g < L.groups; ++g) {
+      OzOp& op = ops[(size_t)g];
+      const long long c0 = g * L.gw;
+      op.M = (int)rows;
+      op.C = c + r0 * ldc + c0;
+      op.ldc = ldc;
+      op.S = S ? S + r0 * lds + c0 : nullptr;
+      op.lds = lds;
+      const int r = oz_gemm_prepared(op, st);
+      if (r < 0) return r;
+    }
   }
   return 0;
 }

@@ -102,13 +102,12 @@ class KernelOps:
 
     def xmul(self, x_rows, panel, shift_alpha=0.0, shift_src=None):
         """X_g·P for the n-wide products (sketch.py:75/:79/:82, projection.py:104): on the
-        INT8 tensor cores as an exact FP64 emulation (X_g streamed in row chunks) when the
-        FP64 engine is "int8" and w ≤ 512, else the DMMA GEMM."""
+        INT8 tensor cores as an exact FP64 emulation (X_g streamed in row chunks, panels wider
+        than 512 columns in column groups) when the FP64 engine is "int8", else the DMMA GEMM."""
         from . import projection
         m, k = x_rows.shape
         n = panel.shape[1]
-        if (projection._FP64_ENGINE != "int8" or n > 512 or x_rows.stride(1) != 1
-                or panel.stride(1) != 1):
+        if projection._FP64_ENGINE != "int8" or x_rows.stride(1) != 1 or panel.stride(1) != 1:
             return self.matmul(x_rows, panel, shift_alpha=shift_alpha, shift_src=shift_src)
         out = self.empty((m, n))
         chunk = 8192

@@ -118,7 +118,8 @@ def _int8_stream(ours, a, p, alpha=0.0, s=None, chunk=0):
     return c
 
 
-@pytest.mark.parametrize("m,n,k,chunk", [(350, 40, 300, 100), (1000, 272, 777, 256), (64, 17, 33000, 0)])
+@pytest.mark.parametrize("m,n,k,chunk", [(350, 40, 300, 100), (1000, 272, 777, 256), (64, 17, 33000, 0),
+                                         (300, 544, 600, 128), (90, 1100, 200, 0)])
 def test_streamed_general_gemm(ours, m, n, k, chunk):
     """General (non-symmetric) A streamed in row chunks, panel prepared once."""
     g = torch.Generator(device="cpu").manual_seed(m + n + k)
