@@ -662,7 +662,9 @@ int ensure_oz(psd_plan* p) {
   if (p->oz_failed) return PSD_ERR_NO_MEMORY;
   const int L = psd::oz_num_moduli();
   const ll ldk = (p->n + 127) / 128 * 128;
-  const ll wpad = (p->w + 15) / 16 * 16;
+  const int groups = (int)((p->w + 511) / 512);
+  const ll gw_pad = ((p->w + groups - 1) / groups + 15) / 16 * 16;
+  const ll wpad = gw_pad * groups;   // column groups of ≤ 512 (TMEM), each padded to 16
   auto balloc = [&](size_t bytes) -> void* {
     return static_cast<void*>(alloc(p, (bytes + 7) / 8));
   };
@@ -670,7 +672,7 @@ int ensure_oz(psd_plan* p) {
   p->oz_br = static_cast<int8_t*>(balloc((size_t)L * wpad * ldk));
   p->oz_e = static_cast<int*>(balloc((size_t)p->n * sizeof(int)));
   p->oz_f = static_cast<int*>(balloc((size_t)wpad * sizeof(int)));
-  p->oz_res_elems = (size_t)L * 8 * p->n * wpad;
+  p->oz_res_elems = (size_t)L * 8 * p->n * (gw_pad + 16);
   p->oz_res = static_cast<uint8_t*>(balloc(p->oz_res_elems));
   if (!p->oz_ar || !p->oz_br || !p->oz_e || !p->oz_f || !p->oz_res) {
     p->oz_failed = true;
@@ -682,36 +684,43 @@ int ensure_oz(psd_plan* p) {
   return PSD_OK;
 }
 
-// X·P (X bitwise symmetric, residues prepared) as 16 INT8 GEMMs + CRT.
+// X·P (X bitwise symmetric, residues prepared) as 16 INT8 GEMMs + CRT, panels
+// wider than 512 columns (TMEM) in column groups of ≤ 512.
 int xmul_oz(psd_plan* p, ll n, const double* P, ll ldP, int w, double* out, ll ldo, double alpha,
             cudaStream_t st) {
   Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
-  psd::OzOp op;
-  op.ar = p->oz_ar;
-  op.ldar = p->oz_ldk;
-  op.e = p->oz_e;
-  op.P = P;
-  op.ldp = ldP;
-  op.M = (int)n;
-  op.N = w;
-  op.K = (int)n;
-  op.br = p->oz_br;
-  op.ldbr = p->oz_ldk;
-  op.f = p->oz_f;
-  op.res = p->oz_res;
-  op.res_elems = p->oz_res_elems;
-  op.C = out;
-  op.ldc = ldo;
-  op.alpha = alpha;
-  op.S = P;
-  op.lds = ldP;
-  if (p->prof) {
-    op.ev_gemm[0] = take_event(p);
-    op.ev_gemm[1] = take_event(p);
+  const int groups = (w + 511) / 512;
+  const int gw = (w + groups - 1) / groups;
+  const ll gw_pad = (gw + 15) / 16 * 16;
+  for (int g = 0; g < groups; ++g) {
+    const int c0 = g * gw;
+    psd::OzOp op;
+    op.ar = p->oz_ar;
+    op.ldar = p->oz_ldk;
+    op.e = p->oz_e;
+    op.P = P + c0;
+    op.ldp = ldP;
+    op.M = (int)n;
+    op.N = std::min(gw, w - c0);
+    op.K = (int)n;
+    op.br = p->oz_br + (size_t)g * psd::oz_num_moduli() * gw_pad * p->oz_ldk;
+    op.ldbr = p->oz_ldk;
+    op.f = p->oz_f + (size_t)g * gw_pad;
+    op.res = p->oz_res;
+    op.res_elems = p->oz_res_elems;
+    op.C = out + c0;
+    op.ldc = ldo;
+    op.alpha = alpha;
+    op.S = P + c0;
+    op.lds = ldP;
+    if (p->prof) {
+      op.ev_gemm[0] = take_event(p);
+      op.ev_gemm[1] = take_event(p);
+    }
+    const int r = psd::oz_gemm(op, st);
+    if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "INT8-emulated GEMM rejected its operands (%d)", r);
+    if (p->prof) p->marks.push_back({PSD_STAGE_INT8_GEMM, {op.ev_gemm[0], op.ev_gemm[1]}});
   }
-  const int r = psd::oz_gemm(op, st);
-  if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "INT8-emulated GEMM rejected its operands (%d)", r);
-  if (p->prof) p->marks.push_back({PSD_STAGE_INT8_GEMM, {op.ev_gemm[0], op.ev_gemm[1]}});
   return PSD_OK;
 }
 
@@ -844,7 +853,7 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     const char* e = getenv("PSD_FP64_OZAKI");
     return !(e && e[0] == '0');
   }();
-  bool oz = !f32 && oz_on && !(flags & PSD_FLAG_FP64_DMMA) && !use_t && w <= 512;
+  bool oz = !f32 && oz_on && !(flags & PSD_FLAG_FP64_DMMA) && !use_t;
   if (oz && ensure_oz(p) != PSD_OK) {   // no room for the residue planes: DMMA products
     cudaGetLastError();
     oz = false;

@@ -187,10 +187,12 @@ def test_ran_proj_scal_int8_engine(ours):
     assert np.linalg.norm(r8.result - ref) / np.linalg.norm(ref) < 1e-10
 
 
-def test_engine_falls_back_to_dmma_for_wide_sketch_and_transpose(ours):
+def test_wide_sketch_column_groups_and_transpose_fallback(ours):
     x = _sym(700, 4)
     wide = ours.ran_proj(x, ours.RangeParams(k=500, l=16, q=0), np.random.default_rng(1))
-    assert wide.device_info["sketch_engine"] == 0          # w = 516 > 512 TMEM columns
+    assert wide.device_info["sketch_engine"] == 1          # w = 516 > 512: two column groups
+    ref = orc.ran_proj(x, 500, 16, 0, rng=np.random.default_rng(1)).result
+    assert np.linalg.norm(wide.result - ref) / np.linalg.norm(ref) < 1e-10
     y = x.copy()
     y[0, 1] += 1e-14                                        # not bitwise symmetric → Xᵀ·P kernel
     t = ours.ran_proj(y, ours.RangeParams(k=20, l=8, q=1), np.random.default_rng(1))
