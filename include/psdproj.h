@@ -66,7 +66,8 @@ typedef struct psd_report {
   int32_t qr_shifted;      /* 1 if a shifted CholeskyQR pass was needed */
   int32_t eig_sweeps;      /* block-Jacobi sweeps of the k x k eigensolve */
   int32_t gpu_launches;    /* kernels this call launched */
-  int32_t sketch_engine;   /* n x n products ran on: 0 FP64 DMMA, 1 INT8-emulated FP64 (Ozaki II), 2 3xTF32 */
+  int32_t sketch_engine;   /* n x n products ran on: 0 FP64 DMMA, 1 INT8-emulated FP64 (Ozaki II),
+                              2 3xTF32, 3 X·P on INT8 and X^T·P on DMMA (X not bitwise symmetric) */
   double residual_frob;    /* PSD_FLAG_DIAGNOSTICS only, else NaN */
   double max_abs;          /* max|x_ij| (symmetric.py:51) */
   double sym_defect;       /* max|x_ij - x_ji| (symmetric.py:52) */

@@ -853,19 +853,20 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     const char* e = getenv("PSD_FP64_OZAKI");
     return !(e && e[0] == '0');
   }();
-  bool oz = !f32 && oz_on && !(flags & PSD_FLAG_FP64_DMMA) && !use_t;
+  bool oz = !f32 && oz_on && !(flags & PSD_FLAG_FP64_DMMA);
   if (oz && ensure_oz(p) != PSD_OK) {   // no room for the residue planes: DMMA products
     cudaGetLastError();
     oz = false;
   }
-  r.sketch_engine = f32 ? 2 : (oz ? 1 : 0);
+  // 3: X·P products on the INT8 engine, Xᵀ·P (X not bitwise symmetric) on DMMA
+  r.sketch_engine = f32 ? 2 : (oz ? (use_t ? 3 : 1) : 0);
   if (oz) {
     Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
     psd::oz_prepare_rows(x64, n, n, ldx, p->oz_e, p->oz_ar, p->oz_ldk, st);
   }
   const MulFn mul = [&](const double* P, ll ldP, int ww, double* out, ll ldo2, bool t) {
     if (f32) return xmul_tc32(p, n, xhi, ldhi, P, ldP, ww, out, ldo2, alpha, st);
-    if (oz) return xmul_oz(p, n, P, ldP, ww, out, ldo2, alpha, st);
+    if (oz && !(t && use_t)) return xmul_oz(p, n, P, ldP, ww, out, ldo2, alpha, st);
     return xmul(p, x64, n, ldx, P, ldP, ww, out, ldo2, alpha, t && use_t, st);
   };
   int qb = 0, wk = 0;

@@ -187,7 +187,7 @@ def test_ran_proj_scal_int8_engine(ours):
     assert np.linalg.norm(r8.result - ref) / np.linalg.norm(ref) < 1e-10
 
 
-def test_wide_sketch_column_groups_and_transpose_fallback(ours):
+def test_wide_sketch_column_groups_and_transpose_on_dmma(ours):
     x = _sym(700, 4)
     wide = ours.ran_proj(x, ours.RangeParams(k=500, l=16, q=0), np.random.default_rng(1))
     assert wide.device_info["sketch_engine"] == 1          # w = 516 > 512: two column groups
@@ -196,7 +196,9 @@ def test_wide_sketch_column_groups_and_transpose_fallback(ours):
     y = x.copy()
     y[0, 1] += 1e-14                                        # not bitwise symmetric → Xᵀ·P kernel
     t = ours.ran_proj(y, ours.RangeParams(k=20, l=8, q=1), np.random.default_rng(1))
-    assert t.device_info["sketch_engine"] == 0 and t.device_info["used_transpose"] == 1
+    assert t.device_info["sketch_engine"] == 3 and t.device_info["used_transpose"] == 1
+    ref = orc.ran_proj(y, 20, 8, 1, rng=np.random.default_rng(1)).result
+    assert np.linalg.norm(t.result - ref) / np.linalg.norm(ref) < 1e-10
 
 
 def test_set_fp64_engine_validation(ours):
