@@ -52,7 +52,7 @@ def _bound(a, p):
 
 
 @pytest.mark.parametrize("m,n,k", [(256, 16, 128), (300, 40, 200), (1000, 272, 1000), (513, 37, 4099),
-                                   (64, 512, 300), (130, 264, 4096), (7, 1, 1)])
+                                   (64, 512, 300), (130, 264, 4096), (7, 1, 1), (192, 40, 640), (77, 272, 1024)])
 def test_gemm_matches_fp64(ours, m, n, k):
     g = torch.Generator(device="cpu").manual_seed(m * 7 + n + k)
     a = torch.randn(m, k, generator=g, dtype=torch.float64).cuda()
@@ -66,19 +66,21 @@ def test_gemm_matches_fp64(ours, m, n, k):
     assert float((c - ref).norm() / ref.norm()) < 1e-14
 
 
-def test_gemm_integer_inputs_exact(ours):
+@pytest.mark.parametrize("k", [2048, 2040])
+def test_gemm_integer_inputs_exact(ours, k):
     g = torch.Generator(device="cpu").manual_seed(3)
-    a = torch.randint(-2 ** 20, 2 ** 20, (384, 2048), generator=g, dtype=torch.int64)
-    p = torch.randint(-2 ** 20, 2 ** 20, (2048, 96), generator=g, dtype=torch.int64)
+    a = torch.randint(-2 ** 20, 2 ** 20, (384, k), generator=g, dtype=torch.int64)
+    p = torch.randint(-2 ** 20, 2 ** 20, (k, 96), generator=g, dtype=torch.int64)
     ref = a @ p                        # |entries| < 2^51: exact in fp64
     c = _oz(ours, a.double().cuda(), p.double().cuda())
     assert torch.equal(c.cpu(), ref.double())
 
 
-def test_gemm_zero_rows_extreme_scales(ours):
+@pytest.mark.parametrize("k", [640, 650])   # k % 64 == 0: byte-MMA residues; else the fp32-limb kernel
+def test_gemm_zero_rows_extreme_scales(ours, k):
     g = torch.Generator(device="cpu").manual_seed(5)
-    a = torch.randn(200, 640, generator=g, dtype=torch.float64)
-    p = torch.randn(640, 48, generator=g, dtype=torch.float64)
+    a = torch.randn(200, k, generator=g, dtype=torch.float64)
+    p = torch.randn(k, 48, generator=g, dtype=torch.float64)
     a[3] = 0.0
     a[4] *= 1e-300
     a[5] *= 1e300
