@@ -64,8 +64,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the config-3 FP32 (3xTF32) leg")
-    ap.add_argument("--fp64-engine", choices=["int8", "dmma"], default="int8",
-                    help="FP64 sketch products: exact emulation on the INT8 tensor cores (default) or DMMA")
+    ap.add_argument("--fp64-engine", choices=["auto", "int8", "dmma"], default="auto",
+                    help="FP64 n×n products: exact emulation on the INT8 tensor cores (auto: n >= 3072), or DMMA")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     for key in ("n", "k", "p", "q"):

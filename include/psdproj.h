@@ -41,6 +41,7 @@ enum psd_status {
 #define PSD_FLAG_SKIP_SYMCHECK 4u /* caller already ran psd_require_symmetric on X */
 #define PSD_FLAG_ASSUME_SYMMETRIC 8u /* X is bitwise symmetric: X^T·P computed as X·P */
 #define PSD_FLAG_FP64_DMMA 16u     /* keep the FP64 n x n products on the DMMA kernel (no INT8 emulation) */
+#define PSD_FLAG_FP64_INT8 32u     /* INT8-emulated FP64 products at any n (default: n >= 3072) */
 
 typedef struct psd_plan psd_plan;
 

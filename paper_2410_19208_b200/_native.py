@@ -50,6 +50,7 @@ FLAG_STRICT = 2
 FLAG_SKIP_SYMCHECK = 4
 FLAG_ASSUME_SYMMETRIC = 8
 FLAG_FP64_DMMA = 16
+FLAG_FP64_INT8 = 32
 
 # name → (restype, argtypes); the full exported surface of include/psdproj.h
 SIGNATURES = {

@@ -853,7 +853,10 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     const char* e = getenv("PSD_FP64_OZAKI");
     return !(e && e[0] == '0');
   }();
-  bool oz = !f32 && oz_on && !(flags & PSD_FLAG_FP64_DMMA);
+  // below n ≈ 3k the per-product residue/CRT passes cost more than DMMA saves
+  // (C1 n=1000: 606 vs 697 projections/s; n=2048 par; n=4096: 227 vs 205)
+  const bool oz_size = n >= 3072 || (flags & PSD_FLAG_FP64_INT8);
+  bool oz = !f32 && oz_on && oz_size && !(flags & PSD_FLAG_FP64_DMMA);
   if (oz && ensure_oz(p) != PSD_OK) {   // no room for the residue planes: DMMA products
     cudaGetLastError();
     oz = false;

@@ -82,16 +82,18 @@ def resolve_dtype(dtype):
     raise errors.error("InvalidParams", f"unsupported dtype {dtype!r} (fp64 or fp32)")
 
 
-_FP64_ENGINE = "int8"
+_FP64_ENGINE = "auto"
+INT8_MIN_N = 3072   # "auto": INT8 emulation from this n up (measured crossover)
 
 
 def set_fp64_engine(engine):
-    """Tensor-core engine of the FP64 n×n sketch products: "int8" (default; FP64
-    emulated exactly on the INT8 tensor cores, Ozaki scheme II, when X is bitwise
-    symmetric) or "dmma" (the FP64 DMMA kernel).  Returns the previous setting."""
+    """Tensor-core engine of the FP64 n×n products: "auto" (default: FP64 emulated
+    exactly on the INT8 tensor cores, Ozaki scheme II, for n ≥ 3072; DMMA below),
+    "int8" (emulation at any n) or "dmma" (the FP64 DMMA kernel).  Returns the
+    previous setting."""
     global _FP64_ENGINE
-    if engine not in ("int8", "dmma"):
-        raise errors.error("InvalidParams", f"unknown FP64 engine {engine!r} (int8 or dmma)")
+    if engine not in ("auto", "int8", "dmma"):
+        raise errors.error("InvalidParams", f"unknown FP64 engine {engine!r} (auto, int8 or dmma)")
     prev, _FP64_ENGINE = _FP64_ENGINE, engine
     return prev
 
@@ -136,6 +138,8 @@ def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, m
             flags |= _native.FLAG_ASSUME_SYMMETRIC
         if _FP64_ENGINE == "dmma":
             flags |= _native.FLAG_FP64_DMMA
+        elif _FP64_ENGINE == "int8":
+            flags |= _native.FLAG_FP64_INT8
     if collect_diagnostics:
         flags |= _native.FLAG_DIAGNOSTICS
     rep = _native.PsdReport()

@@ -107,7 +107,9 @@ class KernelOps:
         from . import projection
         m, k = x_rows.shape
         n = panel.shape[1]
-        if projection._FP64_ENGINE != "int8" or x_rows.stride(1) != 1 or panel.stride(1) != 1:
+        eng = projection._FP64_ENGINE
+        use = eng == "int8" or (eng == "auto" and k >= projection.INT8_MIN_N)
+        if not use or x_rows.stride(1) != 1 or panel.stride(1) != 1:
             return self.matmul(x_rows, panel, shift_alpha=shift_alpha, shift_src=shift_src)
         out = self.empty((m, n))
         chunk = 8192

@@ -183,7 +183,11 @@ def test_ran_proj_int8_engine_matches_dmma_and_oracle(ours, q):
 def test_ran_proj_scal_int8_engine(ours):
     x = _sym(520, 21)
     params = ours.RangeParams(k=30, l=10, q=1)
-    r8 = ours.ran_proj_scal(x, params, 0.75, np.random.default_rng(2))
+    prev = ours.set_fp64_engine("int8")
+    try:
+        r8 = ours.ran_proj_scal(x, params, 0.75, np.random.default_rng(2))
+    finally:
+        ours.set_fp64_engine(prev)
     assert r8.device_info["sketch_engine"] == 1
     ref = orc.ran_proj_scal(x, 30, 10, 1, 0.75, rng=np.random.default_rng(2)).result
     assert np.linalg.norm(r8.result - ref) / np.linalg.norm(ref) < 1e-10
@@ -191,13 +195,17 @@ def test_ran_proj_scal_int8_engine(ours):
 
 def test_wide_sketch_column_groups_and_transpose_on_dmma(ours):
     x = _sym(700, 4)
-    wide = ours.ran_proj(x, ours.RangeParams(k=500, l=16, q=0), np.random.default_rng(1))
+    prev = ours.set_fp64_engine("int8")
+    try:
+        wide = ours.ran_proj(x, ours.RangeParams(k=500, l=16, q=0), np.random.default_rng(1))
+        y = x.copy()
+        y[0, 1] += 1e-14                                    # not bitwise symmetric → Xᵀ·P kernel
+        t = ours.ran_proj(y, ours.RangeParams(k=20, l=8, q=1), np.random.default_rng(1))
+    finally:
+        ours.set_fp64_engine(prev)
     assert wide.device_info["sketch_engine"] == 1          # w = 516 > 512: two column groups
     ref = orc.ran_proj(x, 500, 16, 0, rng=np.random.default_rng(1)).result
     assert np.linalg.norm(wide.result - ref) / np.linalg.norm(ref) < 1e-10
-    y = x.copy()
-    y[0, 1] += 1e-14                                        # not bitwise symmetric → Xᵀ·P kernel
-    t = ours.ran_proj(y, ours.RangeParams(k=20, l=8, q=1), np.random.default_rng(1))
     assert t.device_info["sketch_engine"] == 3 and t.device_info["used_transpose"] == 1
     ref = orc.ran_proj(y, 20, 8, 1, rng=np.random.default_rng(1)).result
     assert np.linalg.norm(t.result - ref) / np.linalg.norm(ref) < 1e-10
@@ -206,3 +214,14 @@ def test_wide_sketch_column_groups_and_transpose_on_dmma(ours):
 def test_set_fp64_engine_validation(ours):
     with pytest.raises(Exception):
         ours.set_fp64_engine("fp16")
+
+
+def test_auto_engine_size_threshold(ours):
+    """auto: DMMA below n = 3072 (measured crossover), INT8 emulation from there."""
+    assert ours.set_fp64_engine("auto") in ("auto", "int8", "dmma")
+    small = ours.ran_proj(_sym(600, 3), ours.RangeParams(k=20, l=6, q=0), np.random.default_rng(0))
+    assert small.device_info["sketch_engine"] == 0
+    xs = torch.randn(3072, 3072, dtype=torch.float64, device="cuda")
+    xs = (xs + xs.T) / 2
+    big = ours.ran_proj(xs, ours.RangeParams(k=20, l=6, q=0), np.random.default_rng(0))
+    assert big.device_info["sketch_engine"] == 1

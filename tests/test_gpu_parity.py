@@ -35,8 +35,17 @@ def ours():
     return m
 
 
+@pytest.fixture(params=["auto", "int8"])
+def engine(request, ours):
+    """FP64 product engine: "auto" (DMMA below n = 3072, INT8 emulation above) and
+    "int8" forced at every size, so the golden parity runs on both engines."""
+    prev = ours.set_fp64_engine(request.param)
+    yield request.param
+    ours.set_fp64_engine(prev)
+
+
 @pytest.mark.parametrize("name", RAN_CASES)
-def test_ran_proj_golden(ours, name):
+def test_ran_proj_golden(ours, engine, name):
     d = gio.load(name)
     params = ours.RangeParams(k=int(d["k"]), l=int(d["l"]), q=int(d["q"]))
     alpha = float(d["alpha"])
@@ -60,7 +69,7 @@ def test_ran_proj_golden(ours, name):
 
 
 @pytest.mark.parametrize("name", gio.names("project_") + ["config1_project_scaled"])
-def test_project_scaled_golden(ours, name):
+def test_project_scaled_golden(ours, engine, name):
     d = gio.load(name)
     params = ours.RangeParams(k=int(d["k"]), l=int(d["l"]), q=int(d["q"]))
     if "alpha_override" in d:
@@ -99,7 +108,7 @@ def test_eigh_golden(ours):
 
 
 @pytest.mark.parametrize("n,k,l,q,seed", [(300, 20, 6, 0, 1), (513, 40, 9, 1, 2), (777, 30, 10, 3, 3)])
-def test_ran_proj_vs_oracle_random_shapes(ours, n, k, l, q, seed):
+def test_ran_proj_vs_oracle_random_shapes(ours, engine, n, k, l, q, seed):
     x = orc.wigner(n, seed=seed)
     om = np.random.default_rng(seed + 100).standard_normal((n, k + l))
     ref = orc.ran_proj(x, k, l, q, omega=om)
@@ -109,7 +118,7 @@ def test_ran_proj_vs_oracle_random_shapes(ours, n, k, l, q, seed):
 
 
 @pytest.mark.parametrize("n", [2048, 4096])
-def test_config3_shape_reduced_n(ours, n):
+def test_config3_shape_reduced_n(ours, engine, n):
     """C3 spectrum (rank-200 ± parts + 1e-3 Wigner), k=256, p=16, q=1: the
     unstabilised, κ(Y)≈1e8 case that stresses the CholeskyQR path."""
     x = orc.c3_matrix(n, seed=7)
