@@ -411,9 +411,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   C' = S − k·M evaluated mod 2^128 (|C'| < 2^127, so the wrapped value is exact).
 // Four columns per thread (ldo % 4 == 0; columns ≥ N are padding and not stored).
 // alpha > 0: C = (C + α·S)/α (the shifted sketch of Alg. 3).
-__global__ void crt_kernel(const uint8_t* __restrict__ res, int splits, long long M, int N, long long ldo,
-                           const int* __restrict__ e, const int* __restrict__ f, double* __restrict__ C,
-                           long long ldc, double alpha, const double* __restrict__ S, long long lds) {
+template <bool ONE>   // ONE: a single K split (all 16 plane words loaded up front)
+__global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ res, int splits, long long M, int N,
+                                                  long long ldo, const int* __restrict__ e,
+                                                  const int* __restrict__ f, double* __restrict__ C, long long ldc,
+                                                  double alpha, const double* __restrict__ S, long long lds) {
   const int n4 = (N + 3) / 4;
   const long long total = M * n4;
   const long long plane = M * ldo;
@@ -423,27 +425,39 @@ __global__ void crt_kernel(const uint8_t* __restrict__ res, int splits, long lon
     const long long i = t / n4;
     const int j0 = (int)(t % n4) * 4;
     const uint8_t* base = res + i * ldo + j0;
+    uint32_t wv[kNumMod];
+    if (ONE) {
+#pragma unroll
+      for (int l = 0; l < kNumMod; ++l) wv[l] = __ldcs(reinterpret_cast<const uint32_t*>(base + l * plane));
+    }
     float ks[4] = {0.f, 0.f, 0.f, 0.f};
     unsigned __int128 acc[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int l = 0; l < kNumMod; ++l) {
       int sum[4] = {0, 0, 0, 0};
-      for (int sp = 0; sp < splits; ++sp) {
-        const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(base + ((long long)l * splits + sp) * plane));
+      if (ONE) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) sum[q] += (int)(int8_t)(w >> (8 * q));
+        for (int q = 0; q < 4; ++q) sum[q] = (int)(int8_t)(wv[l] >> (8 * q));
+      } else {
+        for (int sp = 0; sp < splits; ++sp) {
+          const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(base + ((long long)l * splits + sp) * plane));
+#pragma unroll
+          for (int q = 0; q < 4; ++q) sum[q] += (int)(int8_t)(w >> (8 * q));
+        }
       }
       const float m = c_modf[l], rm = c_rmodf[l], winv = c_wInvf[l];
       const unsigned __int128 W = ((unsigned __int128)c_W[l][1] << 64) | c_W[l][0];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        float y = sym_mod_f((float)sum[q] * winv, m, rm);   // |sum·winv| < 2^19: exact
-        y = y < 0.f ? y + m : y;                             // y ∈ [0, m]
+        const float sf = __int_as_float(sum[q] + 0x4B400000) - kMagic;   // exact: |sum| < 2^22
+        float y = sym_mod_f(sf * winv, m, rm);                          // |sum·winv| < 2^19: exact
+        y = y < 0.f ? y + m : y;                                         // y ∈ [0, m]
         ks[q] = fmaf(y, rm, ks[q]);
         const uint32_t yi = __float_as_uint(y + kMagic) - 0x4B400000u;
         acc[q] += W * yi;
       }
     }
+    const int ei = e[i];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int j = j0 + q;
@@ -455,7 +469,9 @@ __global__ void crt_kernel(const uint8_t* __restrict__ res, int splits, long lon
       const unsigned long long hi = (unsigned long long)(mag >> 64), lo = (unsigned long long)mag;
       double val = fma((double)hi, 18446744073709551616.0, (double)lo);
       if (neg) val = -val;
-      val = ldexp(val, e[i] + f[j] - 106);
+      const int ex = ei + f[j] - 106;
+      if (ex > -1000 && ex < 1000) val *= __longlong_as_double((long long)(ex + 1023) << 52);   // exact 2^ex
+      else val = ldexp(val, ex);
       if (alpha > 0.0) val = (val + alpha * S[i * lds + j]) / alpha;
       C[i * ldc + j] = val;
     }
@@ -672,9 +688,15 @@ int oz_gemm_prepared(const OzOp& op, cudaStream_t st) {
   if (cudaLaunchKernelEx(&cfg, i8_gemm2_kernel, ma, mb, mb2, p) != cudaSuccess) return -6;
   if (op.ev_gemm[1]) cudaEventRecord(op.ev_gemm[1], st);
   count_launch();
-  crt_kernel<<<grid_oz((long long)op.M * ((op.N + 3) / 4), 256), 256, 0, st>>>(op.res, p.splits, op.M, op.N, p.ldo,
-                                                                   op.e, op.f, op.C, op.ldc, op.alpha,
-                                                                   op.S, op.lds);
+  {
+    const unsigned g = (unsigned)grid_oz((long long)op.M * ((op.N + 3) / 4), 256);
+    if (p.splits == 1)
+      crt_kernel<true><<<g, 256, 0, st>>>(op.res, 1, op.M, op.N, p.ldo, op.e, op.f, op.C, op.ldc, op.alpha,
+                                          op.S, op.lds);
+    else
+      crt_kernel<false><<<g, 256, 0, st>>>(op.res, p.splits, op.M, op.N, p.ldo, op.e, op.f, op.C, op.ldc,
+                                           op.alpha, op.S, op.lds);
+  }
   count_launch();
   return p.splits;
 }
