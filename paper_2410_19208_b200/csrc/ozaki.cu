@@ -210,9 +210,14 @@ __global__ void residues_rows1_kernel(const double* __restrict__ x, long long ro
   }
 }
 // residues of a K×N panel, transposed and column-scaled: R[ℓ][j][k], j < nrows_pad (zero rows j ≥ N)
-__global__ void residues_panel_t_kernel(const double* __restrict__ p, long long K, int N, long long ldp,
-                                        const int* __restrict__ f, int8_t* __restrict__ r, long long ldr,
-                                        long long plane, int nrows_pad) {
+// Residues of the panel, transposed and column-scaled: R[ℓ][j][k], j < nrows_pad (zero
+// rows j ≥ N).  A 32(k) × 32(j) tile is staged through shared memory; thread (j, k4)
+// then reduces 4 consecutive k of row j with the 13-bit-limb fp32 arithmetic of
+// residues_rows_kernel and stores one 32-bit word per modulus.
+__global__ void __launch_bounds__(256) residues_panel_t_kernel(const double* __restrict__ p, long long K, int N,
+                                                               long long ldp, const int* __restrict__ f,
+                                                               int8_t* __restrict__ r, long long ldr,
+                                                               long long plane, int nrows_pad) {
   __shared__ double tile[32][33];
   const long long k0 = (long long)blockIdx.x * 32;
   const int j0 = blockIdx.y * 32;
@@ -223,15 +228,50 @@ __global__ void residues_panel_t_kernel(const double* __restrict__ p, long long 
     tile[yy][tx] = (k < K && j < N) ? p[k * ldp + j] : 0.0;
   }
   __syncthreads();
-  for (int yy = ty; yy < 32; yy += 8) {
-    const int j = j0 + yy;
-    const long long k = k0 + tx;
-    if (j < nrows_pad && k < K) {
-      const double b = (j < N) ? rint(ldexp(tile[tx][yy], 53 - f[j])) : 0.0;
-      int8_t* out = r + (long long)j * ldr + k;
+  const int tid = ty * 32 + tx;
+  const int jl = tid >> 3, kq = (tid & 7) * 4;        // row j0 + jl, columns k0 + kq .. +3
+  const int j = j0 + jl;
+  const long long k = k0 + kq;
+  if (j >= nrows_pad || k >= K) return;
+  const int fj = j < N ? f[j] : 0;
+  const int sh = fj > -2000 ? 53 - fj : 0;          // all-zero column: f stays at its fill value
+  const double s1 = ldexp(1.0, sh / 2), s2 = ldexp(1.0, sh - sh / 2);
+  float fl[4][4];
+  uint32_t lowb[4];
 #pragma unroll
-      for (int l = 0; l < kNumMod; ++l) out[l * plane] = sym_res(mod_pos(b, l), l);
+  for (int q = 0; q < 4; ++q) {
+    const long long a = (j < N) ? __double2ll_rn(tile[kq + q][jl] * s1 * s2) : 0;
+    lowb[q] = (uint32_t)a;
+    fl[q][0] = u2f_small((uint32_t)a & 8191u);
+    fl[q][1] = u2f_small((uint32_t)(a >> 13) & 8191u);
+    fl[q][2] = u2f_small((uint32_t)(a >> 26) & 8191u);
+    fl[q][3] = u2f_small((uint32_t)((a >> 39) + 16384)) - 16384.0f;
+  }
+  int8_t* out = r + (long long)j * ldr + k;
+  const bool full4 = k + 3 < K;
+  uint32_t w = pack4(lowb[0], lowb[1], lowb[2], lowb[3]);
+  if (full4) *reinterpret_cast<uint32_t*>(out) = w;
+  else for (int q = 0; k + q < K; ++q) out[q] = (int8_t)(w >> (8 * q));
+#pragma unroll
+  for (int l = 1; l < kNumMod; ++l) {
+    const float m = c_modf[l], rm = c_rmodf[l];
+    const float p1 = c_pow13f[1][l], p2 = c_pow13f[2][l], p3 = c_pow13f[3][l];
+    const uint32_t nmi = c_nmod[l];
+    uint32_t bq[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float sacc = fmaf(fl[q][3], p3, fmaf(fl[q][2], p2, fmaf(fl[q][1], p1, fl[q][0])));
+      if (l == 1) {
+        float rr = sym_mod_f(sacc, m, rm);
+        rr = rr > 127.5f ? rr - m : rr;
+        bq[q] = low_bits(rr);
+      } else {
+        bq[q] = __float_as_uint(fmaf(sacc, rm, kMagic)) * nmi + __float_as_uint(sacc + kMagic);
+      }
     }
+    w = pack4(bq[0], bq[1], bq[2], bq[3]);
+    if (full4) *reinterpret_cast<uint32_t*>(out + l * plane) = w;
+    else for (int q = 0; k + q < K; ++q) out[l * plane + q] = (int8_t)(w >> (8 * q));
   }
 }
 
