@@ -33,6 +33,21 @@ namespace oz {
 constexpr int kNumMod = 16;
 constexpr int kMods[kNumMod] = {256, 255, 253, 251, 247, 241, 239, 233,
                                 229, 227, 223, 217, 211, 199, 197, 193};
+// compile-time modulus tables: inside the residue loops l is a template constant, so
+// the limb weights, 1/m and −m become instruction immediates (FFMA immediate form
+// issues at twice the rate of the constant-bank form on the fma pipe)
+__host__ __device__ constexpr int mod_at(int l) {
+  return l == 0 ? 256 : l == 1 ? 255 : l == 2 ? 253 : l == 3 ? 251 : l == 4 ? 247 : l == 5 ? 241 :
+         l == 6 ? 239 : l == 7 ? 233 : l == 8 ? 229 : l == 9 ? 227 : l == 10 ? 223 : l == 11 ? 217 :
+         l == 12 ? 211 : l == 13 ? 199 : l == 14 ? 197 : 193;
+}
+__host__ __device__ constexpr float pow13_sym(int l, int t) {   // 2^(13t) mod m in (−m/2, m/2]
+  long long v = 1;
+  for (int i = 0; i < t; ++i) v = (v * 8192) % mod_at(l);
+  return (float)(v > mod_at(l) / 2 ? v - mod_at(l) : v);
+}
+static_assert(mod_at(15) == 193, "modulus table");
+
 __constant__ int c_mod[kNumMod];
 __constant__ double c_rmod[kNumMod];        // 1 / m
 __constant__ float c_rmodf[kNumMod];        // 1 / m (fp32) for small non-negative operands
@@ -117,6 +132,34 @@ __global__ void col_exp_kernel(const double* __restrict__ p, long long rows, int
 }
 
 // ---- residues of a row-scaled matrix: R[ℓ][i][k] (int8), ld ldr bytes ---------------
+template <int L>
+PSD_DEVINL void res_limb_store8(const float (&f)[8][4], int8_t* out, long long plane) {
+  constexpr float m = (float)mod_at(L), rm = 1.0f / (float)mod_at(L);
+  constexpr float p1 = pow13_sym(L, 1), p2 = pow13_sym(L, 2), p3 = pow13_sym(L, 3);
+  constexpr uint32_t nmi = 0u - (uint32_t)mod_at(L);
+  uint32_t b[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float sacc = fmaf(f[q][3], p3, fmaf(f[q][2], p2, fmaf(f[q][1], p1, f[q][0])));
+    if constexpr (L == 1) {   // m = 255: |r| can reach 128 — fold into int8 range
+      float rr = sym_mod_f(sacc, m, rm);
+      rr = rr > 127.5f ? rr - m : rr;
+      b[q] = low_bits(rr);
+    } else {                  // |r| ≤ 0.503·m ≤ 127
+      b[q] = __float_as_uint(fmaf(sacc, rm, kMagic)) * nmi + __float_as_uint(sacc + kMagic);
+    }
+  }
+  *reinterpret_cast<uint2*>(out + L * plane) =
+      make_uint2(pack4(b[0], b[1], b[2], b[3]), pack4(b[4], b[5], b[6], b[7]));
+}
+template <int L>
+PSD_DEVINL void res_limb_all(const float (&f)[8][4], int8_t* out, long long plane) {
+  if constexpr (L < kNumMod) {
+    res_limb_store8<L>(f, out, plane);
+    res_limb_all<L + 1>(f, out, plane);
+  }
+}
+
 __global__ void __launch_bounds__(256) residues_rows_kernel(const double* __restrict__ x, long long rows,
                                                           long long cols, long long ldx, int* __restrict__ e,
                                                           int8_t* __restrict__ r, long long ldr,
@@ -172,26 +215,7 @@ __global__ void __launch_bounds__(256) residues_rows_kernel(const double* __rest
       int8_t* out = orow + 8 * k8;
       *reinterpret_cast<uint2*>(out) =
           make_uint2(pack4(lowb[0], lowb[1], lowb[2], lowb[3]), pack4(lowb[4], lowb[5], lowb[6], lowb[7]));
-#pragma unroll
-      for (int l = 1; l < kNumMod; ++l) {
-        out += plane;
-        const float m = c_modf[l], rm = c_rmodf[l];
-        const float p1 = c_pow13f[1][l], p2 = c_pow13f[2][l], p3 = c_pow13f[3][l];
-        const uint32_t nmi = c_nmod[l];   // −m (mod 2^32)
-        uint32_t b[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float sacc = fmaf(f[q][3], p3, fmaf(f[q][2], p2, fmaf(f[q][1], p1, f[q][0])));
-          if (l == 1) {   // m = 255: |r| can reach 128 — fold into int8 range
-            float rr = sym_mod_f(sacc, m, rm);
-            rr = rr > 127.5f ? rr - m : rr;
-            b[q] = low_bits(rr);
-          } else {        // |r| ≤ 0.503·m ≤ 127
-            b[q] = __float_as_uint(fmaf(sacc, rm, kMagic)) * nmi + __float_as_uint(sacc + kMagic);
-          }
-        }
-        *reinterpret_cast<uint2*>(out) = make_uint2(pack4(b[0], b[1], b[2], b[3]), pack4(b[4], b[5], b[6], b[7]));
-      }
+      res_limb_all<1>(f, out, plane);
     }
   }
 }
