@@ -297,6 +297,19 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
   double hs[4];
   for (int pass = 0; pass < 10; ++pass) {
     PSD_TRY(panel_tn(p, bufs[cur], bufs[cur], ld, n, w, p->G, true, st));
+    if (unshifted_run >= 2) {
+      // verification Gram after two unshifted passes: accept if ‖QᵀQ − I‖_max small
+      // (checked before factoring it, so an accepted basis costs no third Cholesky)
+      psd::identity_defect(p->G, w, w, p->scal + 3, st);
+      double dev = 0.0;
+      PSD_CUDA_CHECK(cudaMemcpyAsync(&dev, p->scal + 3, sizeof(double), cudaMemcpyDeviceToHost, st),
+                     "orthogonality defect");
+      PSD_TRY(sync(st, "orthogonality defect"));
+      if (dev <= 1e-13 * std::max(1, w)) {
+        verified = true;
+        break;
+      }
+    }
     if (psd::chol_fast(p->G, w, w, 0.0, p->L, w, p->Rinv, w, p->dinv, p->qrstat, st) != 0)
       return fail(PSD_ERR_INVALID_PARAMS, "width %d too large for the CholeskyQR kernel", w);
     PSD_CUDA_CHECK(cudaMemcpyAsync(hs, p->qrstat, sizeof(hs), cudaMemcpyDeviceToHost, st), "qr status");
@@ -311,18 +324,6 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
       }
     }
     if (!std::isfinite(trace)) return fail(PSD_ERR_CONVERGENCE, "non-finite Gram matrix in QR");
-    if (unshifted_run >= 2) {
-      // verification Gram of an ill-conditioned input: accept if ‖QᵀQ − I‖_max small
-      psd::identity_defect(p->G, w, w, p->scal + 3, st);
-      double dev = 0.0;
-      PSD_CUDA_CHECK(cudaMemcpyAsync(&dev, p->scal + 3, sizeof(double), cudaMemcpyDeviceToHost, st),
-                     "orthogonality defect");
-      PSD_TRY(sync(st, "orthogonality defect"));
-      if (dev <= 1e-13 * std::max(1, w)) {
-        verified = true;
-        break;
-      }
-    }
     const bool bad = hs[0] != 0.0 || !std::isfinite(hs[2]) || !std::isfinite(hs[3]);
     const double kest = (hs[2] > 0.0) ? hs[3] / hs[2] : INFINITY;
     if (pass == 0) kest0 = kest;
