@@ -302,7 +302,7 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
       // (checked before factoring it, so an accepted basis costs no third Cholesky)
       psd::identity_defect(p->G, w, w, p->scal + 3, st);
       double dev = 0.0;
-      PSD_CUDA_CHECK(cudaMemcpyAsync(&dev, p->scal + 3, sizeof(double), cudaMemcpyDeviceToHost, st),
+      PSD_CUDA_CHECK(psd::read_small(&dev, p->scal + 3, sizeof(double), st),
                      "orthogonality defect");
       PSD_TRY(sync(st, "orthogonality defect"));
       if (dev <= 1e-13 * std::max(1, w)) {
@@ -312,7 +312,7 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
     }
     if (psd::chol_fast(p->G, w, w, 0.0, p->L, w, p->Rinv, w, p->dinv, p->qrstat, st) != 0)
       return fail(PSD_ERR_INVALID_PARAMS, "width %d too large for the CholeskyQR kernel", w);
-    PSD_CUDA_CHECK(cudaMemcpyAsync(hs, p->qrstat, sizeof(hs), cudaMemcpyDeviceToHost, st), "qr status");
+    PSD_CUDA_CHECK(psd::read_small(hs, p->qrstat, sizeof(hs), st), "qr status");
     PSD_TRY(sync(st, "cholesky"));
     const double trace = hs[1];
     if (pass == 0) {
@@ -332,7 +332,7 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
       // Fukaya et al. shifted CholeskyQR: s = 11(mn + n(n+1))·u·‖Y‖²
       const double s = 11.0 * ((double)n * w + (double)w * (w + 1)) * u * trace;
       psd::chol_fast(p->G, w, w, s, p->L, w, p->Rinv, w, p->dinv, p->qrstat, st);
-      PSD_CUDA_CHECK(cudaMemcpyAsync(hs, p->qrstat, sizeof(hs), cudaMemcpyDeviceToHost, st),
+      PSD_CUDA_CHECK(psd::read_small(hs, p->qrstat, sizeof(hs), st),
                      "qr status");
       PSD_TRY(sync(st, "shifted cholesky"));
       if (hs[0] != 0.0)
@@ -365,7 +365,7 @@ int symcheck(psd_plan* p, const double* x, ll n, ll ldx, SymInfo* si, cudaStream
     psd::sym_stats(x, n, ldx, p->stats, st);
   }
   double h[3];
-  PSD_CUDA_CHECK(cudaMemcpyAsync(h, p->stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st),
+  PSD_CUDA_CHECK(psd::read_small(h, p->stats, 3 * sizeof(double), st),
                  "stats");
   PSD_TRY(sync(st, "symmetry check"));
   int flags = 0;
@@ -411,7 +411,7 @@ int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* o
     return PSD_OK;
   }
   std::vector<double> rd(w);
-  PSD_CUDA_CHECK(cudaMemcpyAsync(rd.data(), p->rdiag, w * sizeof(double), cudaMemcpyDeviceToHost, st),
+  PSD_CUDA_CHECK(psd::read_small(rd.data(), p->rdiag, w * sizeof(double), st),
                  "rdiag");
   PSD_TRY(sync(st, "rdiag"));
   std::vector<int> keep;
@@ -546,8 +546,8 @@ static int power_iteration_impl(psd_plan* p, const double* x, ll n, ll ldx, doub
   psd::sum_partials(p->gpart, nb, p->scal + 1, 1, st);
   double h[2];
   int hflag = 0;
-  PSD_CUDA_CHECK(cudaMemcpyAsync(h, p->scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "pi");
-  PSD_CUDA_CHECK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "pi flag");
+  PSD_CUDA_CHECK(psd::read_small(h, p->scal, 2 * sizeof(double), st), "pi");
+  PSD_CUDA_CHECK(psd::read_small(&hflag, flag, sizeof(int), st), "pi flag");
   PSD_TRY(sync(st, "power iteration"));
   *result = hflag ? 0.0 : h[1];
   return PSD_OK;
@@ -763,7 +763,7 @@ int symcheck32(psd_plan* p, const float* x, ll n, ll ldx, bool raw, SymInfo* si,
     psd::symsplit_f32(x, n, ldx, p->stats, raw ? nullptr : p->xh, p->xl, p->ldx32, st);
   }
   double h[3];
-  PSD_CUDA_CHECK(cudaMemcpyAsync(h, p->stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st),
+  PSD_CUDA_CHECK(psd::read_small(h, p->stats, 3 * sizeof(double), st),
                  "stats");
   PSD_TRY(sync(st, "symmetry check"));
   int flags = 0;
@@ -912,7 +912,7 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   psd::sort_eigs(p->vals, p->V, wk, wk, offset, p->vals_sorted, p->U, wk, p->ints + p->w,
                  p->ints, st);
   int npos = 0;
-  PSD_CUDA_CHECK(cudaMemcpyAsync(&npos, p->ints + p->w, sizeof(int), cudaMemcpyDeviceToHost, st),
+  PSD_CUDA_CHECK(psd::read_small(&npos, p->ints + p->w, sizeof(int), st),
                  "npos");
   PSD_TRY(sync(st, "eigh"));
   eig_mark.close();
@@ -998,8 +998,7 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
                    "resid partials");
     psd::gemm_f64(op, p->ws, p->ws_elems, st);
     psd::sum_partials(p->rpart, psd::gemm_resid_ctas(op), p->scal + 2, 1, st);
-    PSD_CUDA_CHECK(cudaMemcpyAsync(&r.residual_frob, p->scal + 2, sizeof(double),
-                                   cudaMemcpyDeviceToHost, st),
+    PSD_CUDA_CHECK(psd::read_small(&r.residual_frob, p->scal + 2, sizeof(double), st),
                    "residual");
   }
   PSD_TRY(sync(st, "ran_proj"));

@@ -609,8 +609,7 @@ int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long
     return -3;
   count_launch();
   int out[2] = {0, 0};
-  cudaMemcpyAsync(out, A.out, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
-  cudaStreamSynchronize(st);
+  read_small(out, A.out, 2 * sizeof(int), st);
   jacobi_diag_kernel<<<(m + 255) / 256, 256, 0, st>>>(a, lda, ws, m, A.out, values);
   count_launch();
   if (out[1]) copy_matrix(ws, m, a, lda, m, m, st);

@@ -3,6 +3,7 @@
 // split-K reduction and small panel utilities.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "launch.h"
 
@@ -575,6 +576,44 @@ void set_identity(double* a, long long ld, int m, cudaStream_t st) {
   const int blocks = (int)std::min<long long>((total + 255) / 256, 4096);
   set_identity_kernel<<<blocks, 256, 0, st>>>(a, ld, m);
   count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// Small device→host status reads through a kernel storing into host-mapped
+// pinned memory instead of cudaMemcpy: device→host DMA copies share the copy
+// engine with any big transfer in flight on other streams (ran_proj_many's
+// 8.6 GB downloads), and a status read queued behind one waits for all of it.
+// ---------------------------------------------------------------------------
+__global__ void copy_to_mapped_kernel(unsigned char* __restrict__ dst, const unsigned char* __restrict__ src,
+                                      size_t bytes) {
+  for (size_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t read_small(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t st) {
+  constexpr size_t kCap = 64 << 10;
+  struct Staging {
+    unsigned char* h = nullptr;
+    unsigned char* d = nullptr;
+  };
+  thread_local Staging stage[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Staging& sg = stage[dev & 15];
+  if (bytes > kCap) {   // not a status read: plain copy
+    cudaError_t e = cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, st);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(st);
+  }
+  if (!sg.h) {
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&sg.h), kCap, cudaHostAllocMapped);
+    if (e != cudaSuccess) return e;
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&sg.d), sg.h, 0);
+    if (e != cudaSuccess) return e;
+  }
+  copy_to_mapped_kernel<<<1, 256, 0, st>>>(sg.d, static_cast<const unsigned char*>(dev_src), bytes);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return e;
+  std::memcpy(host_dst, sg.h, bytes);
+  return cudaGetLastError();
 }
 
 }  // namespace psd

@@ -89,6 +89,9 @@ struct OzOp {
   long long lds = 0;
   cudaEvent_t ev_gemm[2] = {nullptr, nullptr};   // optional: recorded around the INT8 kernel
 };
+// device→host read of a few status bytes that does not queue behind DMA copies
+// (kernel store into host-mapped memory, then a stream sync); > 64 KB: cudaMemcpy
+cudaError_t read_small(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t st);
 int oz_num_moduli();
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
                      long long ldr, cudaStream_t st);
