@@ -405,6 +405,7 @@ template <bool AMN>
 __global__ void __launch_bounds__(kThreads, 1)
     tc32_gemm2_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                       const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
+                      const __grid_constant__ CUtensorMap mBh2, const __grid_constant__ CUtensorMap mBl2,
                       const Params p) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], acc_bar;
@@ -412,8 +413,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
-  const int bn_tot = p.bn * p.n_mma;
-  const int hb = p.bn / 2;                       // B rows per CTA per MMA
+  const bool two = p.n_mma > 1;
+  const int bn_tot = p.bn + (two ? p.bn2 : 0);   // e.g. 272 = 144 + 128: no padded columns
+  const int hb = p.bn / 2, hb2 = p.bn2 / 2;      // B rows per CTA for the first / second MMA
   int u = blockIdx.x >> 1;
   const int ng = u % p.n_groups;
   u /= p.n_groups;
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t sbase = (sraw + 1023u) & ~1023u;
-  const uint32_t a_bytes = BM * SWZ, b_bytes = (uint32_t)p.n_mma * hb * SWZ;
+  const uint32_t a_bytes = BM * SWZ, b_bytes = (uint32_t)(hb + (two ? hb2 : 0)) * SWZ;
   const uint32_t st_bytes = 2 * a_bytes + 2 * b_bytes;
   const uint32_t tcols = tmem_cols_for(bn_tot);
 
@@ -479,11 +481,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d_pair(sA, &mAh, kc, m0, fb);
           tma_load_2d_pair(sA + a_bytes, &mAl, kc, m0, fb);
         }
-        for (int h = 0; h < p.n_mma; ++h) {
-          const uint32_t off = (uint32_t)h * hb * SWZ;
-          const int nrow = n0 + h * p.bn + (int)rank * hb;
-          tma_load_2d_pair(sB + off, &mBh, kc, nrow, fb);
-          tma_load_2d_pair(sB + b_bytes + off, &mBl, kc, nrow, fb);
+        {
+          const int nrow = n0 + (int)rank * hb;
+          tma_load_2d_pair(sB, &mBh, kc, nrow, fb);
+          tma_load_2d_pair(sB + b_bytes, &mBl, kc, nrow, fb);
+        }
+        if (two) {
+          const uint32_t off = (uint32_t)hb * SWZ;
+          const int nrow = n0 + p.bn + (int)rank * hb2;
+          tma_load_2d_pair(sB + off, &mBh2, kc, nrow, fb);
+          tma_load_2d_pair(sB + b_bytes + off, &mBl2, kc, nrow, fb);
         }
       }
       __syncwarp();
@@ -499,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dbl = smem_desc(sbase + 2 * a_bytes + b_bytes);
       constexpr uint32_t a_kstep = (AMN ? 1024u : 32u) >> 4, b_kstep = 32u >> 4;
       const uint32_t b_half = (uint32_t)(hb * SWZ) >> 4;
-      const bool two = p.n_mma > 1;
+      const uint32_t idesc2 = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(p.bn2 >> 3) << 17);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % p.stages;
         const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
@@ -517,9 +524,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_tf32_pair(tmem, ah, bh0, idesc, 1u);
             if (two) {
               const uint32_t d1 = tmem + (uint32_t)p.bn;
-              mma_tf32_pair(d1, al, bh0 + b_half, idesc, acc0);
-              mma_tf32_pair(d1, ah, bl0 + b_half, idesc, 1u);
-              mma_tf32_pair(d1, ah, bh0 + b_half, idesc, 1u);
+              mma_tf32_pair(d1, al, bh0 + b_half, idesc2, acc0);
+              mma_tf32_pair(d1, ah, bl0 + b_half, idesc2, 1u);
+              mma_tf32_pair(d1, ah, bh0 + b_half, idesc2, 1u);
             }
           }
           mma_commit_pair(smem_u32(&empty_bar[s]));   // frees slot s in both CTAs
@@ -1103,7 +1110,11 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
   } else {
     p.n_mma = n_tot > 256 ? 2 : 1;
     p.bn = (n_tot / p.n_mma + 15) / 16 * 16;
-    n_tot = p.bn * p.n_mma;
+    p.bn2 = p.bn;
+    const bool pair_split = op.mode == PARTIAL && p.n_mma == 2 &&
+                            !(getenv("PSD_TC32_PAIR") && getenv("PSD_TC32_PAIR")[0] == '0');
+    if (pair_split) p.bn2 = n_tot - p.bn;            // unequal halves, no padded columns (272 = 144 + 128)
+    n_tot = p.bn + (p.n_mma > 1 ? p.bn2 : 0);
   }
   p.n_groups = (op.N + n_tot - 1) / n_tot;
   p.m_tiles = (op.M + BM - 1) / BM;
@@ -1161,7 +1172,8 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     p.nprod = e ? std::max(1, std::min(3, atoi(e))) : 3;
   }
   const int sb = ts ? 2 * BM * sw + (256 + p.bn) * sw
-                    : (pair ? 2 * BM * sw + p.bn * p.n_mma * sw : 2 * BM * sw + 2 * p.bn * p.n_mma * sw);
+                    : (pair ? 2 * BM * sw + (p.bn + (p.n_mma > 1 ? p.bn2 : 0)) * sw
+                            : 2 * BM * sw + 2 * p.bn * p.n_mma * sw);
   const int epi_bytes = op.mode == MIRROR ? kMirrorEpi * 32 * 33 * 4 : 0;   // epilogue transpose tiles
   const int avail = (int)device_info().max_smem - 1024 - 2048 - epi_bytes;
   p.stages = std::min(8, avail / sb);
@@ -1180,6 +1192,10 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     ok = map_f32(&mah, op.a_hi, op.K, op.M, op.lda, BM, sw) && map_f32(&mal, op.a_lo, op.K, op.M, lda_lo, BM, sw);
   }
   ok = ok && map_f32(&mbh, op.b_hi, op.K, op.N, op.ldb, brows, sw) && map_f32(&mbl, op.b_lo, op.K, op.N, op.ldb, brows, sw);
+  CUtensorMap mbh2 = mbh, mbl2 = mbl;
+  if (pair && p.n_mma > 1 && p.bn2 != p.bn)
+    ok = ok && map_f32(&mbh2, op.b_hi, op.K, op.N, op.ldb, p.bn2 / 2, sw) &&
+         map_f32(&mbl2, op.b_lo, op.K, op.N, op.ldb, p.bn2 / 2, sw);
   if (!ok) return -5;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1239,8 +1255,9 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t le = amn ? cudaLaunchKernelEx(&cfg, tc32_gemm2_kernel<true>, mah, mal, mbh, mbl, p)
-                               : cudaLaunchKernelEx(&cfg, tc32_gemm2_kernel<false>, mah, mal, mbh, mbl, p);
+    const cudaError_t le =
+        amn ? cudaLaunchKernelEx(&cfg, tc32_gemm2_kernel<true>, mah, mal, mbh, mbl, mbh2, mbl2, p)
+            : cudaLaunchKernelEx(&cfg, tc32_gemm2_kernel<false>, mah, mal, mbh, mbl, mbh2, mbl2, p);
     if (le != cudaSuccess) return -6;
   } else {
     static size_t attr64[16] = {}, attr128[16] = {};

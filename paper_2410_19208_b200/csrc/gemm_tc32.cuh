@@ -34,6 +34,7 @@ enum Mode { PARTIAL = 0, MIRROR = 1 };
 struct Params {
   int M, N, K;
   int bn, n_mma;        // N per MMA (multiple of 16, ≤ 256), MMAs per k-step along N (1–2)
+  int bn2;              // CTA-pair kernel: N of the second MMA (n_mma = 2), may differ from bn
   int kblocks, kb_per_split;
   int m_tiles, n_groups, splits;
   int stages;
