@@ -43,6 +43,7 @@ struct JacobiArgs {
   double* jbuf;     // P × kJS²
   double* sbuf;     // P × kJS²
   int* counters;    // per-sweep rotation counts (zeroed)
+  unsigned long long* maxoff;   // per sweep: max |a_ij|, i ≠ j, after its last round (double bits, zeroed)
   int* flags;       // dataflow flags: sflag[P], aflag[P²], vflag[P·vch], jread[2P] (zeroed)
   double* norm;     // [0] = ‖A‖_F
   int* out;         // [0] = sweeps (or −1), [1] = 1 if result is in b
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
   double* X = sm + 4 * kJTile;
   __shared__ int ia[kJS], ib[kJS];
   __shared__ int stop_flag;
+  __shared__ double red8[kJT / 32];
   const int m = A.m, nblk = A.nblk, P = nblk / 2, rounds = nblk - 1;
   const int vch = (m + 2 * kJS - 1) / (2 * kJS);       // 64-row V chunks
   const int ntask = P + P * P + P * vch;
@@ -359,6 +361,8 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
           __syncthreads();
           const long long tw1 = clock64();
           double c[2][2];
+          const bool last = (r == rounds - 1);
+          double lmax = 0.0;
           if (pa == pb) {
             const double* Sp = Sslot + (size_t)pa * kJS * kJS;
             constexpr int NS = kJS * kJS / kJT;
@@ -368,7 +372,10 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
 #pragma unroll
             for (int u = 0; u < NS; ++u) {
               const int e = tid + u * kJT, gi = ia[e / kJS], gj = ib[e % kJS];
-              if (gi < m && gj < m) nxt[(long long)gi * ldn + gj] = vs[u];
+              if (gi < m && gj < m) {
+                nxt[(long long)gi * ldn + gj] = vs[u];
+                if (gi != gj) lmax = fmax(lmax, fabs(vs[u]));
+              }
             }
           } else {
             const double* Ja = Jslot + (size_t)pa * kJS * kJS;
@@ -410,11 +417,23 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
                 int row, col;
                 mm32_coord(j, e, row, col);
                 const int gi = ia[row], gj = ib[col];
-                if (gi < m && gj < m) nxt[(long long)gi * ldn + gj] = c[j][e];
+                if (gi < m && gj < m) {
+                  nxt[(long long)gi * ldn + gj] = c[j][e];
+                  lmax = fmax(lmax, fabs(c[j][e]));   // pa ≠ pb: all entries off-diagonal
+                }
               }
+          }
+          if (last) {
+            lmax = warp_max(lmax);
+            if ((tid & 31) == 0) red8[tid >> 5] = lmax;
           }
           __syncthreads();
           if (tid == 0) {
+            if (last) {
+              double bm = 0.0;
+              for (int w = 0; w < kJT / 32; ++w) bm = fmax(bm, red8[w]);
+              if (bm > 0.0) atomicMax(&A.maxoff[sweep], (unsigned long long)__double_as_longlong(bm));
+            }
             atomicAdd(&jread[(R & 1) * P + pa], 1);
             if (pb != pa) atomicAdd(&jread[(R & 1) * P + pb], 1);
             flag_set(&aflag[pa * P + pb], R + 1);
@@ -490,7 +509,16 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
     const int Rlast = sweep * rounds + rounds - 1;
     if (tid == 0) {
       for (int p = 0; p < P; ++p) flag_wait(&sflag[p], Rlast + 1);
-      stop_flag = (*((volatile int*)&A.counters[sweep]) == 0);
+      const int rots = *((volatile int*)&A.counters[sweep]);
+      int stop = rots == 0;
+      if (!stop && rots <= 2 * m) {   // nearly converged: worth waiting for the last A-items
+        // every off-diagonal entry already at or below the rotation threshold: the
+        // next sweep would rotate nothing — stop now instead of running it
+        for (int q = 0; q < P * P; ++q) flag_wait(&aflag[q], Rlast + 1);
+        const double mo = __longlong_as_double((long long)*((volatile unsigned long long*)&A.maxoff[sweep]));
+        stop = mo <= abs_tol;
+      }
+      stop_flag = stop;
     }
     __syncthreads();
     if (stop_flag) {
@@ -545,7 +573,7 @@ size_t jacobi_ws_elems(int m) {
   int nblk, P;
   jacobi_geometry(m, nblk, P);
   return (size_t)m * m + (size_t)4 * P * kJS * kJS + 8 + kJacobiMaxSweeps + 8 +
-         (size_t)(jacobi_nflags(m, P) + 1) / 2 + 8;
+         (size_t)(jacobi_nflags(m, P) + 1) / 2 + 8 + kJacobiMaxSweeps + 1;
 }
 
 int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long long ldv,
@@ -573,6 +601,11 @@ int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long
   A.out = ints + kJacobiMaxSweeps + 2;
   A.flags = ints + kJacobiMaxSweeps + 8;
   const int nflags = jacobi_nflags(m, P);
+  {
+    const size_t int_words = (size_t)kJacobiMaxSweeps + 8 + nflags;
+    A.maxoff = reinterpret_cast<unsigned long long*>(A.norm + 8 + (int_words + 1) / 2 + 1);
+    cudaMemsetAsync(A.maxoff, 0, kJacobiMaxSweeps * sizeof(unsigned long long), st);
+  }
   A.m = m;
   A.nblk = nblk;
   A.max_sweeps = kJacobiMaxSweeps;
