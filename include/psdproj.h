@@ -73,6 +73,9 @@ typedef struct psd_report {
   double max_abs;          /* max|x_ij| (symmetric.py:51) */
   double sym_defect;       /* max|x_ij - x_ji| (symmetric.py:52) */
   double alpha_used;       /* alpha (ran_proj_scal) or 0 */
+  int32_t recon_engine;    /* reconstruction SYRK ran on: 0 FP64 DMMA (or 3xTF32 for FP32),
+                              1 INT8 tensor cores (Ozaki I digit slices, ozaki_syrk.cu) */
+  int32_t reserved0;
 } psd_report;
 
 /* Thread-local description of the last non-OK status. */
@@ -163,6 +166,15 @@ int psd_gemm_f64_int8_ws_bytes(int64_t m, int64_t n, int64_t k, int64_t chunk_ro
 int psd_gemm_f64_int8(const double* a, int64_t lda, const double* p, int64_t ldp, int64_t m, int64_t n,
                       int64_t k, double* c, int64_t ldc, double alpha, const double* s, int64_t lds,
                       void* ws, int64_t ws_bytes, int64_t chunk_rows, void* stream);
+
+/* Reconstruction X = W diag(d) W^T (projection.py:72-78, d > 0) on the INT8
+ * tensor cores (test entry, allocates its own scratch): V = W diag(sqrt d) split
+ * into 7 signed base-128 int8 digit planes per row-scaled 49-bit integer, the
+ * 28 digit products of level <= 6 accumulated exactly in s32 TMEM, levels
+ * combined in FP64; lower 128x32 tiles stored twice (bitwise-symmetric result).
+ * W n x r row-major (r <= 640), result n x n. */
+int psd_syrk_f64_int8(const double* w, int64_t ldw, const double* d, int64_t n, int32_t r,
+                      double* result, int64_t ldr, void* stream);
 
 /* The 3xTF32 tcgen05 GEMM itself (test entry; allocates its own scratch):
  * mode 0: C (fp64, m x n) = A · B^T; mode 1: mirrored fp32 C (m == n) from

@@ -24,7 +24,7 @@ INCLUDE = os.path.join(REPO, "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
-SOURCES = ["gemm_f64.cu", "gemm_tma.cu", "gemm_tc32.cu", "ozaki.cu", "kernels_misc.cu", "kernels_dense.cu", "jacobi.cu", "sdls_kernels.cu", "api.cu"]
+SOURCES = ["gemm_f64.cu", "gemm_tma.cu", "gemm_tc32.cu", "ozaki.cu", "ozaki_syrk.cu", "kernels_misc.cu", "kernels_dense.cu", "jacobi.cu", "sdls_kernels.cu", "api.cu"]
 
 
 def _nvcc():

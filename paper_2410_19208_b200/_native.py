@@ -37,6 +37,8 @@ class PsdReport(ctypes.Structure):
         ("max_abs", ctypes.c_double),
         ("sym_defect", ctypes.c_double),
         ("alpha_used", ctypes.c_double),
+        ("recon_engine", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
     ]
 
     def as_dict(self):
@@ -101,6 +103,9 @@ SIGNATURES = {
                                           ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                           ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                           ctypes.c_void_p]),
+    "psd_syrk_f64_int8": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                         ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+                                         ctypes.c_int64, ctypes.c_void_p]),
     "psd_gemm_tf32x3": (ctypes.c_int, [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
                                        ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,

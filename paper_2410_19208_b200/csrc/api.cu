@@ -858,6 +858,11 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   // (C1 n=1000: 606 vs 697 projections/s; n=2048 par; n=4096: 227 vs 205)
   const bool oz_size = n >= 3072 || (flags & PSD_FLAG_FP64_INT8);
   bool oz = !f32 && oz_on && oz_size && !(flags & PSD_FLAG_FP64_DMMA);
+  // reconstruction SYRK on the INT8 engine too (PSD_OZ_SYRK=0 keeps it on DMMA)
+  static const bool oz_syrk_on = [] {
+    const char* e = getenv("PSD_OZ_SYRK");
+    return !(e && e[0] == '0');
+  }();
   if (oz && ensure_oz(p) != PSD_OK) {   // no room for the residue planes: DMMA products
     cudaGetLastError();
     oz = false;
@@ -944,6 +949,13 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
       op.ldc32 = ldr;
       const int rr = psd::gemm_tf32x3(op, st);
       if (rr < 0) return fail(PSD_ERR_INVALID_PARAMS, "3xTF32 reconstruction rejected its operands (%d)", rr);
+    } else if (have_result && oz && oz_syrk_on && npos <= 640) {
+      // V = W·diag(√d) as 7 int8 digit planes, X̂₊ = V·Vᵀ from 28 exact slice products
+      // per K step on the INT8 tensor cores (Ozaki I, ozaki_syrk.cu); the X residue
+      // partials buffer is dead here and holds the planes.
+      const int rr = psd::oz_syrk(W, n, npos, ld, p->dvec, result64, ldr, p->oz_res, p->oz_res_elems, st);
+      if (rr < 0) return fail(PSD_ERR_INVALID_PARAMS, "INT8 reconstruction rejected its operands (%d)", rr);
+      r.recon_engine = 1;
     } else if (have_result) {
       psd::scale_columns(W, ld, p->dvec, WD, ld, n, npos, st);
       psd::GemmOp op;
@@ -1048,6 +1060,26 @@ int psd_ran_proj_f32(psd_plan* p, const float* x, int64_t n, int64_t ldx, const 
     cudaStreamSynchronize(st);
     collect_marks(p);
   }
+  return status;
+}
+
+int psd_syrk_f64_int8(const double* w, int64_t ldw, const double* d, int64_t n, int32_t r,
+                      double* result, int64_t ldr, void* stream) {
+  if (!w || !d || !result) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
+  if (n < 1 || r < 1 || r > 640 || ldw < r || ldr < n) return fail(PSD_ERR_INVALID_PARAMS, "bad syrk shape (r <= 640)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t bytes = psd::oz_syrk_ws_bytes(n, r);
+  void* ws = nullptr;
+  if (cudaMalloc(&ws, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PSD_ERR_NO_MEMORY, "syrk scratch allocation failed");
+  }
+  int status = PSD_OK;
+  const int rr = psd::oz_syrk(w, n, r, ldw, d, result, ldr, ws, bytes, st);
+  if (rr < 0) status = fail(PSD_ERR_INVALID_PARAMS, "INT8 SYRK rejected its operands (%d: %s)", rr, cudaGetErrorString(cudaGetLastError()));
+  if (status == PSD_OK) status = sync(st, "int8 syrk");
+  cudaStreamSynchronize(st);
+  cudaFree(ws);
   return status;
 }
 

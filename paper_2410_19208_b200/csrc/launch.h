@@ -102,6 +102,11 @@ size_t oz_stream_ws_bytes(long long m, long long n, long long k, long long chunk
 int oz_gemm_stream(const double* a, long long lda, const double* P, long long ldp, long long m, int n,
                    long long k, double* c, long long ldc, double alpha, const double* S, long long lds,
                    void* ws, size_t ws_bytes, long long chunk, cudaStream_t st);
+// X̂₊ = W·diag(d)·Wᵀ (n×n, bitwise symmetric) on the INT8 tensor cores (ozaki_syrk.cu);
+// W n×r (ld ldw), d[r] > 0; ws ≥ oz_syrk_ws_bytes(n, r).  0 ok, < 0 rejected.
+size_t oz_syrk_ws_bytes(long long n, int r);
+int oz_syrk(const double* w, long long n, int r, long long ldw, const double* d, double* c, long long ldc,
+            void* ws, size_t ws_bytes, cudaStream_t st);
 // Returns the K-split count used (≥ 1) or < 0 on error (−2 alignment, −3 workspace).
 int gemm_tf32x3(const Tc32Op& op, cudaStream_t st);
 long long tc32_ws_elems(long long M, int N, int max_splits);
