@@ -158,19 +158,23 @@ PSD_DEVINL void unit_tile(long long u, int& I, int& J) {
   J = (int)(u - 2LL * i * (i + 1));
 }
 
-template <int D>
+// AR (A resident): the D digit slices of the current 128-row block for ALL k-steps stay
+// in shared memory (nkb·28 KB) while the CTA walks that block's column tiles; only the
+// 7 KB B slices stream per k-step.  Otherwise A and B stream together per k-step.
+template <int D, bool AR>
 __global__ void __launch_bounds__(kThreads, 1)
     i8_syrk_kernel(const SyrkParams p) {
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], accf_bar[2], acce_bar[2];
+  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], accf_bar[2], acce_bar[2], afull_bar, aempty_bar;
   __shared__ uint32_t tmem_slot;
   constexpr uint32_t a_bytes = D * BM * KB, b_bytes = D * BN * KB;
-  constexpr uint32_t st_bytes = a_bytes + b_bytes;
+  constexpr uint32_t st_bytes = AR ? b_bytes : a_bytes + b_bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t sbase = (sraw + 1023u) & ~1023u;
   const long long u0 = p.units * blockIdx.x / gridDim.x, u1 = p.units * (blockIdx.x + 1) / gridDim.x;
   const int nkb = p.kblocks;
+  const uint32_t sring = AR ? sbase + (uint32_t)nkb * a_bytes : sbase;   // AR: A block first, then the B ring
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -181,6 +185,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&accf_bar[b]), 1);
       mbar_init(smem_u32(&acce_bar[b]), kEpi);
     }
+    mbar_init(smem_u32(&afull_bar), 1);
+    mbar_init(smem_u32(&aempty_bar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -196,10 +202,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = tmem_slot;
 
   if (warp == 0) {
-    int it = 0;
+    int it = 0, aload = 0, curI = -1;
     int I, J;
     unit_tile(u0, I, J);
     for (long long u = u0; u < u1; ++u) {
+      if (AR && I != curI) {
+        // the previous block's MMAs have all retired (aempty) → load this block's A slices
+        tc32::mbar_wait_t(smem_u32(&aempty_bar), ((uint32_t)aload & 1u) ^ 1u);
+        if (tc32::elect_one()) {
+          const uint32_t ab = smem_u32(&afull_bar);
+          mbar_expect_tx(ab, (uint32_t)nkb * a_bytes);
+          for (int kb = 0; kb < nkb; ++kb)
+            bulk_load(sbase + (uint32_t)kb * a_bytes, p.ta + ((long long)I * nkb + kb) * a_bytes, a_bytes, ab);
+        }
+        __syncwarp();
+        ++aload;
+        curI = I;
+      }
       for (int kb = 0; kb < nkb; ++kb, ++it) {
         const int s = it % p.stages;
         const uint32_t ph = (uint32_t)(it / p.stages) & 1u;
@@ -207,9 +226,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tc32::elect_one()) {
           const uint32_t fb = smem_u32(&full_bar[s]);
           mbar_expect_tx(fb, st_bytes);
-          const uint32_t sA = sbase + s * st_bytes;
-          bulk_load(sA, p.ta + ((long long)I * nkb + kb) * a_bytes, a_bytes, fb);
-          bulk_load(sA + a_bytes, p.tb + ((long long)J * nkb + kb) * b_bytes, b_bytes, fb);
+          const uint32_t sS = sring + s * st_bytes;
+          if (AR) {
+            bulk_load(sS, p.tb + ((long long)J * nkb + kb) * b_bytes, b_bytes, fb);
+          } else {
+            bulk_load(sS, p.ta + ((long long)I * nkb + kb) * a_bytes, a_bytes, fb);
+            bulk_load(sS + a_bytes, p.tb + ((long long)J * nkb + kb) * b_bytes, b_bytes, fb);
+          }
         }
         __syncwarp();
       }
@@ -219,9 +242,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    int it = 0, j = 0;
+    int it = 0, j = 0, aload = 0, curI = -1;
+    int I, J;
+    unit_tile(u0, I, J);
     for (long long u = u0; u < u1; ++u, ++j) {
       const int b = j & 1;
+      if (AR && I != curI) {
+        if (curI >= 0) {   // release the old A block once its MMAs retire
+          if (tc32::elect_one()) tc32::mma_commit(smem_u32(&aempty_bar));
+          __syncwarp();
+        }
+        tc32::mbar_wait_t(smem_u32(&afull_bar), (uint32_t)aload & 1u);
+        ++aload;
+        curI = I;
+      }
       tc32::mbar_wait_t(smem_u32(&acce_bar[b]), (((uint32_t)j >> 1) & 1u) ^ 1u);
       tc32::tc_fence_after();
       const uint32_t dbuf = tmem + (uint32_t)(b * kBufCols);
@@ -231,8 +265,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc32::mbar_wait_t(smem_u32(&full_bar[s]), ph);
         tc32::tc_fence_after();
         if (tc32::elect_one()) {
-          const uint32_t sA = sbase + s * st_bytes;
-          const uint64_t db = desc_sw32(sA + a_bytes);
+          const uint32_t sS = sring + s * st_bytes;
+          const uint32_t sA = AR ? sbase + (uint32_t)kb * a_bytes : sS;
+          const uint64_t db = desc_sw32(AR ? sS : sS + a_bytes);
 #pragma unroll
           for (int t = 0; t < D; ++t) {
             // kind::i8: D s32, A/B signed, K-major, M = 128, N = 32·(D − t)
@@ -244,6 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (kb == nkb - 1) tc32::mma_commit(smem_u32(&accf_bar[b]));
         }
         __syncwarp();
+      }
+      if (++J >= min(4 * (I + 1), p.nt)) {
+        ++I;
+        J = 0;
       }
     }
   } else {
@@ -381,18 +420,24 @@ int launch_syrk(const double* w, long long n, int r, long long ldw, const double
   p.rs = rs;
   p.cs = cs;
   p.vec = ((uintptr_t)c % 32 == 0 && ldc % 4 == 0) ? 1 : 0;
-  constexpr int st_bytes = D * (BM + BN) * KB;
-  p.stages = std::min(8, ((int)device_info().max_smem - 2048) / st_bytes);
-  const size_t smem = (size_t)p.stages * st_bytes + 1024;
-  static size_t attr[16] = {};
+  // A resident when the block's slices leave room for a ≥ 4-deep B ring
+  const int budget = (int)device_info().max_smem - 2048;
+  const int a_blk = p.kblocks * D * BM * KB, b_st = D * BN * KB;
+  static const bool ar_on = [] { const char* e = getenv("PSD_OZ_SYRK_AR"); return !(e && e[0] == '0'); }();
+  const bool ar = ar_on && a_blk + 4 * b_st <= budget;
+  const int st_bytes = ar ? b_st : D * (BM + BN) * KB;
+  p.stages = std::min(8, (budget - (ar ? a_blk : 0)) / st_bytes);
+  const size_t smem = (size_t)(ar ? a_blk : 0) + (size_t)p.stages * st_bytes + 1024;
+  auto kern = ar ? i8_syrk_kernel<D, true> : i8_syrk_kernel<D, false>;
+  static size_t attr[2][16] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (attr[dev] < smem) {
-    cudaFuncSetAttribute(i8_syrk_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[dev] = smem;
+  if (attr[ar][dev] < smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[ar][dev] = smem;
   }
   const int grid = (int)std::min<long long>(device_info().sms, p.units);
-  i8_syrk_kernel<D><<<grid, kThreads, smem, st>>>(p);
+  kern<<<grid, kThreads, smem, st>>>(p);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
 }

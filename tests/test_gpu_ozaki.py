@@ -173,6 +173,7 @@ def test_ran_proj_int8_engine_matches_dmma_and_oracle(ours, q):
     finally:
         ours.set_fp64_engine(prev)
     assert r8.device_info["sketch_engine"] == 1 and rd.device_info["sketch_engine"] == 0
+    assert r8.device_info["recon_engine"] == 1 and rd.device_info["recon_engine"] == 0
     ref = orc.ran_proj(x, 40, 8, q, rng=np.random.default_rng(5)).result
     for r in (r8, rd):
         assert np.linalg.norm(r.result - ref) / np.linalg.norm(ref) < 1e-10
