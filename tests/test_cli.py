@@ -69,7 +69,7 @@ def test_solve_rejects_exact_and_bad_problem(capsys, tmp_path):
 
 def test_fig4_beta_order_exit_2(capsys, tmp_path):
     code, _, err = _run(capsys, ["fig4", "--betas", "1,2,3,4", "--out", str(tmp_path / "f.csv")])
-    assert code == 2 and "β1 > β2" in _err(err)["message"]
+    assert code == 2 and "beta3 > beta1" in _err(err)["message"]
 
 
 @pytest.mark.gpu
@@ -123,7 +123,7 @@ def test_solve_tiny_problem(capsys, tmp_path):
 @pytest.mark.gpu
 def test_fig4_csv(capsys, tmp_path):
     out = tmp_path / "f.csv"
-    code, _, err = _run(capsys, ["fig4", "--n", "200", "--betas", "3,2,1,0.5", "--l", "5", "--q", "0",
+    code, _, err = _run(capsys, ["fig4", "--n", "200", "--betas", "3,1,6,2", "--l", "5", "--q", "0",
                                  "--k-grid", "20,40", "--trials", "1", "--seed", "1", "--out", str(out)])
     assert code == 0, err
     lines = out.read_text().splitlines()
