@@ -13,12 +13,22 @@ projected on the caller's stream.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
 from . import errors
 from .projection import ran_proj, ran_proj_scal, resolve_dtype
 from ._tensors import default_device
+
+
+# PSD_PIPE_STAGGER=1: start X_i's projection only after the download of X̂₊_{i−1}
+# finished (kept as an option; tools/probe_e2e.py at C3 on the B200 box, round 1:
+# staggered 3.62 projections/s, fully overlapped 4.70/s over 8 steps — both copy
+# directions then run at ≈45 GB/s each for the whole step and the 30 ms projection
+# hides under them).
+_STAGGER = os.environ.get("PSD_PIPE_STAGGER", "0") == "1"
 
 
 def _host_tensor(x, dtype):
@@ -83,12 +93,8 @@ def ran_proj_many(xs, params, rng, *, alpha=None, out=None, dtype=None, assume_s
         if i + 1 < len(hosts):
             upload(i + 1)                # overlaps the projection of X_i
         compute.wait_event(uploaded[s])
-        # Stagger: X_i is projected once the previous download finished, so each
-        # download overlaps only part of the next upload.  Measured on the B200 box
-        # (tools/probe_e2e.py): both 8.6 GB copies fully overlapped move ≈64 GB/s
-        # together, the staggered schedule ≈76 GB/s (4.3 vs 3.7 projections/s).
         prev = downloaded[(i - 1) % len(xbuf)] if i > 0 else None
-        if prev is not None:
+        if prev is not None and _STAGGER:
             compute.wait_event(prev)
         if downloaded[s] is not None:
             compute.wait_event(downloaded[s])

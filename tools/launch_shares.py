@@ -6,7 +6,9 @@ import sys
 
 path = sys.argv[1]
 title = sys.argv[2] if len(sys.argv) > 2 else path
-OURS = ("psd::", "tc32::", "oz::", "<unnamed>::")   # kernels of libpsdproj.so (workload generators excluded)
+OURS = ("psd::", "tc32::", "oz::", "ozs::", "<unnamed>::")   # kernels of libpsdproj.so
+# n×n symmetrize launches belong to the seeded workload generators (workloads.c3_device), not the projection
+EXCLUDE = ("psd::symmetrize_kernel",)
 with open(path) as f:
     lines = [l for l in f if l.startswith('"')]
 agg = collections.OrderedDict()
@@ -19,7 +21,7 @@ for r in csv.DictReader(lines):
     unit = r.get("Metric Unit", "ns")
     ms = v * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(unit, 1e-6)
     name = r["Kernel Name"].split("(")[0]
-    if not any(t in name for t in OURS) or name.startswith(("void at::", "at::")):
+    if not any(t in name for t in OURS) or name.startswith(("void at::", "at::")) or any(e in name for e in EXCLUDE):
         continue
     a = agg.setdefault(name, [0.0, 0])
     a[0] += ms
