@@ -73,9 +73,9 @@ __global__ void __launch_bounds__(256) syrk_slices_kernel(const double* __restri
     ei = mx > 0.0 ? ilogb(mx) + 1 : 0;
   }
   // X̂_ij = C·2^(e_i + e_j − 7D − 5), split as 2^(e_i − 32) · 2^(e_j − 7D + 27)
-  if (lane == 0 && i < (n + 7) / 8 * 8) {
+  if (lane == 0) {   // padded to the 128-row (rs) / 32-row (cs) tiles
     rs[i] = i < n ? ldexp(1.0, ei - 32) : 0.0;
-    cs[i] = i < n ? ldexp(1.0, ei - 7 * D + 27) : 0.0;
+    if (i < rows_b) cs[i] = i < n ? ldexp(1.0, ei - 7 * D + 27) : 0.0;
   }
   const double sc = ldexp(1.0, 7 * D - 1 - ei);
   const long long ia = i >> 7, ib = i >> 5;
@@ -111,8 +111,8 @@ struct SyrkParams {
   const int8_t* tb;   // pre-swizzled B tiles [J][kb][t][32][32]
   double* c;
   long long ldc;
-  const double* rs;   // 2^(e_i − 32)      (row scale)
-  const double* cs;   // 2^(e_j − 7D + 27) (column scale), padded to a multiple of 8
+  const double* rs;   // 2^(e_i − 32)      (row scale), padded to the 128-row tiles
+  const double* cs;   // 2^(e_j − 7D + 27) (column scale), padded to the 32-row tiles
   int stages;
   int vec;   // 1: C and ldc allow 32-byte row stores
 };
@@ -166,6 +166,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     i8_syrk_kernel(const SyrkParams p) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], accf_bar[2], acce_bar[2], afull_bar, aempty_bar;
+  // per-unit row / column scales, 4 slots filled by the producer with the unit's bulk copies
+  __shared__ __align__(8) uint64_t sfull_bar[4], sempty_bar[4];
+  __shared__ __align__(16) double s_rs[4][BM], s_cs[4][BN];
   __shared__ uint32_t tmem_slot;
   constexpr uint32_t a_bytes = D * BM * KB, b_bytes = D * BN * KB;
   constexpr uint32_t st_bytes = AR ? b_bytes : a_bytes + b_bytes;
@@ -185,6 +188,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&accf_bar[b]), 1);
       mbar_init(smem_u32(&acce_bar[b]), kEpi);
     }
+    for (int b = 0; b < 4; ++b) {
+      mbar_init(smem_u32(&sfull_bar[b]), 1);
+      mbar_init(smem_u32(&sempty_bar[b]), kEpi);
+    }
     mbar_init(smem_u32(&afull_bar), 1);
     mbar_init(smem_u32(&aempty_bar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -202,10 +209,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = tmem_slot;
 
   if (warp == 0) {
-    int it = 0, aload = 0, curI = -1;
+    int it = 0, aload = 0, curI = -1, j = 0;
     int I, J;
     unit_tile(u0, I, J);
-    for (long long u = u0; u < u1; ++u) {
+    for (long long u = u0; u < u1; ++u, ++j) {
+      {   // this unit's 128 row scales and 32 column scales → slot j mod 4
+        const int sb = j & 3;
+        tc32::mbar_wait_t(smem_u32(&sempty_bar[sb]), (((uint32_t)j >> 2) & 1u) ^ 1u);
+        if (tc32::elect_one()) {
+          const uint32_t sf = smem_u32(&sfull_bar[sb]);
+          mbar_expect_tx(sf, (BM + BN) * sizeof(double));
+          bulk_load(smem_u32(&s_rs[sb][0]), p.rs + (long long)I * BM, BM * sizeof(double), sf);
+          bulk_load(smem_u32(&s_cs[sb][0]), p.cs + (long long)J * BN, BN * sizeof(double), sf);
+        }
+        __syncwarp();
+      }
       if (AR && I != curI) {
         // the previous block's MMAs have all retired (aempty) → load this block's A slices
         tc32::mbar_wait_t(smem_u32(&aempty_bar), ((uint32_t)aload & 1u) ^ 1u);
@@ -293,9 +311,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     unit_tile(u0, I, J);
     int j = 0;
     for (long long u = u0; u < u1; ++u, ++j) {
-      const int b = j & 1;
+      const int b = j & 1, sb = j & 3;
       tc32::mbar_wait_t(smem_u32(&accf_bar[b]), ((uint32_t)j >> 1) & 1u);
       tc32::tc_fence_after();
+      tc32::mbar_wait_t(smem_u32(&sfull_bar[sb]), ((uint32_t)j >> 2) & 1u);
       const int ib = I * BM + quad * 32;
       const int i = ib + lane;
       const int jb = J * BN + slice * 16;
@@ -312,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld8(tmem + tq + (uint32_t)(b * kBufCols + L * BN + slice * 16 + 8 * g), v[g][L]);
         }
       }
+      const double si = s_rs[sb][quad * 32 + lane];
       if (active[0]) asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       // the accumulator is in registers: hand the TMEM buffer back before the math and stores
       tc32::tc_fence_before();
@@ -319,18 +339,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(smem_u32(&acce_bar[b]));
       const bool row_ok = i < p.n;
       const long long ldc = p.ldc;
-      const double si = p.rs[min(i, p.n - 1)];
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
         if (!active[g]) continue;
         const int j0 = jb + 8 * g;
-        double sj[8];
-        {
-          const double4* cs = reinterpret_cast<const double4*>(p.cs + j0);   // cs padded to 8
-          const double4 c0 = cs[0], c1 = cs[1];
-          sj[0] = c0.x; sj[1] = c0.y; sj[2] = c0.z; sj[3] = c0.w;
-          sj[4] = c1.x; sj[5] = c1.y; sj[6] = c1.z; sj[7] = c1.w;
-        }
+        const double* sj = &s_cs[sb][slice * 16 + 8 * g];   // broadcast smem reads
         double val[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -365,6 +378,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j0 + q < jl2) dst[q] = val[q];
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&sempty_bar[sb]));   // scale slot read
       if (++J >= min(4 * (I + 1), p.nt)) {
         ++I;
         J = 0;
@@ -402,13 +417,12 @@ int launch_syrk(const double* w, long long n, int r, long long ldw, const double
   p.mt = (int)((n + BM - 1) / BM);
   p.nt = (int)((n + BN - 1) / BN);
   const size_t ta_bytes = (size_t)p.mt * p.kblocks * D * BM * KB, tb_bytes = (size_t)p.nt * p.kblocks * D * BN * KB;
-  const size_t n8 = (size_t)(n + 7) / 8 * 8;
-  if (ws_bytes < ta_bytes + tb_bytes + 2 * n8 * sizeof(double) || (uintptr_t)ws % 256) return -3;
+  const long long rows_a = (long long)p.mt * BM, rows_b = (long long)p.nt * BN;
+  if (ws_bytes < ta_bytes + tb_bytes + (size_t)(rows_a + rows_b) * sizeof(double) || (uintptr_t)ws % 256) return -3;
   int8_t* ta = static_cast<int8_t*>(ws);
   int8_t* tb = ta + ta_bytes;
   double* rs = reinterpret_cast<double*>(tb + tb_bytes);
-  double* cs = rs + n8;
-  const long long rows_a = (long long)p.mt * BM, rows_b = (long long)p.nt * BN;
+  double* cs = rs + rows_a;
   syrk_slices_kernel<D><<<(unsigned)((rows_a + 7) / 8), 256, 0, st>>>(w, n, r, ldw, d, ta, tb, p.kblocks, rows_a,
                                                                        rows_b, rs, cs);
   count_launch();
@@ -447,7 +461,7 @@ int launch_syrk(const double* w, long long n, int r, long long ldw, const double
 size_t oz_syrk_ws_bytes(long long n, int r) {
   const size_t kb = (size_t)(r + 31) / 32;
   const size_t rows_a = (size_t)(n + 127) / 128 * 128, rows_b = (size_t)(n + 31) / 32 * 32;
-  return 7 * kb * 32 * (rows_a + rows_b) + 2 * (size_t)((n + 7) / 8 * 8) * sizeof(double);
+  return 7 * kb * 32 * (rows_a + rows_b) + (rows_a + rows_b) * sizeof(double);
 }
 
 // C (n×n) = W·diag(d)·Wᵀ, all d > 0, written as a bitwise-symmetric matrix.
