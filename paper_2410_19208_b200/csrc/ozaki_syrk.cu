@@ -435,7 +435,9 @@ int launch_syrk(const double* w, long long n, int r, long long ldw, const double
   p.cs = cs;
   p.vec = ((uintptr_t)c % 32 == 0 && ldc % 4 == 0) ? 1 : 0;
   // A resident when the block's slices leave room for a ≥ 4-deep B ring
-  const int budget = (int)device_info().max_smem - 2048;
+  // dynamic budget: opt-in maximum minus the kernel's static shared memory (barriers, scale
+  // slots ≈ 5.4 KB) and the 1 KB alignment slack
+  const int budget = (int)device_info().max_smem - 8192;
   const int a_blk = p.kblocks * D * BM * KB, b_st = D * BN * KB;
   static const bool ar_on = [] { const char* e = getenv("PSD_OZ_SYRK_AR"); return !(e && e[0] == '0'); }();
   const bool ar = ar_on && a_blk + 4 * b_st <= budget;

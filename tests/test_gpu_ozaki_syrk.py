@@ -56,7 +56,8 @@ def _check(w, d, c):
 
 
 @pytest.mark.parametrize("n,r", [(256, 16), (300, 40), (1000, 50), (129, 33), (1, 1), (33, 7),
-                                 (2048, 158), (4096, 272), (640, 544), (777, 640)])
+                                 (2048, 158), (4096, 272), (640, 544), (777, 640),
+                                 (1000, 170), (1100, 200), (900, 224), (700, 225)])
 def test_syrk_matches_fp64(ours, n, r):
     g = torch.Generator(device="cpu").manual_seed(n * 31 + r)
     w = torch.linalg.qr(torch.randn(n, r, generator=g, dtype=torch.float64))[0] if n >= r else \
@@ -117,3 +118,33 @@ def test_syrk_rejects_wide_factor(ours):
     d = torch.ones(641, dtype=torch.float64, device="cuda")
     with pytest.raises(Exception):
         _syrk(ours, w, d)
+
+
+@int8_enabled
+@pytest.mark.parametrize("k,l,q,alpha", [(118, 20, 1, 0.0), (63, 13, 1, 0.913), (169, 25, 2, 0.429)])
+def test_rank_deficient_sketch_within_reference_sensitivity(ours, k, l, q, alpha):
+    """X of numerical rank 60 (+1e-4 noise), n ≥ 3072 (INT8 products and reconstruction).
+    With the sketch wider than that rank at q = 1 the reference's own output moves by
+    ~1e-9 under a one-ulp perturbation of X; ours must stay within 10× of that (and
+    within 1e-10 whenever the problem is well conditioned)."""
+    from oracle import psd_oracle as orc
+    rs = np.random.default_rng(k + l + q)
+    n = 3100
+    u = np.linalg.qr(rs.standard_normal((n, 60)))[0]
+    s = np.geomspace(1e3, 1e-2, 60) * rs.choice([-1.0, 1.0], 60)
+    x = (u * s) @ u.T + 1e-4 * orc.wigner(n, seed=k)
+    x = (x + x.T) / 2
+    om = rs.standard_normal((n, k + l))
+    run = (lambda xx: orc.ran_proj_scal(xx, k, l, q, alpha, omega=om)) if alpha > 0 else \
+        (lambda xx: orc.ran_proj(xx, k, l, q, omega=om))
+    ref = run(x)
+    e = rs.choice([-1.0, 1.0], (n, n))
+    e = np.triu(e) + np.triu(e, 1).T
+    sens = np.linalg.norm(run(x * (1 + 2.0 ** -53 * e)).result - ref.result) / np.linalg.norm(ref.result)
+    xd, omd = torch.from_numpy(x).cuda(), torch.from_numpy(om).cuda()
+    prm = ours.RangeParams(k=k, l=l, q=q)
+    rep = ours.ran_proj_scal(xd, prm, alpha, None, omega=omd) if alpha > 0 else ours.ran_proj(xd, prm, None, omega=omd)
+    assert rep.device_info["recon_engine"] == 1
+    assert rep.basis_width == ref.basis_width and rep.effective_rank == ref.effective_rank
+    err = np.linalg.norm(rep.result.cpu().numpy() - ref.result) / np.linalg.norm(ref.result)
+    assert err <= max(1e-10, 10 * sens), (err, sens)

@@ -1,0 +1,90 @@
+"""Randomised parity sweep on the GPU: shapes around the INT8-engine threshold
+(n ≥ 3072: INT8 products and INT8 reconstruction), odd sizes, both algorithms,
+FP64 and FP32, against the CPU oracle on identical X and Ω.
+
+Each case also measures the reference's own sensitivity: the oracle re-run on X
+perturbed by one ulp per entry (symmetric ±2^-53 relative — what a different
+GEMM summation order does).  Rank-deficient sketches (width > numerical rank of
+X at q = 1) and clipping thresholds inside a near-degenerate eigenvalue cluster
+leave the result determined by roundoff at the 1e-9..1e-8 level in ANY FP64
+implementation; a case passes when the GPU result is within 1e-10 of the oracle
+or within 10× that self-sensitivity.
+
+    python tools/stress_parity.py [cases] [seed]
+"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2410_19208_b200 as psd  # noqa: E402
+from oracle import psd_oracle as orc  # noqa: E402
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 12
+    rs = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    worst = {"fp64": 0.0, "fp32": 0.0}
+    for c in range(cases):
+        n = int(rs.integers(2900, 4700))
+        k = int(rs.integers(1, 200))
+        l = int(rs.integers(0, 40))
+        q = int(rs.integers(0, 3))
+        kind = ["wigner", "lowrank"][c % 2]
+        if kind == "wigner":
+            x = orc.wigner(n, seed=1000 + c)
+        else:
+            u = np.linalg.qr(rs.standard_normal((n, 60)))[0]
+            s = np.geomspace(1e3, 1e-2, 60) * rs.choice([-1.0, 1.0], 60)
+            x = (u * s) @ u.T + 1e-4 * orc.wigner(n, seed=2000 + c)
+            x = (x + x.T) / 2
+        om = rs.standard_normal((n, k + l))
+        alpha = float(rs.uniform(0.1, 2.0)) if c % 3 == 2 else 0.0
+        t0 = time.perf_counter()
+        if alpha > 0:
+            o = orc.ran_proj_scal(x, k, l, q, alpha, omega=om)
+        else:
+            o = orc.ran_proj(x, k, l, q, omega=om)
+        t_cpu = time.perf_counter() - t0
+        e = rs.choice([-1.0, 1.0], (n, n))
+        e = np.triu(e) + np.triu(e, 1).T
+        xp = x * (1 + 2.0 ** -53 * e)
+        op = orc.ran_proj_scal(xp, k, l, q, alpha, omega=om) if alpha > 0 else orc.ran_proj(xp, k, l, q, omega=om)
+        self_sens = np.linalg.norm(op.result - o.result) / max(np.linalg.norm(o.result), 1e-300)
+        del e, xp
+        xd, omd = torch.from_numpy(x).cuda(), torch.from_numpy(om).cuda()
+        prm = psd.RangeParams(k=k, l=l, q=q)
+        if alpha > 0:
+            r = psd.ran_proj_scal(xd, prm, alpha, None, omega=omd)
+        else:
+            r = psd.ran_proj(xd, prm, None, omega=omd)
+        res = r.result.cpu().numpy()
+        nrm = max(np.linalg.norm(o.result), 1e-300)
+        e64 = np.linalg.norm(res - o.result) / nrm
+        sym = bool(np.array_equal(res, res.T))
+        # FP32 path on the fp32-rounded X / Ω, against the oracle on the same rounded values
+        x32, om32 = x.astype(np.float32), om.astype(np.float32)
+        if alpha > 0:
+            o32 = orc.ran_proj_scal(x32.astype(np.float64), k, l, q, alpha, omega=om32.astype(np.float64))
+            r32 = psd.ran_proj_scal(x32, prm, alpha, None, omega=om32, dtype="fp32")
+        else:
+            o32 = orc.ran_proj(x32.astype(np.float64), k, l, q, omega=om32.astype(np.float64))
+            r32 = psd.ran_proj(x32, prm, None, omega=om32, dtype="fp32")
+        e32 = np.linalg.norm(r32.result.astype(np.float64) - o32.result) / max(np.linalg.norm(o32.result), 1e-300)
+        worst["fp64"] = max(worst["fp64"], e64)
+        worst["fp32"] = max(worst["fp32"], e32)
+        info = r.device_info
+        # FP32: ≤1e-4 unless the problem is roundoff-determined even in FP64 (then FP32 is moot)
+        ok = (e64 <= max(1e-10, 10 * self_sens) and (e32 <= 1e-4 or self_sens > 1e-12) and sym
+              and r.effective_rank == o.effective_rank and r.basis_width == o.basis_width)
+        print(f"case {c:2d} {kind:7s} n={n} k={k} l={l} q={q} alpha={alpha:.3f} rank={r.effective_rank}/"
+              f"{o.effective_rank} width={r.basis_width}/{o.basis_width} engines={info['sketch_engine']}/{info['recon_engine']} fp64 {e64:.2e} (ref 1-ulp {self_sens:.1e}) "
+              f"sym={sym} fp32 {e32:.2e} cpu {t_cpu:.1f}s {'OK' if ok else 'FAIL'}", flush=True)
+    print(f"worst fp64 {worst['fp64']:.2e} (bar 1e-10), fp32 {worst['fp32']:.2e} (bar 1e-4)")
+
+
+if __name__ == "__main__":
+    main()
