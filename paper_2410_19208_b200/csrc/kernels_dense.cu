@@ -169,13 +169,17 @@ __global__ void sort_eigs_kernel(const double* vals, const double* vecs, long lo
                                  double offset, double* vals_out, double* vecs_out, long long ldo,
                                  int* npos, int* perm) {
   __shared__ int pos_count;
+  constexpr int kSm = 2048;
+  __shared__ double sv[kSm];
   if (threadIdx.x == 0) pos_count = 0;
+  for (int i = threadIdx.x; i < min(m, kSm); i += blockDim.x) sv[i] = vals[i];
   __syncthreads();
+  const double* v = m <= kSm ? sv : vals;
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    const double li = vals[i];
+    const double li = v[i];
     int rank = 0;
     for (int j = 0; j < m; ++j) {
-      const double lj = vals[j];
+      const double lj = v[j];
       rank += (lj > li) || (lj == li && j < i);
     }
     perm[rank] = i;
@@ -184,32 +188,51 @@ __global__ void sort_eigs_kernel(const double* vals, const double* vecs, long lo
   }
   __syncthreads();
   if (threadIdx.x == 0) npos[0] = pos_count;
-  // orientation + column permutation: one warp per output column
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int col = warp; col < m; col += blockDim.x >> 5) {
-    const int src = perm[col];
-    double best = -1.0;
-    int bidx = 0x7fffffff;
-    for (int r = lane; r < m; r += 32) {
-      const double x = fabs(vecs[(long long)r * ldv + src]);
-      if (x > best) {
-        best = x;
-        bidx = r;
-      }
+}
+
+// one CTA per output column: gather the permuted source column, find its first
+// largest-|entry| (block argmax), store it with that entry made positive
+__global__ void __launch_bounds__(256) orient_columns_kernel(const double* __restrict__ vecs, long long ldv, int m,
+                                                             const int* __restrict__ perm,
+                                                             double* __restrict__ vecs_out, long long ldo) {
+  const int col = blockIdx.x;
+  const int src = perm[col];
+  __shared__ double sb[8];
+  __shared__ int si[8];
+  double best = -1.0;
+  int bidx = 0x7fffffff;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    const double x = fabs(vecs[(long long)r * ldv + src]);
+    if (x > best) {
+      best = x;
+      bidx = r;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
-      if (ob > best || (ob == best && oi < bidx)) {
-        best = ob;
-        bidx = oi;
-      }
-    }
-    const double anchor = vecs[(long long)bidx * ldv + src];
-    const double sg = (anchor < 0.0) ? -1.0 : 1.0;
-    for (int r = lane; r < m; r += 32) vecs_out[(long long)r * ldo + col] = sg * vecs[(long long)r * ldv + src];
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (ob > best || (ob == best && oi < bidx)) {
+      best = ob;
+      bidx = oi;
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sb[warp] = best;
+    si[warp] = bidx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (sb[w] > sb[0] || (sb[w] == sb[0] && si[w] < si[0])) {
+        sb[0] = sb[w];
+        si[0] = si[w];
+      }
+  }
+  __syncthreads();
+  const double sg = (vecs[(long long)si[0] * ldv + src] < 0.0) ? -1.0 : 1.0;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) vecs_out[(long long)r * ldo + col] = sg * vecs[(long long)r * ldv + src];
 }
 
 void sort_eigs(const double* vals, const double* vecs, long long ldv, int m, double offset,
@@ -217,7 +240,8 @@ void sort_eigs(const double* vals, const double* vecs, long long ldv, int m, dou
                cudaStream_t st) {
   sort_eigs_kernel<<<1, 1024, 0, st>>>(vals, vecs, ldv, m, offset, vals_out, vecs_out, ldo, npos,
                                        perm);
-  count_launch();
+  orient_columns_kernel<<<m, 256, 0, st>>>(vecs, ldv, m, perm, vecs_out, ldo);
+  count_launch(2);
 }
 
 }  // namespace psd
