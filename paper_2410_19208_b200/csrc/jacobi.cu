@@ -535,10 +535,12 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
 __global__ void jacobi_norm_kernel(const double* a, long long lda, int m, double* out) {
   __shared__ double red[32];
   double s = 0.0;
-  for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
-    const double x = a[(e / m) * lda + e % m];
-    s = fma(x, x, s);
-  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = warp; i < m; i += nw)   // warp per row: coalesced, no index division
+    for (int j = lane; j < m; j += 32) {
+      const double x = a[(long long)i * lda + j];
+      s = fma(x, x, s);
+    }
   s = warp_sum(s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();

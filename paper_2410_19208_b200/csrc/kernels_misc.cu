@@ -102,10 +102,9 @@ static void sym_stats_t(const T* x, long long n, long long ldx, double* stats, c
 __global__ void identity_defect_kernel(const double* __restrict__ g, int w, long long ldg, double* out) {
   __shared__ double red[32];
   double m = 0.0;
-  for (long long e = threadIdx.x; e < (long long)w * w; e += blockDim.x) {
-    const int i = (int)(e / w), j = (int)(e % w);
-    m = fmax(m, fabs(g[(long long)i * ldg + j] - (i == j ? 1.0 : 0.0)));
-  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = warp; i < w; i += nw)   // warp per row: coalesced, no index division
+    for (int j = lane; j < w; j += 32) m = fmax(m, fabs(g[(long long)i * ldg + j] - (i == j ? 1.0 : 0.0)));
   m = warp_max(m);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
