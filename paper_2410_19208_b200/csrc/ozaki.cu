@@ -160,6 +160,34 @@ PSD_DEVINL void res_limb_all(const float (&f)[8][4], int8_t* out, long long plan
   }
 }
 
+// 4 consecutive k (one 32-bit word per modulus), compile-time modulus constants
+template <int L>
+PSD_DEVINL void res_limb_store4(const float (&f)[4][4], int8_t* out, long long plane) {
+  constexpr float m = (float)mod_at(L), rm = 1.0f / (float)mod_at(L);
+  constexpr float p1 = pow13_sym(L, 1), p2 = pow13_sym(L, 2), p3 = pow13_sym(L, 3);
+  constexpr uint32_t nmi = 0u - (uint32_t)mod_at(L);
+  uint32_t b[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float sacc = fmaf(f[q][3], p3, fmaf(f[q][2], p2, fmaf(f[q][1], p1, f[q][0])));
+    if constexpr (L == 1) {
+      float rr = sym_mod_f(sacc, m, rm);
+      rr = rr > 127.5f ? rr - m : rr;
+      b[q] = low_bits(rr);
+    } else {
+      b[q] = __float_as_uint(fmaf(sacc, rm, kMagic)) * nmi + __float_as_uint(sacc + kMagic);
+    }
+  }
+  *reinterpret_cast<uint32_t*>(out + L * plane) = pack4(b[0], b[1], b[2], b[3]);
+}
+template <int L>
+PSD_DEVINL void res_limb_all4(const float (&f)[4][4], int8_t* out, long long plane) {
+  if constexpr (L < kNumMod) {
+    res_limb_store4<L>(f, out, plane);
+    res_limb_all4<L + 1>(f, out, plane);
+  }
+}
+
 __global__ void __launch_bounds__(256) residues_rows_kernel(const double* __restrict__ x, long long rows,
                                                           long long cols, long long ldx, int* __restrict__ e,
                                                           int8_t* __restrict__ r, long long ldr,
@@ -274,8 +302,12 @@ __global__ void __launch_bounds__(256) residues_panel_t_kernel(const double* __r
   int8_t* out = r + (long long)j * ldr + k;
   const bool full4 = k + 3 < K;
   uint32_t w = pack4(lowb[0], lowb[1], lowb[2], lowb[3]);
-  if (full4) *reinterpret_cast<uint32_t*>(out) = w;
-  else for (int q = 0; k + q < K; ++q) out[q] = (int8_t)(w >> (8 * q));
+  if (full4) {   // common case: immediate-form modulus constants, one 32-bit store per modulus
+    *reinterpret_cast<uint32_t*>(out) = w;
+    res_limb_all4<1>(fl, out, plane);
+    return;
+  }
+  for (int q = 0; k + q < K; ++q) out[q] = (int8_t)(w >> (8 * q));
 #pragma unroll
   for (int l = 1; l < kNumMod; ++l) {
     const float m = c_modf[l], rm = c_rmodf[l];
@@ -294,8 +326,7 @@ __global__ void __launch_bounds__(256) residues_panel_t_kernel(const double* __r
       }
     }
     w = pack4(bq[0], bq[1], bq[2], bq[3]);
-    if (full4) *reinterpret_cast<uint32_t*>(out + l * plane) = w;
-    else for (int q = 0; k + q < K; ++q) out[l * plane + q] = (int8_t)(w >> (8 * q));
+    for (int q = 0; k + q < K; ++q) out[l * plane + q] = (int8_t)(w >> (8 * q));
   }
 }
 
