@@ -121,14 +121,22 @@ __global__ void row_exp_kernel(const double* __restrict__ x, long long rows, lon
 // column exponents of a K×N row-major panel: atomicMax over per-element exponents
 __global__ void col_exp_kernel(const double* __restrict__ p, long long rows, int cols, long long ldp,
                                int* __restrict__ f) {
-  const int j = blockIdx.y * 32 + (threadIdx.x & 31);
-  if (j >= cols) return;
-  int mx = -100000;
-  for (long long k = blockIdx.x * 8 + (threadIdx.x >> 5); k < rows; k += (long long)gridDim.x * 8) {
-    const double v = fabs(p[k * ldp + j]);
-    if (v > 0.0) mx = max(mx, ilogb(v) + 1);
+  // max over the block's rows in registers (doubles: the exponent is taken once per column),
+  // the 8 warps combined in shared memory, then ONE atomic per column per block
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = blockIdx.y * 32 + lane;
+  double mx = 0.0;
+  if (j < cols)
+    for (long long k = blockIdx.x * 8 + warp; k < rows; k += (long long)gridDim.x * 8)
+      mx = fmax(mx, fabs(p[k * ldp + j]));
+  red[warp][lane] = mx;
+  __syncthreads();
+  if (warp == 0 && j < cols) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w][lane]);
+    if (mx > 0.0) atomicMax(&f[j], ilogb(mx) + 1);
   }
-  if (mx > -100000) atomicMax(&f[j], mx);
 }
 
 // ---- residues of a row-scaled matrix: R[ℓ][i][k] (int8), ld ldr bytes ---------------
