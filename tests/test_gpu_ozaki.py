@@ -173,7 +173,8 @@ def test_ran_proj_int8_engine_matches_dmma_and_oracle(ours, q):
     finally:
         ours.set_fp64_engine(prev)
     assert r8.device_info["sketch_engine"] == 1 and rd.device_info["sketch_engine"] == 0
-    assert r8.device_info["recon_engine"] == 1 and rd.device_info["recon_engine"] == 0
+    if os.environ.get("PSD_OZ_SYRK", "") != "0":   # PSD_OZ_SYRK=0 keeps the DMMA reconstruction
+        assert r8.device_info["recon_engine"] == 1 and rd.device_info["recon_engine"] == 0
     ref = orc.ran_proj(x, 40, 8, q, rng=np.random.default_rng(5)).result
     for r in (r8, rd):
         assert np.linalg.norm(r.result - ref) / np.linalg.norm(ref) < 1e-10
@@ -194,6 +195,7 @@ def test_ran_proj_scal_int8_engine(ours):
     assert np.linalg.norm(r8.result - ref) / np.linalg.norm(ref) < 1e-10
 
 
+@int8_enabled
 def test_wide_sketch_column_groups_and_transpose_on_dmma(ours):
     x = _sym(700, 4)
     prev = ours.set_fp64_engine("int8")
@@ -217,6 +219,7 @@ def test_set_fp64_engine_validation(ours):
         ours.set_fp64_engine("fp16")
 
 
+@int8_enabled
 def test_auto_engine_size_threshold(ours):
     """auto: DMMA below n = 3072 (measured crossover), INT8 emulation from there."""
     assert ours.set_fp64_engine("auto") in ("auto", "int8", "dmma")
