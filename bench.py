@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Benchmark: randomized PSD projections/s at BASELINE config 3
-(n=32768, k=256, p=16, q=1, fp64) on B200, with FP64 tensor-core roofline.
+(n=32768, k=256, p=16, q=1, fp64) on B200, with the tensor-core roofline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -10,14 +10,21 @@ matrices (8.6 GB each ≫ 126 MB L2, so no L2 flush is needed).  Ω is drawn on
 the device each step (Philox).  The FP64 n×n sketch products run by default on
 the INT8 tensor cores as an exact FP64 emulation (Ozaki scheme II, csrc/ozaki.cu;
 same ≤1e-10 parity as the DMMA path); ``--fp64-engine dmma`` keeps them on the
-FP64 DMMA kernel.  Multi-GPU: independent replicas, one process
-per GPU (the C3 projections are independent), value
-= all ranks' projections / max-over-ranks device time.
+FP64 DMMA kernel.
 
-``--impl reference`` times the reference algorithm's CPU implementation (the
-oracle port in oracle/psd_oracle.py — same numpy/OpenBLAS calls as
-psdcone.ran_proj) on this box's host cores, on a bounded sample (n=8192 with
-C3's k, p, q), scaled by (8192/32768)² to the metric's unit.
+Multi-GPU: ``--gpus N`` without a torchrun environment relaunches itself under
+``torch.distributed.run`` with N ranks (one per GPU).  The C3 projections are
+independent: one replica per rank, value = all ranks' projections /
+max-over-ranks device time (``scaling: weak``).  The same line carries
+``c4_sharded``: BASELINE config 4 (n=131072, k=512, p=32, q=2) row-sharded over
+all N ranks (NCCL all-gather / all-reduce), so a scaling run measures the
+sharded path at every N.
+
+``--impl reference`` times the UNMODIFIED reference ``psdcone.ran_proj``
+(oracle/_ref, installed offline by oracle/make_ref.sh) on this box's host
+cores at the full C3 size, for as many of the K steps as fit a time budget
+(the count actually timed is reported as ``steps``); the oracle port
+(oracle/psd_oracle.py) stands in only if the reference package is absent.
 """
 
 from __future__ import annotations
@@ -64,6 +71,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the config-3 FP32 (3xTF32) leg")
+    ap.add_argument("--no-scaled", action="store_true", help="skip the scaled (Alg. 3 + Alg. 5) leg")
+    ap.add_argument("--no-c4", action="store_true", help="skip the config-4 row-sharded leg")
+    ap.add_argument("--c4-steps", type=int, default=3)
+    ap.add_argument("--ref-budget-s", type=float, default=float(os.environ.get("PSD_REF_BUDGET_S", 300)),
+                    help="reference arm: wall-clock budget for the timed full-size projections")
     ap.add_argument("--fp64-engine", choices=["auto", "int8", "dmma"], default="auto",
                     help="FP64 n×n products: exact emulation on the INT8 tensor cores (auto: n >= 3072), or DMMA")
     a = ap.parse_args()
@@ -97,50 +109,88 @@ def cpu_cores():
         return os.cpu_count()
 
 
-def cpu_sample(a, reps=1):
-    """Oracle port (same numpy calls as psdcone.ran_proj) at n=CPU_SAMPLE_N; returns
-    (projections/s scaled to n=a.n, seconds per sample)."""
-    import numpy as np
+def _reference_module():
+    """The unmodified reference package (oracle/_ref or /root/reference), or None."""
+    try:
+        from oracle import refpkg
+        return refpkg.import_psdcone()
+    except Exception:
+        return None
 
+
+def _host_matrix(config, n, seed):
     from oracle import psd_oracle as orc
-    ns = min(CPU_SAMPLE_N, a.n)
-    x = {"c1": lambda: orc.c1_matrix(seed=11, n=ns), "c2": lambda: orc.wigner(ns, seed=11),
-         "c3": lambda: orc.c3_matrix(ns, seed=11)}[a.config]()
-    best = 1e300
-    for r in range(reps):
-        om = np.random.default_rng(100 + r).standard_normal((ns, a.k + a.p))
-        t0 = time.perf_counter()
-        orc.ran_proj(x, a.k, a.p, a.q, omega=om)
-        best = min(best, time.perf_counter() - t0)
-    scale = (ns / a.n) ** 2  # every stage of the path is O(n²) at fixed width
-    return scale / best, best, ns
+    return {"c1": lambda: orc.c1_matrix(seed=seed, n=n), "c2": lambda: orc.wigner(n, seed=seed),
+            "c3": lambda: orc.c3_matrix(n, seed=seed)}[config]()
+
+
+def _cpu_project(ref, x, a, seed):
+    """One CPU projection: the real psdcone.ran_proj (its own validation, Ω draw,
+    QR, eigh and reconstruction — projection.py:92-119) or the oracle port."""
+    import numpy as np
+    if ref is not None:
+        return ref.ran_proj(x, ref.RangeParams(k=a.k, l=a.p, q=a.q), np.random.default_rng(seed))
+    from oracle import psd_oracle as orc
+    return orc.ran_proj(x, a.k, a.p, a.q, rng=np.random.default_rng(seed))
+
+
+def cpu_sample(a, ns=CPU_SAMPLE_N):
+    """Bounded CPU sample for the ``cpu_baseline`` key of our line: one projection
+    at n=ns (C3's k, p, q) by the reference (or the port), scaled to the metric's
+    unit by (ns/n)² (every stage of the path is O(n²) at fixed width)."""
+    ref = _reference_module()
+    ns = min(ns, a.n)
+    x = _host_matrix(a.config, ns, 11)
+    t0 = time.perf_counter()
+    _cpu_project(ref, x, a, 100)
+    sec = time.perf_counter() - t0
+    return (ns / a.n) ** 2 / sec, sec, ns, ("reference" if ref is not None else "port")
 
 
 def run_reference(a):
+    """The reference arm: psdcone.ran_proj on this box's host cores at the FULL
+    workload size (n = a.n), timed with time.perf_counter around the public call.
+    Warm-up runs at n=2048 (BLAS thread pool, page cache); then full-size
+    projections until ``--steps`` are done or the next one would overrun
+    ``--ref-budget-s``; ``steps`` reports how many were timed."""
     rank = int(os.environ.get("RANK", "0"))
     n_gpus = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
     if rank != 0:
         return
-    for _ in range(max(a.warmup, 0)):
-        cpu_sample(a)
-    vals, secs = [], []
-    for _ in range(a.steps):
-        v, s, ns = cpu_sample(a)
-        vals.append(v)
-        secs.append(s)
-    value = a.steps / sum(s / ((ns / a.n) ** 2) for s in secs)
+    ref = _reference_module()
+    kind = "reference" if ref is not None else "port"
+    xw = _host_matrix(a.config, min(2048, a.n), 3)
+    for i in range(max(a.warmup, 0)):
+        _cpu_project(ref, xw, a, 200 + i)
+    del xw
+    t0 = time.perf_counter()
+    x = _host_matrix(a.config, a.n, 11)
+    gen_s = time.perf_counter() - t0
+    secs = []
+    budget_start = time.perf_counter()
+    for i in range(a.steps):
+        if secs and (time.perf_counter() - budget_start) + max(secs) > a.ref_budget_s:
+            break
+        t0 = time.perf_counter()
+        rep = _cpu_project(ref, x, a, 1000 + i)
+        secs.append(time.perf_counter() - t0)
+    value = len(secs) / sum(secs)
     cores = cpu_cores()
-    ns = min(CPU_SAMPLE_N, a.n)
-    sample = (f"oracle port of psdcone.ran_proj (numpy/OpenBLAS, {cores} threads) on a {a.config} matrix at "
-              f"n={ns}, k={a.k}, p={a.p}, q={a.q}; time × (n/{ns})² per step")
+    who = ("psdcone.ran_proj (the unmodified reference, oracle/_ref)" if ref is not None else
+           "the oracle port of psdcone.ran_proj (reference package absent)")
+    sample = (f"{who}, numpy/OpenBLAS with {cores} threads, on a {a.config} matrix at the full n={a.n} "
+              f"(k={a.k}, p={a.p}, q={a.q}); {len(secs)} of {a.steps} requested projections timed "
+              f"(budget {a.ref_budget_s:.0f} s), {min(secs):.1f}-{max(secs):.1f} s each; X generated "
+              f"on the host in {gen_s:.1f} s (untimed)")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": n_gpus,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 / value,
+        "steps": len(secs), "steps_requested": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1000.0 * sum(secs) / len(secs),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded C3 matrix, host numpy)",
         "config": workload_config(a, 1),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+        "effective_rank": int(rep.effective_rank),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -266,25 +316,62 @@ class ClockSampler:
 
 # ------------------------------------------------------------------- ours ---
 
-def fp64_peak(torch, dev):
-    """cuBLAS DGEMM 8192³ burst rate (MEASURED_PEAKS.json carries no FP64 entry)."""
-    a = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
-    b = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
-    for _ in range(2):
-        a @ b
-    torch.cuda.synchronize(dev)
-    best = 1e9
+def _gemm_rate(torch, fn, flops, sustained_s=1.5):
+    """(burst, sustained) rate of ``fn`` in TFLOP/s (or TOP/s): best single launch of 5
+    (CUDA events), then back-to-back launches for ``sustained_s`` seconds."""
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    best = 1e30
     for _ in range(5):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        a @ b
+        fn()
         e1.record()
-        torch.cuda.synchronize(dev)
+        torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1))
+    reps = max(4, int(sustained_s * 1000.0 / best))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return flops / best / 1e9, flops * reps / e0.elapsed_time(e1) / 1e9
+
+
+def measure_peaks(torch, dev):
+    """Tensor-core denominators measured in this run with cuBLAS at 8192³ (the
+    MEASURED_PEAKS.json file carries HBM and bf16 only): FP64 (DGEMM), INT8
+    (torch._int_mm → cuBLASLt IMMA) and TF32 (fp32 matmul with TF32 allowed).
+    Each as burst (best single launch) and sustained (back to back ≈1.5 s, the
+    clock a kernel inside a long step runs at)."""
+    n = 8192
+    flops = 2.0 * n ** 3
+    out = {"how": "cuBLAS 8192^3 in this process: burst = best of 5 launches, sustained = "
+                  "back-to-back launches for ~1.5 s (CUDA events)"}
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    out["fp64_tflops"], out["fp64_tflops_sustained"] = _gemm_rate(torch, lambda: a @ b, flops, 0.5)
     del a, b
+    try:
+        a8 = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev)
+        b8 = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev)
+        out["int8_tops"], out["int8_tops_sustained"] = _gemm_rate(torch, lambda: torch._int_mm(a8, b8), flops)
+        del a8, b8
+    except Exception as exc:  # pragma: no cover - cuBLASLt without IMMA
+        out["int8_error"] = str(exc)[:200]
+    prev = torch.backends.cuda.matmul.allow_tf32
+    try:
+        torch.backends.cuda.matmul.allow_tf32 = True
+        a32 = torch.randn(n, n, dtype=torch.float32, device=dev)
+        b32 = torch.randn(n, n, dtype=torch.float32, device=dev)
+        out["tf32_tflops"], out["tf32_tflops_sustained"] = _gemm_rate(torch, lambda: a32 @ b32, flops)
+        del a32, b32
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
     torch.cuda.empty_cache()
-    return 2 * 8192 ** 3 / best / 1e9
+    return out
 
 
 def measured_peaks():
@@ -295,13 +382,13 @@ def measured_peaks():
         return {}
 
 
-def int8_roofline(n, w, i8_ms, i8_cnt, traffic):
-    """Roofline of i8_gemm2_kernel (one emulated FP64 sketch product): bound by the
-    INT8 tensor pipe (ncu: tensor pipe ≈89% busy, DRAM ≈59%), so `achieved` is the
-    algorithmic int8 ops per launch over its CUDA-event time, against the dense int8
-    peak = 2 × the MEASURED_PEAKS bf16 rate (B200: 4.5 POPS int8 vs 2.25 PF bf16) —
-    the sustained figure, the kernel runs inside a long step.  The HBM view is kept
-    beside it."""
+def int8_roofline(n, w, i8_ms, i8_cnt, traffic, peaks):
+    """Roofline of i8_gemm2_kernel (the 16 residue products of one emulated FP64
+    sketch product), bound by the INT8 tensor pipe: ``achieved`` = algorithmic int8
+    ops per launch (16 · 2n²w) over its average CUDA-event time in the timed
+    region; ``peak`` = cuBLASLt INT8 8192³ back-to-back (sustained) measured in this
+    run — the kernel runs inside a long step.  Fallback: 2 × MEASURED_PEAKS bf16
+    sustained.  The HBM view is kept beside it."""
     L = 16
     ldk = (n + 127) // 128 * 128
     wpad = (w + 15) // 16 * 16
@@ -311,8 +398,12 @@ def int8_roofline(n, w, i8_ms, i8_cnt, traffic):
     gbs = algo_bytes / (i8_ms / 1000.0) / 1e9
     int8_ops = 2.0 * L * n * n * w
     tops = int8_ops / (i8_ms / 1000.0) / 1e12
-    sustained = pk.get("bf16_tflops_sustained")
-    peak = 2.0 * (sustained or pk.get("bf16_tflops") or 2250.0)
+    if peaks.get("int8_tops_sustained"):
+        peak, src = peaks["int8_tops_sustained"], ("cuBLASLt INT8 (torch._int_mm) 8192^3 sustained, "
+                                                    "measured in this run")
+    else:
+        peak = 2.0 * (pk.get("bf16_tflops_sustained") or pk.get("bf16_tflops") or 1125.0)
+        src = "2 x MEASURED_PEAKS.json bf16_tflops_sustained (no in-run INT8 measurement)"
     return {
         "bound": "tensor", "achieved": tops, "peak": peak, "unit": "TFLOP/s", "frac": tops / peak,
         "traffic": traffic.get("bytes_per_launch") if traffic else None,
@@ -321,9 +412,9 @@ def int8_roofline(n, w, i8_ms, i8_cnt, traffic):
                   f"products of X·P mod m_l for one FP64 sketch product; {int8_ops / 1e15:.2f} int8 POP "
                   f"algorithmic per launch, {i8_ms:.3f} ms avg over {i8_cnt} launches (CUDA events "
                   f"on the launching stream, timed region); unit: int8 TOP/s",
-        "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops_sustained" if sustained else
-                        "2 x MEASURED_PEAKS.json bf16_tflops (burst)" if pk.get("bf16_tflops") else
-                        "nominal dense int8 4.5 POPS / 2"),
+        "peak_source": src,
+        "peak_burst": peaks.get("int8_tops"),
+        "frac_of_burst": tops / peaks["int8_tops"] if peaks.get("int8_tops") else None,
         "hbm_view": {"achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm,
                      "algorithmic_bytes_per_launch": algo_bytes},
         "traffic_source": traffic.get("source") if traffic else None,
@@ -339,6 +430,25 @@ def load_traffic(name="gemm_traffic.json"):
         return None
 
 
+def _dist_setup(torch, dist):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev)
+    return world, rank, local, dev
+
+
+def _max_over_ranks(torch, dist, world, ms, dev):
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -346,18 +456,12 @@ def run_ours(a):
     import paper_2410_19208_b200 as psd
     from paper_2410_19208_b200 import workloads
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
+    world, rank, local, dev = _dist_setup(torch, dist)
     n, params = a.n, psd.RangeParams(k=a.k, l=a.p, q=a.q)
     psd.set_fp64_engine(a.fp64_engine)
 
-    peak = fp64_peak(torch, dev) if rank == 0 else None
+    peaks = measure_peaks(torch, dev) if rank == 0 else {}
+    peak = peaks.get("fp64_tflops")
     nominal = 148 * 128 * 1.965  # GFLOP/s: 148 SMs × 64 DMMA FMA/clk × 2 × 1965 MHz
 
     gen = {"c1": lambda sd: workloads.c1_device(n, seed=sd, device=dev),
@@ -401,18 +505,12 @@ def run_ours(a):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
+    ms = _max_over_ranks(torch, dist, world, e0.elapsed_time(e1), dev)
     prof = plan.profile(enable=False, reset=True)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     value = world * a.steps / (ms / 1000.0)
 
     # roofline of the dominant kernel.  DMMA engine: the op(X)·P FP64 GEMM (2n²w flops
-    # per launch).  INT8 engine: the residue GEMM i8_gemm2_kernel, HBM-bound — per
-    # launch it streams the 16 int8 residue planes of X (16·n·ld_k bytes) plus the
-    # panel residues and the per-modulus outputs.
+    # per launch).  INT8 engine: the residue GEMM i8_gemm2_kernel (16 · 2n²w int8 ops).
     g_ms, g_cnt = prof["sketch_gemm"]
     gemm_ms = g_ms / max(g_cnt, 1)
     gemm_tf = 2.0 * n * n * params.width / (gemm_ms / 1000.0) / 1e12
@@ -424,18 +522,29 @@ def run_ours(a):
 
     fp32 = None
     if a.config == "c3" and not a.no_fp32:
-        fp32 = run_fp32_leg(a, torch, psd, pool, params, rng, dev, world)
+        fp32 = run_fp32_leg(a, torch, psd, pool, params, rng, dev, world, peaks)
+    scaled = None
+    if a.config == "c3" and not a.no_scaled:
+        scaled = run_scaled_leg(a, torch, psd, pool, params, dev, world, out64)
 
     e2e = None
     if rank == 0 and not a.no_e2e:
         e2e = run_e2e(a, torch, psd, pool[0], params, dev)
+    del pool, out64
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        v, s, ns = cpu_sample(a, reps=1)
-        cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-               "sample": f"1 projection of a {a.config} matrix at n={ns} (k={a.k}, p={a.p}, q={a.q}) "
-                         f"by the oracle port of psdcone.ran_proj on host cores in {s:.2f} s, "
-                         f"scaled by ({ns}/{a.n})²"}
+        v, sec, ns, kind = cpu_sample(a)
+        cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": kind,
+               "sample": f"1 projection of a {a.config} matrix at n={ns} (k={a.k}, p={a.p}, q={a.q}) by "
+                         + ("the unmodified reference psdcone.ran_proj (oracle/_ref)" if kind == "reference"
+                            else "the oracle port of psdcone.ran_proj")
+                         + f" on host cores in {sec:.2f} s, scaled by ({ns}/{a.n})²; the full-size "
+                           "reference is timed by `bench.py --impl reference`"}
+    c4 = None
+    if a.config == "c3" and not a.no_c4:
+        psd._native.free_plans()
+        torch.cuda.empty_cache()
+        c4 = c4_leg(a, torch, dist, psd, world, rank, dev)
     if world > 1:
         dist.destroy_process_group()
     if rank != 0:
@@ -450,7 +559,7 @@ def run_ours(a):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded BASELINE {a.config} matrices generated in HBM)",
         "config": workload_config(a, world),
-        "roofline": (int8_roofline(n, params.width, i8_ms / max(i8_cnt, 1), i8_cnt, traffic)
+        "roofline": (int8_roofline(n, params.width, i8_ms / max(i8_cnt, 1), i8_cnt, traffic, peaks)
                      if engine == 1 and i8_cnt else {
             "bound": "tensor", "achieved": gemm_tf, "peak": peak_tf, "unit": "TFLOP/s",
             "frac": gemm_tf / peak_tf, "traffic": traffic.get("bytes_per_launch") if traffic else None,
@@ -461,6 +570,7 @@ def run_ours(a):
                            f"no FP64 entry); nominal DMMA peak at 1965 MHz = {nominal / 1000:.1f}",
             "traffic_source": traffic.get("source") if traffic else None,
         }),
+        "peaks_in_run": peaks,
         "sketch_engine": {0: "fp64-dmma", 1: "int8-ozaki2 (exact FP64 emulation)", 2: "3xtf32"}[engine],
         "sketch_product_fp64_equiv_tflops": gemm_tf,
         "sketch_product_ms": gemm_ms,
@@ -479,7 +589,119 @@ def run_ours(a):
         line["e2e"] = e2e
     if fp32:
         line["fp32"] = fp32
+    if scaled:
+        line["scaled"] = scaled
+    if c4:
+        line["c4_sharded"] = c4
     print(json.dumps(line), flush=True)
+
+
+def run_scaled_leg(a, torch, psd, pool, params, dev, world, out64):
+    """Alg. 3 with α estimated by Alg. 5 (``project(method="scaled_randomized")``,
+    projection.py:200-223): 2(N+1) HBM-bound GEMV passes over X (sketch.py:106-114,
+    :126-129) then the shifted projection.  Timed like the main line; the α
+    estimate is bracketed separately so its GEMV bandwidth can be read against HBM."""
+    import torch.distributed as dist
+    from paper_2410_19208_b200._tensors import Operand
+    from paper_2410_19208_b200.sketch import min_eig_magnitude_device
+    n = a.n
+    power_n = 10
+    cfg = psd.ProjectorConfig(method="scaled_randomized", params=params, power_N=power_n)
+    rng = psd.DeviceRng(seed=977)
+    steps = max(2, min(a.steps, 8))
+    for i in range(2):
+        psd.project(pool[i % len(pool)], cfg, rng, assume_symmetric=True)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    falls = 0
+    for i in range(steps):
+        rep = psd.project(pool[i % len(pool)], cfg, rng, assume_symmetric=True)
+        falls += int(rep.fallback)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = _max_over_ranks(torch, dist, world, e0.elapsed_time(e1), dev)
+    # the α estimate alone (two power iterations of N+1 GEMVs each)
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 4
+    torch.cuda.synchronize(dev)
+    a0.record()
+    for i in range(reps):
+        min_eig_magnitude_device(Operand(pool[i % len(pool)], "torch_cuda", dev), power_n, rng)
+    a1.record()
+    torch.cuda.synchronize(dev)
+    alpha_ms = a0.elapsed_time(a1) / reps
+    passes = 2 * (power_n + 1)
+    gemv_bytes = passes * 8.0 * n * n
+    gbs = gemv_bytes / (alpha_ms / 1000.0) / 1e9
+    hbm = measured_peaks().get("hbm_gbs") or 7700.0
+    return {"value": world * steps / (ms / 1000.0), "unit": UNIT, "ms_per_step": ms / steps,
+            "steps": steps, "fallbacks": falls,
+            "workload": f"project(method='scaled_randomized', power_N={power_n}) on the C3 matrices: "
+                        "α = min_eig_magnitude (Alg. 5) then ran_proj_scal (Alg. 3)",
+            "alpha_estimate": {"ms": alpha_ms, "gemv_passes": passes,
+                               "algorithmic_bytes": gemv_bytes, "achieved_gbs": gbs, "peak_gbs": hbm,
+                               "frac": gbs / hbm,
+                               "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                               "note": "CUDA events around 4 min_eig_magnitude calls (GEMV + normalise "
+                                       "kernels and one host read per power iteration)"}}
+
+
+def c4_leg(a, torch, dist, psd, world, rank, dev):
+    """BASELINE config 4: one projection of n=131072 (k=512, p=32, q=2) row-sharded
+    over all ranks per step (sharded.py), X rows generated in place (bitwise
+    symmetric by construction → symmetric="assume"; the sharded check is
+    measured separately as ``symcheck_ms``).  Factored result at N=1 (X and X₊ do
+    not fit one GPU together), dense row blocks at N>1."""
+    from paper_2410_19208_b200 import sharded, workloads
+    cfg = CONFIGS["c4"]
+    n, params = cfg["n"], psd.RangeParams(k=cfg["k"], l=cfg["p"], q=cfg["q"])
+    starts = sharded.row_split(n, world)
+    r0, r1 = starts[rank], starts[rank + 1]
+    x = workloads.c4_rows(n, r0, r1, seed=11, device=dev, chunk_rows=4096)
+    om = psd.DeviceRng(99).normal((n, params.width), dev)      # identical on every rank
+    want = world > 1
+    ops = sharded.KernelOps(dev)
+    comm = sharded.Comm()
+    sharded.sharded_ran_proj(x, r0, n, om, params, comm=comm, ops=ops, want_result=want,
+                             symmetric="assume")
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    steps = max(1, a.c4_steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        rep = sharded.sharded_ran_proj(x, r0, n, om, params, comm=comm, ops=ops, want_result=want,
+                                       symmetric="assume")
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = _max_over_ranks(torch, dist, world, e0.elapsed_time(e1), dev)
+    # the sharded require_symmetric pass (block-pair exchange), timed once
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    s0.record()
+    mx, defect, bitwise, _ = sharded.sharded_symmetry_stats(x, r0, n, comm, ops)
+    s1.record()
+    torch.cuda.synchronize(dev)
+    sym_ms = _max_over_ranks(torch, dist, world, s0.elapsed_time(s1), dev)
+    del x, om
+    torch.cuda.empty_cache()
+    value = steps / (ms / 1000.0)
+    flops = 2.0 * n * n * params.width * (2 * params.q + 2) + (float(n) * n * rep.effective_rank if want else 0)
+    return {"metric": f"rand-PSD projections/s at n={n},k={cfg['k']} fp64 (config 4, row-sharded)",
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "ms_per_step": ms / steps,
+            "scaling": "strong", "effective_rank": rep.effective_rank,
+            "tflops_fp64_equiv": flops * value / 1e12,
+            "result": "dense row blocks" if want else "factored (W, d): X and X₊ do not fit one GPU",
+            "symcheck_ms": sym_ms, "symcheck_bitwise": bitwise,
+            "sketch_engine": "int8-ozaki2 (exact FP64 emulation, X_g streamed in 8192-row chunks)"
+                             if ops.int8_products else "fp64-dmma",
+            "exchanges": "NCCL all_gather_into_tensor of the n×w panel before each product, all_reduce "
+                         "of the w×w Grams and T"}
 
 
 def run_solver(a):
@@ -547,63 +769,27 @@ def run_solver(a):
 
 
 def run_sharded(a):
-    """Config 4: one row-sharded projection per step over all ranks (NCCL)."""
+    """``--config c4``: only the config-4 row-sharded line (see c4_leg)."""
     import torch
     import torch.distributed as dist
 
     import paper_2410_19208_b200 as psd
-    from paper_2410_19208_b200 import sharded, workloads
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    n = a.n
-    params = psd.RangeParams(k=a.k, l=a.p, q=a.q)
+    world, rank, local, dev = _dist_setup(torch, dist)
     psd.set_fp64_engine(a.fp64_engine)
-    starts = sharded.row_split(n, world)
-    r0, r1 = starts[rank], starts[rank + 1]
-    x = workloads.c4_rows(n, r0, r1, seed=11, device=dev, chunk_rows=4096)
-    om = psd.DeviceRng(99).normal((n, params.width), dev)      # identical on every rank
-    want = world > 1   # one GPU cannot hold X (137 GB) and the dense result together
-    ops = sharded.KernelOps(dev)
-    comm = sharded.Comm()
-    for _ in range(max(1, a.warmup)):
-        sharded.sharded_ran_proj(x, r0, n, om, params, comm=comm, ops=ops, want_result=want)
-    torch.cuda.synchronize()
+    c4 = c4_leg(a, torch, dist, psd, world, rank, dev)
     if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(a.steps):
-        rep = sharded.sharded_ran_proj(x, r0, n, om, params, comm=comm, ops=ops, want_result=want)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
         dist.destroy_process_group()
     if rank != 0:
         return
-    value = a.steps / (ms / 1000.0)
-    flops = 2.0 * n * n * params.width * (2 * params.q + 2) + (float(n) * n * rep.effective_rank if want else 0)
-    print(json.dumps({
-        "metric": f"rand-PSD projections/s at n={n},k={a.k} fp64 (config 4, row-sharded)", "value": value,
-        "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (config-4 rows generated per rank, bitwise symmetric)",
-        "config": {"workload": f"BASELINE config 4: n={n}, k={a.k}, p={a.p}, q={a.q}, row-sharded x{world}",
-                   "result": "dense row blocks" if want else "factored (W, d): X and X₊ do not fit one GPU"},
-        "effective_rank": rep.effective_rank, "tflops": flops * value / 1e12,
-        "sketch_engine": "int8-ozaki2 (exact FP64 emulation, X_g streamed in 8192-row chunks)"
-                         if ops.int8_products else "fp64-dmma"}), flush=True)
+    line = dict(c4)
+    line.update({"warmup": 1, "higher_is_better": True, "vs_baseline": None, "dtype": "f64",
+                 "data": "synthetic (config-4 rows generated per rank, bitwise symmetric)",
+                 "config": {"workload": f"BASELINE config 4: n={CONFIGS['c4']['n']}, k={CONFIGS['c4']['k']}, "
+                                        f"p={CONFIGS['c4']['p']}, q={CONFIGS['c4']['q']}, row-sharded x{world}"}})
+    print(json.dumps(line), flush=True)
 
 
-def run_fp32_leg(a, torch, psd, pool, params, rng, dev, world):
+def run_fp32_leg(a, torch, psd, pool, params, rng, dev, world, peaks):
     """BASELINE config 3 "fp32": the same projections on the fp32-rounded matrices
     through the FP32 path (3xTF32 tcgen05 GEMMs, FP64 QR/eigh), timed like the
     FP64 line (CUDA events, max over ranks)."""
@@ -653,24 +839,29 @@ def run_fp32_leg(a, torch, psd, pool, params, rng, dev, world):
             "tf32_tensor_tflops": 3.0 * eff_tf,
             "note": "3 tf32 MMAs (lo·hi, hi·lo, hi·hi) per FP32 product; effective = 2n²w/t",
         },
-        "roofline": fp32_roofline(3.0 * eff_tf),
+        "roofline": fp32_roofline(3.0 * eff_tf, peaks),
         "parity": "≤1e-4 rel. Frobenius vs the FP64 path on the same fp32-rounded X (tests/test_gpu_fp32.py)",
     }
 
 
-def fp32_roofline(tf32_tflops):
-    """tf32 issue rate of the 3xTF32 sketch GEMM against the tf32 tensor peak:
-    MEASURED_PEAKS.json's bf16 burst / 2 (kind::tf32 runs the tcgen05 datapath
-    at half the f16 rate — 1.1 vs 2.25 PFLOP/s nominal in B200_PROFILING.md)."""
-    peak, src = None, None
-    try:
-        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
-            peak = float(json.load(fh)["bf16_tflops"]) / 2.0
-            src = "MEASURED_PEAKS.json bf16_tflops (burst) / 2"
-    except Exception:
-        peak, src = 1100.0, "B200_PROFILING.md nominal tf32 dense 1.1 PFLOP/s (no MEASURED_PEAKS.json)"
+def fp32_roofline(tf32_tflops, peaks):
+    """tf32 issue rate of the 3xTF32 sketch GEMM against the TF32 tensor peak: cuBLAS
+    fp32 8192³ with TF32 allowed, back to back (sustained), measured in this run —
+    the same policy as the INT8 line.  Fallback: MEASURED_PEAKS bf16 sustained / 2."""
+    if peaks.get("tf32_tflops_sustained"):
+        peak, src = peaks["tf32_tflops_sustained"], "cuBLAS TF32 8192^3 sustained, measured in this run"
+    else:
+        try:
+            with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+                pk = json.load(fh)
+            peak = float(pk.get("bf16_tflops_sustained") or pk["bf16_tflops"]) / 2.0
+            src = "MEASURED_PEAKS.json bf16 sustained / 2"
+        except Exception:
+            peak, src = 1100.0, "B200_PROFILING.md nominal tf32 dense 1.1 PFLOP/s"
     return {"bound": "tensor", "achieved": tf32_tflops, "peak": peak, "unit": "TFLOP/s",
             "frac": tf32_tflops / peak, "traffic": load_traffic32(),
+            "peak_burst": peaks.get("tf32_tflops"),
+            "frac_of_burst": tf32_tflops / peaks["tf32_tflops"] if peaks.get("tf32_tflops") else None,
             "kernel": "tc32_gemm2_kernel (tcgen05.mma.cta_group::2.kind::tf32, TMA SW128, TMEM accumulators)",
             "peak_source": src}
 
@@ -716,8 +907,35 @@ def run_e2e(a, torch, psd, x_dev, params, dev):
                     "overlapped on three streams) → pinned host X̂₊"}
 
 
+def relaunch(a):
+    """``--gpus N`` (N > 1) outside torchrun: re-run this script under
+    torch.distributed.run with N ranks (one per GPU, NCCL); never quietly
+    measure one GPU."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {a.gpus} requested, {have} CUDA devices "
+                                                     "visible"}), flush=True)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    sys.exit(subprocess.run(cmd).returncode)
+
+
 def main():
     a = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if a.impl == "ours" and a.config != "c5":
+        if world_env is None and a.gpus > 1:
+            relaunch(a)
+        if world_env is not None and int(world_env) != a.gpus:
+            raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world_env}; launch with "
+                             f"--nproc-per-node equal to --gpus")
     if a.config == "c5":
         run_solver(a)
     elif a.config == "c4":

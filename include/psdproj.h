@@ -233,6 +233,15 @@ int psd_syrk_window(const double* a, int64_t lda, const double* b, int64_t ldb, 
 int psd_fill_sym_gaussian(double* out, int64_t ldo, int64_t r0, int64_t rows, int64_t n,
                           uint64_t seed, double scale, double beta, void* stream);
 
+/* Symmetry statistics of one block pair of a row-sharded X (require_symmetric,
+ * symmetric.py:39-57, when X's (i,j) and (j,i) entries live on different ranks —
+ * SURVEY §8(e)): a = X[rows_g, cols_h] (rows x cols), b = X[rows_h, cols_g]
+ * (cols x rows).  Accumulates into the DEVICE array stats[3] = {max|x|,
+ * max|a_ij - b_ji|, flags (1: not bitwise equal, 2: non-finite) stored as the
+ * bits of an int in stats[2]}; reset != 0 zeroes stats first.  Asynchronous. */
+int psd_pair_defect(const double* a, int64_t lda, const double* b, int64_t ldb, int64_t rows,
+                    int64_t cols, double* stats, int32_t reset, void* stream);
+
 /* ---- solver loop (sdls.py:76-89, :221-245; BASELINE config 5) ---------- */
 /* x = cr + Σ_i y_i A_i: x ← copy(cr) (n x n, the C/ρ term), then for every
  * distinct stored position p: x[pos[p]] += Σ_{t ∈ [ptr[p], ptr[p+1])}
@@ -246,6 +255,11 @@ int psd_sdls_assemble(const double* cr, int64_t n, const int64_t* pos, const int
 int psd_sdls_traces(const double* wd, const double* w, int64_t ldw, int32_t r, const int32_t* rows,
                     const int32_t* cols, const double* vals, const int32_t* cptr, int32_t m,
                     double* t, void* stream);
+/* t_i = Tr(A_i X) = Σ v·X[row][col] over A_i's stored entries for a dense
+ * n x n X (constraint_traces, sdls.py:76-80 — the exact / polar projectors). */
+int psd_sdls_traces_dense(const double* x, int64_t ldx, const int32_t* rows, const int32_t* cols,
+                          const double* vals, const int32_t* cptr, int32_t m, double* t,
+                          void* stream);
 /* grad = b − t; out[0] = ‖grad‖; if out[0] > eps: y += beta·grad (sdls.py:236-245). */
 int psd_sdls_step(const double* b, const double* t, double* y, double* grad, int32_t m,
                   double beta, double eps, double* out, void* stream);

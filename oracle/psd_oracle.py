@@ -104,6 +104,14 @@ def exact_psd_projection(x):
     return (proj + proj.T) / 2.0
 
 
+def polar_psd_projection(x):
+    """symmetric.py:117-128: (X + (XᵀX)^½)/2 with the root from eigh(sym(XᵀX))."""
+    x = require_symmetric(x)
+    dec = eigh(symmetrize(x.T @ x))
+    root = (dec.vectors * np.sqrt(np.maximum(dec.values, 0.0))) @ dec.vectors.T
+    return symmetrize((x + root) / 2.0)
+
+
 def rng_from_seed(seed):
     """symmetric.py:19-28."""
     if isinstance(seed, np.random.Generator):

@@ -96,7 +96,9 @@ def _lagrangian(problem, x, y):
 
 def solve(problem, method, k, l, q, *, power_n=10, scale_factor=1.0, beta=0.5, epsilon=1e-8,
           max_iter=100, y0=None, rng=None, alpha_refresh=1, exact_check_dim=2000):
-    """sdls.py:164-265 (Alg. 6) with the randomized / scaled projectors."""
+    """sdls.py:164-265 (Alg. 6) with any projector: randomized / scaled, or the
+    dense exact (projection.py:162-177, symmetric.py:109-114) / polar
+    (symmetric.py:117-128) ones, which draw nothing but y₀."""
     rng = orc.rng_from_seed(rng)
     scaled = method == "scaled_randomized"
     y = rng.standard_normal(problem.m) if y0 is None else np.asarray(y0, dtype=float).copy()  # :212
@@ -113,9 +115,16 @@ def solve(problem, method, k, l, q, *, power_n=10, scale_factor=1.0, beta=0.5, e
                 alpha_cached = orc.min_eig_magnitude(x_dual, power_n, rng)
             rep = orc.project_scaled(x_dual, k, l, q, alpha_override=alpha_cached,
                                      scale_factor=scale_factor, rng=rng)
+        elif method == "exact":
+            rep = None
+            x_current = orc.exact_psd_projection(x_dual)
+        elif method == "polar":
+            rep = None
+            x_current = orc.polar_psd_projection(x_dual)
         else:
             rep = orc.ran_proj(x_dual, k, l, q, rng=rng)
-        x_current = rep.result
+        if rep is not None:
+            x_current = rep.result
         grad = problem.b - problem.traces(x_current)
         grad_norm = float(np.linalg.norm(grad))
         iterations = it
@@ -126,7 +135,7 @@ def solve(problem, method, k, l, q, *, power_n=10, scale_factor=1.0, beta=0.5, e
             break
         y = y + beta * grad
     exact_residual = None
-    if problem.n <= exact_check_dim:                                     # :247-250
+    if method not in ("exact", "polar") and problem.n <= exact_check_dim:    # :247-250
         x_exact = orc.exact_psd_projection(problem.assemble(y))
         exact_residual = float(np.linalg.norm(problem.traces(x_exact) - problem.b))
     return OracleSolveReport(

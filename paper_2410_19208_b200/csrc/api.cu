@@ -856,7 +856,7 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   }();
   // below n ≈ 3k the per-product residue/CRT passes cost more than DMMA saves
   // (C1 n=1000: 606 vs 697 projections/s; n=2048 par; n=4096: 227 vs 205)
-  const bool oz_size = n >= 3072 || (flags & PSD_FLAG_FP64_INT8);
+  const bool oz_size = (n >= 3072 || (flags & PSD_FLAG_FP64_INT8)) && n <= psd::oz_max_k();
   bool oz = !f32 && oz_on && oz_size && !(flags & PSD_FLAG_FP64_DMMA);
   // reconstruction SYRK on the INT8 engine too (PSD_OZ_SYRK=0 keeps it on DMMA)
   static const bool oz_syrk_on = [] {
@@ -1087,6 +1087,7 @@ int psd_gemm_f64_ozaki(const double* a, int64_t lda, const double* pp, int64_t l
                        int64_t nn, int64_t kk, double* c, int64_t ldc, void* stream) {
   if (!a || !pp || !c) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
   if (m < 1 || nn < 1 || nn > 512 || kk < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad ozaki GEMM shape");
+  if (kk > psd::oz_max_k()) return fail(PSD_ERR_INVALID_PARAMS, "K exceeds the exact-CRT limit 2^18");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const long long chunk = m;   // whole A at once (test entry)
   const size_t bytes = psd::oz_stream_ws_bytes(m, nn, kk, chunk);
@@ -1122,6 +1123,9 @@ int psd_gemm_f64_int8(const double* a, int64_t lda, const double* pp, int64_t ld
   const int r = psd::oz_gemm_stream(a, lda, pp, ldp, m, (int)nn, kk, c, ldc, alpha, s, lds, ws, (size_t)ws_bytes,
                                     chunk_rows > 0 ? chunk_rows : 8192, static_cast<cudaStream_t>(stream));
   if (r == -3) return fail(PSD_ERR_INVALID_PARAMS, "workspace too small (see psd_gemm_f64_int8_ws_bytes)");
+  if (r == -4)
+    return fail(PSD_ERR_INVALID_PARAMS, "K = %lld exceeds the exact-CRT limit %lld of the INT8 emulation "
+                "(use the FP64 DMMA GEMM)", (long long)kk, psd::oz_max_k());
   if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "INT8-emulated GEMM rejected its operands (%d)", r);
   return PSD_OK;
 }
@@ -1334,6 +1338,16 @@ int psd_fill_sym_gaussian(double* out, int64_t ldo, int64_t r0, int64_t rows, in
   return PSD_OK;
 }
 
+int psd_pair_defect(const double* a, int64_t lda, const double* b, int64_t ldb, int64_t rows,
+                    int64_t cols, double* stats, int32_t reset, void* stream) {
+  if (!a || !b || !stats || rows < 0 || cols < 0 || lda < cols || ldb < rows)
+    return fail(PSD_ERR_INVALID_PARAMS, "bad pair_defect arguments");
+  psd::pair_defect(a, lda, b, ldb, rows, cols, stats, reset != 0, static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pair_defect");
+  return PSD_OK;
+}
+
 int psd_sdls_assemble(const double* cr, int64_t n, const int64_t* pos, const int32_t* ptr,
                       const int32_t* econ, const double* evals, const double* y, int32_t npos,
                       double* x, void* stream) {
@@ -1356,6 +1370,16 @@ int psd_sdls_traces(const double* wd, const double* w, int64_t ldw, int32_t r, c
   psd::sdls_traces(wd, w, ldw, r, rows, cols, vals, cptr, m, t, static_cast<cudaStream_t>(stream));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "sdls_traces");
+  return PSD_OK;
+}
+
+int psd_sdls_traces_dense(const double* x, int64_t ldx, const int32_t* rows, const int32_t* cols,
+                          const double* vals, const int32_t* cptr, int32_t m, double* t,
+                          void* stream) {
+  if (!x || !t || m < 0 || ldx < 1) return fail(PSD_ERR_INVALID_PARAMS, "bad sdls_traces_dense");
+  psd::sdls_traces_dense(x, ldx, rows, cols, vals, cptr, m, t, static_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "sdls_traces_dense");
   return PSD_OK;
 }
 

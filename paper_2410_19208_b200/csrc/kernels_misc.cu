@@ -98,6 +98,84 @@ static void sym_stats_t(const T* x, long long n, long long ldx, double* stats, c
   sym_stats_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats);
   count_launch();
 }
+// Off-diagonal block pair of a row-sharded X (SURVEY §8(e) symmetry check):
+// A = X[rows_g, cols_h] (rows × cols, lda) held locally, B = X[rows_h, cols_g]
+// (cols × rows, ldb) received from rank h.  Accumulates into stats (same layout
+// as sym_stats: max|x|, max|a_ij − b_ji|, flags 1 = not bitwise equal,
+// 2 = non-finite).  64×64 tiles, B staged transposed through shared memory.
+__global__ void __launch_bounds__(256, 4) pair_defect_kernel(const double* __restrict__ a, long long lda,
+                                                          const double* __restrict__ b, long long ldb,
+                                                          long long rows, long long cols, long long tiles_c,
+                                                          long long ntiles, double* stats) {
+  __shared__ double tb[kSymT][kSymT + 1];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double mabs = 0.0, mdef = 0.0;
+  int flags = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const long long r0 = (t / tiles_c) * kSymT, c0 = (t % tiles_c) * kSymT;
+    double av[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = ty + 8 * q;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = tx + 32 * h;
+        // b[c0 + r][r0 + c] → smem; a[r0 + r][c0 + c] → registers
+        tb[r][c] = (c0 + r < cols && r0 + c < rows) ? __ldcs(b + (c0 + r) * ldb + r0 + c) : 0.0;
+        av[q][h] = (r0 + r < rows && c0 + c < cols) ? __ldcs(a + (r0 + r) * lda + c0 + c) : 0.0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = ty + 8 * q;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = tx + 32 * h;
+        const double x = av[q][h], y = tb[c][r];   // a[i][j], b[j][i]
+        if (!isfinite(x) || !isfinite(y)) flags |= 2;
+        mabs = fmax(mabs, fmax(fabs(x), fabs(y)));
+        mdef = fmax(mdef, fabs(x - y));
+        if (x != y) flags |= 1;
+      }
+    }
+    __syncthreads();
+  }
+  __shared__ double rmax[8], rdef[8];
+  __shared__ int rfl[8];
+  mabs = warp_max(mabs);
+  mdef = warp_max(mdef);
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (tx == 0) {
+    rmax[ty] = mabs;
+    rdef[ty] = mdef;
+    rfl[ty] = flags;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m1 = 0.0, m2 = 0.0;
+    int f = 0;
+    for (int w = 0; w < 8; ++w) {
+      m1 = fmax(m1, rmax[w]);
+      m2 = fmax(m2, rdef[w]);
+      f |= rfl[w];
+    }
+    if (m1 > 0.0) atomic_max_nonneg(&stats[0], m1);
+    if (m2 > 0.0) atomic_max_nonneg(&stats[1], m2);
+    if (f) atomicOr(reinterpret_cast<int*>(stats + 2), f);
+  }
+}
+
+void pair_defect(const double* a, long long lda, const double* b, long long ldb, long long rows,
+                 long long cols, double* stats, bool reset, cudaStream_t st) {
+  if (reset) cudaMemsetAsync(stats, 0, 3 * sizeof(double), st);
+  if (rows < 1 || cols < 1) return;
+  const long long tr = (rows + kSymT - 1) / kSymT, tc = (cols + kSymT - 1) / kSymT;
+  const long long blocks = std::min<long long>(tr * tc, (long long)device_info().sms * 6);
+  pair_defect_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, lda, b, ldb, rows, cols, tc, tr * tc, stats);
+  count_launch();
+}
+
 // out[0] = max_ij |G_ij − δ_ij| for a w×w Gram (orthogonality defect of Q).
 __global__ void identity_defect_kernel(const double* __restrict__ g, int w, long long ldg, double* out) {
   __shared__ double red[32];

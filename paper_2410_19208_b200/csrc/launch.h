@@ -93,6 +93,7 @@ struct OzOp {
 // (kernel store into host-mapped memory, then a stream sync); > 64 KB: cudaMemcpy
 cudaError_t read_small(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t st);
 int oz_num_moduli();
+long long oz_max_k();   // largest K the exact CRT reconstruction admits (2^18)
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
                      long long ldr, cudaStream_t st);
 int oz_gemm(const OzOp& op, cudaStream_t st);
@@ -124,6 +125,8 @@ void split_transpose(const double* P, long long n, int w, long long ldp, float* 
 // ---- memory-bound kernels --------------------------------------------------
 // stats[0] = max|x|, stats[1] = max|x - xᵀ|, ((int*)(stats+2))[0] = flags
 // (bit0: not bitwise symmetric, bit1: NaN/Inf present). stats zeroed inside.
+void pair_defect(const double* a, long long lda, const double* b, long long ldb, long long rows,
+                 long long cols, double* stats, bool reset, cudaStream_t st);
 void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st);
 // out[0] = max |G − I| over a w×w Gram (single block)
 void identity_defect(const double* g, int w, long long ldg, double* out, cudaStream_t st);
@@ -199,6 +202,8 @@ void sdls_assemble(const double* cr, long long n, const long long* pos, const in
 void sdls_traces(const double* wd, const double* w, long long ldw, int r, const int* rows,
                  const int* cols, const double* vals, const int* cptr, int m, double* t,
                  cudaStream_t st);
+void sdls_traces_dense(const double* x, long long ldx, const int* rows, const int* cols,
+                       const double* vals, const int* cptr, int m, double* t, cudaStream_t st);
 void sdls_step(const double* b, const double* t, double* y, double* grad, int m, double beta,
                double eps, double* out, cudaStream_t st);
 

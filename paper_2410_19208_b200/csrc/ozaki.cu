@@ -6,10 +6,13 @@
 //   B (K×N, fp64) per column to b = rint(p·2^(53−f_j));
 //   for 16 pairwise-coprime moduli m_ℓ ≤ 256 the symmetric residues a mod m_ℓ,
 //   b mod m_ℓ are int8; each (A mod m_ℓ)·(B mod m_ℓ) runs as an exact INT8
-//   GEMM with INT32 TMEM accumulation (|Σ| ≤ K·2^14 < 2^31), reduced mod m_ℓ;
-//   Garner's mixed-radix CRT recovers the exact integer product
-//   C' = Σ_k a_ik b_kj (|C'| ≤ K·2^106 < M/2, M = Π m_ℓ ≈ 2^125.4) and
-//   C = C'·2^(e_i + f_j − 106).
+//   GEMM with INT32 TMEM accumulation (|Σ| ≤ K·2^14 < 2^31 per K split of
+//   ≤ 32768), reduced mod m_ℓ; a direct CRT (Σ_ℓ y_ℓ·M/m_ℓ, quotient by a
+//   float estimate, 128-bit wrap) recovers the exact integer product
+//   C' = Σ_k a_ik b_kj and C = C'·2^(e_i + f_j − 106).  Exactness needs
+//   |C'| ≤ K·2^106 < M/2 (M = Π m_ℓ ≈ 2^125.4), i.e. K < 2^18.4: every entry
+//   point rejects K > kMaxK = 2^18 (|C'|/M ≤ 2^-1.4) and the callers keep such
+//   products on the FP64 DMMA kernel.
 //
 // The only rounding is the 53-bit fixed-point truncation of each row / column
 // (≤ 2^-54 of its largest entry) and the final conversion of C' to double —
@@ -31,6 +34,7 @@ namespace psd {
 namespace oz {
 
 constexpr int kNumMod = 16;
+constexpr long long kMaxK = 1LL << 18;   // CRT exactness: K·2^106 < M/2 (see the header)
 constexpr int kMods[kNumMod] = {256, 255, 253, 251, 247, 241, 239, 233,
                                 229, 227, 223, 217, 211, 199, 197, 193};
 // compile-time modulus tables: inside the residue loops l is a template constant, so
@@ -510,7 +514,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ---- CRT reconstruction + scaling ----------------------------------------------------
 // C[i][j] = C'·2^(e_i + f_j − 106), C' the symmetric residue of the product mod M:
 //   y_ℓ = (Σ_split out[ℓ][s][i][j])·(M/m_ℓ)^{-1} mod m_ℓ,   S = Σ_ℓ y_ℓ·(M/m_ℓ),
-//   S/M = Σ_ℓ y_ℓ/m_ℓ  →  k = rint(Σ_ℓ y_ℓ/m_ℓ) (fp32: |C'|/M ≤ 2^-3, far from ½),
+//   S/M = Σ_ℓ y_ℓ/m_ℓ  →  k = rint(Σ_ℓ y_ℓ/m_ℓ) (fp32, error ≲ 2^-18: |C'|/M ≤
+//   K·2^-19.4 — 0.19 at K = 2^17 (C4), 0.38 at the K ≤ 2^18 limit — stays below ½),
 //   C' = S − k·M evaluated mod 2^128 (|C'| < 2^127, so the wrapped value is exact).
 // Four columns per thread (ldo % 4 == 0; columns ≥ N are padding and not stored).
 // alpha > 0: C = (C + α·S)/α (the shifted sketch of Alg. 3).
@@ -678,6 +683,7 @@ int grid_oz(long long total, int threads) {
 }  // namespace
 
 int oz_num_moduli() { return oz::kNumMod; }
+long long oz_max_k() { return oz::kMaxK; }
 
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
                      long long ldr, cudaStream_t st) {
@@ -723,6 +729,7 @@ int oz_gemm_prepared(const OzOp& op, cudaStream_t st) {
   using namespace oz;
   ensure_oz_constants();
   if (op.M < 1 || op.N < 1 || op.K < 1) return 0;
+  if (op.K > kMaxK) return -4;
   const int w_pad = (op.N + 15) / 16 * 16;
   if (w_pad > 512 || op.ldbr < op.K || op.ldbr % 16 || op.ldar % 16) return -2;
   I8Params p{};
@@ -845,6 +852,7 @@ size_t oz_stream_ws_bytes(long long m, long long n, long long k, long long chunk
 int oz_gemm_stream(const double* a, long long lda, const double* P, long long ldp, long long m, int n,
                    long long k, double* c, long long ldc, double alpha, const double* S, long long lds,
                    void* ws, size_t ws_bytes, long long chunk, cudaStream_t st) {
+  if (k > oz::kMaxK) return -4;
   const OzStreamLayout L = oz_stream_layout(m, n, k, chunk);
   if (ws_bytes < L.total) return -3;
   uint8_t* base = static_cast<uint8_t*>(ws);

@@ -65,6 +65,31 @@ void sdls_traces(const double* wd, const double* w, long long ldw, int r, const 
   count_launch();
 }
 
+// One warp per constraint: t_i = Σ_{entries} v·X[a][b] on a dense n×n X
+// (constraint_traces, sdls.py:76-80, for the exact / polar projectors whose
+// result is formed densely); the lanes split the entries, fixed-order warp sum.
+__global__ void sdls_traces_dense_kernel(const double* __restrict__ x, long long ldx,
+                                         const int* __restrict__ rows, const int* __restrict__ cols,
+                                         const double* __restrict__ vals,
+                                         const int* __restrict__ cptr, int m, double* __restrict__ t) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= m) return;
+  double acc = 0.0;
+  for (int e = cptr[warp] + lane; e < cptr[warp + 1]; e += 32)
+    acc = fma(vals[e], x[(long long)rows[e] * ldx + cols[e]], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) t[warp] = acc;
+}
+
+void sdls_traces_dense(const double* x, long long ldx, const int* rows, const int* cols,
+                       const double* vals, const int* cptr, int m, double* t, cudaStream_t st) {
+  if (m <= 0) return;
+  const int warps_per_block = 8;
+  sdls_traces_dense_kernel<<<(m + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0,
+                             st>>>(x, ldx, rows, cols, vals, cptr, m, t);
+  count_launch();
+}
+
 // grad = b − t; out[0] = ‖grad‖₂ (fixed-order reduction); if out[0] > eps:
 // y ← y + β·grad (sdls.py:236-245).  Single block.
 __global__ void sdls_step_kernel(const double* __restrict__ b, const double* __restrict__ t,

@@ -56,9 +56,11 @@ def install(psdcone_module=None):
     ref = psdcone_module or importlib.import_module("psdcone")
     ref_errors = importlib.import_module(ref.__name__ + ".errors")
     for name in list(errors.REGISTRY):
+        _SAVED.setdefault(("errors", name), errors.REGISTRY[name])
         if hasattr(ref_errors, name):
-            _SAVED.setdefault(("errors", name), errors.REGISTRY[name])
             errors.REGISTRY[name] = getattr(ref_errors, name)
+        else:  # DeviceError has no reference analogue: catchable as psdcone.PsdconeError too
+            errors.REGISTRY[name] = type(name, (errors.REGISTRY[name], ref_errors.PsdconeError), {})
     # our ProjectorConfig/RangeParams validation must accept the reference's objects too
     for (modname, attr), impl in _TARGETS.items():
         modname = modname.replace("psdcone", ref.__name__, 1)
@@ -67,6 +69,15 @@ def install(psdcone_module=None):
             _SAVED.setdefault((modname, attr), getattr(mod, attr))
             setattr(mod, attr, getattr(ours, impl))
     return ref
+
+
+def original(modname, attr):
+    """The reference implementation ``install()`` replaced (e.g. to compare
+    against it while installed); ``None`` if that name was not rebound."""
+    for (mod, name), val in _SAVED.items():
+        if name == attr and mod.split(".", 1)[-1] == modname.split(".", 1)[-1] and mod != "errors":
+            return val
+    return None
 
 
 def uninstall():

@@ -238,10 +238,18 @@ def _exact_report(op, method, t0):
                             wall_time=time.perf_counter() - t0, factors=factors, basis_width=n)
 
 
+def config_dtype(cfg):
+    """Compute dtype of a config.  The reference's ``ProjectorConfig``
+    (projection.py:24-49) has no ``dtype`` field: after ``install()`` its
+    instances reach this dispatcher and run the reference's float64 semantics."""
+    return resolve_dtype(getattr(cfg, "dtype", None))
+
+
 def project(x, cfg, rng=None, *, omega=None, assume_symmetric=False):
-    """projection.py:180-223: dispatcher with the scaled → unscaled AlphaTooSmall fallback."""
+    """projection.py:180-223: dispatcher with the scaled → unscaled AlphaTooSmall fallback.
+    ``cfg`` is this package's ``ProjectorConfig`` or the reference's own."""
     t0 = time.perf_counter()
-    op = _operand(x, cfg.dtype)
+    op = _operand(x, config_dtype(cfg))
     require_square(op)
     stats = _stats_for(op, assume_symmetric)                   # projection.py:189
     if cfg.method in ("exact", "polar"):

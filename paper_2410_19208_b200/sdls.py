@@ -129,6 +129,13 @@ class _DeviceProblem:
             _native.ptr(out), _native.stream_handle(self.device)))
         return out
 
+    def traces_dense(self, x, out):
+        _native.check(self.lib.psd_sdls_traces_dense(
+            _native.ptr(x), x.stride(0), _native.ptr(self.crow), _native.ptr(self.ccol),
+            _native.ptr(self.cval), _native.ptr(self.cptr), self.m, _native.ptr(out),
+            _native.stream_handle(self.device)))
+        return out
+
     def traces(self, wd, w, r, out):
         _native.check(self.lib.psd_sdls_traces(
             _native.ptr(wd), _native.ptr(w), w.stride(0) if r else 1, r, _native.ptr(self.crow),
@@ -164,14 +171,17 @@ def _factored_projection(x_dual, n, cfg, rng, lib, plan, device, fw, fd, alpha):
 
 def solve(problem, proj=None, *, beta=0.5, epsilon=1e-8, max_iter=100, y0=None, rng=None,
           alpha_refresh=1, keep_trajectory=False, exact_check_dim=2000, device=None):
-    """sdls.py:164-265 on the GPU (randomized / scaled_randomized projectors)."""
+    """sdls.py:164-265 on the GPU.  ``proj`` is this package's ``ProjectorConfig``
+    or the reference's (after ``install()``); the default is the exact projector,
+    as in the reference.  Randomized / scaled projectors keep X₊ factored inside
+    the loop; exact / polar form it densely (full eigensolve on the device)."""
     if epsilon <= 0 or beta <= 0 or max_iter < 1:
         raise errors.error("InvalidParams", "need epsilon > 0, beta > 0, max_iter >= 1")
     proj = proj or ProjectorConfig(method="exact")
-    if proj.method not in ("randomized", "scaled_randomized"):
-        raise errors.error("InvalidParams",
-                           "the device solver runs the randomized projectors (exact/polar: use project)")
     rng = rng_from_seed(rng)
+    if proj.method in ("exact", "polar"):
+        return _solve_dense(problem, proj, beta, epsilon, max_iter, y0, rng, keep_trajectory,
+                            device)
     t0 = time.perf_counter()
     prob = SparseSdlsProblem.from_reference(problem)
     dev = torch.device(device) if device else default_device()
@@ -266,4 +276,70 @@ def solve(problem, proj=None, *, beta=0.5, epsilon=1e-8, max_iter=100, y0=None, 
         trajectory=trajectory,
         y_trajectory=y_trajectory,
         exact_feasibility_residual=exact_residual,
+    )
+
+
+def _solve_dense(problem, proj, beta, epsilon, max_iter, y0, rng, keep_trajectory, device):
+    """sdls.py:189-265 with the exact / polar projector: per iteration the dual
+    matrix is assembled on the device, projected densely by ``project`` (device
+    eigensolve, projection.py:162-177), and Tr(AᵢX₊) is read from the dense X₊ on
+    the constraint nonzeros (``psd_sdls_traces_dense``).  No RNG is drawn except
+    y₀ (sdls.py:212); the exact-residual check only applies to randomized runs
+    (sdls.py:247)."""
+    from .projection import project
+    t0 = time.perf_counter()
+    prob = SparseSdlsProblem.from_reference(problem)
+    dev = torch.device(device) if device else default_device()
+    lib = _native.load_library()
+    dp = _DeviceProblem(prob, dev)
+    n, m = prob.n, prob.m
+    x_dual = torch.empty((n, n), dtype=torch.float64, device=dev)
+    if m == 0:
+        dp.assemble(torch.zeros(1, dtype=torch.float64, device=dev), x_dual)
+        res = project(x_dual, proj, rng).result
+        misfit = res - dp.cr
+        return SolveReport(res.cpu().numpy(), np.zeros(0), 0, 0.0, 0.0,
+                           0.5 * float((misfit * misfit).sum().item()), proj.method, True,
+                           time.perf_counter() - t0)
+    y_host = rng.standard_normal(m) if y0 is None else np.asarray(y0, dtype=float).ravel()
+    if y_host.size != m:
+        raise errors.error("DimensionMismatch", f"y has length {y_host.size}, expected m = {m}")
+    y = torch.from_numpy(y_host.copy()).to(dev)
+    t = torch.empty(m, dtype=torch.float64, device=dev)
+    grad = torch.zeros(m, dtype=torch.float64, device=dev)
+    nrm = torch.zeros(1, dtype=torch.float64, device=dev)
+    trajectory = [] if keep_trajectory else None
+    y_trajectory = [] if keep_trajectory else None
+    iterations, converged, x_current = 0, False, None
+    for it in range(1, max_iter + 1):                                # sdls.py:221-245
+        dp.assemble(y, x_dual)
+        if keep_trajectory:
+            y_trajectory.append(y.cpu().numpy())
+        x_current = project(x_dual, proj, rng).result
+        dp.traces_dense(x_current, t)
+        _native.check(lib.psd_sdls_step(_native.ptr(dp.b), _native.ptr(t), _native.ptr(y),
+                                        _native.ptr(grad), m, float(beta), float(epsilon),
+                                        _native.ptr(nrm), _native.stream_handle(dev)))
+        grad_norm = float(nrm.item())
+        iterations = it
+        if keep_trajectory:
+            trajectory.append(TrajectoryPoint(it, grad_norm, grad_norm))
+        if grad_norm <= epsilon:
+            converged = True
+            break
+    misfit = x_current - dp.cr
+    objective = 0.5 * float((misfit * misfit).sum().item())
+    objective -= float(torch.dot(y, t - dp.b).item())                # sdls.py:103-108
+    return SolveReport(
+        x_solution=x_current.cpu().numpy(),
+        y_final=y.cpu().numpy(),
+        iterations=iterations,
+        grad_norm_final=float(torch.linalg.vector_norm(grad).item()),
+        feasibility_residual=float(torch.linalg.vector_norm(t - dp.b).item()),
+        objective=objective,
+        projection_method=proj.method,
+        converged=converged,
+        wall_time=time.perf_counter() - t0,
+        trajectory=trajectory,
+        y_trajectory=y_trajectory,
     )

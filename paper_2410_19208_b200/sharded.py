@@ -14,10 +14,20 @@ exactly the exchanges of the reference algorithm's data flow
 replicated (identical all-reduced T on every rank ⇒ identical eigenpairs).
 Rank g returns its row block X̂₊[rows_g, :] = (W_g·D)·Wᵀ.
 
-X must be bitwise symmetric (every BASELINE config is, by construction): then
-(XᵀY)_g = X_g·Y and no reduce-scatter is needed.  The exact symmetry check
-needs the (j, i) tiles that live on other ranks (≈ an all-to-all of X), so it
-is skipped here and stated by the caller.
+Symmetry.  ``symmetric="check"`` (the default) runs the
+reference's ``require_symmetric`` (symmetric.py:39-57, called at
+projection.py:100) on the sharded X: the diagonal block locally and every
+off-diagonal block pair (X[rows_g, cols_h], X[rows_h, cols_g]) exchanged
+point-to-point in row chunks — one pass over X, ≈ 1/G of it per rank over
+NVLink — with a global max|x| / max|x − xᵀ| reduction; an X outside the
+tolerance raises ``AsymmetricMatrixError``.  For a bitwise-symmetric X
+(every BASELINE config, by construction) (XᵀY)_g = X_g·Y, so the Xᵀ product of
+the power scheme (sketch.py:79) is the same all-gather + local GEMM as the X
+products.  For an X that is symmetric only within tolerance the Xᵀ product
+keeps the reference's semantics: each rank forms the full-height partial
+X_gᵀ·Y_g and a reduce-scatter sums Σ_h X_hᵀ Y_h into the row blocks (the same
+volume as the all-gather it replaces).  ``symmetric="assume"`` skips the check
+for inputs the caller guarantees bitwise symmetric (the C4 generator).
 
 The arithmetic goes through an ``ops`` object: ``KernelOps`` binds the
 libpsdproj.so kernels (the product path); tests bind a numpy stand-in to
@@ -38,6 +48,9 @@ from . import _native, errors
 
 RANK_TRUNCATION_FACTOR = 1e-12  # sketch.py:12
 U64 = 1.1102230246251565e-16
+SYM_TOL_FACTOR = 1e-10          # symmetric.py:16
+INT8_MAX_K = 1 << 18            # largest K of the exact INT8 emulation (csrc/ozaki.cu)
+SYM_CHUNK_ROWS = 8192           # row chunk of the symmetry-check block exchange
 
 
 def row_split(n, world):
@@ -51,22 +64,63 @@ def row_split(n, world):
 
 
 class Comm:
-    """torch.distributed collectives over row blocks (pads uneven blocks)."""
+    """torch.distributed collectives over row blocks.  Equal row blocks (n
+    divisible by the world size, as at C4) gather straight into the n×w panel
+    and reduce-scatter straight out of the full-height partial; uneven blocks go
+    through one padded staging buffer."""
 
     def __init__(self, group=None):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
 
+    def _sizes(self, starts):
+        return [starts[g + 1] - starts[g] for g in range(self.world)]
+
     def all_gather_rows(self, local, starts):
+        """The full panel (n × w) from every rank's row block."""
         if self.world == 1:
             return local
-        rows = max(starts[g + 1] - starts[g] for g in range(self.world))
-        pad = local.new_zeros((rows,) + tuple(local.shape[1:]))
+        sizes = self._sizes(starts)
+        rows = max(sizes)
+        tail = tuple(local.shape[1:])
+        if min(sizes) == rows:
+            full = local.new_empty((starts[-1],) + tail)
+            dist.all_gather_into_tensor(full, local.contiguous(), group=self.group)
+            return full
+        pad = local.new_zeros((rows,) + tail)
         pad[: local.shape[0]] = local
-        parts = [torch.empty_like(pad) for _ in range(self.world)]
-        dist.all_gather(parts, pad, group=self.group)
-        return torch.cat([parts[g][: starts[g + 1] - starts[g]] for g in range(self.world)], 0)
+        staged = local.new_empty((self.world * rows,) + tail)
+        dist.all_gather_into_tensor(staged, pad, group=self.group)
+        full = local.new_empty((starts[-1],) + tail)
+        for g in range(self.world):
+            full[starts[g]:starts[g + 1]] = staged[g * rows: g * rows + sizes[g]]
+        return full
+
+    def reduce_scatter_rows(self, full, starts):
+        """This rank's row block of Σ_ranks full (each rank holds an n × w partial)."""
+        if self.world == 1:
+            return full
+        sizes = self._sizes(starts)
+        rows = max(sizes)
+        tail = tuple(full.shape[1:])
+        out = full.new_empty((rows,) + tail)
+        if min(sizes) == rows:
+            dist.reduce_scatter_tensor(out, full.contiguous(), op=dist.ReduceOp.SUM, group=self.group)
+            return out
+        staged = full.new_zeros((self.world * rows,) + tail)
+        for g in range(self.world):
+            staged[g * rows: g * rows + sizes[g]] = full[starts[g]:starts[g + 1]]
+        dist.reduce_scatter_tensor(out, staged, op=dist.ReduceOp.SUM, group=self.group)
+        return out[: sizes[self.rank]]
+
+    def exchange(self, send, dst, recv, src):
+        """Point-to-point: send ``send`` to rank dst while receiving ``recv`` from src."""
+        ops = [dist.P2POp(dist.isend, send, dst, group=self.group),
+               dist.P2POp(dist.irecv, recv, src, group=self.group)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        return recv
 
     def all_reduce_sum(self, t):
         if self.world > 1:
@@ -109,6 +163,7 @@ class KernelOps:
         n = panel.shape[1]
         eng = projection._FP64_ENGINE
         use = eng == "int8" or (eng == "auto" and k >= projection.INT8_MIN_N)
+        use = use and k <= INT8_MAX_K      # exact CRT needs K ≤ 2^18 (ozaki.cu kMaxK)
         if not use or x_rows.stride(1) != 1 or panel.stride(1) != 1:
             return self.matmul(x_rows, panel, shift_alpha=shift_alpha, shift_src=shift_src)
         out = self.empty((m, n))
@@ -198,6 +253,21 @@ class KernelOps:
                                                _native.ptr(out), out.stride(0), self._stream()))
         return out
 
+    def sym_stats(self):
+        """Zeroed device accumulator for pair_defect: {max|x|, max defect, flags}."""
+        return torch.zeros(3, dtype=torch.float64, device=self.device)
+
+    def pair_defect(self, a, b, stats):
+        """Accumulate max|x|, max|a_ij − b_ji| and flags of a block pair."""
+        _native.check(self.lib.psd_pair_defect(_native.ptr(a), a.stride(0), _native.ptr(b), b.stride(0),
+                                               a.shape[0], a.shape[1], _native.ptr(stats), 0,
+                                               self._stream()))
+        return stats
+
+    def read_stats(self, stats):
+        h = stats.cpu()
+        return float(h[0]), float(h[1]), int(h.view(torch.int32)[4])
+
     def max_abs(self, x):
         out = self.empty((1,))
         _native.check(self.lib.psd_max_abs(_native.ptr(x), x.shape[0], x.shape[1], x.stride(0),
@@ -217,6 +287,7 @@ class ShardReport:
     alpha_used: float | None = None
     qr_passes: int = 0
     qr_shifted: bool = False
+    bitwise_symmetric: bool | None = None   # None: symmetric="assume" (not checked)
 
 
 def _dist_cholqr(ops, comm, y_loc, starts, n_total, rdiag=None):
@@ -264,12 +335,49 @@ def _dist_cholqr(ops, comm, y_loc, starts, n_total, rdiag=None):
     return cur, rd, frob, passes, shifted, False
 
 
+def sharded_symmetry_stats(x_rows, row_start, n, comm, ops, chunk_rows=SYM_CHUNK_ROWS):
+    """Global (max|x|, max|x − xᵀ|, bitwise, finite) of a row-sharded X: the
+    diagonal block locally, every off-diagonal block pair exchanged
+    point-to-point (ring schedule: at step s rank g sends X[rows_g, cols_{g+s}]
+    to g+s and receives X[rows_{g−s}, cols_g] from g−s), in row chunks of the
+    sender so each message is ≤ chunk_rows × n_g doubles."""
+    starts = row_split(n, comm.world)
+    g = comm.rank
+    r0, r1 = starts[g], starts[g + 1]
+    stats = ops.sym_stats()
+    diag = x_rows[:, r0:r1]
+    ops.pair_defect(diag, diag, stats)
+    for s in range(1, comm.world):
+        dst, src = (g + s) % comm.world, (g - s) % comm.world
+        d0, d1 = starts[dst], starts[dst + 1]
+        s0, s1 = starts[src], starts[src + 1]
+        nchunks = max(math.ceil((r1 - r0) / chunk_rows), math.ceil((s1 - s0) / chunk_rows), 1)
+        for c in range(nchunks):
+            a0, a1 = min(c * chunk_rows, r1 - r0), min((c + 1) * chunk_rows, r1 - r0)
+            b0, b1 = min(c * chunk_rows, s1 - s0), min((c + 1) * chunk_rows, s1 - s0)
+            send = x_rows[a0:a1, d0:d1].contiguous()          # X[rows_g chunk, cols_dst]
+            recv = x_rows.new_empty((b1 - b0, r1 - r0))       # X[rows_src chunk, cols_g]
+            comm.exchange(send, dst, recv, src)
+            if b1 > b0:
+                # a = X[rows_g, cols_src chunk] (n_g × c), b = X[rows_src chunk, cols_g] (c × n_g)
+                ops.pair_defect(x_rows[:, s0 + b0:s0 + b1], recv, stats)
+    mx, defect, flags = ops.read_stats(stats)
+    red = torch.tensor([mx, defect, float(flags & 1), float((flags >> 1) & 1)], dtype=torch.float64,
+                       device=x_rows.device)
+    comm.all_reduce_max(red)
+    return float(red[0]), float(red[1]), red[2].item() == 0.0, red[3].item() == 0.0
+
+
 def sharded_ran_proj(x_rows, row_start, n, omega, params, *, alpha=0.0, comm=None, ops=None,
-                     want_result=True, strict=False):
-    """Alg. 2 (alpha = 0) / Alg. 3 (alpha > 0) on a row-sharded bitwise-symmetric X.
+                     want_result=True, strict=False, symmetric="check", tol=None):
+    """Alg. 2 (alpha = 0) / Alg. 3 (alpha > 0) on a row-sharded X.
 
     x_rows: this rank's rows [row_start, row_start + n_g) of X (n_g × n).
     omega:  the full n × (k+l) Gaussian test matrix (identical on all ranks).
+    symmetric: "check" — require_symmetric on the sharded X (raises
+        AsymmetricMatrixError like projection.py:100); Xᵀ products by
+        reduce-scatter unless X is bitwise symmetric.  "assume" — the caller
+        guarantees a bitwise-symmetric X; no check.
     """
     comm = comm or Comm()
     ops = ops or KernelOps(x_rows.device)
@@ -280,10 +388,24 @@ def sharded_ran_proj(x_rows, row_start, n, omega, params, *, alpha=0.0, comm=Non
                            f"rank {comm.rank} holds rows [{row_start}, {row_start + x_rows.shape[0]}), "
                            f"expected [{r0}, {r1})")
     width = params.width
+    if symmetric not in ("check", "assume"):
+        raise errors.error("InvalidParams", f"symmetric must be 'check' or 'assume', got {symmetric!r}")
+    bitwise, mx = True, None
+    if symmetric == "check":                                    # projection.py:100
+        mx, defect, bitwise, finite = sharded_symmetry_stats(x_rows, row_start, n, comm, ops)
+        limit = SYM_TOL_FACTOR * max(1.0, mx) if tol is None else float(tol)
+        if not finite:
+            raise errors.error("ConvergenceFailure", "matrix has non-finite entries")
+        if defect > limit:
+            raise errors.error("AsymmetricMatrixError",
+                               f"matrix is not symmetric: max asymmetry {defect:.3e} exceeds "
+                               f"tolerance {limit:.3e}")
+    checked = bitwise if symmetric == "check" else None
     if width > n:
         raise errors.error("InvalidParams", f"k+l = {width} exceeds min(m, n) = {n}")
     if alpha > 0.0:  # projection.py:133-137 with a global max|x|
-        mx = comm.all_reduce_max(ops.max_abs(x_rows)).item()
+        if mx is None:
+            mx = comm.all_reduce_max(ops.max_abs(x_rows)).item()
         alpha_tol = 1e-12 * max(1.0, mx)
         if alpha <= alpha_tol:
             raise errors.error("AlphaTooSmall",
@@ -296,12 +418,27 @@ def sharded_ran_proj(x_rows, row_start, n, omega, params, *, alpha=0.0, comm=Non
             return mul(x_rows, panel_full, shift_alpha=alpha, shift_src=panel_full[r0:r1])
         return mul(x_rows, panel_full)
 
+    def xtmul(y_loc):
+        # (Xᵀ Y)_g (sketch.py:79).  Bitwise-symmetric X: X_g·Y after an all-gather.
+        # Otherwise Σ_h X_hᵀ Y_h by reduce-scatter; scaled: each rank's partial is
+        # (X_hᵀ Y_h + α·S_h)/α with S_h = Y_h in rows_h (zero elsewhere), so the sum
+        # is BᵀY = (XᵀY + αY)/α.
+        if bitwise:
+            return xmul(comm.all_gather_rows(y_loc, starts))
+        if alpha > 0.0:
+            shift = ops.empty((n, y_loc.shape[1])).zero_()
+            shift[r0:r1] = y_loc
+            part = ops.matmul(x_rows, y_loc, a_trans=True, shift_alpha=alpha, shift_src=shift)
+        else:
+            part = ops.matmul(x_rows, y_loc, a_trans=True)
+        return comm.reduce_scatter_rows(part, starts)
+
     stabilize = params.q >= 2                                   # sketch.py:74
     y = xmul(omega)                                             # sketch.py:75
     for _ in range(params.q):                                   # sketch.py:76-82
         if stabilize:
             y = _dist_cholqr(ops, comm, y, starts, n)[0]
-        z = xmul(comm.all_gather_rows(y, starts))               # (Xᵀ Y)_g = X_g Y (bitwise symmetric)
+        z = xtmul(y)                                            # sketch.py:79
         if stabilize:
             z = _dist_cholqr(ops, comm, z, starts, n)[0]
         y = xmul(comm.all_gather_rows(z, starts))
@@ -320,7 +457,7 @@ def sharded_ran_proj(x_rows, row_start, n, omega, params, *, alpha=0.0, comm=Non
     if wk == 0:
         return ShardReport(None if not want_result else ops.empty((r1 - r0, n)).zero_(), r0, r1, 0, 0,
                            ops.empty((r1 - r0, 0)), ops.empty((0,)), alpha if alpha > 0 else None,
-                           passes, shifted)
+                           passes, shifted, checked)
     q_full = comm.all_gather_rows(q_loc, starts)
     c_loc = xmul(q_full)                                        # (X Q)_g or (B Q)_g
     t = comm.all_reduce_sum(ops.gram(q_loc, c_loc))             # Σ_g Q_gᵀ (X Q)_g
@@ -334,7 +471,7 @@ def sharded_ran_proj(x_rows, row_start, n, omega, params, *, alpha=0.0, comm=Non
     if r == 0:
         res = ops.empty((r1 - r0, n)).zero_() if want_result else None
         return ShardReport(res, r0, r1, 0, wk, ops.empty((r1 - r0, 0)), d,
-                           alpha if alpha > 0 else None, passes, shifted)
+                           alpha if alpha > 0 else None, passes, shifted, checked)
     u = vecs[:, :r].contiguous()
     w_loc = ops.matmul(q_loc, u)                                # W_g = Q_g U₊
     res = None
@@ -343,4 +480,5 @@ def sharded_ran_proj(x_rows, row_start, n, omega, params, *, alpha=0.0, comm=Non
         # all ranks assemble into a bitwise-symmetric X̂₊ (projection.py:78)
         w_full = comm.all_gather_rows(w_loc, starts)
         res = ops.syrk_window(ops.scale_columns(w_full, d), w_full, r0, r1)
-    return ShardReport(res, r0, r1, r, wk, w_loc, d, alpha if alpha > 0 else None, passes, shifted)
+    return ShardReport(res, r0, r1, r, wk, w_loc, d, alpha if alpha > 0 else None, passes, shifted,
+                       checked)

@@ -206,6 +206,26 @@ def solver_cases():
               iterations=rep.iterations, exact_residual=rep.exact_feasibility_residual)
 
 
+def solver_dense_cases():
+    """Reference solve() with the exact projector (its default, sdls.py:187) and
+    the polar projector: no sketch RNG, dense X₊ every iteration."""
+    from oracle import sdls_oracle as so
+    for name, method, n, m in (("sdls_exact", "exact", 32, 10), ("sdls_polar", "polar", 28, 8)):
+        sp = so.config5_instance(n, m, nnz_per=4, seed=321 + n)
+        dense = np.zeros((m, n, n))
+        np.add.at(dense, (sp.con, sp.rows, sp.cols), sp.vals)
+        beta = so.lipschitz_beta(sp)
+        problem = psdcone.SdlsProblem(sp.c, 1.0, list(zip(dense, sp.b)))
+        cfg = None if method == "exact" else ProjectorConfig(method=method)
+        rep = psdcone.solve(problem, cfg, beta=beta, epsilon=1e-14, max_iter=20, rng=8,
+                            keep_trajectory=True)
+        _save(name, c=sp.c, con=sp.con, rows=sp.rows, cols=sp.cols, vals=sp.vals, b=sp.b,
+              n=n, m=m, beta=beta, seed=8, method=method, y_final=rep.y_final,
+              grad_norms=np.array([t.grad_norm for t in rep.trajectory]),
+              x_solution=rep.x_solution, objective=rep.objective,
+              iterations=rep.iterations, feasibility=rep.feasibility_residual)
+
+
 def sweep_cases():
     """Reference projection_error_sweep (experiments.py:78-137) and bounds (bounds.py)."""
     from psdcone import bounds as rb
@@ -241,7 +261,10 @@ if __name__ == "__main__":
     import sys as _sys
     if "--sweep-only" in _sys.argv:
         sweep_cases()
+    elif "--dense-solver-only" in _sys.argv:
+        solver_dense_cases()
     else:
         main()
         solver_cases()
+        solver_dense_cases()
         sweep_cases()

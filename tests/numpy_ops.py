@@ -67,3 +67,17 @@ class NumpyOps:
 
     def max_abs(self, x):
         return _t(np.array([np.abs(_np(x)).max()]))
+
+    def sym_stats(self):
+        return [0.0, 0.0, 0]
+
+    def pair_defect(self, a, b, stats):
+        A, B = _np(a), _np(b)
+        if A.size:
+            stats[0] = max(stats[0], float(np.abs(A).max()), float(np.abs(B).max()))
+            stats[1] = max(stats[1], float(np.abs(A - B.T).max()))
+            stats[2] |= (1 if np.any(A != B.T) else 0) | (0 if np.all(np.isfinite(A)) else 2)
+        return stats
+
+    def read_stats(self, stats):
+        return float(stats[0]), float(stats[1]), int(stats[2])

@@ -129,7 +129,9 @@ def test_rank_deficient_sketch_within_reference_sensitivity(ours, k, l, q, alpha
     """X of numerical rank 60 (+1e-4 noise), n ≥ 3072 (INT8 products and reconstruction).
     With the sketch wider than that rank at q = 1 the reference's own output moves by
     ~1e-9 under a one-ulp perturbation of X; ours must stay within 10× of that (and
-    within 1e-10 whenever the problem is well conditioned)."""
+    within 1e-10 whenever the problem is well conditioned).  The reference's
+    sensitivity is the larger of two independent one-ulp perturbations, and ours must
+    stay within 2x of it (README "Parity bar": the ill-conditioned exception)."""
     from oracle import psd_oracle as orc
     rs = np.random.default_rng(k + l + q)
     n = 3100
@@ -141,9 +143,12 @@ def test_rank_deficient_sketch_within_reference_sensitivity(ours, k, l, q, alpha
     run = (lambda xx: orc.ran_proj_scal(xx, k, l, q, alpha, omega=om)) if alpha > 0 else \
         (lambda xx: orc.ran_proj(xx, k, l, q, omega=om))
     ref = run(x)
-    e = rs.choice([-1.0, 1.0], (n, n))
-    e = np.triu(e) + np.triu(e, 1).T
-    sens = np.linalg.norm(run(x * (1 + 2.0 ** -53 * e)).result - ref.result) / np.linalg.norm(ref.result)
+    sens = 0.0
+    for _ in range(2):
+        e = rs.choice([-1.0, 1.0], (n, n))
+        e = np.triu(e) + np.triu(e, 1).T
+        sens = max(sens, np.linalg.norm(run(x * (1 + 2.0 ** -53 * e)).result - ref.result)
+                   / np.linalg.norm(ref.result))
     xd, omd = torch.from_numpy(x).cuda(), torch.from_numpy(om).cuda()
     prm = ours.RangeParams(k=k, l=l, q=q)
     rep = ours.ran_proj_scal(xd, prm, alpha, None, omega=omd) if alpha > 0 else ours.ran_proj(xd, prm, None, omega=omd)
@@ -151,4 +156,4 @@ def test_rank_deficient_sketch_within_reference_sensitivity(ours, k, l, q, alpha
         assert rep.device_info["recon_engine"] == 1
     assert rep.basis_width == ref.basis_width and rep.effective_rank == ref.effective_rank
     err = np.linalg.norm(rep.result.cpu().numpy() - ref.result) / np.linalg.norm(ref.result)
-    assert err <= max(1e-10, 10 * sens), (err, sens)
+    assert err <= max(1e-10, 2 * sens), (err, sens)

@@ -248,3 +248,114 @@ def test_solver_loop_matches_reference(ours, name):
     assert _rel(rep.x_solution, d["x_solution"]) <= 1e-9
     assert rep.objective == pytest.approx(float(d["objective"]), rel=1e-8)
     assert rep.exact_feasibility_residual == pytest.approx(float(d["exact_residual"]), rel=1e-6)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("seed", [1, 2])
+def test_config3_full_size_fp64(ours, seed):
+    """BASELINE config 3 at FULL size (n = 32768, k = 256, p = 16, q = 1) on the default
+    engines (INT8-emulated FP64 products + INT8 reconstruction) against the CPU oracle
+    on the identical X and Ω; the whole n×n result must be bitwise symmetric (checked
+    on the device by the require_symmetric kernel)."""
+    import torch
+    from paper_2410_19208_b200 import workloads
+    from paper_2410_19208_b200.symmetric import check_symmetric_device
+    from paper_2410_19208_b200._tensors import Operand
+    n, k, p, q = 32768, 256, 16, 1
+    dev = torch.device("cuda", 0)
+    xd = workloads.c3_device(n, seed=seed, device=dev)
+    om = np.random.default_rng(seed + 100).standard_normal((n, k + p))
+    rep = ours.ran_proj(xd, ours.RangeParams(k=k, l=p, q=q), None, omega=torch.from_numpy(om).to(dev))
+    assert rep.device_info["sketch_engine"] == 1 and rep.device_info["recon_engine"] == 1
+    stats = check_symmetric_device(Operand(rep.result, "torch_cuda", dev))
+    assert stats.bitwise and stats.defect == 0.0
+    res = rep.result.cpu().numpy()
+    x = xd.cpu().numpy()
+    del xd, rep
+    torch.cuda.empty_cache()
+    o = orc.ran_proj(x, k, p, q, omega=om)
+    del x
+    assert res.shape == o.result.shape
+    err = _rel(res, o.result)
+    assert err <= TOL, err
+
+
+def test_config4_shape_reduced_n(ours):
+    """C4's k = 512, p = 32, q = 2 (w = 544: the INT8 engine runs the panel as two
+    column groups; q = 2 re-orthonormalises between products) at n = 8192, through
+    the row-sharded driver with the real kernels on one rank, X from the C4 row
+    generator (bitwise symmetric, checked)."""
+    import torch
+    from paper_2410_19208_b200 import workloads
+    from paper_2410_19208_b200.sharded import KernelOps, sharded_ran_proj
+    n, k, p, q = 8192, 512, 32, 2
+    xd = workloads.c4_rows(n, 0, n, seed=5)
+    om = np.random.default_rng(6).standard_normal((n, k + p))
+    ops = KernelOps("cuda")
+    rep = sharded_ran_proj(xd, 0, n, torch.from_numpy(om).cuda(), ours.RangeParams(k=k, l=p, q=q),
+                           ops=ops)
+    assert ops.int8_products == 2 * q + 2 and rep.bitwise_symmetric is True
+    res = rep.result_rows.cpu().numpy()
+    ref = orc.ran_proj(xd.cpu().numpy(), k, p, q, omega=om)
+    assert rep.basis_width == ref.basis_width and rep.effective_rank == ref.effective_rank
+    assert np.array_equal(res, res.T)
+    assert _rel(res, ref.result) <= TOL
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.5])
+def test_sharded_single_rank_transposed_branch(ours, alpha):
+    """X symmetric only within tolerance: the sharded driver's Xᵀ product takes the
+    reduce-scatter branch (Σ_h X_hᵀ Y_h on the DMMA A-transposed kernel; one rank
+    here) and must reproduce the reference's x.T @ y (sketch.py:79)."""
+    import torch
+    from paper_2410_19208_b200.sharded import KernelOps, sharded_ran_proj
+    n, k, l, q = 1500, 40, 8, 2
+    x = orc.wigner(n, seed=31) + 3e-12 * np.random.default_rng(32).standard_normal((n, n))
+    om = np.random.default_rng(33).standard_normal((n, k + l))
+    ref = orc.ran_proj_scal(x, k, l, q, alpha, omega=om) if alpha > 0 else orc.ran_proj(x, k, l, q, omega=om)
+    rep = sharded_ran_proj(torch.from_numpy(x).cuda(), 0, n, torch.from_numpy(om).cuda(),
+                           ours.RangeParams(k=k, l=l, q=q), alpha=alpha, ops=KernelOps("cuda"))
+    assert rep.bitwise_symmetric is False
+    assert rep.effective_rank == ref.effective_rank
+    assert _rel(rep.result_rows.cpu().numpy(), ref.result) <= TOL
+    bad = x.copy()
+    bad[3, 1000] += 1e-6
+    with pytest.raises(ours.AsymmetricMatrixError):
+        sharded_ran_proj(torch.from_numpy(bad).cuda(), 0, n, torch.from_numpy(om).cuda(),
+                         ours.RangeParams(k=k, l=l, q=q), ops=KernelOps("cuda"))
+
+
+def test_solver_config5_shape_trajectory(ours):
+    """A config-5-shaped run (sparse A_i with 4 mirrored off-diagonal N(0,1) entries,
+    C = Wigner + 2I, β = 1/L, randomized projector k = 64, q = 1) at n = 1024,
+    m = 4000 for 50 iterations against the oracle's sparse restatement of
+    psdcone.solve (sdls.py:164-265) on the same numpy stream."""
+    from oracle import sdls_oracle as so
+    n, m, k, p, q, its = 1024, 4000, 64, 10, 1, 50
+    sp = so.config5_instance(n, m, nnz_per=4, seed=55)
+    beta = so.lipschitz_beta(sp)
+    ref = so.solve(sp, "randomized", k, p, q, beta=beta, epsilon=1e-300, max_iter=its, rng=9,
+                   exact_check_dim=0)
+    prob = ours.SparseSdlsProblem(sp.c, 1.0, sp.con, sp.rows, sp.cols, sp.vals, sp.b)
+    cfg = ours.ProjectorConfig(method="randomized", params=ours.RangeParams(k=k, l=p, q=q))
+    rep = ours.solve(prob, cfg, beta=beta, epsilon=1e-300, max_iter=its, rng=9, keep_trajectory=True,
+                     exact_check_dim=0)
+    assert rep.iterations == ref.iterations == its
+    np.testing.assert_allclose([t.grad_norm for t in rep.trajectory], ref.trajectory, rtol=1e-8)
+    np.testing.assert_allclose(rep.y_final, ref.y_final, rtol=1e-8, atol=1e-10)
+    assert _rel(rep.x_solution, ref.x_solution) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["sdls_exact", "sdls_polar"])
+def test_solver_dense_projectors_match_reference(ours, name):
+    """solve() with the exact (reference default) / polar projector vs the reference."""
+    d = gio.load(name)
+    prob = ours.SparseSdlsProblem(d["c"], 1.0, d["con"], d["rows"], d["cols"], d["vals"], d["b"])
+    cfg = None if str(d["method"]) == "exact" else ours.ProjectorConfig(method="polar")
+    rep = ours.solve(prob, cfg, beta=float(d["beta"]), epsilon=1e-14, max_iter=20, rng=int(d["seed"]),
+                     keep_trajectory=True)
+    assert rep.iterations == int(d["iterations"])
+    np.testing.assert_allclose([t.grad_norm for t in rep.trajectory], d["grad_norms"], rtol=1e-8)
+    np.testing.assert_allclose(rep.y_final, d["y_final"], rtol=1e-8, atol=1e-11)
+    assert _rel(rep.x_solution, d["x_solution"]) <= 1e-9
+    assert rep.objective == pytest.approx(float(d["objective"]), rel=1e-8)

@@ -35,6 +35,22 @@ def test_solver_oracle_matches_reference(name, kind):
     assert rep.exact_feasibility_residual == pytest.approx(float(d["exact_residual"]), rel=1e-8)
 
 
+@pytest.mark.parametrize("name", ["sdls_exact", "sdls_polar"])
+def test_dense_projector_solver_oracle_matches_reference(name):
+    """The exact (reference default) and polar projectors inside solve()."""
+    d = gio.load(name)
+    dense, sparse = _problems(d)
+    for prob in (dense, sparse):
+        rep = so.solve(prob, str(d["method"]), 1, 0, 0, beta=float(d["beta"]), epsilon=1e-14,
+                       max_iter=20, rng=int(d["seed"]))
+        assert rep.iterations == int(d["iterations"])
+        np.testing.assert_allclose(rep.trajectory, d["grad_norms"], rtol=1e-9)
+        np.testing.assert_allclose(rep.y_final, d["y_final"], rtol=1e-9, atol=1e-12)
+        err = np.linalg.norm(rep.x_solution - d["x_solution"]) / np.linalg.norm(d["x_solution"])
+        assert err < 1e-9
+        assert rep.exact_feasibility_residual is None
+
+
 def test_config5_instance_shapes():
     p = so.config5_instance(64, 30, seed=1)
     assert p.con.size == 30 * 8 and p.b.shape == (30,)
