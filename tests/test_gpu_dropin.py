@@ -131,7 +131,8 @@ def test_reference_range_finder_power_and_min_eig(installed):
     """range_finder / power_iteration / min_eig_magnitude under the reference names.
     The basis is compared as the projector QQᵀ (Householder vs CholeskyQR columns
     agree up to sign)."""
-    from paper_2410_19208_b200 import install as inst
+    import importlib
+    inst = importlib.import_module("paper_2410_19208_b200.install")
     ref_rf = inst.original("psdcone.sketch", "range_finder")
     x = gio.load("wigner64_q1")["x"]
     for q in (0, 1, 2):
