@@ -613,7 +613,7 @@ def run_scaled_leg(a, torch, psd, pool, params, dev, world, out64):
     rng = psd.DeviceRng(seed=977)
     steps = max(2, min(a.steps, 8))
     for i in range(2):
-        psd.project(pool[i % len(pool)], cfg, rng, assume_symmetric=True)
+        psd.project(pool[i % len(pool)], cfg, rng)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -621,7 +621,7 @@ def run_scaled_leg(a, torch, psd, pool, params, dev, world, out64):
     e0.record()
     falls = 0
     for i in range(steps):
-        rep = psd.project(pool[i % len(pool)], cfg, rng, assume_symmetric=True)
+        rep = psd.project(pool[i % len(pool)], cfg, rng)
         falls += int(rep.fallback)
     e1.record()
     torch.cuda.synchronize(dev)

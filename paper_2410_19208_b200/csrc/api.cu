@@ -47,6 +47,7 @@ struct psd_plan {
   // FP64-on-INT8 (Ozaki II) path (ensure_oz): X residues, panel residues, exponents, partials
   int8_t *oz_ar = nullptr, *oz_br = nullptr;
   int *oz_e = nullptr, *oz_f = nullptr;
+  unsigned* oz_rowmax = nullptr;  // high words of max_j |x_ij| from the symmetry pass (row scales)
   uint8_t* oz_res = nullptr;
   ll oz_ldk = 0;
   bool oz_failed = false;
@@ -359,10 +360,11 @@ struct SymInfo {
   bool bitwise = true, nonfinite = false;
 };
 
-int symcheck(psd_plan* p, const double* x, ll n, ll ldx, SymInfo* si, cudaStream_t st) {
+int symcheck(psd_plan* p, const double* x, ll n, ll ldx, SymInfo* si, cudaStream_t st,
+             unsigned* rowmax = nullptr) {
   {
     Stage mark(p, PSD_STAGE_SYMCHECK, st);
-    psd::sym_stats(x, n, ldx, p->stats, st);
+    psd::sym_stats(x, n, ldx, p->stats, st, rowmax);
   }
   double h[3];
   PSD_CUDA_CHECK(psd::read_small(h, p->stats, 3 * sizeof(double), st),
@@ -672,10 +674,11 @@ int ensure_oz(psd_plan* p) {
   p->oz_ar = static_cast<int8_t*>(balloc((size_t)L * p->n * ldk));
   p->oz_br = static_cast<int8_t*>(balloc((size_t)L * wpad * ldk));
   p->oz_e = static_cast<int*>(balloc((size_t)p->n * sizeof(int)));
+  p->oz_rowmax = static_cast<unsigned*>(balloc((size_t)p->n * sizeof(unsigned)));
   p->oz_f = static_cast<int*>(balloc((size_t)wpad * sizeof(int)));
   p->oz_res_elems = (size_t)L * 8 * p->n * (gw_pad + 16);
   p->oz_res = static_cast<uint8_t*>(balloc(p->oz_res_elems));
-  if (!p->oz_ar || !p->oz_br || !p->oz_e || !p->oz_f || !p->oz_res) {
+  if (!p->oz_ar || !p->oz_br || !p->oz_e || !p->oz_f || !p->oz_res || !p->oz_rowmax) {
     p->oz_failed = true;
     return fail(PSD_ERR_NO_MEMORY, "device allocation failed for the INT8-emulation buffers");
   }
@@ -808,10 +811,32 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   if (f32) PSD_TRY(ensure_f32(p, !raw));
   const float* xhi = raw ? x32 : p->xh;
   const ll ldhi = raw ? ldx : p->ldx32;
+  // FP64 n×n products on the INT8 tensor cores (Ozaki II) when X is bitwise
+  // symmetric (Xᵀ·P = X·P, the residues of X's rows serve both); PSD_FP64_OZAKI=0
+  // keeps them on the FP64 DMMA kernel.
+  static const bool oz_on = [] {
+    const char* e = getenv("PSD_FP64_OZAKI");
+    return !(e && e[0] == '0');
+  }();
+  // below n ≈ 3k the per-product residue/CRT passes cost more than DMMA saves
+  // (C1 n=1000: 606 vs 697 projections/s; n=2048 par; n=4096: 227 vs 205)
+  const bool oz_size = (n >= 3072 || (flags & PSD_FLAG_FP64_INT8)) && n <= psd::oz_max_k();
+  bool oz = !f32 && oz_on && oz_size && !(flags & PSD_FLAG_FP64_DMMA);
+  // reconstruction SYRK on the INT8 engine too (PSD_OZ_SYRK=0 keeps it on DMMA)
+  static const bool oz_syrk_on = [] {
+    const char* e = getenv("PSD_OZ_SYRK");
+    return !(e && e[0] == '0');
+  }();
+  if (oz && ensure_oz(p) != PSD_OK) {   // no room for the residue planes: DMMA products
+    cudaGetLastError();
+    oz = false;
+  }
+  bool have_rowmax = false;
   if (!(flags & PSD_FLAG_SKIP_SYMCHECK)) {
     SymInfo si;
     if (f32) PSD_TRY(symcheck32(p, x32, n, ldx, raw, &si, st));
-    else PSD_TRY(symcheck(p, x64, n, ldx, &si, st));
+    else PSD_TRY(symcheck(p, x64, n, ldx, &si, st, oz ? p->oz_rowmax : nullptr));
+    have_rowmax = oz;
     r.max_abs = si.max_abs;
     r.sym_defect = si.defect;
     if (si.nonfinite) return fail(PSD_ERR_CONVERGENCE, "matrix has non-finite entries");
@@ -847,31 +872,14 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     omega = p->panel[3];
     ldo_eff = ld;
   }
-  // FP64 n×n products on the INT8 tensor cores (Ozaki II) when X is bitwise
-  // symmetric (Xᵀ·P = X·P, the residues of X's rows serve both); PSD_FP64_OZAKI=0
-  // keeps them on the FP64 DMMA kernel.
-  static const bool oz_on = [] {
-    const char* e = getenv("PSD_FP64_OZAKI");
-    return !(e && e[0] == '0');
-  }();
-  // below n ≈ 3k the per-product residue/CRT passes cost more than DMMA saves
-  // (C1 n=1000: 606 vs 697 projections/s; n=2048 par; n=4096: 227 vs 205)
-  const bool oz_size = (n >= 3072 || (flags & PSD_FLAG_FP64_INT8)) && n <= psd::oz_max_k();
-  bool oz = !f32 && oz_on && oz_size && !(flags & PSD_FLAG_FP64_DMMA);
-  // reconstruction SYRK on the INT8 engine too (PSD_OZ_SYRK=0 keeps it on DMMA)
-  static const bool oz_syrk_on = [] {
-    const char* e = getenv("PSD_OZ_SYRK");
-    return !(e && e[0] == '0');
-  }();
-  if (oz && ensure_oz(p) != PSD_OK) {   // no room for the residue planes: DMMA products
-    cudaGetLastError();
-    oz = false;
-  }
   // 3: X·P products on the INT8 engine, Xᵀ·P (X not bitwise symmetric) on DMMA
   r.sketch_engine = f32 ? 2 : (oz ? (use_t ? 3 : 1) : 0);
   if (oz) {
     Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
-    psd::oz_prepare_rows(x64, n, n, ldx, p->oz_e, p->oz_ar, p->oz_ldk, st);
+    if (have_rowmax)   // row scales from the symmetry pass: one read of X
+      psd::oz_prepare_rows_max(x64, n, n, ldx, p->oz_rowmax, p->oz_e, p->oz_ar, p->oz_ldk, st);
+    else
+      psd::oz_prepare_rows(x64, n, n, ldx, p->oz_e, p->oz_ar, p->oz_ldk, st);
   }
   const MulFn mul = [&](const double* P, ll ldP, int ww, double* out, ll ldo2, bool t) {
     if (f32) return xmul_tc32(p, n, xhi, ldhi, P, ldP, ww, out, ldo2, alpha, st);

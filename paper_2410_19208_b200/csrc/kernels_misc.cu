@@ -3,6 +3,7 @@
 // split-K reduction and small panel utilities.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "launch.h"
@@ -19,19 +20,40 @@ constexpr int kSymT = 64;
 // (I ≥ J): tile (J,I) is staged transposed through shared memory, tile (I,J)
 // is read straight into registers, so every element of X is read once
 // (diagonal tiles twice).  One atomic per block per statistic at the end.
+// rowmax != nullptr: also the HIGH WORD of max_j |x_ij| per row i (non-negative doubles
+// order like their bit patterns; the high word carries the exponent, all the INT8
+// engine's residue pass needs for its row scale — ozaki.cu — so that pass reads X once
+// instead of twice).  One REDUX.MAX per tile row and warp, one 32-bit atomic per tile
+// row; zeroed by the caller.
 template <typename T>
 __global__ void __launch_bounds__(256, 4) sym_stats_kernel(const T* __restrict__ x, long long n,
                                                         long long ldx, long long npairs,
-                                                        double* stats) {
+                                                        double* stats, unsigned* __restrict__ rowmax,
+                                                        int diag) {
   __shared__ T tj[kSymT][kSymT + 1];
+  __shared__ unsigned rred[8][kSymT];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
   double mabs = 0.0, mdef = 0.0;
   int flags = 0;
+  const long long nt = (n + kSymT - 1) / kSymT;
   for (long long b = blockIdx.x; b < npairs; b += gridDim.x) {
-    long long ti = (long long)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
-    while ((ti + 1) * (ti + 2) / 2 <= b) ++ti;
-    while (ti * (ti + 1) / 2 > b) --ti;
-    const long long tjx = b - ti * (ti + 1) / 2;
+    // diag: diagonal-major order — pair b lies on diagonal d = ti − tjx, which starts at
+    // o(d) = d·nt − d(d−1)/2; concurrently running blocks then hold distinct row blocks,
+    // so the row-maximum atomics below do not pile onto the same addresses.
+    long long ti, tjx;
+    if (diag) {
+      const double fn = (double)nt + 0.5;
+      long long d = (long long)(fn - sqrt(fmax(fn * fn - 2.0 * (double)b, 0.0)));
+      while (d > 0 && d * nt - d * (d - 1) / 2 > b) --d;
+      while ((d + 1) * nt - (d + 1) * d / 2 <= b) ++d;
+      tjx = b - (d * nt - d * (d - 1) / 2);
+      ti = tjx + d;
+    } else {   // row-major over the lower triangle
+      ti = (long long)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+      while ((ti + 1) * (ti + 2) / 2 <= b) ++ti;
+      while (ti * (ti + 1) / 2 > b) --ti;
+      tjx = b - ti * (ti + 1) / 2;
+    }
     const long long r0 = ti * kSymT, c0 = tjx * kSymT;
     T a[8][2];
 #pragma unroll
@@ -48,6 +70,10 @@ __global__ void __launch_bounds__(256, 4) sym_stats_kernel(const T* __restrict__
       }
     }
     __syncthreads();
+    // compute: defect / max|x| / flags; with rowmax also the row maxima — rows r0 + r from the
+    // register tile (one REDUX across the lanes per q), rows c0 + c from the values this thread
+    // reads transposed out of smem (max over q in registers, then over the 8 warps in smem)
+    unsigned bm[2] = {0u, 0u};
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int r = ty + 8 * q;
@@ -60,7 +86,24 @@ __global__ void __launch_bounds__(256, 4) sym_stats_kernel(const T* __restrict__
         mabs = fmax(mabs, fmax(fabs(av), fabs(bt)));
         mdef = fmax(mdef, fabs(av - bt));
         if (av != bt) flags |= 1;
+        if (rowmax != nullptr) bm[h] = max(bm[h], (unsigned)__double2hiint(fabs(bt)));
       }
+      if (rowmax != nullptr && r0 != c0) {
+        const unsigned mi = __reduce_max_sync(
+            0xffffffffu, (unsigned)__double2hiint(fmax(fabs((double)a[q][0]), fabs((double)a[q][1]))));
+        if (tx == 0 && r0 + r < n && mi) atomicMax(&rowmax[r0 + r], mi);
+      }
+    }
+    if (rowmax != nullptr) {
+      rred[ty][tx] = bm[0];
+      rred[ty][tx + 32] = bm[1];
+    }
+    __syncthreads();
+    if (rowmax != nullptr && threadIdx.x < kSymT) {
+      unsigned m = rred[0][threadIdx.x];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) m = max(m, rred[w][threadIdx.x]);
+      if (c0 + threadIdx.x < n && m) atomicMax(&rowmax[c0 + threadIdx.x], m);
     }
     __syncthreads();
   }
@@ -90,12 +133,15 @@ __global__ void __launch_bounds__(256, 4) sym_stats_kernel(const T* __restrict__
 }
 
 template <typename T>
-static void sym_stats_t(const T* x, long long n, long long ldx, double* stats, cudaStream_t st) {
+static void sym_stats_t(const T* x, long long n, long long ldx, double* stats, unsigned* rowmax,
+                        cudaStream_t st) {
   cudaMemsetAsync(stats, 0, 3 * sizeof(double), st);
+  if (rowmax) cudaMemsetAsync(rowmax, 0, (size_t)n * sizeof(unsigned), st);
   const long long nt = (n + kSymT - 1) / kSymT;
   const long long npairs = nt * (nt + 1) / 2;
   const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * 6);
-  sym_stats_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats);
+  static const int diag = [] { const char* e = getenv("PSD_SYM_ORDER"); return e && e[0] == 'd' ? 1 : 0; }();
+  sym_stats_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats, rowmax, diag);
   count_launch();
 }
 // Off-diagonal block pair of a row-sharded X (SURVEY §8(e) symmetry check):
@@ -197,11 +243,12 @@ void identity_defect(const double* g, int w, long long ldg, double* out, cudaStr
   count_launch();
 }
 
-void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st) {
-  sym_stats_t(x, n, ldx, stats, st);
+void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st,
+               unsigned* rowmax) {
+  sym_stats_t(x, n, ldx, stats, rowmax, st);
 }
 void sym_stats_f32(const float* x, long long n, long long ldx, double* stats, cudaStream_t st) {
-  sym_stats_t(x, n, ldx, stats, st);
+  sym_stats_t(x, n, ldx, stats, static_cast<unsigned*>(nullptr), st);
 }
 
 __global__ void convert_f32_f64_kernel(const float* __restrict__ src, long long lds, double* dst,

@@ -94,6 +94,10 @@ struct OzOp {
 cudaError_t read_small(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t st);
 int oz_num_moduli();
 long long oz_max_k();   // largest K the exact CRT reconstruction admits (2^18)
+// residues of X's rows when the high words of max_j |x_ij| are already known (rowmax_hi,
+// from sym_stats): one pass over X
+void oz_prepare_rows_max(const double* x, long long rows, long long cols, long long ldx,
+                         const unsigned* rowmax_hi, int* e, int8_t* r, long long ldr, cudaStream_t st);
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
                      long long ldr, cudaStream_t st);
 int oz_gemm(const OzOp& op, cudaStream_t st);
@@ -127,7 +131,8 @@ void split_transpose(const double* P, long long n, int w, long long ldp, float* 
 // (bit0: not bitwise symmetric, bit1: NaN/Inf present). stats zeroed inside.
 void pair_defect(const double* a, long long lda, const double* b, long long ldb, long long rows,
                  long long cols, double* stats, bool reset, cudaStream_t st);
-void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st);
+void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st,
+               unsigned* rowmax = nullptr);
 // out[0] = max |G − I| over a w×w Gram (single block)
 void identity_defect(const double* g, int w, long long ldg, double* out, cudaStream_t st);
 void sym_stats_f32(const float* x, long long n, long long ldx, double* stats, cudaStream_t st);

@@ -200,6 +200,126 @@ PSD_DEVINL void res_limb_all4(const float (&f)[4][4], int8_t* out, long long pla
   }
 }
 
+// ---- residues via paired moduli on the FP64 pipe ------------------------------------
+// The 16 moduli form 8 pairs (m_P, m_{15−P}) with M_P = m_P·m_{15−P} < 2^16.  For the
+// 53-bit integer a (exact in a double): r = a − M_P·rint(a/M_P) by two DFMA and a DADD
+// (|r| < M_P/2 + 1 < 2^15), its low word comes out of one more DADD onto 1.5·2^52, and
+// the two residues are r mod m_P and r mod m_{15−P} with the fp32 trick of
+// res_limb_store8 (one FFMA + one IMAD each, r exact in fp32).  m = 256 (pair 0) is the
+// low byte of r.  Per (element, modulus) ≈ 5 issue slots instead of ≈ 9 for the
+// 13-bit-limb form, spread over the FP64 and FP32 pipes.
+constexpr double kMagicD = 6755399441055744.0;   // 1.5·2^52
+template <int P>
+PSD_DEVINL void res_pair_store8(const double (&a)[8], int8_t* out, long long plane) {
+  constexpr int lo = P, hi = kNumMod - 1 - P;
+  constexpr int m1 = mod_at(lo), m2 = mod_at(hi);
+  constexpr double M = (double)(m1 * m2);
+  constexpr double rM = 1.0 / M;
+  constexpr float rm1 = 1.0f / (float)m1, rm2 = 1.0f / (float)m2;
+  constexpr uint32_t n1 = 0u - (uint32_t)m1, n2 = 0u - (uint32_t)m2;
+  uint32_t b1[8], b2[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const double qd = fma(a[q], rM, kMagicD) - kMagicD;     // rint(a/M) (±1: |r| < M/2 + 1)
+    const double r = fma(-qd, M, a[q]);                      // exact
+    const uint32_t ri = (uint32_t)__double2loint(r + kMagicD);   // r in the low word
+    const uint32_t sb = ri + 0x4B400000u;                    // bits of (float)r + kMagic
+    const float rf = __uint_as_float(sb) - kMagic;
+    if constexpr (m1 == 256) b1[q] = ri;
+    else b1[q] = __float_as_uint(fmaf(rf, rm1, kMagic)) * n1 + sb;
+    b2[q] = __float_as_uint(fmaf(rf, rm2, kMagic)) * n2 + sb;
+  }
+  *reinterpret_cast<uint2*>(out + lo * plane) =
+      make_uint2(pack4(b1[0], b1[1], b1[2], b1[3]), pack4(b1[4], b1[5], b1[6], b1[7]));
+  *reinterpret_cast<uint2*>(out + hi * plane) =
+      make_uint2(pack4(b2[0], b2[1], b2[2], b2[3]), pack4(b2[4], b2[5], b2[6], b2[7]));
+}
+template <int P>
+PSD_DEVINL void res_pair_all(const double (&a)[8], int8_t* out, long long plane) {
+  if constexpr (P < kNumMod / 2) {
+    res_pair_store8<P>(a, out, plane);
+    res_pair_all<P + 1>(a, out, plane);
+  }
+}
+static_assert(mod_at(0) == 256 && 256 * mod_at(15) < 65536 && mod_at(1) * mod_at(14) < 65536 &&
+                  mod_at(7) * mod_at(8) < 65536, "moduli pairs must multiply below 2^16");
+
+__global__ void __launch_bounds__(256) residues_rows_dp_kernel(const double* __restrict__ x, long long rows,
+                                                             long long cols, long long ldx, int* __restrict__ e,
+                                                             int8_t* __restrict__ r, long long ldr,
+                                                             long long plane) {
+  // as residues_rows_kernel (one block per row, pass 1 = row exponent, pass 2 from L2),
+  // residues by res_pair_store8
+  __shared__ double red[8];
+  const long long c4 = cols / 4;
+  for (long long i = blockIdx.x; i < rows; i += gridDim.x) {
+    const double* row = x + i * ldx;
+    double mx = 0.0;
+    for (long long k4 = threadIdx.x; k4 < c4; k4 += blockDim.x) {
+      const double2 v01 = reinterpret_cast<const double2*>(row)[2 * k4];
+      const double2 v23 = reinterpret_cast<const double2*>(row)[2 * k4 + 1];
+      mx = fmax(mx, fmax(fmax(fabs(v01.x), fabs(v01.y)), fmax(fabs(v23.x), fabs(v23.y))));
+    }
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    double t = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+    __syncthreads();
+    const int ei = t > 0.0 ? ilogb(t) + 1 : 0;
+    if (threadIdx.x == 0) e[i] = ei;
+    const int sh = 53 - ei;
+    const double s1 = ldexp(1.0, sh / 2), s2 = ldexp(1.0, sh - sh / 2);
+    int8_t* orow = r + i * ldr;
+    for (long long k8 = threadIdx.x; k8 < c4 / 2; k8 += blockDim.x) {
+      const double2* src = reinterpret_cast<const double2*>(row) + 4 * k8;
+      double a[8];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 v = __ldcs(src + h);
+        a[2 * h] = rint(v.x * s1 * s2);        // |a| < 2^53, exact integer
+        a[2 * h + 1] = rint(v.y * s1 * s2);
+      }
+      res_pair_all<0>(a, orow + 8 * k8, plane);
+    }
+  }
+}
+
+// Single pass: the row maxima come from the symmetry check (sym_stats, kernels_misc.cu),
+// so X is read once here (25.8 GB moved at C3 instead of 8.6 + 16.5 read + 17.2 written:
+// pass 2 of the two-pass kernels re-reads the row from DRAM — 1184 rows of 256 KB in
+// flight exceed L2).
+// rowmax_hi[i] = high word of max_j |x_ij|: the exponent is all the row scale needs (a row
+// whose maximum is below 2^-1042, i.e. high word 0, is treated as zero, as its entries
+// are far below FP64 resolution of any product).
+__global__ void __launch_bounds__(256) residues_rows_max_kernel(const double* __restrict__ x, long long rows,
+                                                              long long cols, long long ldx,
+                                                              const unsigned* __restrict__ rowmax_hi,
+                                                              int* __restrict__ e, int8_t* __restrict__ r,
+                                                              long long ldr, long long plane) {
+  const long long c8 = cols / 8;
+  for (long long i = blockIdx.x; i < rows; i += gridDim.x) {
+    const unsigned hi = rowmax_hi[i];
+    const int ei = hi ? ilogb(__hiloint2double((int)hi, 0)) + 1 : 0;
+    if (threadIdx.x == 0) e[i] = ei;
+    const int sh = 53 - ei;
+    const double s1 = ldexp(1.0, sh / 2), s2 = ldexp(1.0, sh - sh / 2);
+    const double* row = x + i * ldx;
+    int8_t* orow = r + i * ldr;
+    for (long long k8 = threadIdx.x; k8 < c8; k8 += blockDim.x) {
+      const double2* src = reinterpret_cast<const double2*>(row) + 4 * k8;
+      double a[8];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 v = __ldcs(src + h);
+        a[2 * h] = rint(v.x * s1 * s2);
+        a[2 * h + 1] = rint(v.y * s1 * s2);
+      }
+      res_pair_all<0>(a, orow + 8 * k8, plane);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) residues_rows_kernel(const double* __restrict__ x, long long rows,
                                                           long long cols, long long ldx, int* __restrict__ e,
                                                           int8_t* __restrict__ r, long long ldr,
@@ -685,13 +805,30 @@ int grid_oz(long long total, int threads) {
 int oz_num_moduli() { return oz::kNumMod; }
 long long oz_max_k() { return oz::kMaxK; }
 
+void oz_prepare_rows_max(const double* x, long long rows, long long cols, long long ldx,
+                         const unsigned* rowmax, int* e, int8_t* r, long long ldr, cudaStream_t st) {
+  ensure_oz_constants();
+  if (cols % 8 == 0 && ldx % 2 == 0 && ldr % 8 == 0 && (uintptr_t)x % 16 == 0) {
+    const unsigned grid = (unsigned)std::min<long long>(rows, (long long)device_info().sms * 8);
+    oz::residues_rows_max_kernel<<<grid, 256, 0, st>>>(x, rows, cols, ldx, rowmax, e, r, ldr, ldr * rows);
+    count_launch();
+  } else {
+    oz_prepare_rows(x, rows, cols, ldx, e, r, ldr, st);
+  }
+}
+
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
                      long long ldr, cudaStream_t st) {
   ensure_oz_constants();
   if (cols % 8 == 0 && ldx % 2 == 0 && ldr % 8 == 0 && (uintptr_t)x % 16 == 0) {
-    // row exponents fused: one block per row
-    oz::residues_rows_kernel<<<(unsigned)std::min<long long>(rows, (long long)device_info().sms * 8), 256, 0,
-                               st>>>(x, rows, cols, ldx, e, r, ldr, ldr * rows);
+    // row exponents fused: one block per row.  Residues by paired moduli on the FP64 pipe
+    // (PSD_OZ_RES=limb keeps the 13-bit-limb fp32 form)
+    static const bool limb = [] { const char* v = getenv("PSD_OZ_RES"); return v && v[0] == 'l'; }();
+    const unsigned grid = (unsigned)std::min<long long>(rows, (long long)device_info().sms * 8);
+    if (limb)
+      oz::residues_rows_kernel<<<grid, 256, 0, st>>>(x, rows, cols, ldx, e, r, ldr, ldr * rows);
+    else
+      oz::residues_rows_dp_kernel<<<grid, 256, 0, st>>>(x, rows, cols, ldx, e, r, ldr, ldr * rows);
     count_launch();
   } else {
     oz::row_exp_kernel<<<(unsigned)rows, 256, 0, st>>>(x, rows, cols, ldx, e);

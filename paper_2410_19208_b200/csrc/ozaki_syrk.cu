@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "gemm_tc32.cuh"
@@ -41,7 +42,15 @@ namespace ozs {
 constexpr int BM = 128;        // tile rows (TMEM lanes)
 constexpr int BN = 32;         // tile columns per level
 constexpr int KB = 32;         // K bytes per stage (one kind::i8 MMA)
-constexpr int kEpi = 8;        // epilogue warps: 2 per TMEM lane quadrant, 16 columns (2 groups of 8) each
+#ifndef PSD_SYRK_EPI
+#define PSD_SYRK_EPI 8
+#endif
+// epilogue warps: kEpi/4 per TMEM lane quadrant, each owning kGroups groups of 8 columns of
+// the 32-column tile.  8 warps × 2 groups (168 registers) measured 2.46 ms at C3; 16 warps ×
+// 1 group is capped at 96 registers by the 576-thread block and spills: 2.73 ms.
+constexpr int kEpi = PSD_SYRK_EPI;
+constexpr int kGroups = 32 / (kEpi / 4) / 8;
+static_assert(kGroups >= 1 && (kEpi / 4) * kGroups * 8 == 32, "epilogue warps must tile 32 columns");
 constexpr int kThreads = (2 + kEpi) * 32;
 constexpr int kBufCols = 256;  // TMEM column offset of the second accumulator
 
@@ -162,8 +171,7 @@ PSD_DEVINL void unit_tile(long long u, int& I, int& J) {
 // in shared memory (nkb·28 KB) while the CTA walks that block's column tiles; only the
 // 7 KB B slices stream per k-step.  Otherwise A and B stream together per k-step.
 template <int D, bool AR>
-__global__ void __launch_bounds__(kThreads, 1)
-    i8_syrk_kernel(const SyrkParams p) {
+__global__ void __launch_bounds__(kThreads, 1) i8_syrk_kernel(const SyrkParams p) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], accf_bar[2], acce_bar[2], afull_bar, aempty_bar;
   // per-unit row / column scales, 4 slots filled by the producer with the unit's bulk copies
@@ -209,7 +217,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = tmem_slot;
 
   if (warp == 0) {
-    int it = 0, aload = 0, curI = -1, j = 0;
+    int aload = 0, curI = -1, j = 0, rs = 0;
+    uint32_t rph = 0;
     int I, J;
     unit_tile(u0, I, J);
     for (long long u = u0; u < u1; ++u, ++j) {
@@ -237,14 +246,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++aload;
         curI = I;
       }
-      for (int kb = 0; kb < nkb; ++kb, ++it) {
-        const int s = it % p.stages;
-        const uint32_t ph = (uint32_t)(it / p.stages) & 1u;
-        tc32::mbar_wait_t(smem_u32(&empty_bar[s]), ph ^ 1u);
+      for (int kb = 0; kb < nkb; ++kb) {
+        tc32::mbar_wait_t(smem_u32(&empty_bar[rs]), rph ^ 1u);
         if (tc32::elect_one()) {
-          const uint32_t fb = smem_u32(&full_bar[s]);
+          const uint32_t fb = smem_u32(&full_bar[rs]);
           mbar_expect_tx(fb, st_bytes);
-          const uint32_t sS = sring + s * st_bytes;
+          const uint32_t sS = sring + rs * st_bytes;
           if (AR) {
             bulk_load(sS, p.tb + ((long long)J * nkb + kb) * b_bytes, b_bytes, fb);
           } else {
@@ -253,6 +260,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         __syncwarp();
+        if (++rs == p.stages) {   // ring position kept incrementally (no division per k-step)
+          rs = 0;
+          rph ^= 1u;
+        }
       }
       if (++J >= min(4 * (I + 1), p.nt)) {
         ++I;
@@ -260,9 +271,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    int it = 0, j = 0, aload = 0, curI = -1;
+    int j = 0, aload = 0, curI = -1, rs = 0;
+    uint32_t rph = 0;
     int I, J;
     unit_tile(u0, I, J);
+    // descriptors built once; per MMA only the start-address field moves (byte offset >> 4,
+    // smem addresses < 2^18 so the 14-bit field never carries)
+    const uint64_t a_desc0 = desc_sw32(AR ? sbase : sring);
+    const uint64_t b_desc0 = desc_sw32(AR ? sring : sring + a_bytes);
     for (long long u = u0; u < u1; ++u, ++j) {
       const int b = j & 1;
       if (AR && I != curI) {
@@ -277,26 +293,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc32::mbar_wait_t(smem_u32(&acce_bar[b]), (((uint32_t)j >> 1) & 1u) ^ 1u);
       tc32::tc_fence_after();
       const uint32_t dbuf = tmem + (uint32_t)(b * kBufCols);
-      for (int kb = 0; kb < nkb; ++kb, ++it) {
-        const int s = it % p.stages;
-        const uint32_t ph = (uint32_t)(it / p.stages) & 1u;
-        tc32::mbar_wait_t(smem_u32(&full_bar[s]), ph);
+      for (int kb = 0; kb < nkb; ++kb) {
+        tc32::mbar_wait_t(smem_u32(&full_bar[rs]), rph);
         tc32::tc_fence_after();
         if (tc32::elect_one()) {
-          const uint32_t sS = sring + s * st_bytes;
-          const uint32_t sA = AR ? sbase + (uint32_t)kb * a_bytes : sS;
-          const uint64_t db = desc_sw32(AR ? sS : sS + a_bytes);
+          const uint32_t soff = (uint32_t)rs * st_bytes;
+          const uint64_t ad = a_desc0 + ((AR ? (uint32_t)kb * a_bytes : soff) >> 4);
+          const uint64_t db = b_desc0 + (soff >> 4);
 #pragma unroll
           for (int t = 0; t < D; ++t) {
             // kind::i8: D s32, A/B signed, K-major, M = 128, N = 32·(D − t)
-            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
-                                   ((uint32_t)((BN * (D - t)) >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-            mma_i8(dbuf + (uint32_t)(t * BN), desc_sw32(sA + t * BM * KB), db, idesc, (kb | t) != 0);
+            constexpr uint32_t base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BM >> 4) << 24);
+            const uint32_t idesc = base | ((uint32_t)((BN * (D - t)) >> 3) << 17);
+            mma_i8(dbuf + (uint32_t)(t * BN), ad + (uint64_t)((t * BM * KB) >> 4), db, idesc, (kb | t) != 0);
           }
-          tc32::mma_commit(smem_u32(&empty_bar[s]));
+          tc32::mma_commit(smem_u32(&empty_bar[rs]));
           if (kb == nkb - 1) tc32::mma_commit(smem_u32(&accf_bar[b]));
         }
         __syncwarp();
+        if (++rs == p.stages) {
+          rs = 0;
+          rph ^= 1u;
+        }
       }
       if (++J >= min(4 * (I + 1), p.nt)) {
         ++I;
@@ -305,30 +323,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quad = warp & 3;
-    const int slice = (warp - 2) >> 2;          // columns 16·slice … +16 of each level
+    const int slice = (warp - 2) >> 2;          // columns 8·kGroups·slice … of each level
     const uint32_t tq = (uint32_t)(quad * 32) << 16;
+    // barrier addresses hoisted (each smem_u32 of a __shared__ object costs an S2R)
+    const uint32_t accf0 = smem_u32(&accf_bar[0]), acce0 = smem_u32(&acce_bar[0]);
+    const uint32_t sfull0 = smem_u32(&sfull_bar[0]), sempty0 = smem_u32(&sempty_bar[0]);
     int I, J;
     unit_tile(u0, I, J);
     int j = 0;
     for (long long u = u0; u < u1; ++u, ++j) {
       const int b = j & 1, sb = j & 3;
-      tc32::mbar_wait_t(smem_u32(&accf_bar[b]), ((uint32_t)j >> 1) & 1u);
+      tc32::mbar_wait_t(accf0 + 8u * (uint32_t)b, ((uint32_t)j >> 1) & 1u);
       tc32::tc_fence_after();
-      tc32::mbar_wait_t(smem_u32(&sfull_bar[sb]), ((uint32_t)j >> 2) & 1u);
+      tc32::mbar_wait_t(sfull0 + 8u * (uint32_t)sb, ((uint32_t)j >> 2) & 1u);
       const int ib = I * BM + quad * 32;
       const int i = ib + lane;
-      const int jb = J * BN + slice * 16;
+      const int jb = J * BN + slice * 8 * kGroups;
       // warp-uniform: the 8-column group g holds some (i, j) with j ≤ i
-      bool active[2];
-      uint32_t v[2][D][8];
+      bool active[kGroups];
+      uint32_t v[kGroups][D][8];
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
+      for (int g = 0; g < kGroups; ++g) {
         const int j0 = jb + 8 * g;
         active[g] = j0 <= ib + 31 && j0 < p.n && ib < p.n;
         if (active[g]) {
 #pragma unroll
           for (int L = 0; L < D; ++L)
-            tmem_ld8(tmem + tq + (uint32_t)(b * kBufCols + L * BN + slice * 16 + 8 * g), v[g][L]);
+            tmem_ld8(tmem + tq + (uint32_t)(b * kBufCols + L * BN + slice * 8 * kGroups + 8 * g), v[g][L]);
         }
       }
       const double si = s_rs[sb][quad * 32 + lane];
@@ -336,14 +357,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the accumulator is in registers: hand the TMEM buffer back before the math and stores
       tc32::tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&acce_bar[b]));
+      if (lane == 0) mbar_arrive(acce0 + 8u * (uint32_t)b);
       const bool row_ok = i < p.n;
       const long long ldc = p.ldc;
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
+      for (int g = 0; g < kGroups; ++g) {
         if (!active[g]) continue;
         const int j0 = jb + 8 * g;
-        const double* sj = &s_cs[sb][slice * 16 + 8 * g];   // broadcast smem reads
+        const double* sj = &s_cs[sb][slice * 8 * kGroups + 8 * g];   // broadcast smem reads
         double val[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -379,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&sempty_bar[sb]));   // scale slot read
+      if (lane == 0) mbar_arrive(sempty0 + 8u * (uint32_t)sb);   // scale slot read
       if (++J >= min(4 * (I + 1), p.nt)) {
         ++I;
         J = 0;
@@ -455,7 +476,15 @@ int launch_syrk(const double* w, long long n, int r, long long ldw, const double
   const int grid = (int)std::min<long long>(device_info().sms, p.units);
   kern<<<grid, kThreads, smem, st>>>(p);
   count_launch();
-  return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
+  if (cudaPeekAtLastError() != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    fprintf(stderr, "i8_syrk launch failed: %s (regs %d, maxThreadsPerBlock %d, static smem %zu, dyn smem %zu, "
+            "threads %d)\n", cudaGetErrorString(cudaPeekAtLastError()), fa.numRegs, fa.maxThreadsPerBlock,
+            fa.sharedSizeBytes, smem, kThreads);
+    return -6;
+  }
+  return 0;
 }
 
 }  // namespace

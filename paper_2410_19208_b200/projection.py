@@ -24,8 +24,7 @@ import torch
 from . import _native, errors
 from ._tensors import as_device, draw_gaussian, require_square
 from .sketch import RangeParams, min_eig_magnitude_device
-from .symmetric import (SymStats, check_symmetric_device, eigh_device, reconstruct_device,
-                        rng_from_seed)
+from .symmetric import check_symmetric_device, eigh_device, reconstruct_device, rng_from_seed
 
 METHODS = ("exact", "polar", "randomized", "scaled_randomized")  # projection.py:21
 ALPHA_TOL_FACTOR = 1e-12  # projection.py:133
@@ -102,12 +101,13 @@ def _operand(x, dtype):
     return as_device(x, dtype=torch.float32 if resolve_dtype(dtype) == "fp32" else torch.float64)
 
 
-def _stats_for(op, assume_symmetric):
-    if op.t.dtype == torch.float32:
-        return None  # the FP32 entry point validates on the device itself
-    if assume_symmetric:
-        return None
-    return check_symmetric_device(op)
+def _validate_in_library(op, assume_symmetric):
+    """require_symmetric (symmetric.py:39-57, at projection.py:100/:132) and the
+    alpha_tol test (projection.py:133-137) run inside psd_ran_proj[_f32] — its
+    symmetry pass also yields the row scales of the INT8 engine, so X is read once
+    for both.  ``assume_symmetric`` (FP64 only) skips the pass: the caller
+    guarantees a bitwise-symmetric X."""
+    return op.t.dtype == torch.float32 or not assume_symmetric
 
 
 def _result_buffer(out, n, op):
@@ -120,10 +120,10 @@ def _result_buffer(out, n, op):
     return out
 
 
-def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, method, t0, out=None):
+def _run(op, n, params, om, alpha, validate, collect_diagnostics, return_factors, method, t0, out=None):
     width = params.width
     lib = _native.load_library()
-    plan = _native.get_plan(n, width, op.device)
+    plan = _native.get_plan(n, min(width, n), op.device)   # width > n: raised after the symmetry check
     dev = op.device
     f32 = op.t.dtype == torch.float32
     result = _result_buffer(out, n, op)
@@ -133,9 +133,7 @@ def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, m
         flags = 0  # psd_ran_proj_f32 runs require_symmetric / alpha_tol on the fp32 X
         om = om.to(torch.float32).contiguous()
     else:
-        flags = _native.FLAG_SKIP_SYMCHECK
-        if stats is None or stats.bitwise:
-            flags |= _native.FLAG_ASSUME_SYMMETRIC
+        flags = 0 if validate else _native.FLAG_SKIP_SYMCHECK | _native.FLAG_ASSUME_SYMMETRIC
         if _FP64_ENGINE == "dmma":
             flags |= _native.FLAG_FP64_DMMA
         elif _FP64_ENGINE == "int8":
@@ -153,8 +151,6 @@ def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, m
     if return_factors:
         factors = (op.give_back(fw[:, :r].contiguous()), op.give_back(fd[:r].contiguous()))
     info = rep.as_dict()
-    if stats is not None:
-        info["max_abs"], info["sym_defect"] = stats.max_abs, stats.defect
     return ProjectionReport(
         result=op.give_back(result),
         method=method,
@@ -168,13 +164,13 @@ def _run(op, n, params, om, alpha, stats, collect_diagnostics, return_factors, m
     )
 
 
-def _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, stats, t0, out=None):
+def _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, validate, t0, out=None):
     n = require_square(op)
     width = params.width
-    if width > n:                                               # sketch.py:67-69
+    if width > n and not validate:   # sketch.py:67-69 (else raised by the library after its check)
         raise errors.error("InvalidParams", f"k+l = {width} exceeds min(m, n) = {n}")
     om = as_device(omega, op.device).t if omega is not None else draw_gaussian(rng, (n, width), op.device)
-    return _run(op, n, params, om, 0.0, stats, collect_diagnostics, return_factors, "randomized", t0,
+    return _run(op, n, params, om, 0.0, validate, collect_diagnostics, return_factors, "randomized", t0,
                 out)
 
 
@@ -184,27 +180,25 @@ def ran_proj(x, params, rng, collect_diagnostics=False, return_factors=False, *,
     t0 = time.perf_counter()
     op = _operand(x, dtype)
     require_square(op)
-    stats = _stats_for(op, assume_symmetric)                   # projection.py:100
-    return _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, stats, t0, out)
+    validate = _validate_in_library(op, assume_symmetric)      # projection.py:100
+    return _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, validate, t0, out)
 
 
-def _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factors, omega, stats, t0,
+def _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factors, omega, validate, t0,
                       out=None):
     n = require_square(op)
-    if op.t.dtype != torch.float32:  # FP32: alpha_tol is tested inside psd_ran_proj_f32
-        if stats is None:  # assume_symmetric: still need max|x| for alpha_tol (one HBM pass)
-            stats = check_symmetric_device(op)
-        max_abs = stats.max_abs
+    if not validate:  # assume_symmetric: the library skips its pass, alpha_tol needs max|x| here
+        max_abs = check_symmetric_device(op).max_abs
         alpha_tol = ALPHA_TOL_FACTOR * max(1.0, max_abs)            # projection.py:133
         if alpha <= alpha_tol:
             raise errors.error(
                 "AlphaTooSmall",
                 f"alpha = {alpha:.3e} is at or below tolerance {alpha_tol:.3e}; input is numerically PSD")
     width = params.width
-    if width > n:
+    if width > n and not validate:
         raise errors.error("InvalidParams", f"k+l = {width} exceeds min(m, n) = {n}")
     om = as_device(omega, op.device).t if omega is not None else draw_gaussian(rng, (n, width), op.device)
-    return _run(op, n, params, om, float(alpha), stats, collect_diagnostics, return_factors,
+    return _run(op, n, params, om, float(alpha), validate, collect_diagnostics, return_factors,
                 "scaled_randomized", t0, out)
 
 
@@ -214,9 +208,9 @@ def ran_proj_scal(x, params, alpha, rng, collect_diagnostics=False, return_facto
     t0 = time.perf_counter()
     op = _operand(x, dtype)
     require_square(op)
-    stats = _stats_for(op, assume_symmetric)
+    validate = _validate_in_library(op, assume_symmetric)
     return _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factors, omega,
-                             stats, t0, out)
+                             validate, t0, out)
 
 
 def _exact_report(op, method, t0):
@@ -251,8 +245,12 @@ def project(x, cfg, rng=None, *, omega=None, assume_symmetric=False):
     t0 = time.perf_counter()
     op = _operand(x, config_dtype(cfg))
     require_square(op)
-    stats = _stats_for(op, assume_symmetric)                   # projection.py:189
+    # require_symmetric (projection.py:189): the dense methods validate here; the
+    # randomized ones inside the library call (with the same exceptions)
+    validate = _validate_in_library(op, assume_symmetric)
     if cfg.method in ("exact", "polar"):
+        if op.t.dtype != torch.float32 and validate:
+            check_symmetric_device(op)
         if op.t.dtype == torch.float32:  # dense eigh stays FP64; result handed back as fp32
             op64 = type(op)(op.t.double(), op.kind, op.device)
             check_symmetric_device(op64)
@@ -264,7 +262,7 @@ def project(x, cfg, rng=None, *, omega=None, assume_symmetric=False):
     rng = rng_from_seed(rng if rng is not None else (cfg.params.seed if cfg.params else None))
     if cfg.method == "randomized":
         report = _ran_proj_op(op, cfg.params, rng, cfg.collect_diagnostics, cfg.return_factors,
-                              omega, stats, t0)
+                              omega, validate, t0)
         report.wall_time = time.perf_counter() - t0
         return report
 
@@ -277,10 +275,10 @@ def project(x, cfg, rng=None, *, omega=None, assume_symmetric=False):
     alpha *= cfg.scale_factor
     try:
         report = _ran_proj_scal_op(op, cfg.params, alpha, rng, cfg.collect_diagnostics,
-                                   cfg.return_factors, omega, stats, t0)
+                                   cfg.return_factors, omega, validate, t0)
     except errors.REGISTRY["AlphaTooSmall"]:
         report = _ran_proj_op(op, cfg.params, rng, cfg.collect_diagnostics, cfg.return_factors,
-                              omega, stats, t0)
+                              omega, validate, t0)
         report.fallback = True
         report.alpha_used = float(alpha)
     report.wall_time = time.perf_counter() - t0
