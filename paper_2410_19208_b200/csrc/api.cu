@@ -387,11 +387,15 @@ using MulFn = std::function<int(const double* P, ll ldP, int w, double* out, ll 
 
 int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* omega, ll ldo, int w,
                       int q, bool always_stabilize, bool strict, double** bufs, int* qidx,
-                      int* width_out, QrInfo* qi, cudaStream_t st) {
+                      int* width_out, QrInfo* qi, cudaStream_t st,
+                      const std::function<int()>& after_first = nullptr) {
   const ll ld = p->ldp;
   const bool stabilize = q >= 2 || always_stabilize;               // sketch.py:74
   int y = 0;
   PSD_TRY(mul(omega, ldo, w, bufs[0], ld, false));                 // :75
+  // deferred input validation (psd_ran_proj): the host collects the symmetry statistics
+  // while the first product runs, before anything depends on them
+  if (after_first) PSD_TRY(after_first());
   for (int it = 0; it < q; ++it) {                                 // :76-82
     QrInfo tmp;
     if (stabilize) PSD_TRY(cholqr(p, bufs, y, (y + 1) % 3, m, w, nullptr, &y, &tmp, st, true));
@@ -832,11 +836,12 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     oz = false;
   }
   bool have_rowmax = false;
-  if (!(flags & PSD_FLAG_SKIP_SYMCHECK)) {
-    SymInfo si;
-    if (f32) PSD_TRY(symcheck32(p, x32, n, ldx, raw, &si, st));
-    else PSD_TRY(symcheck(p, x64, n, ldx, &si, st, oz ? p->oz_rowmax : nullptr));
-    have_rowmax = oz;
+  // require_symmetric's verdict (and alpha_tol) — evaluated now for FP32, and for FP64 once
+  // the first product is enqueued (sym_pending): the statistics travel through an
+  // event-tracked mapped-memory read, so the GPU never idles on this host round trip.
+  // Nothing observable (the result, factors) is written before the verdict.
+  bool sym_pending = false;
+  auto judge = [&](const SymInfo& si) -> int {
     r.max_abs = si.max_abs;
     r.sym_defect = si.defect;
     if (si.nonfinite) return fail(PSD_ERR_CONVERGENCE, "matrix has non-finite entries");
@@ -852,9 +857,45 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
                     "alpha = %.3e is at or below tolerance %.3e; input is numerically PSD", alpha,
                     alpha_tol);
     }
-    use_t = use_t && !si.bitwise;
+    use_t = use_t && !si.bitwise && !f32;
+    return PSD_OK;
+  };
+  auto resolve_sym = [&]() -> int {
+    if (!sym_pending) return PSD_OK;
+    sym_pending = false;
+    double h[3];
+    PSD_CUDA_CHECK(psd::read_small_wait(h, sizeof(h)), "stats");
+    SymInfo si;
+    int fl = 0;
+    std::memcpy(&fl, &h[2], sizeof(int));
+    si.max_abs = h[0];
+    si.defect = h[1];
+    si.bitwise = (fl & 1) == 0;
+    si.nonfinite = (fl & 2) != 0;
+    PSD_TRY(judge(si));
+    r.used_transpose = use_t ? 1 : 0;
+    r.sketch_engine = oz ? (use_t ? 3 : 1) : 0;
+    return PSD_OK;
+  };
+  if (!(flags & PSD_FLAG_SKIP_SYMCHECK)) {
+    if (f32) {
+      SymInfo si;
+      PSD_TRY(symcheck32(p, x32, n, ldx, raw, &si, st));
+      PSD_TRY(judge(si));
+    } else {
+      {
+        Stage mark(p, PSD_STAGE_SYMCHECK, st);
+        psd::sym_stats(x64, n, ldx, p->stats, st, oz ? p->oz_rowmax : nullptr);
+      }
+      PSD_CUDA_CHECK(psd::read_small_async(p->stats, 3 * sizeof(double), st), "stats");
+      sym_pending = true;
+      have_rowmax = oz;
+    }
   }
-  if (w > n) return fail(PSD_ERR_INVALID_PARAMS, "k+l = %d exceeds min(m, n) = %lld", w, (ll)n);
+  if (w > n) {
+    PSD_TRY(resolve_sym());
+    return fail(PSD_ERR_INVALID_PARAMS, "k+l = %d exceeds min(m, n) = %lld", w, (ll)n);
+  }
   // FP32: Xᵀ·P is taken as X·P — X passed the 1e-10·max|X| symmetry test, far
   // below the path's 1e-4 tolerance.
   if (f32) use_t = false;
@@ -889,7 +930,8 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   int qb = 0, wk = 0;
   QrInfo qi;
   PSD_TRY(range_finder_core(p, mul, n, n, omega, ldo_eff, w, q, f32, (flags & PSD_FLAG_STRICT) != 0,
-                            bufs, &qb, &wk, &qi, st));
+                            bufs, &qb, &wk, &qi, st, resolve_sym));
+  PSD_TRY(resolve_sym());
   r.qr_passes = qi.passes;
   r.qr_shifted = qi.shifted;
   r.basis_width = wk;

@@ -713,6 +713,44 @@ __global__ void copy_to_mapped_kernel(unsigned char* __restrict__ dst, const uns
   for (size_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
 }
 
+// Asynchronous variant for one early status word block: the copy kernel and an event are
+// enqueued, the caller keeps enqueueing work and collects the bytes later
+// (read_small_wait), so the stream is never drained for the read.
+struct AsyncSlot {
+  unsigned char* h = nullptr;
+  unsigned char* d = nullptr;
+  cudaEvent_t ev = nullptr;
+};
+static AsyncSlot& async_slot() {
+  thread_local AsyncSlot slot[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return slot[dev & 15];
+}
+
+cudaError_t read_small_async(const void* dev_src, size_t bytes, cudaStream_t st) {
+  AsyncSlot& sl = async_slot();
+  if (bytes > 4096) return cudaErrorInvalidValue;
+  if (!sl.h) {
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&sl.h), 4096, cudaHostAllocMapped);
+    if (e != cudaSuccess) return e;
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&sl.d), sl.h, 0);
+    if (e != cudaSuccess) return e;
+    e = cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  copy_to_mapped_kernel<<<1, 256, 0, st>>>(sl.d, static_cast<const unsigned char*>(dev_src), bytes);
+  return cudaEventRecord(sl.ev, st);
+}
+
+cudaError_t read_small_wait(void* host_dst, size_t bytes) {
+  AsyncSlot& sl = async_slot();
+  cudaError_t e = cudaEventSynchronize(sl.ev);
+  if (e != cudaSuccess) return e;
+  std::memcpy(host_dst, sl.h, bytes);
+  return cudaGetLastError();
+}
+
 cudaError_t read_small(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t st) {
   constexpr size_t kCap = 64 << 10;
   struct Staging {

@@ -92,6 +92,9 @@ struct OzOp {
 // device→host read of a few status bytes that does not queue behind DMA copies
 // (kernel store into host-mapped memory, then a stream sync); > 64 KB: cudaMemcpy
 cudaError_t read_small(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t st);
+// enqueue a status read (≤ 4 KB) without draining the stream; collect with read_small_wait
+cudaError_t read_small_async(const void* dev_src, size_t bytes, cudaStream_t st);
+cudaError_t read_small_wait(void* host_dst, size_t bytes);
 int oz_num_moduli();
 long long oz_max_k();   // largest K the exact CRT reconstruction admits (2^18)
 // residues of X's rows when the high words of max_j |x_ij| are already known (rowmax_hi,
