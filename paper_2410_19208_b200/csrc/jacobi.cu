@@ -28,11 +28,18 @@
 
 namespace psd {
 
-constexpr int kJB = 16;          // indices per block
-constexpr int kJS = 2 * kJB;     // subproblem size (32)
-constexpr int kJT = 256;         // threads per CTA
-constexpr int kJLd = kJS + 4;    // smem row stride ≡ 4 (mod 16): conflict-free DMMA fragments
-constexpr int kJTile = kJS * kJLd;
+// Block size JB (indices per block) is a template parameter: 16 (32×32 subproblems,
+// 256 threads; the default) or 32 (64×64 subproblems, 1024 threads; see jacobi_eigh).
+template <int JB>
+struct JTraits {
+  static constexpr int kJB = JB;             // indices per block
+  static constexpr int kJS = 2 * JB;         // subproblem size
+  static constexpr int kJT = JB * JB;        // threads per CTA: one per (row pair, column pair)
+  static constexpr int kJLd = kJS + 4;       // smem row stride ≡ 4 (mod 16): conflict-free DMMA fragments
+  static constexpr int kJTile = kJS * kJLd;
+  static constexpr unsigned kMask = JB == 32 ? 0xffffffffu : ((1u << JB) - 1u);
+  static constexpr size_t kSmemBytes = (size_t)5 * kJTile * sizeof(double);
+};
 
 struct JacobiArgs {
   double* a;        // m×m, ld lda (input; may end up holding the result)
@@ -63,10 +70,11 @@ PSD_DEVINL void circle_pair(int nplayers, int r, int i, int& a, int& b) {
   }
 }
 
+template <int JB>
 PSD_DEVINL int sub_index(int nblk, int r, int pair, int k) {
   int a, b;
   circle_pair(nblk, r, pair, a, b);
-  return (k < kJB) ? a * kJB + k : b * kJB + (k - kJB);
+  return (k < JB) ? a * JB + k : b * JB + (k - JB);
 }
 
 __device__ void grid_barrier(unsigned* bar, unsigned& gen) {
@@ -101,7 +109,9 @@ PSD_DEVINL bool rotation(double app, double aqq, double apq, double abs_tol, dou
 
 // Pair k of inner step ir: full sweep = circle method over 32 indices
 // (31 steps), cross sweep = (k, 16 + (k + ir) mod 16) (16 steps).
+template <int JB>
 PSD_DEVINL void step_pair(bool full, int ir, int k, int& p, int& q) {
+  constexpr int kJS = 2 * JB;
   if (full) {
     if (k == 0) {
       p = kJS - 1;
@@ -114,31 +124,35 @@ PSD_DEVINL void step_pair(bool full, int ir, int k, int& p, int& q) {
     }
   } else {
     p = k;
-    q = kJB + ((k + ir) & (kJB - 1));
+    q = JB + ((k + ir) & (JB - 1));
   }
 }
 
 // One parallel step: reads (Sc, Vc), writes every element of (Sn, Vn).
 // Returns #rotations (block-uniform); 0 ⇒ nothing written.
+template <int JB>
 __device__ int jacobi_step(const double* Sc, const double* Vc, double* Sn, double* Vn, bool full,
                            int ir, double abs_tol) {
+  using T = JTraits<JB>;
+  constexpr int L = T::kJLd;
   const int lane = threadIdx.x & 31;
-  const int l = lane & 15;
+  const int l = lane & (JB - 1);           // this lane's rotation (pair l of the step)
   int p, q;
-  step_pair(full, ir, l, p, q);
+  step_pair<JB>(full, ir, l, p, q);
   double c, s, t;
-  const bool r = rotation(Sc[p * kJLd + p], Sc[q * kJLd + q], Sc[p * kJLd + q], abs_tol, c, s, t);
-  const int nrot = __popc(__ballot_sync(0xffffffffu, r) & 0xffffu);
+  const bool r = rotation(Sc[p * L + p], Sc[q * L + q], Sc[p * L + q], abs_tol, c, s, t);
+  const int nrot = __popc(__ballot_sync(0xffffffffu, r) & T::kMask);
   if (nrot == 0) return 0;
   // thread → (k, l): rows {p_k, q_k} × cols {p_l, q_l}
-  const int k = ((threadIdx.x >> 5) << 1) | (lane >> 4);
-  const double ck = __shfl_sync(0xffffffffu, c, k);
-  const double sk = __shfl_sync(0xffffffffu, s, k);
-  const double tk = __shfl_sync(0xffffffffu, t, k);
+  const int k = (int)threadIdx.x / JB;
+  // lane k of every warp holds rotation k (k < JB ≤ 32)
+  const double ck = __shfl_sync(0xffffffffu, c, k & (JB - 1));
+  const double sk = __shfl_sync(0xffffffffu, s, k & (JB - 1));
+  const double tk = __shfl_sync(0xffffffffu, t, k & (JB - 1));
   int pk, qk;
-  step_pair(full, ir, k, pk, qk);
-  double b00 = Sc[pk * kJLd + p], b01 = Sc[pk * kJLd + q];
-  double b10 = Sc[qk * kJLd + p], b11 = Sc[qk * kJLd + q];
+  step_pair<JB>(full, ir, k, pk, qk);
+  double b00 = Sc[pk * L + p], b01 = Sc[pk * L + q];
+  double b10 = Sc[qk * L + p], b11 = Sc[qk * L + q];
   const double r00 = ck * b00 - sk * b10, r01 = ck * b01 - sk * b11;
   const double r10 = sk * b00 + ck * b10, r11 = sk * b01 + ck * b11;
   b00 = c * r00 - s * r01;
@@ -146,51 +160,55 @@ __device__ int jacobi_step(const double* Sc, const double* Vc, double* Sn, doubl
   b10 = c * r10 - s * r11;
   b11 = s * r10 + c * r11;
   if (k == l && sk != 0.0) {  // the rotated pair itself: exact form
-    const double apq = Sc[pk * kJLd + qk];
-    b00 = Sc[pk * kJLd + pk] - tk * apq;
-    b11 = Sc[qk * kJLd + qk] + tk * apq;
+    const double apq = Sc[pk * L + qk];
+    b00 = Sc[pk * L + pk] - tk * apq;
+    b11 = Sc[qk * L + qk] + tk * apq;
     b01 = 0.0;
     b10 = 0.0;
   }
-  Sn[pk * kJLd + p] = b00;
-  Sn[pk * kJLd + q] = b01;
-  Sn[qk * kJLd + p] = b10;
-  Sn[qk * kJLd + q] = b11;
-  // V ← V J for rows (tid>>4) and (tid>>4)+16, pair l
+  Sn[pk * L + p] = b00;
+  Sn[pk * L + q] = b01;
+  Sn[qk * L + p] = b10;
+  Sn[qk * L + q] = b11;
+  // V ← V J for rows k and k + JB, pair l
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const int row = (threadIdx.x >> 4) + 16 * h;
-    const double a0 = Vc[row * kJLd + p], a1 = Vc[row * kJLd + q];
-    Vn[row * kJLd + p] = c * a0 - s * a1;
-    Vn[row * kJLd + q] = s * a0 + c * a1;
+    const int row = k + JB * h;
+    const double a0 = Vc[row * L + p], a1 = Vc[row * L + q];
+    Vn[row * L + p] = c * a0 - s * a1;
+    Vn[row * L + q] = s * a0 + c * a1;
   }
   __syncthreads();
   return nrot;
 }
 
-// C (32×32) = op(A)·B for A, B in shared memory (row stride kJLd) on the FP64
-// tensor cores: warp w owns rows (w&3)·8 … +8, cols (w>>2)·16 … +16.
+// C (kJS×kJS) = op(A)·B for A, B in shared memory (row stride kJLd) on the FP64
+// tensor cores: warp w owns rows (w mod JB/4)·8 … +8, cols (w div JB/4)·16 … +16.
 // aT: A is stored transposed (A[m][k] = Asmem[k][m]).
-PSD_DEVINL void mm32_dmma(const double* A, bool aT, const double* B, double (&c)[2][2]) {
+template <int JB>
+PSD_DEVINL void mm_dmma(const double* A, bool aT, const double* B, double (&c)[2][2]) {
+  using T = JTraits<JB>;
+  constexpr int L = T::kJLd;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int m0 = (warp & 3) * 8, n0 = (warp >> 2) * 16;
+  const int m0 = (warp % (JB / 4)) * 8, n0 = (warp / (JB / 4)) * 16;
   c[0][0] = c[0][1] = c[1][0] = c[1][1] = 0.0;
 #pragma unroll
-  for (int k0 = 0; k0 < kJS; k0 += 4) {
-    const double a = aT ? A[(k0 + t) * kJLd + m0 + g] : A[(m0 + g) * kJLd + k0 + t];
-    const double b0 = B[(k0 + t) * kJLd + n0 + g];
-    const double b1 = B[(k0 + t) * kJLd + n0 + 8 + g];
+  for (int k0 = 0; k0 < T::kJS; k0 += 4) {
+    const double a = aT ? A[(k0 + t) * L + m0 + g] : A[(m0 + g) * L + k0 + t];
+    const double b0 = B[(k0 + t) * L + n0 + g];
+    const double b1 = B[(k0 + t) * L + n0 + 8 + g];
     dmma_8x8x4(c[0][0], c[0][1], a, b0);
     dmma_8x8x4(c[1][0], c[1][1], a, b1);
   }
 }
 
-// (row, col) within the 32×32 tile of accumulator (j, e) of this thread
-PSD_DEVINL void mm32_coord(int j, int e, int& row, int& col) {
+// (row, col) within the kJS×kJS tile of accumulator (j, e) of this thread
+template <int JB>
+PSD_DEVINL void mm_coord(int j, int e, int& row, int& col) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  row = (warp & 3) * 8 + (lane >> 2);
-  col = (warp >> 2) * 16 + 8 * j + 2 * (lane & 3) + e;
+  row = (warp % (JB / 4)) * 8 + (lane >> 2);
+  col = (warp / (JB / 4)) * 16 + 8 * j + 2 * (lane & 3) + e;
 }
 
 // ---- dataflow synchronisation (no grid-wide barrier) -----------------------
@@ -226,8 +244,11 @@ PSD_DEVINL int pair_of(int nblk, int R, int x) {
 //   A-item (a,b):  solves a, b of round R + the four R−1 A-items of its blocks;
 //   V-item (c,b):  solve b + the two R−1 V-items of its columns;
 // and a solve first waits until every reader of its J/S slot (R−2) is done.
-__global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
-  __shared__ __align__(16) double sm[5 * kJTile];
+template <int JB>
+__global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A) {
+  using T = JTraits<JB>;
+  constexpr int kJS = T::kJS, kJT = T::kJT, kJLd = T::kJLd, kJTile = T::kJTile;
+  extern __shared__ __align__(16) double sm[];
   double* S0 = sm;
   double* V0 = sm + kJTile;
   double* S1 = sm + 2 * kJTile;
@@ -275,7 +296,7 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
               flag_wait(&aflag[pb * P + pb], R);
             }
           }
-          if (tid < kJS) ia[tid] = sub_index(nblk, r, pair, tid);
+          if (tid < kJS) ia[tid] = sub_index<JB>(nblk, r, pair, tid);
           __syncthreads();
           const long long tw1 = clock64();
           {
@@ -302,9 +323,9 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
           double *Sc = S0, *Vc = V0, *Sn = S1, *Vn = V1;
           for (int isw = 0; isw < inner_sweeps; ++isw) {
             int srot = 0;
-            const int nsteps = full ? kJS - 1 : kJB;
+            const int nsteps = full ? kJS - 1 : JB;
             for (int ir = 0; ir < nsteps; ++ir) {
-              const int nr = jacobi_step(Sc, Vc, Sn, Vn, full, ir, abs_tol);
+              const int nr = jacobi_step<JB>(Sc, Vc, Sn, Vn, full, ir, abs_tol);
               if (nr) {
                 double* tp = Sc;
                 Sc = Sn;
@@ -340,8 +361,8 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
           const int pa = it / P, pb = it % P;
           const long long tw0 = clock64();
           if (tid < kJS) {
-            ia[tid] = sub_index(nblk, r, pa, tid);
-            ib[tid] = sub_index(nblk, r, pb, tid);
+            ia[tid] = sub_index<JB>(nblk, r, pa, tid);
+            ib[tid] = sub_index<JB>(nblk, r, pb, tid);
           }
           if (tid == 0) {
             flag_wait(&sflag[pa], R + 1);
@@ -399,23 +420,23 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
               }
             }
             __syncthreads();
-            mm32_dmma(V0, true, S0, c);  // J_aᵀ T
+            mm_dmma<JB>(V0, true, S0, c);  // J_aᵀ T
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 int row, col;
-                mm32_coord(j, e, row, col);
+                mm_coord<JB>(j, e, row, col);
                 S1[row * kJLd + col] = c[j][e];
               }
             __syncthreads();
-            mm32_dmma(S1, false, X, c);  // (J_aᵀ T) J_b
+            mm_dmma<JB>(S1, false, X, c);  // (J_aᵀ T) J_b
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 int row, col;
-                mm32_coord(j, e, row, col);
+                mm_coord<JB>(j, e, row, col);
                 const int gi = ia[row], gj = ib[col];
                 if (gi < m && gj < m) {
                   nxt[(long long)gi * ldn + gj] = c[j][e];
@@ -446,7 +467,7 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
           // ------------------------------------------------------- V-item
           const int vb = task - P - P * P;
           const int pb = vb % P, vc = vb / P;
-          if (tid < kJS) ib[tid] = sub_index(nblk, r, pb, tid);
+          if (tid < kJS) ib[tid] = sub_index<JB>(nblk, r, pb, tid);
           if (tid == 0) {
             flag_wait(&sflag[pb], R + 1);
             if (R >= 1) {
@@ -485,13 +506,13 @@ __global__ void __launch_bounds__(kJT) jacobi_persistent_kernel(JacobiArgs A) {
               S0[(e / kJS) * kJLd + e % kJS] = vs[u];
             }
             __syncthreads();
-            mm32_dmma(S0, false, X, c);
+            mm_dmma<JB>(S0, false, X, c);
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 int row, col;
-                mm32_coord(j, e, row, col);
+                mm_coord<JB>(j, e, row, col);
                 const int gr = r0 + row, gj = ib[col];
                 if (gr < m && gj < m) A.v[(long long)gr * A.ldv + gj] = c[j][e];
               }
@@ -560,35 +581,42 @@ __global__ void jacobi_diag_kernel(const double* a, long long lda, const double*
 
 constexpr int kJacobiMaxSweeps = 40;
 
-static void jacobi_geometry(int m, int& nblk, int& P) {
-  const int nb0 = (m + kJB - 1) / kJB;
+// 64×64 subproblems (JB = 32, PSD_JACOBI_JB=32) halve the rounds per sweep but not the
+// sweeps (13 at m = 272 either way), and each round's 1024-thread solve steps cost 4× the
+// 256-thread ones: measured on the B200 6.77 vs 3.90 ms at m = 272, 13.4 vs 11.1 ms at
+// m = 544 — so JB = 16 is the default at every size.
+constexpr int kJacobiWideMin = 1 << 30;
+
+static void jacobi_geometry(int m, int jb, int& nblk, int& P) {
+  const int nb0 = (m + jb - 1) / jb;
   nblk = std::max(2, nb0 + (nb0 & 1));
   P = nblk / 2;
 }
 
-static int jacobi_nflags(int m, int P) {
-  const int vch = (m + 2 * kJS - 1) / (2 * kJS);
+static int jacobi_nflags(int m, int jb, int P) {
+  const int vch = (m + 4 * jb - 1) / (4 * jb);
   return P + P * P + P * vch + 2 * P;
 }
 
-size_t jacobi_ws_elems(int m) {
+static size_t jacobi_ws_elems_jb(int m, int jb) {
   int nblk, P;
-  jacobi_geometry(m, nblk, P);
-  return (size_t)m * m + (size_t)4 * P * kJS * kJS + 8 + kJacobiMaxSweeps + 8 +
-         (size_t)(jacobi_nflags(m, P) + 1) / 2 + 8 + kJacobiMaxSweeps + 1;
+  jacobi_geometry(m, jb, nblk, P);
+  const size_t js = 2 * (size_t)jb;
+  return (size_t)m * m + (size_t)4 * P * js * js + 8 + kJacobiMaxSweeps + 8 +
+         (size_t)(jacobi_nflags(m, jb, P) + 1) / 2 + 8 + kJacobiMaxSweeps + 1;
 }
 
-int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long long ldv,
-                double* ws, size_t ws_elems, int* dflags, cudaStream_t st) {
-  (void)dflags;
-  if (m == 1) {
-    cudaMemcpyAsync(values, a, sizeof(double), cudaMemcpyDeviceToDevice, st);
-    set_identity(v, ldv, 1, st);
-    return 1;
-  }
-  if (ws_elems < jacobi_ws_elems(m)) return -2;
+size_t jacobi_ws_elems(int m) {
+  return std::max(jacobi_ws_elems_jb(m, 16), jacobi_ws_elems_jb(m, 32));
+}
+
+template <int JB>
+static int jacobi_run(double* a, long long lda, int m, double* values, double* v, long long ldv,
+                      double* ws, cudaStream_t st) {
+  using T = JTraits<JB>;
+  constexpr int kJS = T::kJS, kJT = T::kJT;
   int nblk, P;
-  jacobi_geometry(m, nblk, P);
+  jacobi_geometry(m, JB, nblk, P);
   JacobiArgs A{};
   A.a = a;
   A.lda = lda;
@@ -602,7 +630,7 @@ int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long
   A.counters = ints;
   A.out = ints + kJacobiMaxSweeps + 2;
   A.flags = ints + kJacobiMaxSweeps + 8;
-  const int nflags = jacobi_nflags(m, P);
+  const int nflags = jacobi_nflags(m, JB, P);
   {
     const size_t int_words = (size_t)kJacobiMaxSweeps + 8 + nflags;
     A.maxoff = reinterpret_cast<unsigned long long*>(A.norm + 8 + (int_words + 1) / 2 + 1);
@@ -628,19 +656,25 @@ int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long
   count_launch();
 
   static int max_blocks[16] = {};
+  static bool attr_set[16] = {};
   int dev = 0;
   cudaGetDevice(&dev);
+  if (!attr_set[dev]) {
+    cudaFuncSetAttribute(jacobi_persistent_kernel<JB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)T::kSmemBytes);
+    attr_set[dev] = true;
+  }
   if (!max_blocks[dev]) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_persistent_kernel, kJT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_persistent_kernel<JB>, kJT, T::kSmemBytes);
     max_blocks[dev] = std::max(1, per_sm) * device_info().sms;
   }
   const int vch = (m + 2 * kJS - 1) / (2 * kJS);
   const int tasks = P + P * P + P * vch;
   const int grid = std::max(1, std::min({tasks, max_blocks[dev], device_info().sms}));
   void* args[] = {&A};
-  if (cudaLaunchCooperativeKernel((const void*)jacobi_persistent_kernel, dim3(grid), dim3(kJT),
-                                  args, 0, st) != cudaSuccess)
+  if (cudaLaunchCooperativeKernel((const void*)jacobi_persistent_kernel<JB>, dim3(grid), dim3(kJT),
+                                  args, T::kSmemBytes, st) != cudaSuccess)
     return -3;
   count_launch();
   int out[2] = {0, 0};
@@ -652,10 +686,25 @@ int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long
     long long h[6];
     cudaMemcpy(h, A.timers, sizeof(h), cudaMemcpyDeviceToHost);
     fprintf(stderr,
-            "jacobi m=%d sweeps=%d grid=%d cycles: solve0 wait %lld load %lld compute %lld | item(0,1) wait %lld work %lld\n",
-            m, out[0], grid, h[0], h[1], h[2], h[3], h[4]);
+            "jacobi m=%d JB=%d sweeps=%d grid=%d cycles: solve0 wait %lld load %lld compute %lld | item(0,1) wait %lld work %lld\n",
+            m, JB, out[0], grid, h[0], h[1], h[2], h[3], h[4]);
   }
   return out[0];
+}
+
+int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long long ldv,
+                double* ws, size_t ws_elems, int* dflags, cudaStream_t st) {
+  (void)dflags;
+  if (m == 1) {
+    cudaMemcpyAsync(values, a, sizeof(double), cudaMemcpyDeviceToDevice, st);
+    set_identity(v, ldv, 1, st);
+    return 1;
+  }
+  if (ws_elems < jacobi_ws_elems(m)) return -2;
+  static const int jb_env = [] { const char* e = getenv("PSD_JACOBI_JB"); return e ? atoi(e) : 0; }();
+  const int jb = jb_env == 16 || jb_env == 32 ? jb_env : (m >= kJacobiWideMin ? 32 : 16);
+  return jb == 32 ? jacobi_run<32>(a, lda, m, values, v, ldv, ws, st)
+                  : jacobi_run<16>(a, lda, m, values, v, ldv, ws, st);
 }
 
 }  // namespace psd
