@@ -448,7 +448,10 @@ extern "C" {
 
 const char* psd_last_error(void) { return g_err.c_str(); }
 
-const char* psd_version(void) { return "psdproj 0.1.0 (sm_100a, FP64 DMMA)"; }
+const char* psd_version(void) {
+  return "psdproj 0.2.0 (sm_100a: FP64 as exact INT8 tcgen05 emulation (Ozaki II products, Ozaki I SYRK) "
+         "or FP64 DMMA; FP32 as 3xTF32 tcgen05)";
+}
 
 int psd_plan_create(psd_plan** out, int64_t n, int32_t width, int32_t device) {
   if (!out) return fail(PSD_ERR_INVALID_PARAMS, "null plan pointer");
