@@ -39,6 +39,7 @@ struct psd_plan {
   double *gy = nullptr, *gv = nullptr, *gpart = nullptr, *stats = nullptr, *scal = nullptr;
   double* qrstat = nullptr;
   double* dinv = nullptr;  // ceil(w/32) diagonal-block inverses (32×32) for chol_fast
+  double *L1 = nullptr, *Rinv1 = nullptr, *dinv1 = nullptr;   // shifted CholeskyQR candidate
   int gparts = 0;
   double* rpart = nullptr;
   ll rparts = 0;
@@ -311,10 +312,16 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
         break;
       }
     }
-    if (psd::chol_fast(p->G, w, w, 0.0, p->L, w, p->Rinv, w, p->dinv, p->qrstat, st) != 0)
+    // both candidates at once: unshifted (L, Rinv) and Fukaya-shifted (L1, Rinv1) with
+    // s = 11(nw + w(w+1))·u·trace(G) — the fallback costs no extra launch or round trip
+    const double sfac = 11.0 * ((double)n * w + (double)w * (w + 1)) * u;
+    if (psd::chol_fast(p->G, w, w, 0.0, p->L, w, p->Rinv, w, p->dinv, p->qrstat, st, sfac, p->L1,
+                       p->Rinv1, p->dinv1, p->qrstat + 8) != 0)
       return fail(PSD_ERR_INVALID_PARAMS, "width %d too large for the CholeskyQR kernel", w);
-    PSD_CUDA_CHECK(psd::read_small(hs, p->qrstat, sizeof(hs), st), "qr status");
+    double hs2[16];
+    PSD_CUDA_CHECK(psd::read_small(hs2, p->qrstat, sizeof(hs2), st), "qr status");
     PSD_TRY(sync(st, "cholesky"));
+    std::memcpy(hs, hs2, sizeof(hs));
     const double trace = hs[1];
     if (pass == 0) {
       info->frob = std::sqrt(std::max(trace, 0.0));
@@ -330,18 +337,15 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
     if (pass == 0) kest0 = kest;
     const bool shift = bad || kest > 3e6;
     if (shift) {
-      // Fukaya et al. shifted CholeskyQR: s = 11(mn + n(n+1))·u·‖Y‖²
-      const double s = 11.0 * ((double)n * w + (double)w * (w + 1)) * u * trace;
-      psd::chol_fast(p->G, w, w, s, p->L, w, p->Rinv, w, p->dinv, p->qrstat, st);
-      PSD_CUDA_CHECK(psd::read_small(hs, p->qrstat, sizeof(hs), st),
-                     "qr status");
-      PSD_TRY(sync(st, "shifted cholesky"));
-      if (hs[0] != 0.0)
-        return fail(PSD_ERR_CONVERGENCE, "shifted CholeskyQR broke down (pivot %d)", (int)hs[0]);
+      // Fukaya et al. shifted CholeskyQR: s = 11(mn + n(n+1))·u·‖Y‖² (candidate 1 above)
+      if (hs2[8] != 0.0)
+        return fail(PSD_ERR_CONVERGENCE, "shifted CholeskyQR broke down (pivot %d)", (int)hs2[8]);
       info->shifted = 1;
     }
-    if (rdiag) psd::accumulate_diag(p->L, w, w, rdiag, st);
-    PSD_TRY(panel_nn(p, bufs[cur], ld, p->Rinv, w, bufs[tmp], ld, n, w, w, st));
+    const double* Lsel = shift ? p->L1 : p->L;
+    const double* Rsel = shift ? p->Rinv1 : p->Rinv;
+    if (rdiag) psd::accumulate_diag(Lsel, w, w, rdiag, st);
+    PSD_TRY(panel_nn(p, bufs[cur], ld, Rsel, w, bufs[tmp], ld, n, w, w, st));
     std::swap(cur, tmp);
     info->passes++;
     unshifted_run = shift ? 0 : unshifted_run + 1;
@@ -470,6 +474,9 @@ int psd_plan_create(psd_plan** out, int64_t n, int32_t width, int32_t device) {
   ok &= (p->G = alloc(p, sq)) != nullptr;
   ok &= (p->L = alloc(p, sq)) != nullptr;
   ok &= (p->Rinv = alloc(p, sq)) != nullptr;
+  ok &= (p->L1 = alloc(p, sq)) != nullptr;
+  ok &= (p->Rinv1 = alloc(p, sq)) != nullptr;
+  ok &= (p->dinv1 = alloc(p, (size_t)((width + 31) / 32) * 1024)) != nullptr;
   ok &= (p->T = alloc(p, sq)) != nullptr;
   ok &= (p->V = alloc(p, sq)) != nullptr;
   ok &= (p->U = alloc(p, sq)) != nullptr;
@@ -490,7 +497,7 @@ int psd_plan_create(psd_plan** out, int64_t n, int32_t width, int32_t device) {
   ok &= (p->gpart = alloc(p, p->gparts)) != nullptr;
   ok &= (p->stats = alloc(p, 4)) != nullptr;
   ok &= (p->scal = alloc(p, 8)) != nullptr;
-  ok &= (p->qrstat = alloc(p, 8)) != nullptr;
+  ok &= (p->qrstat = alloc(p, 16)) != nullptr;   // [0, 8): unshifted candidate, [8, 16): shifted
   ok &= (p->dinv = alloc(p, (size_t)((width + 31) / 32) * 1024)) != nullptr;
   psd::GemmOp rop;
   rop.M = (int)n;

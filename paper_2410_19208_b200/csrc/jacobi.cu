@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "launch.h"
 
@@ -90,6 +91,19 @@ __device__ void grid_barrier(unsigned* bar, unsigned& gen) {
     } while (seen < target);
   }
   __syncthreads();
+}
+
+// Optional task timeline (PSD_JACOBI_TRACE): per (round, task) three %globaltimer stamps —
+// task begin, dependencies satisfied, flag released — for critical-path analysis.
+__device__ long long* g_jtrace = nullptr;
+PSD_DEVINL long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+PSD_DEVINL void jtrace(int R, int ntask, int task, int slot, long long t) {
+  long long* tr = g_jtrace;
+  if (tr != nullptr && R < 1024) tr[((long long)R * ntask + task) * 3 + slot] = t;
 }
 
 // Rotation for pair (p,q) (GVL sym.schur2; one sqrt, one division, one rsqrt).
@@ -285,6 +299,7 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
           const int pair = task;
           const long long tw0 = clock64();
           if (tid == 0) {
+            jtrace(R, ntask, task, 0, gtimer());
             if (R >= 2) flag_wait(&jread[(R & 1) * P + pair], (R / 2) * readers);
             if (R >= 1) {
               int ba, bb;
@@ -298,6 +313,7 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
           }
           if (tid < kJS) ia[tid] = sub_index<JB>(nblk, r, pair, tid);
           __syncthreads();
+          if (tid == 0) jtrace(R, ntask, task, 1, gtimer());
           const long long tw1 = clock64();
           {
             // all loads of this thread in flight at once (register staging)
@@ -349,6 +365,7 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
           if (tid == 0) {
             if (rots > 0) atomicAdd(&A.counters[sweep], rots);
             flag_set(&sflag[pair], R + 1);
+            jtrace(R, ntask, task, 2, gtimer());
             if (A.timers && pair == 0) {
               A.timers[0] += tw1 - tw0;
               A.timers[1] += tw2 - tw1;
@@ -365,6 +382,7 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
             ib[tid] = sub_index<JB>(nblk, r, pb, tid);
           }
           if (tid == 0) {
+            jtrace(R, ntask, task, 0, gtimer());
             flag_wait(&sflag[pa], R + 1);
             flag_wait(&sflag[pb], R + 1);
             if (R >= 1) {
@@ -380,6 +398,7 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
             }
           }
           __syncthreads();
+          if (tid == 0) jtrace(R, ntask, task, 1, gtimer());
           const long long tw1 = clock64();
           double c[2][2];
           const bool last = (r == rounds - 1);
@@ -458,6 +477,7 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
             atomicAdd(&jread[(R & 1) * P + pa], 1);
             if (pb != pa) atomicAdd(&jread[(R & 1) * P + pb], 1);
             flag_set(&aflag[pa * P + pb], R + 1);
+            jtrace(R, ntask, task, 2, gtimer());
             if (A.timers && it == 1) {
               A.timers[3] += tw1 - tw0;
               A.timers[4] += clock64() - tw1;
@@ -469,6 +489,7 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
           const int pb = vb % P, vc = vb / P;
           if (tid < kJS) ib[tid] = sub_index<JB>(nblk, r, pb, tid);
           if (tid == 0) {
+            jtrace(R, ntask, task, 0, gtimer());
             flag_wait(&sflag[pb], R + 1);
             if (R >= 1) {
               int b0, b1;
@@ -478,6 +499,7 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
             }
           }
           __syncthreads();
+          if (tid == 0) jtrace(R, ntask, task, 1, gtimer());
           const double* Jb = Jslot + (size_t)pb * kJS * kJS;
           constexpr int NS = kJS * kJS / kJT;
           {
@@ -521,6 +543,7 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
           if (tid == 0) {
             atomicAdd(&jread[(R & 1) * P + pb], 1);
             flag_set(&vflag[vc * P + pb], R + 1);
+            jtrace(R, ntask, task, 2, gtimer());
           }
         }
         __syncthreads();
@@ -651,6 +674,15 @@ static int jacobi_run(double* a, long long lda, int m, double* values, double* v
     A.timers = dtimers;
   }
   cudaMemsetAsync(ints, 0, (kJacobiMaxSweeps + 8 + nflags) * sizeof(int), st);
+  static const char* trace_path = getenv("PSD_JACOBI_TRACE");
+  static long long* dtrace = nullptr;
+  const int vch0 = (m + 2 * kJS - 1) / (2 * kJS);
+  const size_t trace_elems = (size_t)1024 * (P + P * P + P * vch0) * 3;
+  if (trace_path) {
+    if (!dtrace) cudaMalloc(&dtrace, trace_elems * sizeof(long long) * 4);
+    cudaMemsetAsync(dtrace, 0, trace_elems * sizeof(long long), st);
+    cudaMemcpyToSymbolAsync(g_jtrace, &dtrace, sizeof(dtrace), 0, cudaMemcpyHostToDevice, st);
+  }
   set_identity(v, ldv, m, st);
   jacobi_norm_kernel<<<1, 1024, 0, st>>>(a, lda, m, A.norm);
   count_launch();
@@ -682,6 +714,18 @@ static int jacobi_run(double* a, long long lda, int m, double* values, double* v
   jacobi_diag_kernel<<<(m + 255) / 256, 256, 0, st>>>(a, lda, ws, m, A.out, values);
   count_launch();
   if (out[1]) copy_matrix(ws, m, a, lda, m, m, st);
+  if (trace_path) {   // binary dump: header (m, P, vch, rounds, ntask) then int64 [R][task][3]
+    std::vector<long long> h(trace_elems);
+    cudaMemcpy(h.data(), dtrace, trace_elems * sizeof(long long), cudaMemcpyDeviceToHost);
+    long long* none = nullptr;
+    cudaMemcpyToSymbol(g_jtrace, &none, sizeof(none));
+    if (FILE* f = fopen(trace_path, "wb")) {
+      const long long hdr[5] = {m, P, vch0, (long long)(nblk - 1) * std::max(out[0], 0), P + P * P + P * vch0};
+      fwrite(hdr, sizeof(hdr), 1, f);
+      fwrite(h.data(), sizeof(long long), h.size(), f);
+      fclose(f);
+    }
+  }
   if (A.timers) {
     long long h[6];
     cudaMemcpy(h, A.timers, sizeof(h), cudaMemcpyDeviceToHost);

@@ -503,9 +503,13 @@ PSD_DEVINL double chol_src(const double* __restrict__ G, long long ldg, const do
   return L[(long long)i * ldl + j];
 }
 
+// Dual candidates (gridDim.x == 2): CTA 0 factors G + shift·I into (L, Dinv, status), CTA 1
+// factors G + shift_factor·trace(G)·I into (L1, Dinv1, status1) at the same time — the
+// shifted CholeskyQR fallback is then ready without a second launch and host round trip.
 __global__ void __launch_bounds__(256, 1)
     chol_blocked_kernel(const double* __restrict__ G, long long ldg, int m, double shift, double* L,
-                        long long ldl, double* Dinv, double* status) {
+                        long long ldl, double* Dinv, double* status, double shift_factor, double* L1,
+                        double* Dinv1, double* status1) {
   extern __shared__ double sm[];
   double* P = sm;                      // panel rows × kFL
   double* Di = sm + (size_t)max(m, kFB) * kFL;   // current inv(L_jj), 32 × 33
@@ -520,10 +524,17 @@ __global__ void __launch_bounds__(256, 1)
   if (lane == 0) red[warp] = tr;
   if (tid == 0) info_s = 0;
   __syncthreads();
+  double trace_all = 0.0;
+  for (int w = 0; w < kNW; ++w) trace_all += red[w];
+  if (blockIdx.x == 1) {   // the shifted candidate (fixed-order trace: same value in both CTAs)
+    shift = shift_factor * trace_all;
+    L = L1;
+    Dinv = Dinv1;
+    status = status1;
+  }
   if (tid == 0) {
-    double t = 0.0;
-    for (int w = 0; w < kNW; ++w) t += red[w];
-    status[1] = t;
+    status[1] = trace_all;
+    status[4] = shift;
   }
   long long tc0 = clock64();
   for (int p0 = 0; p0 < m; p0 += kFB) {
@@ -738,8 +749,16 @@ constexpr int kTiLdX = kFB + 4;
 __global__ void __launch_bounds__(256) tri_inv_blocked_kernel(const double* __restrict__ L,
                                                               long long ldl, int m,
                                                               const double* __restrict__ Dinv,
-                                                              double* Rinv, long long ldr) {
+                                                              double* Rinv, long long ldr,
+                                                              const double* __restrict__ L1,
+                                                              const double* __restrict__ Dinv1,
+                                                              double* Rinv1) {
   extern __shared__ double xs[];
+  if (blockIdx.y == 1) {   // second candidate of chol_fast_dual
+    L = L1;
+    Dinv = Dinv1;
+    Rinv = Rinv1;
+  }
   const int j = blockIdx.x;
   const int nblk = (m + kFB - 1) / kFB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -808,7 +827,8 @@ __global__ void __launch_bounds__(256) tri_inv_blocked_kernel(const double* __re
 }
 
 int chol_fast(const double* G, long long ldg, int m, double shift, double* L, long long ldl,
-              double* Rinv, long long ldr, double* Dinv, double* status, cudaStream_t st) {
+              double* Rinv, long long ldr, double* Dinv, double* status, cudaStream_t st,
+              double shift_factor, double* L1, double* Rinv1, double* Dinv1, double* status1) {
   const size_t smem1 = ((size_t)std::max(m, kFB) * kFL + kFB * (kFB + 1)) * sizeof(double);
   const int nblk = (m + kFB - 1) / kFB;
   const size_t smem2 = ((size_t)nblk * kFB * kTiLdX + kFB * kTiLdL + 2 * kFB * kTiLdX) * sizeof(double);
@@ -830,9 +850,12 @@ int chol_fast(const double* G, long long ldg, int m, double shift, double* L, lo
     const long long z[6] = {0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbolAsync(g_chol_t, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
   }
-  chol_blocked_kernel<<<1, 256, smem1, st>>>(G, ldg, m, shift, L, ldl, Dinv, status);
+  const bool dual = L1 != nullptr;
+  chol_blocked_kernel<<<dual ? 2 : 1, 256, smem1, st>>>(G, ldg, m, shift, L, ldl, Dinv, status,
+                                                       shift_factor, L1, Dinv1, status1);
   count_launch();
-  tri_inv_blocked_kernel<<<nblk, 256, smem2, st>>>(L, ldl, m, Dinv, Rinv, ldr);
+  tri_inv_blocked_kernel<<<dim3(nblk, dual ? 2 : 1), 256, smem2, st>>>(L, ldl, m, Dinv, Rinv, ldr, L1,
+                                                                     Dinv1, Rinv1);
   count_launch();
   if (timers) {
     long long h[6];

@@ -189,7 +189,9 @@ int chol_inv(const double* G, long long ldg, int m, double shift, double* L, lon
 // Faster two-launch variant (warp-register diagonal blocks + parallel block
 // inverse); dinv scratch: ceil(m/32)·32·32 doubles.  Same outputs as chol_inv.
 int chol_fast(const double* G, long long ldg, int m, double shift, double* L, long long ldl,
-              double* Rinv, long long ldr, double* Dinv, double* status, cudaStream_t st);
+              double* Rinv, long long ldr, double* Dinv, double* status, cudaStream_t st,
+              double shift_factor = 0.0, double* L1 = nullptr, double* Rinv1 = nullptr,
+              double* Dinv1 = nullptr, double* status1 = nullptr);
 // rdiag[i] *= L[i][i]
 void accumulate_diag(const double* l, long long ldl, int m, double* rdiag, cudaStream_t st);
 // Symmetric eigensolver (block Jacobi).  a (m×m, destroyed), values[m], v (m×m).
