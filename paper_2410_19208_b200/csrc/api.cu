@@ -40,6 +40,7 @@ struct psd_plan {
   double* qrstat = nullptr;
   double* dinv = nullptr;  // ceil(w/32) diagonal-block inverses (32×32) for chol_fast
   double *L1 = nullptr, *Rinv1 = nullptr, *dinv1 = nullptr;   // shifted CholeskyQR candidate
+  bool oz_gram = false;   // CholeskyQR Grams on the INT8 engine (set per call by psd_ran_proj)
   int gparts = 0;
   double* rpart = nullptr;
   ll rparts = 0;
@@ -211,8 +212,38 @@ int xmul(psd_plan* p, const double* x, ll n, ll ldx, const double* P, ll ldP, in
 }
 
 // G (w×w, ld w) = Aᵀ·B for n×w panels A, B (symmetrised when A == B or sym)
+// G = YᵀY (w×w) as an exact-integer Gram on the INT8 tensor cores (Ozaki II): Y's column
+// scales and transposed residues (the panel preparation of the X·P products) serve as
+// both operands — A = Yᵀ is B's residue planes read row-wise — K = n unsplit up to 2^15
+// per split, CRT on the w×w output only.  Bitwise symmetric (the integer sums are).
+int gram_oz(psd_plan* p, const double* Y, ll ld, ll n, int w, double* G, cudaStream_t st) {
+  psd::OzOp op;
+  op.P = Y;
+  op.ldp = ld;
+  op.N = w;
+  op.K = (int)n;
+  op.br = p->oz_br;
+  op.ldbr = p->oz_ldk;
+  op.f = p->oz_f;
+  if (psd::oz_prepare_panel(op, st) != 0) return -1;
+  op.ar = op.br;
+  op.ldar = op.ldbr;
+  op.ar_rows = (w + 15) / 16 * 16;
+  op.e = op.f;
+  op.M = w;
+  op.res = p->oz_res;
+  op.res_elems = p->oz_res_elems;
+  op.C = G;
+  op.ldc = w;
+  return psd::oz_gemm_prepared(op, st) < 0 ? -1 : 0;
+}
+
 int panel_tn(psd_plan* p, const double* A, const double* B, ll ld, ll n, int w, double* G,
              bool sym, cudaStream_t st) {
+  if (A == B && p->oz_gram && w <= 512 && n <= psd::oz_max_k()) {
+    if (gram_oz(p, A, ld, n, w, G, st) == 0) return PSD_OK;
+    return fail(PSD_ERR_INVALID_PARAMS, "INT8-emulated Gram rejected its operands");
+  }
   psd::GemmOp op;
   op.a_layout = psd::A_KM;
   op.b_layout = psd::B_KN;
@@ -608,6 +639,7 @@ int psd_range_finder(psd_plan* p, const double* x, int64_t m, int64_t n, int64_t
   DeviceGuard g(p->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   psd::g_launch_count = 0;
+  p->oz_gram = false;
   bool use_t = (m != n) || !(flags & PSD_FLAG_ASSUME_SYMMETRIC);
   if (use_t && m == n) {
     SymInfo si;
@@ -810,6 +842,7 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   DeviceGuard g(p->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   psd::g_launch_count = 0;
+  p->oz_gram = false;
   psd_report r{};
   r.residual_frob = NAN;
   r.alpha_used = alpha;
@@ -925,6 +958,8 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   }
   // 3: X·P products on the INT8 engine, Xᵀ·P (X not bitwise symmetric) on DMMA
   r.sketch_engine = f32 ? 2 : (oz ? (use_t ? 3 : 1) : 0);
+  static const bool oz_gram_on = [] { const char* e = getenv("PSD_OZ_GRAM"); return !(e && e[0] == '0'); }();
+  p->oz_gram = oz && oz_gram_on;
   if (oz) {
     Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
     if (have_rowmax)   // row scales from the symmetry pass: one read of X

@@ -84,6 +84,7 @@ struct OzOp {
   size_t res_elems = 0;
   double* C = nullptr;
   long long ldc = 0;
+  long long ar_rows = 0;       // rows per A residue plane (0: M) — a transposed panel as A
   double alpha = 0.0;          // α > 0: C = (acc + α·S)/α
   const double* S = nullptr;
   long long lds = 0;

@@ -907,7 +907,7 @@ int oz_gemm_prepared(const OzOp& op, cudaStream_t st) {
   p.stages = std::min(8, ((int)device_info().max_smem - 3072) / sb);
   const size_t smem = (size_t)p.stages * sb + 1024;
   CUtensorMap ma, mb, mb2;
-  if (!map_i8_3d(&ma, op.ar, op.K, op.M, op.ldar, kNumMod, BM) ||
+  if (!map_i8_3d(&ma, op.ar, op.K, op.ar_rows ? op.ar_rows : op.M, op.ldar, kNumMod, BM) ||
       !map_i8_3d(&mb, op.br, op.K, w_pad, op.ldbr, kNumMod, p.bn / 2) ||
       !map_i8_3d(&mb2, op.br, op.K, w_pad, op.ldbr, kNumMod, std::max(p.bn2, 16) / 2))
     return -5;
