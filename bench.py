@@ -73,6 +73,9 @@ def parse():
     ap.add_argument("--no-fp32", action="store_true", help="skip the config-3 FP32 (3xTF32) leg")
     ap.add_argument("--no-scaled", action="store_true", help="skip the scaled (Alg. 3 + Alg. 5) leg")
     ap.add_argument("--no-c4", action="store_true", help="skip the config-4 row-sharded leg")
+    ap.add_argument("--no-peaks", action="store_true",
+                    help="skip the in-run cuBLAS peak measurement (profiling runs; roofline then uses "
+                         "MEASURED_PEAKS.json)")
     ap.add_argument("--c4-steps", type=int, default=3)
     ap.add_argument("--ref-budget-s", type=float, default=float(os.environ.get("PSD_REF_BUDGET_S", 300)),
                     help="reference arm: wall-clock budget for the timed full-size projections")
@@ -463,7 +466,7 @@ def run_ours(a):
     n, params = a.n, psd.RangeParams(k=a.k, l=a.p, q=a.q)
     psd.set_fp64_engine(a.fp64_engine)
 
-    peaks = measure_peaks(torch, dev) if rank == 0 else {}
+    peaks = measure_peaks(torch, dev) if rank == 0 and not a.no_peaks else {}
     peak = peaks.get("fp64_tflops")
     nominal = 148 * 128 * 1.965  # GFLOP/s: 148 SMs × 64 DMMA FMA/clk × 2 × 1965 MHz
 

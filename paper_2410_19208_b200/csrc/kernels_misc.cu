@@ -15,6 +15,9 @@ namespace psd {
 // 32×32 tile pairs (I ≤ J): max|x|, max|x − xᵀ| and "bitwise symmetric".
 // ---------------------------------------------------------------------------
 constexpr int kSymT = 64;
+#ifndef PSD_SYM_MINB
+#define PSD_SYM_MINB 3   // blocks per SM the register budget is cut for (4: 64 regs, spills with row maxima)
+#endif
 
 // Persistent blocks walk the lower-triangular list of 64×64 tile pairs
 // (I ≥ J): tile (J,I) is staged transposed through shared memory, tile (I,J)
@@ -26,7 +29,7 @@ constexpr int kSymT = 64;
 // instead of twice).  One REDUX.MAX per tile row and warp, one 32-bit atomic per tile
 // row; zeroed by the caller.
 template <typename T>
-__global__ void __launch_bounds__(256, 4) sym_stats_kernel(const T* __restrict__ x, long long n,
+__global__ void __launch_bounds__(256, PSD_SYM_MINB) sym_stats_kernel(const T* __restrict__ x, long long n,
                                                         long long ldx, long long npairs,
                                                         double* stats, unsigned* __restrict__ rowmax,
                                                         int diag) {
@@ -139,7 +142,7 @@ static void sym_stats_t(const T* x, long long n, long long ldx, double* stats, u
   if (rowmax) cudaMemsetAsync(rowmax, 0, (size_t)n * sizeof(unsigned), st);
   const long long nt = (n + kSymT - 1) / kSymT;
   const long long npairs = nt * (nt + 1) / 2;
-  const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * 6);
+  const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * PSD_SYM_MINB * 2);
   static const int diag = [] { const char* e = getenv("PSD_SYM_ORDER"); return e && e[0] == 'd' ? 1 : 0; }();
   sym_stats_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats, rowmax, diag);
   count_launch();

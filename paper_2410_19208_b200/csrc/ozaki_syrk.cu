@@ -151,6 +151,13 @@ PSD_DEVINL void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
+PSD_DEVINL void tmem_ld16(uint32_t taddr, uint32_t (&r)[8], uint32_t (&q)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7])
+      : "r"(taddr));
+}
 PSD_DEVINL void st_v4_f64(double* p, double a, double b, double c, double d) {
   asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
@@ -346,10 +353,21 @@ __global__ void __launch_bounds__(kThreads, 1) i8_syrk_kernel(const SyrkParams p
       for (int g = 0; g < kGroups; ++g) {
         const int j0 = jb + 8 * g;
         active[g] = j0 <= ib + 31 && j0 < p.n && ib < p.n;
-        if (active[g]) {
+      }
+      if constexpr (kGroups == 2) {   // both groups of a level in one 16-column load
+        if (active[0]) {
 #pragma unroll
           for (int L = 0; L < D; ++L)
-            tmem_ld8(tmem + tq + (uint32_t)(b * kBufCols + L * BN + slice * 8 * kGroups + 8 * g), v[g][L]);
+            tmem_ld16(tmem + tq + (uint32_t)(b * kBufCols + L * BN + slice * 16), v[0][L], v[1][L]);
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < kGroups; ++g) {
+          if (active[g]) {
+#pragma unroll
+            for (int L = 0; L < D; ++L)
+              tmem_ld8(tmem + tq + (uint32_t)(b * kBufCols + L * BN + slice * 8 * kGroups + 8 * g), v[g][L]);
+          }
         }
       }
       const double si = s_rs[sb][quad * 32 + lane];

@@ -6,9 +6,24 @@ import sys
 
 path = sys.argv[1]
 title = sys.argv[2] if len(sys.argv) > 2 else path
-OURS = ("psd::", "tc32::", "oz::", "ozs::", "<unnamed>::")   # kernels of libpsdproj.so
+import re
+import subprocess
+import os
+# kernels of libpsdproj.so, by base name (ncu may print names with or without namespaces)
+_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                    "paper_2410_19208_b200", "libpsdproj.so")
+_sass = subprocess.run(["cuobjdump", "-sass", _LIB], capture_output=True, text=True).stdout
+_mangled = [ln.split()[-1] for ln in _sass.splitlines() if "Function :" in ln]
+_dem = subprocess.run(["c++filt"], input="\n".join(_mangled), capture_output=True, text=True).stdout.split("\n")
+OURS = {re.sub(r"<.*", "", d.split("(")[0].replace("void ", "")).split("::")[-1] for d in _dem if d} - {""}
+
+
+def base(name):
+    return re.sub(r"<.*", "", name.split("(")[0].replace("void ", "")).split("::")[-1]
+
+
 # n×n symmetrize launches belong to the seeded workload generators (workloads.c3_device), not the projection
-EXCLUDE = ("psd::symmetrize_kernel",)
+EXCLUDE = ("symmetrize_kernel",)
 with open(path) as f:
     lines = [l for l in f if l.startswith('"')]
 agg = collections.OrderedDict()
@@ -20,8 +35,8 @@ for r in csv.DictReader(lines):
     v = float(r["Metric Value"].replace(",", ""))
     unit = r.get("Metric Unit", "ns")
     ms = v * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(unit, 1e-6)
-    name = r["Kernel Name"].split("(")[0]
-    if not any(t in name for t in OURS) or name.startswith(("void at::", "at::")) or any(e in name for e in EXCLUDE):
+    name = base(r["Kernel Name"])
+    if name not in OURS or name in EXCLUDE:
         continue
     a = agg.setdefault(name, [0.0, 0])
     a[0] += ms
