@@ -106,18 +106,23 @@ PSD_DEVINL void jtrace(int R, int ntask, int task, int slot, long long t) {
   if (tr != nullptr && R < 1024) tr[((long long)R * ntask + task) * 3 + slot] = t;
 }
 
-// Rotation for pair (p,q) (GVL sym.schur2; one sqrt, one division, one rsqrt).
+// Rotation for pair (p,q) (GVL sym.schur2 in the cos 2θ / sin 2θ form).
 PSD_DEVINL bool rotation(double app, double aqq, double apq, double abs_tol, double& c, double& s,
                          double& t) {
   c = 1.0;
   s = 0.0;
   t = 0.0;
   if (!(fabs(apq) > abs_tol) || !(apq * apq > 1e-30 * fabs(app * aqq))) return false;
+  // two reciprocal-square-root chains instead of sqrt + division + rsqrt (the rotation is
+  // on the critical path of every inner step): with y = 1/r, r = hypot(d, e),
+  // h = (1 + |d|/r)/2 = cos²θ (|θ| ≤ π/4), z = h^-½:  c = h·z, s = ±e·y·z/2, t = s·z = tan θ
   const double d = aqq - app, e = 2.0 * apq;
-  const double r = sqrt(fma(d, d, e * e));
-  t = (d >= 0.0 ? e : -e) / (fabs(d) + r);  // tan θ
-  c = rsqrt(fma(t, t, 1.0));
-  s = t * c;
+  const double y = rsqrt(fma(d, d, e * e));
+  const double h = fma(0.5 * fabs(d), y, 0.5);
+  const double z = rsqrt(h);
+  c = h * z;
+  s = (d >= 0.0 ? 0.5 : -0.5) * e * y * z;
+  t = s * z;
   return true;
 }
 
