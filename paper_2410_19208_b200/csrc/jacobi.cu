@@ -167,7 +167,6 @@ __device__ int jacobi_step(const double* Sc, const double* Vc, double* Sn, doubl
   // lane k of every warp holds rotation k (k < JB ≤ 32)
   const double ck = __shfl_sync(0xffffffffu, c, k & (JB - 1));
   const double sk = __shfl_sync(0xffffffffu, s, k & (JB - 1));
-  const double tk = __shfl_sync(0xffffffffu, t, k & (JB - 1));
   int pk, qk;
   step_pair<JB>(full, ir, k, pk, qk);
   double b00 = Sc[pk * L + p], b01 = Sc[pk * L + q];
@@ -178,10 +177,10 @@ __device__ int jacobi_step(const double* Sc, const double* Vc, double* Sn, doubl
   b01 = s * r00 + c * r01;
   b10 = c * r10 - s * r11;
   b11 = s * r10 + c * r11;
-  if (k == l && sk != 0.0) {  // the rotated pair itself: exact form
+  if (k == l && sk != 0.0) {  // the rotated pair itself (its tan θ is this lane's t): exact form
     const double apq = Sc[pk * L + qk];
-    b00 = Sc[pk * L + pk] - tk * apq;
-    b11 = Sc[qk * L + qk] + tk * apq;
+    b00 = Sc[pk * L + pk] - t * apq;
+    b11 = Sc[qk * L + qk] + t * apq;
     b01 = 0.0;
     b10 = 0.0;
   }

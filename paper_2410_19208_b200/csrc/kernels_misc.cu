@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(256, PSD_SYM_MINB) sym_stats_kernel(const T* _
   __shared__ unsigned rred[8][kSymT];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
   double mabs = 0.0, mdef = 0.0;
+  unsigned diffbits = 0u, hmax = 0u;   // FP64: bitwise-difference and |x| high-word accumulators
   int flags = 0;
   const long long nt = (n + kSymT - 1) / kSymT;
   for (long long b = blockIdx.x; b < npairs; b += gridDim.x) {
@@ -85,11 +86,20 @@ __global__ void __launch_bounds__(256, PSD_SYM_MINB) sym_stats_kernel(const T* _
         const int c = tx + 32 * h;
         const double av = (double)a[q][h];
         const double bt = (double)tj[c][r];  // x[c0 + c][r0 + r] = x[j][i]
-        if (!isfinite(av) || !isfinite(bt)) flags |= 2;
         mabs = fmax(mabs, fmax(fabs(av), fabs(bt)));
         mdef = fmax(mdef, fabs(av - bt));
-        if (av != bt) flags |= 1;
-        if (rowmax != nullptr) bm[h] = max(bm[h], (unsigned)__double2hiint(fabs(bt)));
+        if constexpr (sizeof(T) == 8) {
+          // integer side of the checks (off the FP64 pipe): bitwise equality from the bit
+          // patterns, non-finite from the largest |x| high word (≥ 0x7ff00000 ⇔ Inf/NaN)
+          const unsigned ahi = (unsigned)__double2hiint(av), bhi = (unsigned)__double2hiint(bt);
+          diffbits |= ((unsigned)__double2loint(av) ^ (unsigned)__double2loint(bt)) | (ahi ^ bhi);
+          hmax = max(hmax, max(ahi & 0x7fffffffu, bhi & 0x7fffffffu));
+          if (rowmax != nullptr) bm[h] = max(bm[h], bhi & 0x7fffffffu);
+        } else {
+          if (!isfinite(av) || !isfinite(bt)) flags |= 2;
+          if (av != bt) flags |= 1;
+          if (rowmax != nullptr) bm[h] = max(bm[h], (unsigned)__double2hiint(fabs(bt)));
+        }
       }
       if (rowmax != nullptr && r0 != c0) {
         const unsigned mi = __reduce_max_sync(
@@ -110,6 +120,8 @@ __global__ void __launch_bounds__(256, PSD_SYM_MINB) sym_stats_kernel(const T* _
     }
     __syncthreads();
   }
+  if (diffbits) flags |= 1;
+  if (hmax >= 0x7ff00000u) flags |= 2;
   __shared__ double rmax[8], rdef[8];
   __shared__ int rfl[8];
   mabs = warp_max(mabs);
