@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <functional>
 #include <string>
 #include <vector>
@@ -143,6 +144,16 @@ int cuda_fail(cudaError_t e, const char* where) {
     int _s = (expr);           \
     if (_s != PSD_OK) return _s; \
   } while (0)
+
+// Calls on one device are serialized (each holds its device's lock until its final
+// stream synchronisation): the persistent tcgen05 kernels (TMEM-resident for their
+// lifetime) and the cooperative Jacobi grid must not share a GPU with another call's
+// copies of themselves — three host threads projecting concurrently on separate
+// streams deadlocked the device in a round-2 experiment.
+std::recursive_mutex& device_mutex(int dev) {
+  static std::recursive_mutex mu[16];
+  return mu[dev & 15];
+}
 
 struct DeviceGuard {
   int prev = -1;
@@ -546,6 +557,7 @@ int psd_plan_create(psd_plan** out, int64_t n, int32_t width, int32_t device) {
 void psd_plan_destroy(psd_plan* p) {
   if (!p) return;
   DeviceGuard g(p->device);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   for (auto& m : p->marks) {
     p->ev_pool.push_back(m.second.first);
     p->ev_pool.push_back(m.second.second);
@@ -562,6 +574,7 @@ int psd_require_symmetric(psd_plan* p, const double* x, int64_t n, int64_t ldx, 
   if (!p || !x) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
   if (n < 1) return fail(PSD_ERR_NONSQUARE, "matrix dimension must be at least 1");
   DeviceGuard g(p->device);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   SymInfo si;
   PSD_TRY(symcheck(p, x, n, ldx, &si, st));
@@ -606,6 +619,7 @@ int psd_power_iteration(psd_plan* p, const double* x, int64_t n, int64_t ldx, do
   if (n_iter < 1) return fail(PSD_ERR_INVALID_PARAMS, "power iteration needs n_iter >= 1, got %d", n_iter);
   if (n < 1 || n > p->n) return fail(PSD_ERR_INVALID_PARAMS, "n=%lld outside plan", (ll)n);
   DeviceGuard g(p->device);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   return power_iteration_impl(p, x, n, ldx, shift, v0, n_iter, result,
                               static_cast<cudaStream_t>(stream));
 }
@@ -616,6 +630,7 @@ int psd_min_eig_magnitude(psd_plan* p, const double* x, int64_t n, int64_t ldx, 
   if (n_iter < 1) return fail(PSD_ERR_INVALID_PARAMS, "power iteration needs n_iter >= 1, got %d", n_iter);
   if (n < 1 || n > p->n) return fail(PSD_ERR_INVALID_PARAMS, "n=%lld outside plan", (ll)n);
   DeviceGuard g(p->device);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   double s1 = 0.0, s2 = 0.0;
   PSD_TRY(power_iteration_impl(p, x, n, ldx, 0.0, v1, n_iter, &s1, st));   // sketch.py:126
@@ -637,6 +652,7 @@ int psd_range_finder(psd_plan* p, const double* x, int64_t m, int64_t n, int64_t
     return fail(PSD_ERR_INVALID_PARAMS, "problem exceeds plan capacity");
   if (alpha > 0.0 && m != n) return fail(PSD_ERR_INVALID_PARAMS, "scaled sketch needs a square matrix");
   DeviceGuard g(p->device);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   psd::g_launch_count = 0;
   p->oz_gram = false;
@@ -666,6 +682,7 @@ int psd_eigh(psd_plan* p, double* a, int32_t m, int64_t lda, double* values, dou
   if (!p || !a || !values || !vectors) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
   if (m < 1 || m > p->w) return fail(PSD_ERR_INVALID_PARAMS, "eigh size %d outside plan", m);
   DeviceGuard g(p->device);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   psd::symmetrize_small(a, m, lda, st);  // eigh validates/uses the symmetric part
   const int sw = psd::jacobi_eigh(a, lda, m, p->vals, p->V, m, p->jws, p->jws_elems,
@@ -840,6 +857,7 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   if (n > p->n || std::min<ll>(w, n) > p->w)
     return fail(PSD_ERR_INVALID_PARAMS, "problem exceeds plan capacity");
   DeviceGuard g(p->device);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   psd::g_launch_count = 0;
   p->oz_gram = false;
@@ -1124,6 +1142,7 @@ int psd_ran_proj(psd_plan* p, const double* x, int64_t n, int64_t ldx, const dou
                  psd_report* rep, void* stream) {
   if (!p || !x || !omega) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
   DeviceGuard g(p->device);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int status;
   {
@@ -1144,6 +1163,7 @@ int psd_ran_proj_f32(psd_plan* p, const float* x, int64_t n, int64_t ldx, const 
                      psd_report* rep, void* stream) {
   if (!p || !x || !omega) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
   DeviceGuard g(p->device);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int status;
   {
@@ -1301,6 +1321,7 @@ int psd_reconstruct(psd_plan* p, const double* w, int64_t n, int64_t ldw, const 
   if (!p || !w || !d || !result) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
   if (n < 1 || n > p->n || r < 0 || r > p->w) return fail(PSD_ERR_INVALID_PARAMS, "reconstruct shape outside plan");
   DeviceGuard g(p->device);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (r == 0) {
     psd::fill_zero(result, ldr, n, n, st);
