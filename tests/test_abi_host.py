@@ -94,3 +94,19 @@ def test_install_rebinds_reference_names():
         ours.uninstall()
     assert psdcone.sdls.project is orig
     assert ours.errors.REGISTRY["AlphaTooSmall"] is ours.errors.AlphaTooSmall
+
+
+def test_bench_refuses_to_measure_fewer_gpus_than_asked():
+    """--gpus N outside torchrun relaunches under torch.distributed.run; with fewer
+    CUDA devices than N it must fail loudly instead of measuring one GPU."""
+    import json
+    import subprocess
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("enough GPUs to relaunch for real")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    res = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "2", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=300, env=env)
+    assert res.returncode == 2
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    assert "error" in line and "--gpus 2" in line["error"]
