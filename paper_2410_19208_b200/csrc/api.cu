@@ -42,6 +42,14 @@ struct psd_plan {
   double* dinv = nullptr;  // ceil(w/32) diagonal-block inverses (32×32) for chol_fast
   double *L1 = nullptr, *Rinv1 = nullptr, *dinv1 = nullptr;   // shifted CholeskyQR candidate
   bool oz_gram = false;   // CholeskyQR Grams on the INT8 engine (set per call by psd_ran_proj)
+  // the Gram's own INT8-engine buffers (panel residues, column exponents, partials): ≈ 16·w·n
+  // bytes, so the FP32 path (which has no X residue planes) can use it too
+  int8_t* g_br = nullptr;
+  int* g_f = nullptr;
+  uint8_t* g_res = nullptr;
+  size_t g_res_elems = 0;
+  ll g_ldk = 0;
+  bool g_failed = false;
   int gparts = 0;
   double* rpart = nullptr;
   ll rparts = 0;
@@ -227,23 +235,45 @@ int xmul(psd_plan* p, const double* x, ll n, ll ldx, const double* P, ll ldP, in
 // scales and transposed residues (the panel preparation of the X·P products) serve as
 // both operands — A = Yᵀ is B's residue planes read row-wise — K = n unsplit up to 2^15
 // per split, CRT on the w×w output only.  Bitwise symmetric (the integer sums are).
+int ensure_gram_oz(psd_plan* p) {
+  if (p->g_ldk) return PSD_OK;
+  if (p->g_failed || p->w > 512) return -1;
+  const int L = psd::oz_num_moduli();
+  const ll ldk = (p->n + 127) / 128 * 128;
+  const ll wpad = (p->w + 15) / 16 * 16;
+  auto balloc = [&](size_t bytes) -> void* { return static_cast<void*>(alloc(p, (bytes + 7) / 8)); };
+  p->g_br = static_cast<int8_t*>(balloc((size_t)L * wpad * ldk));
+  p->g_f = static_cast<int*>(balloc((size_t)wpad * sizeof(int)));
+  p->g_res_elems = (size_t)L * 8 * wpad * (wpad + 16);
+  p->g_res = static_cast<uint8_t*>(balloc(p->g_res_elems));
+  if (!p->g_br || !p->g_f || !p->g_res) {
+    cudaGetLastError();
+    p->g_failed = true;
+    return -1;
+  }
+  cudaMemset(p->g_br, 0, (size_t)L * wpad * ldk);   // K padding stays zero
+  p->g_ldk = ldk;
+  return PSD_OK;
+}
+
 int gram_oz(psd_plan* p, const double* Y, ll ld, ll n, int w, double* G, cudaStream_t st) {
+  if (ensure_gram_oz(p) != PSD_OK) return -1;
   psd::OzOp op;
   op.P = Y;
   op.ldp = ld;
   op.N = w;
   op.K = (int)n;
-  op.br = p->oz_br;
-  op.ldbr = p->oz_ldk;
-  op.f = p->oz_f;
+  op.br = p->g_br;
+  op.ldbr = p->g_ldk;
+  op.f = p->g_f;
   if (psd::oz_prepare_panel(op, st) != 0) return -1;
   op.ar = op.br;
   op.ldar = op.ldbr;
   op.ar_rows = (w + 15) / 16 * 16;
   op.e = op.f;
   op.M = w;
-  op.res = p->oz_res;
-  op.res_elems = p->oz_res_elems;
+  op.res = p->g_res;
+  op.res_elems = p->g_res_elems;
   op.C = G;
   op.ldc = w;
   return psd::oz_gemm_prepared(op, st) < 0 ? -1 : 0;
@@ -251,10 +281,8 @@ int gram_oz(psd_plan* p, const double* Y, ll ld, ll n, int w, double* G, cudaStr
 
 int panel_tn(psd_plan* p, const double* A, const double* B, ll ld, ll n, int w, double* G,
              bool sym, cudaStream_t st) {
-  if (A == B && p->oz_gram && w <= 512 && n <= psd::oz_max_k()) {
-    if (gram_oz(p, A, ld, n, w, G, st) == 0) return PSD_OK;
-    return fail(PSD_ERR_INVALID_PARAMS, "INT8-emulated Gram rejected its operands");
-  }
+  if (A == B && p->oz_gram && w <= 512 && n <= psd::oz_max_k() && gram_oz(p, A, ld, n, w, G, st) == 0)
+    return PSD_OK;   // else (buffers unavailable): the DMMA Gram below
   psd::GemmOp op;
   op.a_layout = psd::A_KM;
   op.b_layout = psd::B_KN;
@@ -977,7 +1005,9 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   // 3: X·P products on the INT8 engine, Xᵀ·P (X not bitwise symmetric) on DMMA
   r.sketch_engine = f32 ? 2 : (oz ? (use_t ? 3 : 1) : 0);
   static const bool oz_gram_on = [] { const char* e = getenv("PSD_OZ_GRAM"); return !(e && e[0] == '0'); }();
-  p->oz_gram = oz && oz_gram_on;
+  // Grams on the INT8 engine wherever it pays (same size rule as the products; the
+  // FP32 path's QR is FP64 too)
+  p->oz_gram = oz_gram_on && oz_on && oz_size && !(flags & PSD_FLAG_FP64_DMMA);
   if (oz) {
     Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
     if (have_rowmax)   // row scales from the symmetry pass: one read of X
