@@ -39,7 +39,7 @@ struct JTraits {
   static constexpr int kJLd = kJS + 4;       // smem row stride ≡ 4 (mod 16): conflict-free DMMA fragments
   static constexpr int kJTile = kJS * kJLd;
   static constexpr unsigned kMask = JB == 32 ? 0xffffffffu : ((1u << JB) - 1u);
-  static constexpr size_t kSmemBytes = (size_t)5 * kJTile * sizeof(double);
+  static constexpr size_t kSmemBytes = (size_t)6 * kJTile * sizeof(double);
 };
 
 struct JacobiArgs {
@@ -59,6 +59,12 @@ struct JacobiArgs {
   int inner;        // inner sweeps per pair solve
   long long* timers;  // optional: block 0 clock64 per phase [solve, bar1, apply, bar2]
 };
+
+constexpr int kFS = 32;   // flag stride in ints (128 bytes)
+#ifndef PSD_JACOBI_BACKOFF
+#define PSD_JACOBI_BACKOFF 128
+#endif
+constexpr unsigned kPollBackoff = PSD_JACOBI_BACKOFF;   // ns between polls of off-critical-path waiters
 
 PSD_DEVINL void circle_pair(int nplayers, int r, int i, int& a, int& b) {
   const int M = nplayers - 1;
@@ -109,21 +115,21 @@ PSD_DEVINL void jtrace(int R, int ntask, int task, int slot, long long t) {
 // Rotation for pair (p,q) (GVL sym.schur2 in the cos 2θ / sin 2θ form).
 PSD_DEVINL bool rotation(double app, double aqq, double apq, double abs_tol, double& c, double& s,
                          double& t) {
-  c = 1.0;
-  s = 0.0;
-  t = 0.0;
-  if (!(fabs(apq) > abs_tol) || !(apq * apq > 1e-30 * fabs(app * aqq))) return false;
   // two reciprocal-square-root chains instead of sqrt + division + rsqrt (the rotation is
   // on the critical path of every inner step): with y = 1/r, r = hypot(d, e),
-  // h = (1 + |d|/r)/2 = cos²θ (|θ| ≤ π/4), z = h^-½:  c = h·z, s = ±e·y·z/2, t = s·z = tan θ
+  // h = (1 + |d|/r)/2 = cos²θ (|θ| ≤ π/4), z = h^-½:  c = h·z, s = ±e·y·z/2, t = s·z = tan θ.
+  // Computed unconditionally (the threshold test runs beside the chain, not before it); the
+  // clamp keeps rsqrt off its slow path for a zero pair (padding), whose result is discarded.
   const double d = aqq - app, e = 2.0 * apq;
-  const double y = rsqrt(fma(d, d, e * e));
+  const double y = rsqrt(fmax(fma(d, d, e * e), 2.2250738585072014e-308));
   const double h = fma(0.5 * fabs(d), y, 0.5);
   const double z = rsqrt(h);
-  c = h * z;
-  s = (d >= 0.0 ? 0.5 : -0.5) * e * y * z;
-  t = s * z;
-  return true;
+  const bool rot = fabs(apq) > abs_tol && apq * apq > 1e-30 * fabs(app * aqq);
+  const double sr = (d >= 0.0 ? 0.5 : -0.5) * e * y * z;
+  c = rot ? h * z : 1.0;
+  s = rot ? sr : 0.0;
+  t = rot ? sr * z : 0.0;
+  return rot;
 }
 
 // Pair k of inner step ir: full sweep = circle method over 32 indices
@@ -155,32 +161,39 @@ __device__ int jacobi_step(const double* Sc, const double* Vc, double* Sn, doubl
   using T = JTraits<JB>;
   constexpr int L = T::kJLd;
   const int lane = threadIdx.x & 31;
-  const int l = lane & (JB - 1);           // this lane's rotation (pair l of the step)
-  int p, q;
+  const int l = lane & (JB - 1);           // this lane's column rotation (pair l of the step)
+  const int k = (int)threadIdx.x / JB;     // thread → (k, l): rows {p_k, q_k} × cols {p_l, q_l}
+  int p, q, pk, qk;
   step_pair<JB>(full, ir, l, p, q);
+  step_pair<JB>(full, ir, k, pk, qk);
+  // every shared-memory read of the step issued up front (they depend on the indices only),
+  // so the step's critical path is one LDS round, the rotation chain, the shuffles, the 2×2
+  // products and the barrier.  (Computing rotation k in this thread too, instead of the
+  // shuffles, measured slower: the rotation is MUFU/FP64-throughput-heavy.)
+  const double lpp = Sc[p * L + p], lqq = Sc[q * L + q], lpq = Sc[p * L + q];
+  double b00 = Sc[pk * L + p], b01 = Sc[pk * L + q];
+  double b10 = Sc[qk * L + p], b11 = Sc[qk * L + q];
+  const double v00 = Vc[k * L + p], v01 = Vc[k * L + q];
+  const double v10 = Vc[(k + JB) * L + p], v11 = Vc[(k + JB) * L + q];
   double c, s, t;
-  const bool r = rotation(Sc[p * L + p], Sc[q * L + q], Sc[p * L + q], abs_tol, c, s, t);
+  const bool r = rotation(lpp, lqq, lpq, abs_tol, c, s, t);
   const int nrot = __popc(__ballot_sync(0xffffffffu, r) & T::kMask);
   if (nrot == 0) return 0;
-  // thread → (k, l): rows {p_k, q_k} × cols {p_l, q_l}
-  const int k = (int)threadIdx.x / JB;
   // lane k of every warp holds rotation k (k < JB ≤ 32)
   const double ck = __shfl_sync(0xffffffffu, c, k & (JB - 1));
   const double sk = __shfl_sync(0xffffffffu, s, k & (JB - 1));
-  int pk, qk;
-  step_pair<JB>(full, ir, k, pk, qk);
-  double b00 = Sc[pk * L + p], b01 = Sc[pk * L + q];
-  double b10 = Sc[qk * L + p], b11 = Sc[qk * L + q];
-  const double r00 = ck * b00 - sk * b10, r01 = ck * b01 - sk * b11;
-  const double r10 = sk * b00 + ck * b10, r11 = sk * b01 + ck * b11;
-  b00 = c * r00 - s * r01;
-  b01 = s * r00 + c * r01;
-  b10 = c * r10 - s * r11;
-  b11 = s * r10 + c * r11;
-  if (k == l && sk != 0.0) {  // the rotated pair itself (its tan θ is this lane's t): exact form
-    const double apq = Sc[pk * L + qk];
-    b00 = Sc[pk * L + pk] - t * apq;
-    b11 = Sc[qk * L + qk] + t * apq;
+  // for k == l the rotated pair's own entries are (b00, b11, b01) = (a_pp, a_qq, a_pq)
+  const double kpp = b00, kqq = b11, kpq = b01;
+  // Jₖᵀ·(B·J_l): the column rotation (own c, s) overlaps the shuffles' latency
+  const double r00 = c * b00 - s * b01, r01 = s * b00 + c * b01;
+  const double r10 = c * b10 - s * b11, r11 = s * b10 + c * b11;
+  b00 = ck * r00 - sk * r10;
+  b01 = ck * r01 - sk * r11;
+  b10 = sk * r00 + ck * r10;
+  b11 = sk * r01 + ck * r11;
+  if (k == l && sk != 0.0) {  // the rotated pair itself: exact form from its tan θ
+    b00 = kpp - t * kpq;
+    b11 = kqq + t * kpq;
     b01 = 0.0;
     b10 = 0.0;
   }
@@ -189,13 +202,10 @@ __device__ int jacobi_step(const double* Sc, const double* Vc, double* Sn, doubl
   Sn[qk * L + p] = b10;
   Sn[qk * L + q] = b11;
   // V ← V J for rows k and k + JB, pair l
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int row = k + JB * h;
-    const double a0 = Vc[row * L + p], a1 = Vc[row * L + q];
-    Vn[row * L + p] = c * a0 - s * a1;
-    Vn[row * L + q] = s * a0 + c * a1;
-  }
+  Vn[k * L + p] = c * v00 - s * v01;
+  Vn[k * L + q] = s * v00 + c * v01;
+  Vn[(k + JB) * L + p] = c * v10 - s * v11;
+  Vn[(k + JB) * L + q] = s * v10 + c * v11;
   __syncthreads();
   return nrot;
 }
@@ -221,6 +231,30 @@ PSD_DEVINL void mm_dmma(const double* A, bool aT, const double* B, double (&c)[2
   }
 }
 
+// Two independent products of the mm_dmma form interleaved (same per-element arithmetic).
+template <int JB>
+PSD_DEVINL void mm_dmma2(const double* A1, bool a1T, const double* B1, double (&c1)[2][2], const double* A2,
+                         bool a2T, const double* B2, double (&c2)[2][2]) {
+  using T = JTraits<JB>;
+  constexpr int L = T::kJLd;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int m0 = (warp % (JB / 4)) * 8, n0 = (warp / (JB / 4)) * 16;
+  c1[0][0] = c1[0][1] = c1[1][0] = c1[1][1] = 0.0;
+  c2[0][0] = c2[0][1] = c2[1][0] = c2[1][1] = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < T::kJS; k0 += 4) {
+    const double a1 = a1T ? A1[(k0 + t) * L + m0 + g] : A1[(m0 + g) * L + k0 + t];
+    const double a2 = a2T ? A2[(k0 + t) * L + m0 + g] : A2[(m0 + g) * L + k0 + t];
+    const double b10 = B1[(k0 + t) * L + n0 + g], b11 = B1[(k0 + t) * L + n0 + 8 + g];
+    const double b20 = B2[(k0 + t) * L + n0 + g], b21 = B2[(k0 + t) * L + n0 + 8 + g];
+    dmma_8x8x4(c1[0][0], c1[0][1], a1, b10);
+    dmma_8x8x4(c1[1][0], c1[1][1], a1, b11);
+    dmma_8x8x4(c2[0][0], c2[0][1], a2, b20);
+    dmma_8x8x4(c2[1][0], c2[1][1], a2, b21);
+  }
+}
+
 // (row, col) within the kJS×kJS tile of accumulator (j, e) of this thread
 template <int JB>
 PSD_DEVINL void mm_coord(int j, int e, int& row, int& col) {
@@ -230,13 +264,17 @@ PSD_DEVINL void mm_coord(int j, int e, int& row, int& col) {
 }
 
 // ---- dataflow synchronisation (no grid-wide barrier) -----------------------
-PSD_DEVINL void flag_wait(const int* f, int target) {
+// backoff > 0: pause between polls (waiters off the critical path leave the flags' L2
+// lines to the solves that poll them on it)
+PSD_DEVINL void flag_wait(const int* f, int target, unsigned backoff = 0) {
   int v;
   unsigned spins = 0;
   do {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+    if (v >= target) break;
     if (++spins > (1u << 26)) __trap();   // a dependency that never resolves: fail loudly
-  } while (v < target);
+    if (backoff) __nanosleep(backoff);
+  } while (true);
 }
 // Called by thread 0 after a __syncthreads that orders the CTA's data writes
 // before it; st.release is cumulative over them (PTX memory model).
@@ -272,20 +310,25 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
   double* S1 = sm + 2 * kJTile;
   double* V1 = sm + 3 * kJTile;
   double* X = sm + 4 * kJTile;
-  __shared__ int ia[kJS], ib[kJS];
+  double* Y = sm + 5 * kJTile;
+  __shared__ int ia[kJS], ib[kJS], ic[kJS];
   __shared__ int stop_flag;
   __shared__ double red8[kJT / 32];
   const int m = A.m, nblk = A.nblk, P = nblk / 2, rounds = nblk - 1;
   const int vch = (m + 2 * kJS - 1) / (2 * kJS);       // 64-row V chunks
   const int ntask = P + P * P + P * vch;
-  const int readers = (2 * P - 1) + vch;               // tasks reading J_p per round
+  // tasks reading J_p / S_p of a round: its A-items and V-items, and the next round's
+  // solves holding its two blocks (one solve when P = 1)
+  const int readers = (2 * P - 1) + vch + (P == 1 ? 1 : 2);
   const double abs_tol = 1e-15 * A.norm[0];
   double* buf[2] = {A.a, A.b};
   const long long ldb[2] = {A.lda, (long long)m};
+  // each flag on its own 128-byte line: a writer's release and its pollers' acquires
+  // do not queue behind the polling of unrelated flags at the same L2 line
   int* sflag = A.flags;
-  int* aflag = sflag + P;
-  int* vflag = aflag + P * P;
-  int* jread = vflag + P * vch;                        // [2][P]
+  int* aflag = sflag + kFS * P;
+  int* vflag = aflag + kFS * P * P;
+  int* jread = vflag + kFS * P * vch;                  // [2][P]
   const int tid = threadIdx.x;
   int sweeps_done = -1;
   for (int sweep = 0; sweep < A.max_sweeps; ++sweep) {
@@ -302,26 +345,73 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
           // ------------------------------------------------------- solve
           const int pair = task;
           const long long tw0 = clock64();
-          if (tid == 0) {
+          // R ≥ 1: this pair's blocks a, b sat in pairs pa, pb of round R−1 (halves ha, hb).
+          // Its subproblem is assembled here from round R−1's solves — A_R(a,a), A_R(b,b) from
+          // S_pa, S_pb; A_R(a,b) = [J_paᵀ A_{R−1}(pa,pb) J_pb](a,b) and A_R(b,a) likewise, the
+          // same DMMA products (bit for bit) round R−1's A-items write — so a round's solves
+          // wait only on the previous round's solves, not on its A-items (one flag hop and the
+          // A-item work off the critical path of every round).
+          const int rp = (R + rounds - 1) % rounds;
+          int pa = 0, pb = 0, ha = 0, hb = 0;
+          if (R >= 1) {
+            int ba, bb, x0, x1, y0, y1;
+            circle_pair(nblk, r, pair, ba, bb);
+            pa = pair_of(nblk, R - 1, ba);
+            pb = pair_of(nblk, R - 1, bb);
+            circle_pair(nblk, rp, pa, x0, x1);
+            circle_pair(nblk, rp, pb, y0, y1);
+            ha = ba == x0 ? 0 : 1;
+            hb = bb == y0 ? 0 : 1;
+            // every dependency polled by its own thread (a flag check is an L2 round trip;
+            // eleven of them in one thread's sequence cost microseconds per round)
+            if (tid == 0) jtrace(R, ntask, task, 0, gtimer());
+            const int* fp = nullptr;
+            int ft = 0;
+            if (tid == 0 && R >= 2) {   // the J/S slot this solve overwrites: all its readers done
+              fp = &jread[kFS * ((R & 1) * P + pair)];
+              ft = (R / 2) * readers;
+            } else if (tid >= 1 && tid <= 8 && R >= 2 && pa != pb) {
+              // tiles (pa,pb), (pb,pa) of A_{R−1}: written by round R−2's A-items
+              const int w = tid - 1, i = (w >> 2) & 1, j = (w >> 1) & 1;
+              const int qx = pair_of(nblk, R - 2, i ? x1 : x0), qy = pair_of(nblk, R - 2, j ? y1 : y0);
+              fp = &aflag[kFS * ((w & 1) ? qy * P + qx : qx * P + qy)];
+              ft = R - 1;
+            }
+            if (fp) flag_wait(fp, ft, kPollBackoff);
+          } else if (tid == 0) {
             jtrace(R, ntask, task, 0, gtimer());
-            if (R >= 2) flag_wait(&jread[(R & 1) * P + pair], (R / 2) * readers);
+          }
+          if (tid < kJS) {
+            ia[tid] = sub_index<JB>(nblk, r, pair, tid);
             if (R >= 1) {
-              int ba, bb;
-              circle_pair(nblk, r, pair, ba, bb);
-              const int pa = pair_of(nblk, R - 1, ba), pb = pair_of(nblk, R - 1, bb);
-              flag_wait(&aflag[pa * P + pa], R);
-              flag_wait(&aflag[pa * P + pb], R);
-              flag_wait(&aflag[pb * P + pa], R);
-              flag_wait(&aflag[pb * P + pb], R);
+              ib[tid] = sub_index<JB>(nblk, rp, pa, tid);
+              ic[tid] = sub_index<JB>(nblk, rp, pb, tid);
             }
           }
-          if (tid < kJS) ia[tid] = sub_index<JB>(nblk, r, pair, tid);
           __syncthreads();
+          constexpr int NS = kJS * kJS / kJT;
+          const bool prod = R >= 1 && pa != pb;
+          // the A_{R−1} tiles are final already: their loads fly while round R−1's solves finish
+          double t1[NS], t2[NS];
+          if (prod) {
+            const double* prev = buf[(R - 1) & 1];
+            const long long ldp = ldb[(R - 1) & 1];
+#pragma unroll
+            for (int u = 0; u < NS; ++u) {
+              const int e = tid + u * kJT, i = e / kJS, j = e % kJS;
+              t1[u] = (ib[i] < m && ic[j] < m) ? __ldcg(prev + (long long)ib[i] * ldp + ic[j]) : 0.0;
+              t2[u] = (ic[i] < m && ib[j] < m) ? __ldcg(prev + (long long)ic[i] * ldp + ib[j]) : 0.0;
+            }
+          }
+          if (R >= 1) {
+            if (tid == 0) flag_wait(&sflag[kFS * pa], R);
+            if (tid == 32) flag_wait(&sflag[kFS * pb], R);
+            __syncthreads();
+          }
           if (tid == 0) jtrace(R, ntask, task, 1, gtimer());
           const long long tw1 = clock64();
-          {
+          if (R == 0) {
             // all loads of this thread in flight at once (register staging)
-            constexpr int NS = kJS * kJS / kJT;
             double vs[NS];
 #pragma unroll
             for (int u = 0; u < NS; ++u) {
@@ -333,6 +423,77 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
               const int e = tid + u * kJT, i = e / kJS, j = e % kJS;
               S0[i * kJLd + j] = vs[u];
               V0[i * kJLd + j] = (i == j) ? 1.0 : 0.0;
+            }
+          } else {
+            const size_t prev_slot = (size_t)((R - 1) & 1) * P * kJS * kJS;
+            const double* Sa = A.sbuf + prev_slot + (size_t)pa * kJS * kJS;
+            const double* Sb = A.sbuf + prev_slot + (size_t)pb * kJS * kJS;
+            // diagonal blocks: (a,a) = S_pa[ha-half], (b,b) = S_pb[hb-half]; for pa == pb
+            // (a single pair, P = 1) the off-diagonal blocks come from S_pa as well
+            double dv[NS];
+#pragma unroll
+            for (int u = 0; u < NS; ++u) {
+              const int e = tid + u * kJT, i = e / kJS, j = e % kJS;
+              const int hi = i < JB ? ha : hb, hj = j < JB ? ha : hb;
+              const bool diag = (i < JB) == (j < JB);
+              const double* Ss = (diag && i >= JB) ? Sb : Sa;
+              dv[u] = (diag || pa == pb) ? __ldcg(Ss + (size_t)(hi * JB + i % JB) * kJS + hj * JB + j % JB) : 0.0;
+            }
+            if (prod) {
+              {
+                const double* Ja = A.jbuf + prev_slot + (size_t)pa * kJS * kJS;
+                const double* Jb = A.jbuf + prev_slot + (size_t)pb * kJS * kJS;
+                double va[NS], vb[NS];
+#pragma unroll
+                for (int u = 0; u < NS; ++u) {
+                  va[u] = __ldcg(Ja + tid + u * kJT);
+                  vb[u] = __ldcg(Jb + tid + u * kJT);
+                }
+#pragma unroll
+                for (int u = 0; u < NS; ++u) {
+                  const int e = tid + u * kJT, i = e / kJS, j = e % kJS;
+                  S0[i * kJLd + j] = t1[u];
+                  V1[i * kJLd + j] = t2[u];
+                  V0[i * kJLd + j] = va[u];
+                  X[i * kJLd + j] = vb[u];
+                }
+              }
+              __syncthreads();
+              // both off-diagonal products side by side (two accumulator chains per warp)
+              double c1[2][2], c2[2][2];
+              mm_dmma2<JB>(V0, true, S0, c1, X, true, V1, c2);   // J_paᵀ T(pa,pb), J_pbᵀ T(pb,pa)
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  int row, col;
+                  mm_coord<JB>(j, e, row, col);
+                  S1[row * kJLd + col] = c1[j][e];
+                  Y[row * kJLd + col] = c2[j][e];
+                }
+              __syncthreads();
+              mm_dmma2<JB>(S1, false, X, c1, Y, false, V0, c2);  // (·) J_pb, (·) J_pa
+              __syncthreads();
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  int row, col;
+                  mm_coord<JB>(j, e, row, col);
+                  if (row / JB == ha && col / JB == hb) S0[(row % JB) * kJLd + JB + col % JB] = c1[j][e];
+                  if (row / JB == hb && col / JB == ha) S0[(JB + row % JB) * kJLd + col % JB] = c2[j][e];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < NS; ++u) {
+              const int e = tid + u * kJT, i = e / kJS, j = e % kJS;
+              if ((i < JB) == (j < JB) || pa == pb) S0[i * kJLd + j] = dv[u];
+              V0[i * kJLd + j] = (i == j) ? 1.0 : 0.0;
+            }
+            __syncthreads();
+            if (tid == 0) {   // J/S of round R−1 read: count this solve among the slot's readers
+              atomicAdd(&jread[kFS * (((R - 1) & 1) * P + pa)], 1);
+              if (pb != pa) atomicAdd(&jread[kFS * (((R - 1) & 1) * P + pb)], 1);
             }
           }
           __syncthreads();
@@ -368,7 +529,7 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
           __syncthreads();
           if (tid == 0) {
             if (rots > 0) atomicAdd(&A.counters[sweep], rots);
-            flag_set(&sflag[pair], R + 1);
+            flag_set(&sflag[kFS * (pair)], R + 1);
             jtrace(R, ntask, task, 2, gtimer());
             if (A.timers && pair == 0) {
               A.timers[0] += tw1 - tw0;
@@ -385,21 +546,26 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
             ia[tid] = sub_index<JB>(nblk, r, pa, tid);
             ib[tid] = sub_index<JB>(nblk, r, pb, tid);
           }
-          if (tid == 0) {
-            jtrace(R, ntask, task, 0, gtimer());
-            flag_wait(&sflag[pa], R + 1);
-            flag_wait(&sflag[pb], R + 1);
-            if (R >= 1) {
+          {
+            // one thread per dependency: every solve of round R (not only pa and pb — they
+            // read A_{R−1} from the buffer this item overwrites, nxt; see the solve), and the
+            // four round-(R−1) A-items holding this tile's blocks
+            if (tid == 0) jtrace(R, ntask, task, 0, gtimer());
+            const int* fp = nullptr;
+            int ft = 0;
+            if (tid < P) {
+              fp = &sflag[kFS * tid];
+              ft = R + 1;
+            } else if (tid < P + 4 && R >= 1) {
+              const int w = tid - P;
               int a0, a1, b0, b1;
               circle_pair(nblk, r, pa, a0, a1);
               circle_pair(nblk, r, pb, b0, b1);
-              const int qa0 = pair_of(nblk, R - 1, a0), qa1 = pair_of(nblk, R - 1, a1);
-              const int qb0 = pair_of(nblk, R - 1, b0), qb1 = pair_of(nblk, R - 1, b1);
-              flag_wait(&aflag[qa0 * P + qb0], R);
-              flag_wait(&aflag[qa0 * P + qb1], R);
-              flag_wait(&aflag[qa1 * P + qb0], R);
-              flag_wait(&aflag[qa1 * P + qb1], R);
+              const int qa = pair_of(nblk, R - 1, (w >> 1) ? a1 : a0), qb = pair_of(nblk, R - 1, (w & 1) ? b1 : b0);
+              fp = &aflag[kFS * (qa * P + qb)];
+              ft = R;
             }
+            if (fp) flag_wait(fp, ft, kPollBackoff);
           }
           __syncthreads();
           if (tid == 0) jtrace(R, ntask, task, 1, gtimer());
@@ -478,9 +644,9 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
               for (int w = 0; w < kJT / 32; ++w) bm = fmax(bm, red8[w]);
               if (bm > 0.0) atomicMax(&A.maxoff[sweep], (unsigned long long)__double_as_longlong(bm));
             }
-            atomicAdd(&jread[(R & 1) * P + pa], 1);
-            if (pb != pa) atomicAdd(&jread[(R & 1) * P + pb], 1);
-            flag_set(&aflag[pa * P + pb], R + 1);
+            atomicAdd(&jread[kFS * ((R & 1) * P + pa)], 1);
+            if (pb != pa) atomicAdd(&jread[kFS * ((R & 1) * P + pb)], 1);
+            flag_set(&aflag[kFS * (pa * P + pb)], R + 1);
             jtrace(R, ntask, task, 2, gtimer());
             if (A.timers && it == 1) {
               A.timers[3] += tw1 - tw0;
@@ -494,13 +660,11 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
           if (tid < kJS) ib[tid] = sub_index<JB>(nblk, r, pb, tid);
           if (tid == 0) {
             jtrace(R, ntask, task, 0, gtimer());
-            flag_wait(&sflag[pb], R + 1);
-            if (R >= 1) {
-              int b0, b1;
-              circle_pair(nblk, r, pb, b0, b1);
-              flag_wait(&vflag[vc * P + pair_of(nblk, R - 1, b0)], R);
-              flag_wait(&vflag[vc * P + pair_of(nblk, R - 1, b1)], R);
-            }
+            flag_wait(&sflag[kFS * pb], R + 1, kPollBackoff);
+          } else if (tid >= 32 && tid < 34 && R >= 1) {   // other warp: polled concurrently
+            int b0, b1;
+            circle_pair(nblk, r, pb, b0, b1);
+            flag_wait(&vflag[kFS * (vc * P + pair_of(nblk, R - 1, tid == 32 ? b0 : b1))], R, kPollBackoff);
           }
           __syncthreads();
           if (tid == 0) jtrace(R, ntask, task, 1, gtimer());
@@ -545,8 +709,8 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
             __syncthreads();
           }
           if (tid == 0) {
-            atomicAdd(&jread[(R & 1) * P + pb], 1);
-            flag_set(&vflag[vc * P + pb], R + 1);
+            atomicAdd(&jread[kFS * ((R & 1) * P + pb)], 1);
+            flag_set(&vflag[kFS * (vc * P + pb)], R + 1);
             jtrace(R, ntask, task, 2, gtimer());
           }
         }
@@ -555,14 +719,19 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
     }
     // convergence: every solve of this sweep is done once its last round's flags are up
     const int Rlast = sweep * rounds + rounds - 1;
+    // (flags polled one per thread, concurrently)
+    for (int p = tid; p < P; p += kJT) flag_wait(&sflag[kFS * p], Rlast + 1);
+    __syncthreads();
+    const int rots = *((volatile int*)&A.counters[sweep]);
+    if (rots != 0 && rots <= 2 * m) {   // nearly converged: worth waiting for the last A-items
+      // every off-diagonal entry already at or below the rotation threshold: the
+      // next sweep would rotate nothing — stop now instead of running it
+      for (int q = tid; q < P * P; q += kJT) flag_wait(&aflag[kFS * q], Rlast + 1);
+      __syncthreads();
+    }
     if (tid == 0) {
-      for (int p = 0; p < P; ++p) flag_wait(&sflag[p], Rlast + 1);
-      const int rots = *((volatile int*)&A.counters[sweep]);
       int stop = rots == 0;
-      if (!stop && rots <= 2 * m) {   // nearly converged: worth waiting for the last A-items
-        // every off-diagonal entry already at or below the rotation threshold: the
-        // next sweep would rotate nothing — stop now instead of running it
-        for (int q = 0; q < P * P; ++q) flag_wait(&aflag[q], Rlast + 1);
+      if (!stop && rots <= 2 * m) {
         const double mo = __longlong_as_double((long long)*((volatile unsigned long long*)&A.maxoff[sweep]));
         stop = mo <= abs_tol;
       }
@@ -622,7 +791,7 @@ static void jacobi_geometry(int m, int jb, int& nblk, int& P) {
 
 static int jacobi_nflags(int m, int jb, int P) {
   const int vch = (m + 4 * jb - 1) / (4 * jb);
-  return P + P * P + P * vch + 2 * P;
+  return kFS * (P + P * P + P * vch + 2 * P);
 }
 
 static size_t jacobi_ws_elems_jb(int m, int jb) {
