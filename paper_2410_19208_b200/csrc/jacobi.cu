@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "launch.h"
@@ -723,15 +724,16 @@ __global__ void __launch_bounds__(JB * JB) jacobi_persistent_kernel(JacobiArgs A
     for (int p = tid; p < P; p += kJT) flag_wait(&sflag[kFS * p], Rlast + 1);
     __syncthreads();
     const int rots = *((volatile int*)&A.counters[sweep]);
-    if (rots != 0 && rots <= 2 * m) {   // nearly converged: worth waiting for the last A-items
-      // every off-diagonal entry already at or below the rotation threshold: the
-      // next sweep would rotate nothing — stop now instead of running it
+    if (rots != 0) {
+      // every off-diagonal entry already at or below the rotation threshold: the next sweep
+      // would rotate nothing — stop now instead of running it (the last A-items finish a
+      // flag hop after the last solves; a wasted sweep costs a whole sweep of rounds)
       for (int q = tid; q < P * P; q += kJT) flag_wait(&aflag[kFS * q], Rlast + 1);
       __syncthreads();
     }
     if (tid == 0) {
       int stop = rots == 0;
-      if (!stop && rots <= 2 * m) {
+      if (!stop) {
         const double mo = __longlong_as_double((long long)*((volatile unsigned long long*)&A.maxoff[sweep]));
         stop = mo <= abs_tol;
       }
@@ -887,6 +889,22 @@ static int jacobi_run(double* a, long long lda, int m, double* values, double* v
   jacobi_diag_kernel<<<(m + 255) / 256, 256, 0, st>>>(a, lda, ws, m, A.out, values);
   count_launch();
   if (out[1]) copy_matrix(ws, m, a, lda, m, m, st);
+  static const bool stats = getenv("PSD_JACOBI_STATS") != nullptr;
+  if (stats) {   // per sweep: rotations above threshold, max |off-diagonal| after the sweep
+    std::vector<int> cnt(kJacobiMaxSweeps);
+    std::vector<unsigned long long> mo(kJacobiMaxSweeps);
+    double nrm = 0.0;
+    cudaMemcpy(cnt.data(), A.counters, cnt.size() * sizeof(int), cudaMemcpyDeviceToHost);
+    cudaMemcpy(mo.data(), A.maxoff, mo.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&nrm, A.norm, sizeof(double), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "jacobi m=%d sweeps=%d |A|=%.3e:", m, out[0], nrm);
+    for (int sw = 0; sw < std::max(out[0], 0); ++sw) {
+      double d;
+      std::memcpy(&d, &mo[sw], sizeof(d));
+      fprintf(stderr, " [%d %.1e]", cnt[sw], d / nrm);
+    }
+    fprintf(stderr, "\n");
+  }
   if (trace_path) {   // binary dump: header (m, P, vch, rounds, ntask) then int64 [R][task][3]
     std::vector<long long> h(trace_elems);
     cudaMemcpy(h.data(), dtrace, trace_elems * sizeof(long long), cudaMemcpyDeviceToHost);
