@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--no-fp32", action="store_true", help="skip the config-3 FP32 (3xTF32) leg")
     ap.add_argument("--no-scaled", action="store_true", help="skip the scaled (Alg. 3 + Alg. 5) leg")
     ap.add_argument("--no-c4", action="store_true", help="skip the config-4 row-sharded leg")
+    ap.add_argument("--no-prefetch", action="store_true",
+                    help="do not pipeline consecutive projections (psd_plan_prefetch)")
     ap.add_argument("--no-peaks", action="store_true",
                     help="skip the in-run cuBLAS peak measurement (profiling runs; roofline then uses "
                          "MEASURED_PEAKS.json)")
@@ -98,6 +100,11 @@ def workload_config(a, n_gpus):
         "l2": "inputs larger than L2 (each X is 8·n² bytes ≫ 126 MB)",
         "omega": "device Philox N(0,1) per projection",
         "parallelism": f"replicas x{n_gpus}" if n_gpus > 1 else "single GPU",
+        "pipelining": ("none" if getattr(a, "no_prefetch", False) or a.config == "c1" else
+                       "ran_proj(..., prefetch=next X): projection i+1's symmetry pass and INT8 "
+                       "residue planes run on a low-priority side stream under projection i's "
+                       "CholeskyQR / eigensolver; the first timed step prepares its own X and the "
+                       "last one prefetches nothing, so the K steps do exactly K projections' work"),
     }
 
 
@@ -480,8 +487,12 @@ def run_ours(a):
     plan = psd._native.get_plan(n, params.width, dev)
 
     out64 = torch.empty((n, n), dtype=torch.float64, device=dev)   # no allocation in the timed loop
-    for i in range(max(a.warmup, 3 if a.warmup >= 3 else a.warmup)):
-        psd.ran_proj(pool[i % a.pool], params, rng, out=out64)
+    # pipelined batch: each call names the next X (none across the warm-up/timed boundary
+    # and after the last timed step, so the timed region holds exactly its own work)
+    nxt = (lambda i, last: None if a.no_prefetch or i == last else pool[(i + 1) % a.pool])
+    nwarm = max(a.warmup, 3 if a.warmup >= 3 else a.warmup)
+    for i in range(nwarm):
+        psd.ran_proj(pool[i % a.pool], params, rng, out=out64, prefetch=nxt(i, nwarm - 1))
     torch.cuda.synchronize(dev)
     plan.profile(enable=True, reset=True)
     clocks = ClockSampler(local)
@@ -500,7 +511,7 @@ def run_ours(a):
         marks[i].record()
         if flush is not None:
             flush.zero_()
-        rep = psd.ran_proj(pool[i % a.pool], params, rng, out=out64)
+        rep = psd.ran_proj(pool[i % a.pool], params, rng, out=out64, prefetch=nxt(i, a.steps - 1))
         launches += rep.device_info["gpu_launches"]
         ranks.append(rep.effective_rank)
         engine = rep.device_info["sketch_engine"]

@@ -94,6 +94,17 @@ int64_t psd_plan_bytes(const psd_plan* plan);
  * the accumulators afterwards. */
 int psd_plan_profile(psd_plan* plan, int32_t enable, double* ms_out, int32_t* counts_out,
                      int32_t reset);
+/* Pipelining hint for a batch of projections (C3's 16 sequential projections;
+ * the reference projects one matrix per call, projection.py:92-119): the NEXT
+ * psd_ran_proj call on this plan will project x_next (n x n FP64, device,
+ * leading dimension ldx).  That call starts x_next's require_symmetric pass
+ * and its INT8-engine residue planes on a low-priority side stream once its
+ * own n x n products are done, so they run under its latency-bound CholeskyQR
+ * and eigensolver; the call after it consumes them (same pointer, n, ldx)
+ * instead of reading X again.  Results are identical to unhinted calls; the
+ * caller must not modify x_next until it has been projected.  The hint is
+ * used by exactly one call (NULL clears it); FP32 / DMMA-engine calls ignore it. */
+int psd_plan_prefetch(psd_plan* plan, const double* x_next, int64_t n, int64_t ldx);
 
 /* require_symmetric — symmetric.py:39-57.  tol < 0 selects the reference
  * default 1e-10*max(1, max|x|).  stats_out (HOST, 3 doubles) receives

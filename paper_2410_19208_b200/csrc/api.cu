@@ -67,6 +67,24 @@ struct psd_plan {
   size_t ws32_elems = 0;
   std::vector<void*> allocs;
   size_t bytes = 0;
+  // pipelined batch (psd_plan_prefetch): the next X's symmetry pass and residue planes are
+  // prepared on a low-priority side stream into the *_alt buffers while this call's QR /
+  // eigensolver run; calls involved run on `work`, a high-priority stream joined to the
+  // caller's, so their CTAs are dispatched ahead of the side stream's.
+  cudaStream_t work = nullptr, side = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_pf_stats = nullptr,
+              ev_pf_done = nullptr;
+  int8_t* oz_ar_alt = nullptr;
+  int* oz_e_alt = nullptr;
+  unsigned* oz_rowmax_alt = nullptr;
+  double* stats_alt = nullptr;
+  unsigned char *pf_host = nullptr, *pf_dev = nullptr;   // mapped statistics of the prefetched X
+  const double* hint_x = nullptr;   // set by psd_plan_prefetch, consumed by the next call
+  ll hint_n = 0, hint_ldx = 0;
+  const double* pf_x = nullptr;     // prefetched (in flight or done on `side`)
+  ll pf_n = 0, pf_ldx = 0;
+  bool pf_ready = false;
+  bool pf_failed = false;
   // stage profiling (psd_plan_profile): CUDA events on the caller's stream
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -252,6 +270,9 @@ int ensure_gram_oz(psd_plan* p) {
     return -1;
   }
   cudaMemset(p->g_br, 0, (size_t)L * wpad * ldk);   // K padding stays zero
+  // cudaMemset is asynchronous on the legacy stream: finish it before any call on a
+  // non-blocking stream (the caller's or the plan's pipelined `work` stream) writes here
+  cudaDeviceSynchronize();
   p->g_ldk = ldk;
   return PSD_OK;
 }
@@ -462,7 +483,8 @@ using MulFn = std::function<int(const double* P, ll ldP, int w, double* out, ll 
 int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* omega, ll ldo, int w,
                       int q, bool always_stabilize, bool strict, double** bufs, int* qidx,
                       int* width_out, QrInfo* qi, cudaStream_t st,
-                      const std::function<int()>& after_first = nullptr) {
+                      const std::function<int()>& after_first = nullptr,
+                      const std::function<void()>& before_final_qr = nullptr) {
   const ll ld = p->ldp;
   const bool stabilize = q >= 2 || always_stabilize;               // sketch.py:74
   int y = 0;
@@ -483,6 +505,9 @@ int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* o
     y = ny;
   }
   n = m;  // the final QR and gather act on the m×w sample
+  // the n×n products of the range finder are all enqueued: a pipelined batch starts the
+  // next matrix's preparation here (psd_plan_prefetch)
+  if (before_final_qr) before_final_qr();
   int qb = y;
   PSD_TRY(cholqr(p, bufs, y, (y + 1) % 3, n, w, p->rdiag, &qb, qi, st));   // :84-85
   if (qi->zero) {
@@ -515,6 +540,9 @@ int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* o
   *qidx = qb;
   return PSD_OK;
 }
+
+int ensure_oz(psd_plan* p);
+int ensure_pipeline(psd_plan* p);
 
 }  // namespace
 
@@ -586,6 +614,13 @@ void psd_plan_destroy(psd_plan* p) {
   if (!p) return;
   DeviceGuard g(p->device);
   std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
+  if (p->side) cudaStreamSynchronize(p->side);   // a prefetch may still be writing the alt planes
+  if (p->work) cudaStreamSynchronize(p->work);
+  for (cudaEvent_t e : {p->ev_in, p->ev_out, p->ev_fork, p->ev_pf_stats, p->ev_pf_done})
+    if (e) cudaEventDestroy(e);
+  if (p->side) cudaStreamDestroy(p->side);
+  if (p->work) cudaStreamDestroy(p->work);
+  if (p->pf_host) cudaFreeHost(p->pf_host);
   for (auto& m : p->marks) {
     p->ev_pool.push_back(m.second.first);
     p->ev_pool.push_back(m.second.second);
@@ -596,6 +631,25 @@ void psd_plan_destroy(psd_plan* p) {
 }
 
 int64_t psd_plan_bytes(const psd_plan* p) { return p ? (int64_t)p->bytes : 0; }
+
+int psd_plan_prefetch(psd_plan* p, const double* x_next, int64_t n, int64_t ldx) {
+  if (!p) return fail(PSD_ERR_INVALID_PARAMS, "null plan");
+  if (x_next && (n < 1 || n > p->n || ldx < n))
+    return fail(PSD_ERR_INVALID_PARAMS, "prefetch hint outside the plan (n=%lld, ldx=%lld)", (ll)n, (ll)ldx);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
+  p->hint_x = x_next;
+  p->hint_n = x_next ? n : 0;
+  p->hint_ldx = x_next ? ldx : 0;
+  if (x_next && n < 3072) p->hint_x = nullptr;   // INT8 engine only (its size rule)
+  if (p->hint_x && !p->work) {   // the call's streams exist before it decides to run on them
+    DeviceGuard g(p->device);
+    if (ensure_oz(p) != PSD_OK || ensure_pipeline(p) != PSD_OK) {
+      cudaGetLastError();
+      p->hint_x = nullptr;   // no room for a second set of planes: unpipelined calls
+    }
+  }
+  return PSD_OK;
+}
 
 int psd_require_symmetric(psd_plan* p, const double* x, int64_t n, int64_t ldx, double tol,
                           double* stats_out, void* stream) {
@@ -776,7 +830,64 @@ int ensure_oz(psd_plan* p) {
   p->oz_ldk = ldk;
   cudaMemset(p->oz_ar, 0, (size_t)L * p->n * ldk);   // K padding stays zero
   cudaMemset(p->oz_br, 0, (size_t)L * wpad * ldk);
+  cudaDeviceSynchronize();   // legacy-stream memsets done before non-blocking streams write here
   return PSD_OK;
+}
+
+// Pipelining state (psd_plan_prefetch): streams, events, the mapped statistics slot and a
+// second set of X residue planes / exponents / row maxima (allocated on first use).
+int ensure_pipeline(psd_plan* p) {
+  if (p->oz_ar_alt) return PSD_OK;
+  if (p->pf_failed || !p->oz_ldk) return -1;
+  int least = 0, greatest = 0;
+  bool ok = cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithPriority(&p->work, cudaStreamNonBlocking, greatest) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, least) == cudaSuccess;
+  for (cudaEvent_t* e : {&p->ev_in, &p->ev_out, &p->ev_fork, &p->ev_pf_stats, &p->ev_pf_done})
+    ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaHostAlloc(reinterpret_cast<void**>(&p->pf_host), 64, cudaHostAllocMapped) == cudaSuccess;
+  ok = ok && cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->pf_dev), p->pf_host, 0) == cudaSuccess;
+  if (ok) {
+    const size_t planes = (size_t)psd::oz_num_moduli() * p->n * p->oz_ldk;
+    p->oz_ar_alt = static_cast<int8_t*>(static_cast<void*>(alloc(p, (planes + 7) / 8)));
+    p->oz_e_alt = reinterpret_cast<int*>(alloc(p, ((size_t)p->n + 1) / 2));
+    p->oz_rowmax_alt = reinterpret_cast<unsigned*>(alloc(p, ((size_t)p->n + 1) / 2));
+    p->stats_alt = alloc(p, 4);
+    ok = p->oz_ar_alt && p->oz_e_alt && p->oz_rowmax_alt && p->stats_alt;
+    if (ok) ok = cudaMemset(p->oz_ar_alt, 0, planes) == cudaSuccess;   // K padding stays zero
+    if (ok) ok = cudaDeviceSynchronize() == cudaSuccess;
+  }
+  if (!ok) {
+    cudaGetLastError();
+    p->pf_failed = true;   // no room: calls run unpipelined
+    p->oz_ar_alt = nullptr;
+    return -1;
+  }
+  return PSD_OK;
+}
+
+// Enqueue the hinted next X's require_symmetric pass (statistics → mapped slot) and its
+// residue planes on the side stream, ordered after everything enqueued on `st` so far.
+// Short-lived CTAs (16 tile pairs / 2 rows each) so the work yields SMs to `st`'s
+// latency-bound kernels between CTAs; the side stream has the lowest priority.
+void launch_prefetch(psd_plan* p, const double* x, ll n, ll ldx, cudaStream_t st) {
+  cudaEventRecord(p->ev_fork, st);
+  cudaStreamWaitEvent(p->side, p->ev_fork, 0);
+  static const int pairs = [] { const char* e = getenv("PSD_PF_PAIRS"); return e ? std::max(1, atoi(e)) : 16; }();
+  static const int rows = [] { const char* e = getenv("PSD_PF_ROWS"); return e ? std::max(1, atoi(e)) : 2; }();
+  static const int pad = [] { const char* e = getenv("PSD_PF_SMEM"); return e ? atoi(e) : 0; }();
+  const ll nt = (n + 63) / 64;
+  psd::sym_stats(x, n, ldx, p->stats_alt, p->side, p->oz_rowmax_alt, std::max<ll>(1, nt * (nt + 1) / 2 / pairs),
+                 pad > 36 * 1024 ? pad - 36 * 1024 : 0);
+  psd::copy_to_mapped(p->pf_dev, p->stats_alt, 3 * sizeof(double), p->side);
+  cudaEventRecord(p->ev_pf_stats, p->side);
+  psd::oz_prepare_rows_max(x, n, n, ldx, p->oz_rowmax_alt, p->oz_e_alt, p->oz_ar_alt, p->oz_ldk, p->side,
+                           std::max<ll>(1, n / rows), pad);
+  cudaEventRecord(p->ev_pf_done, p->side);
+  p->pf_x = x;
+  p->pf_n = n;
+  p->pf_ldx = ldx;
+  p->pf_ready = true;
 }
 
 // X·P (X bitwise symmetric, residues prepared) as 16 INT8 GEMMs + CRT, panels
@@ -924,12 +1035,35 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     cudaGetLastError();
     oz = false;
   }
+  // pipelined batch (psd_plan_prefetch): the hint names the NEXT call's X; a finished
+  // prefetch of THIS call's X replaces the symmetry pass and the residue preparation
+  const double* hint_x = p->hint_x;
+  const ll hint_n = p->hint_n, hint_ldx = p->hint_ldx;
+  p->hint_x = nullptr;
+  bool consumed = false;
+  if (p->pf_ready) {
+    if (oz && p->pf_x == x64 && p->pf_n == n && p->pf_ldx == ldx && !(flags & PSD_FLAG_SKIP_SYMCHECK)) {
+      PSD_CUDA_CHECK(cudaStreamWaitEvent(st, p->ev_pf_done, 0), "prefetch join");
+      std::swap(p->oz_ar, p->oz_ar_alt);
+      std::swap(p->oz_e, p->oz_e_alt);
+      std::swap(p->oz_rowmax, p->oz_rowmax_alt);
+      consumed = true;
+    }
+    p->pf_ready = false;   // a mismatched prefetch is dropped (the side stream stays ordered)
+  }
+  static const int pf_at = [] {   // PSD_PREFETCH=0 off, =eigh: start before the eigensolver
+    const char* e = getenv("PSD_PREFETCH");
+    return (e && e[0] == '0') ? 0 : (e && e[0] == 'e') ? 2 : 1;
+  }();
+  const bool prefetch_next = hint_x && oz && pf_at != 0 && hint_n >= 3072 && hint_n <= p->n &&
+                             hint_ldx >= hint_n && ensure_pipeline(p) == PSD_OK;
   bool have_rowmax = false;
   // require_symmetric's verdict (and alpha_tol) — evaluated now for FP32, and for FP64 once
   // the first product is enqueued (sym_pending): the statistics travel through an
   // event-tracked mapped-memory read, so the GPU never idles on this host round trip.
   // Nothing observable (the result, factors) is written before the verdict.
   bool sym_pending = false;
+  bool sym_prefetched = false;   // the verdict comes from the prefetch's mapped slot
   auto judge = [&](const SymInfo& si) -> int {
     r.max_abs = si.max_abs;
     r.sym_defect = si.defect;
@@ -953,7 +1087,12 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     if (!sym_pending) return PSD_OK;
     sym_pending = false;
     double h[3];
-    PSD_CUDA_CHECK(psd::read_small_wait(h, sizeof(h)), "stats");
+    if (sym_prefetched) {
+      PSD_CUDA_CHECK(cudaEventSynchronize(p->ev_pf_stats), "prefetched stats");
+      std::memcpy(h, p->pf_host, sizeof(h));
+    } else {
+      PSD_CUDA_CHECK(psd::read_small_wait(h, sizeof(h)), "stats");
+    }
     SymInfo si;
     int fl = 0;
     std::memcpy(&fl, &h[2], sizeof(int));
@@ -971,6 +1110,9 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
       SymInfo si;
       PSD_TRY(symcheck32(p, x32, n, ldx, raw, &si, st));
       PSD_TRY(judge(si));
+    } else if (consumed) {
+      sym_pending = true;
+      sym_prefetched = true;
     } else {
       {
         Stage mark(p, PSD_STAGE_SYMCHECK, st);
@@ -1008,7 +1150,7 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   // Grams on the INT8 engine wherever it pays (same size rule as the products; the
   // FP32 path's QR is FP64 too)
   p->oz_gram = oz_gram_on && oz_on && oz_size && !(flags & PSD_FLAG_FP64_DMMA);
-  if (oz) {
+  if (oz && !consumed) {
     Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
     if (have_rowmax)   // row scales from the symmetry pass: one read of X
       psd::oz_prepare_rows_max(x64, n, n, ldx, p->oz_rowmax, p->oz_e, p->oz_ar, p->oz_ldk, st);
@@ -1022,8 +1164,12 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   };
   int qb = 0, wk = 0;
   QrInfo qi;
+  auto start_prefetch = [&]() {
+    if (prefetch_next) launch_prefetch(p, hint_x, hint_n, hint_ldx, st);
+  };
   PSD_TRY(range_finder_core(p, mul, n, n, omega, ldo_eff, w, q, f32, (flags & PSD_FLAG_STRICT) != 0,
-                            bufs, &qb, &wk, &qi, st, resolve_sym));
+                            bufs, &qb, &wk, &qi, st, resolve_sym,
+                            pf_at == 1 ? std::function<void()>(start_prefetch) : nullptr));
   PSD_TRY(resolve_sym());
   r.qr_passes = qi.passes;
   r.qr_shifted = qi.shifted;
@@ -1050,6 +1196,7 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     Stage mark(p, PSD_STAGE_COMPRESS, st);
     PSD_TRY(panel_tn(p, Q, C, ld, n, wk, p->T, true, st));
   }
+  if (pf_at == 2) start_prefetch();
   // eigh (projection.py:105 → symmetric.py:68-86)
   Stage eig_mark(p, PSD_STAGE_EIGH, st);
   const int sweeps = psd::jacobi_eigh(p->T, wk, wk, p->vals, p->V, wk, p->jws, p->jws_elems,
@@ -1173,12 +1320,25 @@ int psd_ran_proj(psd_plan* p, const double* x, int64_t n, int64_t ldx, const dou
   if (!p || !x || !omega) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
   DeviceGuard g(p->device);
   std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  cudaStream_t st = caller;
+  // a call in a pipelined batch runs on the plan's high-priority stream, joined to the
+  // caller's at both ends (its CTAs are dispatched ahead of the side stream's)
+  const bool piped = (p->hint_x || p->pf_ready) && p->work;
+  if (piped) {
+    cudaEventRecord(p->ev_in, caller);
+    cudaStreamWaitEvent(p->work, p->ev_in, 0);
+    st = p->work;
+  }
   int status;
   {
     Stage total(p, PSD_STAGE_TOTAL, st);
     status = ran_proj_impl(p, x, nullptr, n, ldx, omega, nullptr, ldo, k, l, q, alpha, flags, result,
-                           nullptr, ldr, factors_w, ldw, factors_d, rep, stream);
+                           nullptr, ldr, factors_w, ldw, factors_d, rep, st);
+  }
+  if (piped) {
+    cudaEventRecord(p->ev_out, st);
+    cudaStreamWaitEvent(caller, p->ev_out, 0);
   }
   if (p->prof) {
     cudaStreamSynchronize(st);

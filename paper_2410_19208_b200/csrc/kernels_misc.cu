@@ -149,14 +149,19 @@ __global__ void __launch_bounds__(256, PSD_SYM_MINB) sym_stats_kernel(const T* _
 
 template <typename T>
 static void sym_stats_t(const T* x, long long n, long long ldx, double* stats, unsigned* rowmax,
-                        cudaStream_t st) {
+                        cudaStream_t st, long long grid = 0, int pad_smem = 0) {
   cudaMemsetAsync(stats, 0, 3 * sizeof(double), st);
   if (rowmax) cudaMemsetAsync(rowmax, 0, (size_t)n * sizeof(unsigned), st);
   const long long nt = (n + kSymT - 1) / kSymT;
   const long long npairs = nt * (nt + 1) / 2;
-  const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * PSD_SYM_MINB * 2);
+  const long long blocks = std::min<long long>(npairs, grid > 0 ? grid : (long long)device_info().sms * PSD_SYM_MINB * 2);
   static const int diag = [] { const char* e = getenv("PSD_SYM_ORDER"); return e && e[0] == 'd' ? 1 : 0; }();
-  sym_stats_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats, rowmax, diag);
+  static int pad_set = 0;
+  if (pad_smem > pad_set) {
+    cudaFuncSetAttribute(sym_stats_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad_smem);
+    pad_set = pad_smem;
+  }
+  sym_stats_kernel<T><<<(unsigned)blocks, 256, pad_smem, st>>>(x, n, ldx, npairs, stats, rowmax, diag);
   count_launch();
 }
 // Off-diagonal block pair of a row-sharded X (SURVEY §8(e) symmetry check):
@@ -259,8 +264,8 @@ void identity_defect(const double* g, int w, long long ldg, double* out, cudaStr
 }
 
 void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st,
-               unsigned* rowmax) {
-  sym_stats_t(x, n, ldx, stats, rowmax, st);
+               unsigned* rowmax, long long grid, int pad_smem) {
+  sym_stats_t(x, n, ldx, stats, rowmax, st, grid, pad_smem);
 }
 void sym_stats_f32(const float* x, long long n, long long ldx, double* stats, cudaStream_t st) {
   sym_stats_t(x, n, ldx, stats, static_cast<unsigned*>(nullptr), st);
@@ -756,6 +761,12 @@ cudaError_t read_small_async(const void* dev_src, size_t bytes, cudaStream_t st)
   }
   copy_to_mapped_kernel<<<1, 256, 0, st>>>(sl.d, static_cast<const unsigned char*>(dev_src), bytes);
   return cudaEventRecord(sl.ev, st);
+}
+
+void copy_to_mapped(void* mapped_dev_dst, const void* dev_src, size_t bytes, cudaStream_t st) {
+  copy_to_mapped_kernel<<<1, 256, 0, st>>>(static_cast<unsigned char*>(mapped_dev_dst),
+                                           static_cast<const unsigned char*>(dev_src), bytes);
+  count_launch();
 }
 
 cudaError_t read_small_wait(void* host_dst, size_t bytes) {

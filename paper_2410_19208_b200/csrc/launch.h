@@ -96,12 +96,17 @@ cudaError_t read_small(void* host_dst, const void* dev_src, size_t bytes, cudaSt
 // enqueue a status read (≤ 4 KB) without draining the stream; collect with read_small_wait
 cudaError_t read_small_async(const void* dev_src, size_t bytes, cudaStream_t st);
 cudaError_t read_small_wait(void* host_dst, size_t bytes);
+// copy a few device bytes into caller-owned host-mapped memory (its device alias) on `st`
+void copy_to_mapped(void* mapped_dev_dst, const void* dev_src, size_t bytes, cudaStream_t st);
 int oz_num_moduli();
 long long oz_max_k();   // largest K the exact CRT reconstruction admits (2^18)
 // residues of X's rows when the high words of max_j |x_ij| are already known (rowmax_hi,
 // from sym_stats): one pass over X
+// grid > 0: that many CTAs instead of the persistent default (short-lived CTAs for work on a
+// low-priority side stream that must yield SMs to the caller's stream — the pipelined prefetch)
 void oz_prepare_rows_max(const double* x, long long rows, long long cols, long long ldx,
-                         const unsigned* rowmax_hi, int* e, int8_t* r, long long ldr, cudaStream_t st);
+                         const unsigned* rowmax_hi, int* e, int8_t* r, long long ldr, cudaStream_t st,
+                         long long grid = 0, int pad_smem = 0);
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
                      long long ldr, cudaStream_t st);
 int oz_gemm(const OzOp& op, cudaStream_t st);
@@ -136,7 +141,7 @@ void split_transpose(const double* P, long long n, int w, long long ldp, float* 
 void pair_defect(const double* a, long long lda, const double* b, long long ldb, long long rows,
                  long long cols, double* stats, bool reset, cudaStream_t st);
 void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st,
-               unsigned* rowmax = nullptr);
+               unsigned* rowmax = nullptr, long long grid = 0, int pad_smem = 0);
 // out[0] = max |G − I| over a w×w Gram (single block)
 void identity_defect(const double* g, int w, long long ldg, double* out, cudaStream_t st);
 void sym_stats_f32(const float* x, long long n, long long ldx, double* stats, cudaStream_t st);

@@ -120,10 +120,26 @@ def _result_buffer(out, n, op):
     return out
 
 
-def _run(op, n, params, om, alpha, validate, collect_diagnostics, return_factors, method, t0, out=None):
+def _prefetch_hint(lib, plan, prefetch, n, op):
+    """psd_plan_prefetch: ``prefetch`` is the matrix the NEXT call will project (a pipelined
+    batch — its validation and INT8 residue planes are prepared on a side stream while this
+    call's CholeskyQR / eigensolver run).  FP64 n×n contiguous CUDA tensors only; anything
+    else clears the hint."""
+    ok = (isinstance(prefetch, torch.Tensor) and prefetch.is_cuda and prefetch.device == op.device
+          and prefetch.dtype == torch.float64 and op.t.dtype == torch.float64
+          and tuple(prefetch.shape) == (n, n) and prefetch.stride(1) == 1)
+    _native.check(lib.psd_plan_prefetch(plan.handle, _native.ptr(prefetch) if ok else None, n,
+                                        prefetch.stride(0) if ok else n))
+    plan.prefetch_ref = prefetch if ok else None   # keep the tensor alive until it is consumed
+
+
+def _run(op, n, params, om, alpha, validate, collect_diagnostics, return_factors, method, t0, out=None,
+         prefetch=None):
     width = params.width
     lib = _native.load_library()
     plan = _native.get_plan(n, min(width, n), op.device)   # width > n: raised after the symmetry check
+    if prefetch is not None or getattr(plan, "prefetch_ref", None) is not None:
+        _prefetch_hint(lib, plan, prefetch, n, op)
     dev = op.device
     f32 = op.t.dtype == torch.float32
     result = _result_buffer(out, n, op)
@@ -164,24 +180,29 @@ def _run(op, n, params, om, alpha, validate, collect_diagnostics, return_factors
     )
 
 
-def _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, validate, t0, out=None):
+def _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, validate, t0, out=None,
+                 prefetch=None):
     n = require_square(op)
     width = params.width
     if width > n and not validate:   # sketch.py:67-69 (else raised by the library after its check)
         raise errors.error("InvalidParams", f"k+l = {width} exceeds min(m, n) = {n}")
     om = as_device(omega, op.device).t if omega is not None else draw_gaussian(rng, (n, width), op.device)
     return _run(op, n, params, om, 0.0, validate, collect_diagnostics, return_factors, "randomized", t0,
-                out)
+                out, prefetch)
 
 
 def ran_proj(x, params, rng, collect_diagnostics=False, return_factors=False, *, omega=None,
-             assume_symmetric=False, dtype=None, out=None):
-    """projection.py:92-119 (Alg. 2): X̂₊ = Q U D₊ Uᵀ Qᵀ."""
+             assume_symmetric=False, dtype=None, out=None, prefetch=None):
+    """projection.py:92-119 (Alg. 2): X̂₊ = Q U D₊ Uᵀ Qᵀ.
+
+    ``prefetch`` (extension for batches of projections): the device matrix the next
+    ``ran_proj`` call will project; see psd_plan_prefetch (include/psdproj.h)."""
     t0 = time.perf_counter()
     op = _operand(x, dtype)
     require_square(op)
     validate = _validate_in_library(op, assume_symmetric)      # projection.py:100
-    return _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, validate, t0, out)
+    return _ran_proj_op(op, params, rng, collect_diagnostics, return_factors, omega, validate, t0, out,
+                        prefetch)
 
 
 def _ran_proj_scal_op(op, params, alpha, rng, collect_diagnostics, return_factors, omega, validate, t0,
