@@ -767,12 +767,15 @@ int psd_eigh(psd_plan* p, double* a, int32_t m, int64_t lda, double* values, dou
   std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   psd::symmetrize_small(a, m, lda, st);  // eigh validates/uses the symmetric part
-  const int sw = psd::jacobi_eigh(a, lda, m, p->vals, p->V, m, p->jws, p->jws_elems,
-                                  p->ints + p->w + 3, st);
-  if (sw < 0) return fail(PSD_ERR_CONVERGENCE, "Jacobi eigensolver did not converge");
+  if (psd::jacobi_eigh(a, lda, m, p->vals, p->V, m, p->jws, p->jws_elems, p->ints + p->w + 1, st) < 0)
+    return fail(PSD_ERR_CONVERGENCE, "Jacobi eigensolver could not be launched");
   psd::sort_eigs(p->vals, p->V, m, m, 0.0, values, vectors, ldv, p->ints + p->w, p->ints, st);
-  if (sweeps_out) *sweeps_out = sw;
-  return sync(st, "eigh");
+  int h[2] = {0, 0};   // {npos, sweeps}: one status read
+  PSD_CUDA_CHECK(psd::read_small(h, p->ints + p->w, sizeof(h), st), "eigh status");
+  PSD_TRY(sync(st, "eigh"));
+  if (h[1] < 0) return fail(PSD_ERR_CONVERGENCE, "Jacobi eigensolver did not converge");
+  if (sweeps_out) *sweeps_out = h[1];
+  return PSD_OK;
 }
 
 }  // extern "C"
@@ -1199,17 +1202,17 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   if (pf_at == 2) start_prefetch();
   // eigh (projection.py:105 → symmetric.py:68-86)
   Stage eig_mark(p, PSD_STAGE_EIGH, st);
-  const int sweeps = psd::jacobi_eigh(p->T, wk, wk, p->vals, p->V, wk, p->jws, p->jws_elems,
-                                      p->ints + p->w + 3, st);
-  if (sweeps < 0) return fail(PSD_ERR_CONVERGENCE, "eigen-decomposition failed: Jacobi did not converge");
-  r.eig_sweeps = sweeps;
+  if (psd::jacobi_eigh(p->T, wk, wk, p->vals, p->V, wk, p->jws, p->jws_elems, p->ints + p->w + 1, st) < 0)
+    return fail(PSD_ERR_CONVERGENCE, "eigen-decomposition failed: Jacobi could not be launched");
   const double offset = alpha > 0.0 ? 1.0 : 0.0;  // max(D − 1, 0) for Alg. 3
   psd::sort_eigs(p->vals, p->V, wk, wk, offset, p->vals_sorted, p->U, wk, p->ints + p->w,
                  p->ints, st);
-  int npos = 0;
-  PSD_CUDA_CHECK(psd::read_small(&npos, p->ints + p->w, sizeof(int), st),
-                 "npos");
+  int eh[2] = {0, 0};   // {npos, sweeps}: the eigensolver's one host round trip
+  PSD_CUDA_CHECK(psd::read_small(eh, p->ints + p->w, sizeof(eh), st), "eigh status");
   PSD_TRY(sync(st, "eigh"));
+  if (eh[1] < 0) return fail(PSD_ERR_CONVERGENCE, "eigen-decomposition failed: Jacobi did not converge");
+  r.eig_sweeps = eh[1];
+  const int npos = eh[0];
   eig_mark.close();
   r.effective_rank = npos;
   Stage recon_mark(p, PSD_STAGE_RECON, st);

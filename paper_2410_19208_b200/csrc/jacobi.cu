@@ -771,8 +771,9 @@ __global__ void jacobi_norm_kernel(const double* a, long long lda, int m, double
 }
 
 __global__ void jacobi_diag_kernel(const double* a, long long lda, const double* b, int m,
-                                   const int* out, double* vals) {
+                                   const int* out, double* vals, int* dsweeps) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *dsweeps = out[0];
   if (i >= m) return;
   vals[i] = out[1] ? b[(long long)i * m + i] : a[(long long)i * lda + i];
 }
@@ -810,7 +811,7 @@ size_t jacobi_ws_elems(int m) {
 
 template <int JB>
 static int jacobi_run(double* a, long long lda, int m, double* values, double* v, long long ldv,
-                      double* ws, cudaStream_t st) {
+                      double* ws, int* dsweeps, cudaStream_t st) {
   using T = JTraits<JB>;
   constexpr int kJS = T::kJS, kJT = T::kJT;
   int nblk, P;
@@ -884,12 +885,13 @@ static int jacobi_run(double* a, long long lda, int m, double* values, double* v
                                   args, T::kSmemBytes, st) != cudaSuccess)
     return -3;
   count_launch();
-  int out[2] = {0, 0};
-  read_small(out, A.out, 2 * sizeof(int), st);
-  jacobi_diag_kernel<<<(m + 255) / 256, 256, 0, st>>>(a, lda, ws, m, A.out, values);
+  // the diagonal comes from whichever buffer holds the result (decided on the device);
+  // `a` is documented as destroyed, so no copy-back — no host round trip here
+  jacobi_diag_kernel<<<(m + 255) / 256, 256, 0, st>>>(a, lda, ws, m, A.out, values, dsweeps);
   count_launch();
-  if (out[1]) copy_matrix(ws, m, a, lda, m, m, st);
   static const bool stats = getenv("PSD_JACOBI_STATS") != nullptr;
+  int out[2] = {0, 0};
+  if (stats || trace_path || A.timers) read_small(out, A.out, 2 * sizeof(int), st);   // diagnostics only
   if (stats) {   // per sweep: rotations above threshold, max |off-diagonal| after the sweep
     std::vector<int> cnt(kJacobiMaxSweeps);
     std::vector<unsigned long long> mo(kJacobiMaxSweeps);
@@ -924,22 +926,25 @@ static int jacobi_run(double* a, long long lda, int m, double* values, double* v
             "jacobi m=%d JB=%d sweeps=%d grid=%d cycles: solve0 wait %lld load %lld compute %lld | item(0,1) wait %lld work %lld\n",
             m, JB, out[0], grid, h[0], h[1], h[2], h[3], h[4]);
   }
-  return out[0];
+  return 0;
 }
 
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+
 int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long long ldv,
-                double* ws, size_t ws_elems, int* dflags, cudaStream_t st) {
-  (void)dflags;
+                double* ws, size_t ws_elems, int* dsweeps, cudaStream_t st) {
   if (m == 1) {
     cudaMemcpyAsync(values, a, sizeof(double), cudaMemcpyDeviceToDevice, st);
     set_identity(v, ldv, 1, st);
-    return 1;
+    set_int_kernel<<<1, 1, 0, st>>>(dsweeps, 1);
+    count_launch();
+    return 0;
   }
   if (ws_elems < jacobi_ws_elems(m)) return -2;
   static const int jb_env = [] { const char* e = getenv("PSD_JACOBI_JB"); return e ? atoi(e) : 0; }();
   const int jb = jb_env == 16 || jb_env == 32 ? jb_env : (m >= kJacobiWideMin ? 32 : 16);
-  return jb == 32 ? jacobi_run<32>(a, lda, m, values, v, ldv, ws, st)
-                  : jacobi_run<16>(a, lda, m, values, v, ldv, ws, st);
+  return jb == 32 ? jacobi_run<32>(a, lda, m, values, v, ldv, ws, dsweeps, st)
+                  : jacobi_run<16>(a, lda, m, values, v, ldv, ws, dsweeps, st);
 }
 
 }  // namespace psd

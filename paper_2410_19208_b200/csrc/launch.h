@@ -200,10 +200,12 @@ int chol_fast(const double* G, long long ldg, int m, double shift, double* L, lo
               double* Dinv1 = nullptr, double* status1 = nullptr);
 // rdiag[i] *= L[i][i]
 void accumulate_diag(const double* l, long long ldl, int m, double* rdiag, cudaStream_t st);
-// Symmetric eigensolver (block Jacobi).  a (m×m, destroyed), values[m], v (m×m).
-// Returns number of sweeps (>0) or −1 on non-convergence.
+// Symmetric eigensolver (block Jacobi, jacobi.cu).
+// a (m×m, destroyed), values[m], v (m×m).  Enqueued only: returns 0 (< 0: launch /
+// workspace error); *dsweeps (DEVICE int) receives the sweep count, or −1 on
+// non-convergence, for the caller's next status read.
 int jacobi_eigh(double* a, long long lda, int m, double* values, double* v, long long ldv,
-                double* ws, size_t ws_elems, int* dflags, cudaStream_t st);
+                double* ws, size_t ws_elems, int* dsweeps, cudaStream_t st);
 size_t jacobi_ws_elems(int m);
 // Sort eigenpairs descending, sign-fix columns (symmetric.py:80-85).
 // vals_out[m], vecs_out (m×m, ld), npos[0] = #(vals − offset > 0).
