@@ -117,6 +117,79 @@ __global__ void __launch_bounds__(NT) k_steps(const double* a, int nsteps, long 
   out[threadIdx.x] = Sc[threadIdx.x] + Vc[threadIdx.x];
 }
 
+
+// FP32 variant of the real step (same structure; rsqrtf, float smem, one SHFL per value)
+__device__ __forceinline__ bool rotation_f(float app, float aqq, float apq, float& c, float& s, float& t) {
+  const float d = aqq - app, e = 2.0f * apq;
+  const float y = rsqrtf(fmaxf(fmaf(d, d, e * e), 1e-37f));
+  const float h = fmaf(0.5f * fabsf(d), y, 0.5f);
+  const float z = rsqrtf(h);
+  const bool rot = fabsf(apq) > 1e-37f;
+  const float sr = (d >= 0.f ? 0.5f : -0.5f) * e * y * z;
+  c = rot ? h * z : 1.f;
+  s = rot ? sr : 0.f;
+  t = rot ? sr * z : 0.f;
+  return rot;
+}
+__device__ int step_f(const float* Sc, const float* Vc, float* Sn, float* Vn, int ir) {
+  const int lane = threadIdx.x & 31, l = lane & (JB - 1), k = threadIdx.x / JB;
+  int p, q, pk, qk;
+  step_pair(ir, l, p, q);
+  step_pair(ir, k, pk, qk);
+  const float lpp = Sc[p * L + p], lqq = Sc[q * L + q], lpq = Sc[p * L + q];
+  float b00 = Sc[pk * L + p], b01 = Sc[pk * L + q], b10 = Sc[qk * L + p], b11 = Sc[qk * L + q];
+  const float v00 = Vc[k * L + p], v01 = Vc[k * L + q], v10 = Vc[(k + JB) * L + p], v11 = Vc[(k + JB) * L + q];
+  float c, s, t;
+  const bool r = rotation_f(lpp, lqq, lpq, c, s, t);
+  const int nrot = __popc(__ballot_sync(0xffffffffu, r) & 0xffffu);
+  if (nrot == 0) return 0;
+  const float ck = __shfl_sync(0xffffffffu, c, k & (JB - 1));
+  const float sk = __shfl_sync(0xffffffffu, s, k & (JB - 1));
+  const float kpp = b00, kqq = b11, kpq = b01;
+  const float r00 = c * b00 - s * b01, r01 = s * b00 + c * b01;
+  const float r10 = c * b10 - s * b11, r11 = s * b10 + c * b11;
+  b00 = ck * r00 - sk * r10;
+  b01 = ck * r01 - sk * r11;
+  b10 = sk * r00 + ck * r10;
+  b11 = sk * r01 + ck * r11;
+  if (k == l && sk != 0.f) {
+    b00 = kpp - t * kpq;
+    b11 = kqq + t * kpq;
+    b01 = 0.f;
+    b10 = 0.f;
+  }
+  Sn[pk * L + p] = b00;
+  Sn[pk * L + q] = b01;
+  Sn[qk * L + p] = b10;
+  Sn[qk * L + q] = b11;
+  Vn[k * L + p] = c * v00 - s * v01;
+  Vn[k * L + q] = s * v00 + c * v01;
+  Vn[(k + JB) * L + p] = c * v10 - s * v11;
+  Vn[(k + JB) * L + q] = s * v10 + c * v11;
+  __syncthreads();
+  return nrot;
+}
+__global__ void __launch_bounds__(NT) k_steps_f(const double* a, long long* cyc, double* out) {
+  __shared__ float S0[JS * L], V0[JS * L], S1[JS * L], V1[JS * L];
+  for (int e = threadIdx.x; e < JS * JS; e += NT) {
+    const int i = e / JS, j = e % JS;
+    S0[i * L + j] = (float)a[e];
+    V0[i * L + j] = i == j;
+  }
+  __syncthreads();
+  float *Sc = S0, *Vc = V0, *Sn = S1, *Vn = V1;
+  const long long t0 = clock64();
+  for (int it = 0; it < 16; ++it) {
+    if (step_f(Sc, Vc, Sn, Vn, it & 15)) {
+      float* x = Sc; Sc = Sn; Sn = x;
+      x = Vc; Vc = Vn; Vn = x;
+    }
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[threadIdx.x] = Sc[threadIdx.x] + Vc[threadIdx.x];
+}
+
 // dependent-chain latencies (cycles per op)
 __global__ void k_lat(double x, long long* cyc, double* out) {
   double v = x, w = x;
@@ -171,6 +244,10 @@ int main() {
     cudaMemcpy(hc, cyc, sizeof(long long), cudaMemcpyDeviceToHost);
     printf("%-55s %6.0f cycles/step (16 steps, first sweep: every pair rotates)\n", names[mode], hc[0] / 16.0);
   }
+  for (int rep = 0; rep < 2; ++rep) k_steps_f<<<1, NT>>>(a, cyc, out);
+  cudaDeviceSynchronize();
+  cudaMemcpy(hc, cyc, sizeof(long long), cudaMemcpyDeviceToHost);
+  printf("%-55s %6.0f cycles/step\n", "FP32 real step", hc[0] / 16.0);
   (void)nsteps;
   cudaError_t e = cudaDeviceSynchronize();
   printf("%s\n", cudaGetErrorString(e));
