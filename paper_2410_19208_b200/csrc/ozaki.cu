@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <utility>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -62,6 +63,9 @@ __constant__ uint32_t c_nmod[kNumMod];      // −m_ℓ mod 2^32
 __constant__ float c_pow13f[4][kNumMod];    // 2^(13t) mod m_ℓ in (−m/2, m/2]
 __constant__ float c_wInvf[kNumMod];        // (M/m_ℓ)^{-1} mod m_ℓ
 __constant__ unsigned long long c_W[kNumMod][2];   // M/m_ℓ as (lo, hi)
+// y-table of the single-split CRT: g_ytab[ℓ][b] = (r·(M/m_ℓ)^{-1} mod m_ℓ) ∈ [0, m_ℓ) for the
+// stored residue byte b (r = (int8)b), four entries per word
+__device__ uint32_t g_ytab[kNumMod * 64];
 
 // fp32 integer tricks.  kMagic = 1.5·2^23: fmaf(s, 1/m, kMagic) − kMagic = rint(s/m)
 // for |s| < 2^22·m; the bits of (r + kMagic) hold the integer r in their low bytes.
@@ -706,6 +710,81 @@ __global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ re
   }
 }
 
+// Single-split CRT (the n×w products) with the per-modulus arithmetic moved into tables
+// and exact integer limbs — the float path above spends ≈20 instructions per (modulus,
+// column) on the residue → y_ℓ step and a 128-bit multiply-accumulate, which made the kernel
+// issue-bound (ncu: 70% issue slots, not_selected the top stall):
+//   y_ℓ = T_ℓ[b]                     one LDS.U8 (b = the stored residue byte)
+//   κ  += y_ℓ·⌊2^27/m_ℓ⌉             k = rint(Σ y_ℓ/m_ℓ) in 5.27 fixed point: the rounding
+//                                     of the 16 weights costs ≤ 16·255·2^-28 < 2^-14
+//   s_t += y_ℓ·w_ℓt (t = 0..3)       the 32-bit limbs of M/m_ℓ; s_t < 16·2^8·2^32 = 2^44, so
+//                                     four IMAD.WIDE per term and one carry pass per output
+// then C' = Σ s_t·2^(32t) − k·M mod 2^128 exactly as before.
+template <int L>
+__host__ __device__ constexpr uint32_t kwt() { return (uint32_t)((134217728.0 / mod_at(L)) + 0.5); }   // ⌊2^27/m⌉
+
+__global__ void __launch_bounds__(256) crt1_kernel(const uint8_t* __restrict__ res, long long M, int N, long long ldo,
+                                                   const int* __restrict__ e, const int* __restrict__ f,
+                                                   double* __restrict__ C, long long ldc, double alpha,
+                                                   const double* __restrict__ S, long long lds) {
+  __shared__ uint32_t ty32[kNumMod * 64];
+  for (int i = threadIdx.x; i < kNumMod * 64; i += blockDim.x) ty32[i] = g_ytab[i];
+  __syncthreads();
+  const uint8_t* ty = reinterpret_cast<const uint8_t*>(ty32);
+  const int n4 = (N + 3) / 4;
+  const long long total = M * n4;
+  const long long plane = M * ldo;
+  const unsigned __int128 Mfull = ((unsigned __int128)c_M[1] << 64) | c_M[0];
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / n4;
+    const int j0 = (int)(t % n4) * 4;
+    const uint8_t* base = res + i * ldo + j0;
+    uint32_t wv[kNumMod];
+#pragma unroll
+    for (int l = 0; l < kNumMod; ++l) wv[l] = __ldcs(reinterpret_cast<const uint32_t*>(base + l * plane));
+    unsigned long long s0[4] = {0, 0, 0, 0}, s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0}, s3[4] = {0, 0, 0, 0};
+    uint32_t kap[4] = {0u, 0u, 0u, 0u};
+    auto term = [&](auto lc) {
+      constexpr int l = decltype(lc)::value;
+      const uint32_t w0 = (uint32_t)c_W[l][0], w1 = (uint32_t)(c_W[l][0] >> 32);
+      const uint32_t w2 = (uint32_t)c_W[l][1], w3 = (uint32_t)(c_W[l][1] >> 32);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t y = ty[l * 256 + ((wv[l] >> (8 * q)) & 255u)];
+        kap[q] += y * kwt<l>();
+        s0[q] += (unsigned long long)y * w0;
+        s1[q] += (unsigned long long)y * w1;
+        s2[q] += (unsigned long long)y * w2;
+        s3[q] += (unsigned long long)y * w3;
+      }
+    };
+    [&]<int... Ls>(std::integer_sequence<int, Ls...>) {
+      (term(std::integral_constant<int, Ls>{}), ...);
+    }(std::make_integer_sequence<int, kNumMod>{});
+    const int ei = e[i];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q;
+      if (j >= N) break;
+      const unsigned k = (kap[q] + (1u << 26)) >> 27;
+      const unsigned __int128 acc = (unsigned __int128)s0[q] + ((unsigned __int128)s1[q] << 32) +
+                                    ((unsigned __int128)s2[q] << 64) + ((unsigned __int128)s3[q] << 96);
+      const unsigned __int128 cs = acc - Mfull * k;        // two's complement of C'
+      const bool neg = (long long)(cs >> 64) < 0;
+      const unsigned __int128 mag = neg ? (unsigned __int128)0 - cs : cs;
+      const unsigned long long hi = (unsigned long long)(mag >> 64), lo = (unsigned long long)mag;
+      double val = fma((double)hi, 18446744073709551616.0, (double)lo);
+      if (neg) val = -val;
+      const int ex = ei + f[j] - 106;
+      if (ex > -1000 && ex < 1000) val *= __longlong_as_double((long long)(ex + 1023) << 52);   // exact 2^ex
+      else val = ldexp(val, ex);
+      if (alpha > 0.0) val = (val + alpha * S[i * lds + j]) / alpha;
+      C[i * ldc + j] = val;
+    }
+  }
+}
+
 }  // namespace oz
 
 namespace {
@@ -764,6 +843,14 @@ void ensure_oz_constants() {
   cudaMemcpyToSymbol(oz::c_nmod, nmod, sizeof(nmod));
   cudaMemcpyToSymbol(oz::c_pow13f, pw, sizeof(pw));
   cudaMemcpyToSymbol(oz::c_wInvf, winv, sizeof(winv));
+  {
+    uint8_t ytab[oz::kNumMod][256];
+    for (int l = 0; l < oz::kNumMod; ++l) {
+      const int m = oz::kMods[l], wi = (int)winv[l];
+      for (int b = 0; b < 256; ++b) ytab[l][b] = (uint8_t)((((int)(int8_t)b * wi) % m + m) % m);
+    }
+    cudaMemcpyToSymbol(oz::g_ytab, ytab, sizeof(ytab));
+  }
   cudaMemcpyToSymbol(oz::c_W, W, sizeof(W));
   // the copies are ordered on the legacy stream only: complete them before kernels on
   // non-blocking streams read the constants
@@ -948,7 +1035,10 @@ int oz_gemm_prepared(const OzOp& op, cudaStream_t st) {
   count_launch();
   {
     const unsigned g = (unsigned)grid_oz((long long)op.M * ((op.N + 3) / 4), 256);
-    if (p.splits == 1)
+    static const bool crt_float = [] { const char* v = getenv("PSD_OZ_CRT"); return v && v[0] == 'f'; }();
+    if (p.splits == 1 && !crt_float)
+      crt1_kernel<<<g, 256, 0, st>>>(op.res, op.M, op.N, p.ldo, op.e, op.f, op.C, op.ldc, op.alpha, op.S, op.lds);
+    else if (p.splits == 1)
       crt_kernel<true><<<g, 256, 0, st>>>(op.res, 1, op.M, op.N, p.ldo, op.e, op.f, op.C, op.ldc, op.alpha,
                                           op.S, op.lds);
     else
