@@ -50,6 +50,11 @@ struct psd_plan {
   size_t g_res_elems = 0;
   ll g_ldk = 0;
   bool g_failed = false;
+  // g_br / g_f hold the residue planes of this n×w panel (set by the last INT8 Gram; cleared by
+  // every write to a panel) — the compression product X·Q and the Gram QᵀC reuse them
+  const double* gq_P = nullptr;
+  ll gq_ld = 0, gq_n = 0;
+  int gq_w = 0;
   int gparts = 0;
   double* rpart = nullptr;
   ll rparts = 0;
@@ -221,6 +226,7 @@ int launched(int k) {
 int xmul_rect(psd_plan* p, const double* x, ll rows, ll cols, ll ldx, const double* P, ll ldP,
               int w, double* out, ll ldo, double alpha, bool transpose, cudaStream_t st) {
   Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
+  if (out == p->gq_P) p->gq_P = nullptr;
   psd::GemmOp op;
   op.a_layout = transpose ? psd::A_KM : psd::A_MK;
   op.b_layout = psd::B_KN;
@@ -288,6 +294,10 @@ int gram_oz(psd_plan* p, const double* Y, ll ld, ll n, int w, double* G, cudaStr
   op.ldbr = p->g_ldk;
   op.f = p->g_f;
   if (psd::oz_prepare_panel(op, st) != 0) return -1;
+  p->gq_P = Y;
+  p->gq_ld = ld;
+  p->gq_n = n;
+  p->gq_w = w;
   op.ar = op.br;
   op.ldar = op.ldbr;
   op.ar_rows = (w + 15) / 16 * 16;
@@ -300,10 +310,42 @@ int gram_oz(psd_plan* p, const double* Y, ll ld, ll n, int w, double* G, cudaStr
   return psd::oz_gemm_prepared(op, st) < 0 ? -1 : 0;
 }
 
+// G = AᵀB for A ≠ B on the INT8 engine when A's planes are already in g_br (the compression
+// Gram QᵀC after the verification Gram of Q): B's panel is prepared into oz_br (free once the
+// product that read it has run), A = Qᵀ is g_br read row-wise.
+int gram2_oz(psd_plan* p, const double* A, const double* B, ll ld, ll n, int w, double* G, cudaStream_t st) {
+  if (!(p->gq_P == A && p->gq_ld == ld && p->gq_n == n && p->gq_w == w) || !p->oz_br || p->w > 512 ||
+      p->g_ldk != p->oz_ldk)
+    return -1;
+  psd::OzOp op;
+  op.P = B;
+  op.ldp = ld;
+  op.N = w;
+  op.K = (int)n;
+  op.br = p->oz_br;
+  op.ldbr = p->oz_ldk;
+  op.f = p->oz_f;
+  if (psd::oz_prepare_panel(op, st) != 0) return -1;
+  op.ar = p->g_br;
+  op.ldar = p->g_ldk;
+  op.ar_rows = (w + 15) / 16 * 16;
+  op.e = p->g_f;
+  op.M = w;
+  op.res = p->g_res;
+  op.res_elems = p->g_res_elems;
+  op.C = G;
+  op.ldc = w;
+  return psd::oz_gemm_prepared(op, st) < 0 ? -1 : 0;
+}
+
 int panel_tn(psd_plan* p, const double* A, const double* B, ll ld, ll n, int w, double* G,
              bool sym, cudaStream_t st) {
   if (A == B && p->oz_gram && w <= 512 && n <= psd::oz_max_k() && gram_oz(p, A, ld, n, w, G, st) == 0)
     return PSD_OK;   // else (buffers unavailable): the DMMA Gram below
+  if (A != B && p->oz_gram && n <= psd::oz_max_k() && gram2_oz(p, A, B, ld, n, w, G, st) == 0) {
+    if (sym) psd::symmetrize_small(G, w, w, st);
+    return PSD_OK;
+  }
   psd::GemmOp op;
   op.a_layout = psd::A_KM;
   op.b_layout = psd::B_KN;
@@ -329,6 +371,7 @@ int panel_tn(psd_plan* p, const double* A, const double* B, ll ld, ll n, int w, 
 // out (n×N) = A (n×K, lda) · B (K×N, ldb)
 int panel_nn(psd_plan* p, const double* A, ll lda, const double* B, ll ldb, double* out, ll ldo,
              ll n, int K, int N, cudaStream_t st) {
+  if (out == p->gq_P) p->gq_P = nullptr;
   psd::GemmOp op;
   op.a_layout = psd::A_MK;
   op.b_layout = psd::B_KN;
@@ -486,6 +529,7 @@ int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* o
                       const std::function<int()>& after_first = nullptr,
                       const std::function<void()>& before_final_qr = nullptr) {
   const ll ld = p->ldp;
+  p->gq_P = nullptr;   // planes of an earlier call's panels are never reused
   const bool stabilize = q >= 2 || always_stabilize;               // sketch.py:74
   int y = 0;
   PSD_TRY(mul(omega, ldo, w, bufs[0], ld, false));                 // :75
@@ -532,6 +576,7 @@ int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* o
                                      cudaMemcpyHostToDevice, st),
                      "keep idx");
       const int dst = (qb + 1) % 3;
+      if (bufs[dst] == p->gq_P) p->gq_P = nullptr;
       psd::gather_columns(bufs[qb], ld, didx, (int)keep.size(), bufs[dst], ld, n, st);
       qb = dst;
     }
@@ -899,6 +944,10 @@ int xmul_oz(psd_plan* p, ll n, const double* P, ll ldP, int w, double* out, ll l
             cudaStream_t st) {
   Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
   const int groups = (w + 511) / 512;
+  // the panel's planes are already in g_br (the verification Gram of the final Q): no preparation
+  const bool reuse = groups == 1 && p->gq_P == P && p->gq_ld == ldP && p->gq_n == n && p->gq_w == w &&
+                     p->g_ldk == p->oz_ldk;
+  if (out == p->gq_P) p->gq_P = nullptr;
   const int gw = (w + groups - 1) / groups;
   const ll gw_pad = (gw + 15) / 16 * 16;
   for (int g = 0; g < groups; ++g) {
@@ -922,11 +971,16 @@ int xmul_oz(psd_plan* p, ll n, const double* P, ll ldP, int w, double* out, ll l
     op.alpha = alpha;
     op.S = P + c0;
     op.lds = ldP;
+    if (reuse) {
+      op.br = p->g_br;
+      op.ldbr = p->g_ldk;
+      op.f = p->g_f;
+    }
     if (p->prof) {
       op.ev_gemm[0] = take_event(p);
       op.ev_gemm[1] = take_event(p);
     }
-    const int r = psd::oz_gemm(op, st);
+    const int r = reuse ? psd::oz_gemm_prepared(op, st) : psd::oz_gemm(op, st);
     if (r < 0) return fail(PSD_ERR_INVALID_PARAMS, "INT8-emulated GEMM rejected its operands (%d)", r);
     if (p->prof) p->marks.push_back({PSD_STAGE_INT8_GEMM, {op.ev_gemm[0], op.ev_gemm[1]}});
   }
@@ -938,6 +992,7 @@ int xmul_oz(psd_plan* p, ll n, const double* P, ll ldP, int w, double* out, ll l
 int xmul_tc32(psd_plan* p, ll n, const float* xhi, ll ldhi, const double* P, ll ldP, int w,
               double* out, ll ldo, double alpha, cudaStream_t st) {
   Stage mark(p, PSD_STAGE_SKETCH_GEMM, st);
+  if (out == p->gq_P) p->gq_P = nullptr;
   psd::split_transpose(P, n, w, ldP, p->f[0], p->f[1], p->ldx32, w, st);
   psd::Tc32Op op;
   op.a_hi = xhi;
@@ -1003,6 +1058,7 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   psd::g_launch_count = 0;
   p->oz_gram = false;
+  p->gq_P = nullptr;
   psd_report r{};
   r.residual_frob = NAN;
   r.alpha_used = alpha;
