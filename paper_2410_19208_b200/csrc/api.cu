@@ -407,6 +407,7 @@ struct QrInfo {
   int shifted = 0;
   double frob = 0.0;  // ‖Y‖_F of the input panel
   bool zero = false;  // Y == 0
+  std::vector<double> rdiag;   // |R_ii| when read together with the last status (no extra round trip)
 };
 
 // CholeskyQR2 with shifted passes (shifted CholeskyQR3 when ill-conditioned).
@@ -438,13 +439,17 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
       // (checked before factoring it, so an accepted basis costs no third Cholesky)
       psd::identity_defect(p->G, w, w, p->scal + 3, st);
       double dev = 0.0;
-      PSD_CUDA_CHECK(psd::read_small(&dev, p->scal + 3, sizeof(double), st),
+      // the final QR's |R_ii| (accumulated through the last pass) ride along with the defect
+      if (rdiag) info->rdiag.assign(w, 0.0);
+      PSD_CUDA_CHECK(psd::read_small2(&dev, p->scal + 3, sizeof(double), rdiag ? info->rdiag.data() : nullptr,
+                                      rdiag, rdiag ? w * sizeof(double) : 0, st),
                      "orthogonality defect");
       PSD_TRY(sync(st, "orthogonality defect"));
       if (dev <= 1e-13 * std::max(1, w)) {
         verified = true;
         break;
       }
+      info->rdiag.clear();
     }
     // both candidates at once: unshifted (L, Rinv) and Fukaya-shifted (L1, Rinv1) with
     // s = 11(nw + w(w+1))·u·trace(G) — the fallback costs no extra launch or round trip
@@ -560,9 +565,12 @@ int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* o
     return PSD_OK;
   }
   std::vector<double> rd(w);
-  PSD_CUDA_CHECK(psd::read_small(rd.data(), p->rdiag, w * sizeof(double), st),
-                 "rdiag");
-  PSD_TRY(sync(st, "rdiag"));
+  if ((int)qi->rdiag.size() == w) {
+    rd = qi->rdiag;   // read with the verification Gram's defect
+  } else {
+    PSD_CUDA_CHECK(psd::read_small(rd.data(), p->rdiag, w * sizeof(double), st), "rdiag");
+    PSD_TRY(sync(st, "rdiag"));
+  }
   std::vector<int> keep;
   for (int i = 0; i < w; ++i)
     if (rd[i] > 1e-12 * qi->frob) keep.push_back(i);               // :86

@@ -778,6 +778,12 @@ cudaError_t read_small_wait(void* host_dst, size_t bytes) {
 }
 
 cudaError_t read_small(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t st) {
+  return read_small2(host_dst, dev_src, bytes, nullptr, nullptr, 0, st);
+}
+
+// two status blocks in one host round trip (two copy kernels, one stream sync)
+cudaError_t read_small2(void* host_dst, const void* dev_src, size_t bytes, void* host_dst2, const void* dev_src2,
+                        size_t bytes2, cudaStream_t st) {
   constexpr size_t kCap = 64 << 10;
   struct Staging {
     unsigned char* h = nullptr;
@@ -787,8 +793,9 @@ cudaError_t read_small(void* host_dst, const void* dev_src, size_t bytes, cudaSt
   int dev = 0;
   cudaGetDevice(&dev);
   Staging& sg = stage[dev & 15];
-  if (bytes > kCap) {   // not a status read: plain copy
+  if (bytes + bytes2 > kCap) {   // not a status read: plain copies
     cudaError_t e = cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && bytes2) e = cudaMemcpyAsync(host_dst2, dev_src2, bytes2, cudaMemcpyDeviceToHost, st);
     return e != cudaSuccess ? e : cudaStreamSynchronize(st);
   }
   if (!sg.h) {
@@ -797,10 +804,14 @@ cudaError_t read_small(void* host_dst, const void* dev_src, size_t bytes, cudaSt
     e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&sg.d), sg.h, 0);
     if (e != cudaSuccess) return e;
   }
+  const size_t off2 = (bytes + 15) / 16 * 16;
   copy_to_mapped_kernel<<<1, 256, 0, st>>>(sg.d, static_cast<const unsigned char*>(dev_src), bytes);
+  if (bytes2)
+    copy_to_mapped_kernel<<<1, 256, 0, st>>>(sg.d + off2, static_cast<const unsigned char*>(dev_src2), bytes2);
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return e;
   std::memcpy(host_dst, sg.h, bytes);
+  if (bytes2) std::memcpy(host_dst2, sg.h + off2, bytes2);
   return cudaGetLastError();
 }
 

@@ -93,6 +93,8 @@ struct OzOp {
 // device→host read of a few status bytes that does not queue behind DMA copies
 // (kernel store into host-mapped memory, then a stream sync); > 64 KB: cudaMemcpy
 cudaError_t read_small(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t st);
+cudaError_t read_small2(void* host_dst, const void* dev_src, size_t bytes, void* host_dst2, const void* dev_src2,
+                        size_t bytes2, cudaStream_t st);
 // enqueue a status read (≤ 4 KB) without draining the stream; collect with read_small_wait
 cudaError_t read_small_async(const void* dev_src, size_t bytes, cudaStream_t st);
 cudaError_t read_small_wait(void* host_dst, size_t bytes);
