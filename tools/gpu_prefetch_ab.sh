@@ -4,6 +4,4 @@ run() { tag=$1; shift; env "$@" timeout 300 python bench.py $F > gpurun_out/b_$t
 for rep in 1 2; do
 run off$rep PSD_PREFETCH=0
 run qr$rep PSD_PREFETCH=1
-
-run eigh$rep PSD_PREFETCH=eigh
 done
