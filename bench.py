@@ -819,8 +819,12 @@ def run_fp32_leg(a, torch, psd, pool, params, rng, dev, world, peaks):
     pool32 = [x.float() for x in pool]
     plan = psd._native.get_plan(n, params.width, dev)
     out32 = torch.empty((n, n), dtype=torch.float32, device=dev)   # no allocation in the timed loop
-    for i in range(max(a.warmup, 2)):
-        psd.ran_proj(pool32[i % len(pool32)], params, rng, dtype="fp32", out=out32)
+    # pipelined like the FP64 line (psd_plan_prefetch_f32): none across the warm-up/timed
+    # boundary and after the last timed step
+    nxt = (lambda i, last: None if a.no_prefetch or i == last else pool32[(i + 1) % len(pool32)])
+    nwarm = max(a.warmup, 2)
+    for i in range(nwarm):
+        psd.ran_proj(pool32[i % len(pool32)], params, rng, dtype="fp32", out=out32, prefetch=nxt(i, nwarm - 1))
     torch.cuda.synchronize(dev)
     plan.profile(enable=True, reset=True)
     if world > 1:
@@ -832,7 +836,8 @@ def run_fp32_leg(a, torch, psd, pool, params, rng, dev, world, peaks):
     e0.record()
     for i in range(a.steps):
         marks[i].record()
-        rep = psd.ran_proj(pool32[i % len(pool32)], params, rng, dtype="fp32", out=out32)
+        rep = psd.ran_proj(pool32[i % len(pool32)], params, rng, dtype="fp32", out=out32,
+                           prefetch=nxt(i, a.steps - 1))
         launches += rep.device_info["gpu_launches"]
     marks[a.steps].record()
     e1.record()

@@ -105,6 +105,9 @@ int psd_plan_profile(psd_plan* plan, int32_t enable, double* ms_out, int32_t* co
  * caller must not modify x_next until it has been projected.  The hint is
  * used by exactly one call (NULL clears it); FP32 / DMMA-engine calls ignore it. */
 int psd_plan_prefetch(psd_plan* plan, const double* x_next, int64_t n, int64_t ldx);
+/* The same for the FP32 path (psd_ran_proj_f32): x_next's require_symmetric pass fused with
+ * its tf32 split runs on the side stream under the current call's QR / eigensolver. */
+int psd_plan_prefetch_f32(psd_plan* plan, const float* x_next, int64_t n, int64_t ldx);
 
 /* require_symmetric — symmetric.py:39-57.  tol < 0 selects the reference
  * default 1e-10*max(1, max|x|).  stats_out (HOST, 3 doubles) receives

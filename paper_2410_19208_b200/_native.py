@@ -65,6 +65,7 @@ SIGNATURES = {
     "psd_plan_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_double_p, c_int32_p,
                                         ctypes.c_int32]),
     "psd_plan_prefetch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64]),
+    "psd_plan_prefetch_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64]),
     "psd_require_symmetric": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                              ctypes.c_int64, ctypes.c_double, c_double_p,
                                              ctypes.c_void_p]),

@@ -90,6 +90,12 @@ struct psd_plan {
   ll pf_n = 0, pf_ldx = 0;
   bool pf_ready = false;
   bool pf_failed = false;
+  // FP32 path (psd_plan_prefetch_f32): the next X's symmetry pass fused with its tf32 lo split
+  const float* hint_x32 = nullptr;
+  const float* pf_x32 = nullptr;
+  bool pf_f32 = false;              // the prefetch in flight is an FP32 one
+  float* xl_alt = nullptr;
+  bool pf32_failed = false;
   // stage profiling (psd_plan_profile): CUDA events on the caller's stream
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -596,6 +602,8 @@ int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* o
 
 int ensure_oz(psd_plan* p);
 int ensure_pipeline(psd_plan* p);
+int ensure_pipeline32(psd_plan* p);
+int ensure_f32(psd_plan* p, bool need_hi);
 
 }  // namespace
 
@@ -691,6 +699,7 @@ int psd_plan_prefetch(psd_plan* p, const double* x_next, int64_t n, int64_t ldx)
     return fail(PSD_ERR_INVALID_PARAMS, "prefetch hint outside the plan (n=%lld, ldx=%lld)", (ll)n, (ll)ldx);
   std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   p->hint_x = x_next;
+  p->hint_x32 = nullptr;
   p->hint_n = x_next ? n : 0;
   p->hint_ldx = x_next ? ldx : 0;
   if (x_next && n < 3072) p->hint_x = nullptr;   // INT8 engine only (its size rule)
@@ -699,6 +708,25 @@ int psd_plan_prefetch(psd_plan* p, const double* x_next, int64_t n, int64_t ldx)
     if (ensure_oz(p) != PSD_OK || ensure_pipeline(p) != PSD_OK) {
       cudaGetLastError();
       p->hint_x = nullptr;   // no room for a second set of planes: unpipelined calls
+    }
+  }
+  return PSD_OK;
+}
+
+int psd_plan_prefetch_f32(psd_plan* p, const float* x_next, int64_t n, int64_t ldx) {
+  if (!p) return fail(PSD_ERR_INVALID_PARAMS, "null plan");
+  if (x_next && (n < 1 || n > p->n || ldx < n))
+    return fail(PSD_ERR_INVALID_PARAMS, "prefetch hint outside the plan (n=%lld, ldx=%lld)", (ll)n, (ll)ldx);
+  std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
+  p->hint_x = nullptr;
+  p->hint_x32 = x_next;
+  p->hint_n = x_next ? n : 0;
+  p->hint_ldx = x_next ? ldx : 0;
+  if (p->hint_x32 && !p->xl_alt) {   // the call's streams and planes exist before it runs on them
+    DeviceGuard g(p->device);
+    if (ensure_f32(p, false) != PSD_OK || ensure_pipeline32(p) != PSD_OK) {
+      cudaGetLastError();
+      p->hint_x32 = nullptr;
     }
   }
   return PSD_OK;
@@ -892,24 +920,33 @@ int ensure_oz(psd_plan* p) {
 
 // Pipelining state (psd_plan_prefetch): streams, events, the mapped statistics slot and a
 // second set of X residue planes / exponents / row maxima (allocated on first use).
-int ensure_pipeline(psd_plan* p) {
-  if (p->oz_ar_alt) return PSD_OK;
-  if (p->pf_failed || !p->oz_ldk) return -1;
+// streams, events and the mapped statistics slot (shared by the FP64 and FP32 prefetch)
+bool ensure_pipe_common(psd_plan* p) {
+  if (p->work) return true;
   int least = 0, greatest = 0;
   bool ok = cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess;
-  ok = ok && cudaStreamCreateWithPriority(&p->work, cudaStreamNonBlocking, greatest) == cudaSuccess;
   ok = ok && cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, least) == cudaSuccess;
   for (cudaEvent_t* e : {&p->ev_in, &p->ev_out, &p->ev_fork, &p->ev_pf_stats, &p->ev_pf_done})
     ok = ok && cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
   ok = ok && cudaHostAlloc(reinterpret_cast<void**>(&p->pf_host), 64, cudaHostAllocMapped) == cudaSuccess;
   ok = ok && cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->pf_dev), p->pf_host, 0) == cudaSuccess;
+  if (!p->stats_alt) ok = ok && (p->stats_alt = alloc(p, 4)) != nullptr;
+  // `work` last: its existence marks the common state complete
+  ok = ok && cudaStreamCreateWithPriority(&p->work, cudaStreamNonBlocking, greatest) == cudaSuccess;
+  if (!ok) cudaGetLastError();
+  return ok;
+}
+
+int ensure_pipeline(psd_plan* p) {
+  if (p->oz_ar_alt) return PSD_OK;
+  if (p->pf_failed || !p->oz_ldk) return -1;
+  bool ok = ensure_pipe_common(p);
   if (ok) {
     const size_t planes = (size_t)psd::oz_num_moduli() * p->n * p->oz_ldk;
     p->oz_ar_alt = static_cast<int8_t*>(static_cast<void*>(alloc(p, (planes + 7) / 8)));
     p->oz_e_alt = reinterpret_cast<int*>(alloc(p, ((size_t)p->n + 1) / 2));
     p->oz_rowmax_alt = reinterpret_cast<unsigned*>(alloc(p, ((size_t)p->n + 1) / 2));
-    p->stats_alt = alloc(p, 4);
-    ok = p->oz_ar_alt && p->oz_e_alt && p->oz_rowmax_alt && p->stats_alt;
+    ok = p->oz_ar_alt && p->oz_e_alt && p->oz_rowmax_alt;
     if (ok) ok = cudaMemset(p->oz_ar_alt, 0, planes) == cudaSuccess;   // K padding stays zero
     if (ok) ok = cudaDeviceSynchronize() == cudaSuccess;
   }
@@ -920,6 +957,39 @@ int ensure_pipeline(psd_plan* p) {
     return -1;
   }
   return PSD_OK;
+}
+
+int ensure_pipeline32(psd_plan* p) {
+  if (p->xl_alt) return PSD_OK;
+  if (p->pf32_failed || !p->xl) return -1;
+  bool ok = ensure_pipe_common(p);
+  if (ok) ok = (p->xl_alt = reinterpret_cast<float*>(alloc(p, ((size_t)p->n * p->ldx32 + 1) / 2))) != nullptr;
+  if (!ok) {
+    cudaGetLastError();
+    p->pf32_failed = true;
+    p->xl_alt = nullptr;
+    return -1;
+  }
+  return PSD_OK;
+}
+
+// FP32: the next X's require_symmetric statistics fused with its tf32 lo split (X itself is
+// the hi operand) into the alternate lo plane, on the side stream.
+void launch_prefetch32(psd_plan* p, const float* x, ll n, ll ldx, cudaStream_t st) {
+  cudaEventRecord(p->ev_fork, st);
+  cudaStreamWaitEvent(p->side, p->ev_fork, 0);
+  const ll nt = (n + 63) / 64;
+  psd::symsplit_f32(x, n, ldx, p->stats_alt, nullptr, p->xl_alt, p->ldx32, p->side,
+                    std::max<ll>(1, nt * (nt + 1) / 2 / 16));
+  psd::copy_to_mapped(p->pf_dev, p->stats_alt, 3 * sizeof(double), p->side);
+  cudaEventRecord(p->ev_pf_stats, p->side);
+  cudaEventRecord(p->ev_pf_done, p->side);
+  p->pf_x = nullptr;
+  p->pf_x32 = x;
+  p->pf_f32 = true;
+  p->pf_n = n;
+  p->pf_ldx = ldx;
+  p->pf_ready = true;
 }
 
 // Enqueue the hinted next X's require_symmetric pass (statistics → mapped slot) and its
@@ -941,6 +1011,8 @@ void launch_prefetch(psd_plan* p, const double* x, ll n, ll ldx, cudaStream_t st
                            std::max<ll>(1, n / rows), pad);
   cudaEventRecord(p->ev_pf_done, p->side);
   p->pf_x = x;
+  p->pf_x32 = nullptr;
+  p->pf_f32 = false;
   p->pf_n = n;
   p->pf_ldx = ldx;
   p->pf_ready = true;
@@ -1105,9 +1177,22 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   // pipelined batch (psd_plan_prefetch): the hint names the NEXT call's X; a finished
   // prefetch of THIS call's X replaces the symmetry pass and the residue preparation
   const double* hint_x = p->hint_x;
+  const float* hint_x32 = p->hint_x32;
   const ll hint_n = p->hint_n, hint_ldx = p->hint_ldx;
   p->hint_x = nullptr;
+  p->hint_x32 = nullptr;
   bool consumed = false;
+  // FP32 X usable as the raw tf32 hi operand (ldx % 4, 16-byte aligned; see symcheck32)
+  auto raw32 = [](const float* x, ll ld) { return ld % 4 == 0 && (uintptr_t)x % 16 == 0 && !getenv("PSD_TF32_RNA"); };
+  if (p->pf_ready && p->pf_f32) {
+    if (f32 && p->pf_x32 == x32 && p->pf_n == n && p->pf_ldx == ldx && raw32(x32, ldx) && p->xl &&
+        !(flags & PSD_FLAG_SKIP_SYMCHECK)) {
+      PSD_CUDA_CHECK(cudaStreamWaitEvent(st, p->ev_pf_done, 0), "prefetch join");
+      std::swap(p->xl, p->xl_alt);
+      consumed = true;
+    }
+    p->pf_ready = false;
+  }
   if (p->pf_ready) {
     if (oz && p->pf_x == x64 && p->pf_n == n && p->pf_ldx == ldx && !(flags & PSD_FLAG_SKIP_SYMCHECK)) {
       PSD_CUDA_CHECK(cudaStreamWaitEvent(st, p->ev_pf_done, 0), "prefetch join");
@@ -1127,6 +1212,8 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   }();
   const bool prefetch_next = hint_x && oz && pf_at != 0 && hint_n >= 3072 && hint_n <= p->n &&
                              hint_ldx >= hint_n && ensure_pipeline(p) == PSD_OK;
+  const bool prefetch_next32 = hint_x32 && f32 && raw && pf_at != 0 && hint_n <= p->n && hint_ldx >= hint_n &&
+                               raw32(hint_x32, hint_ldx) && ensure_pipeline32(p) == PSD_OK;
   bool have_rowmax = false;
   // require_symmetric's verdict (and alpha_tol) — evaluated now for FP32, and for FP64 once
   // the first product is enqueued (sym_pending): the statistics travel through an
@@ -1176,7 +1263,19 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     return PSD_OK;
   };
   if (!(flags & PSD_FLAG_SKIP_SYMCHECK)) {
-    if (f32) {
+    if (f32 && consumed) {   // the verdict of the prefetched symsplit pass
+      PSD_CUDA_CHECK(cudaEventSynchronize(p->ev_pf_stats), "prefetched stats");
+      double h[3];
+      std::memcpy(h, p->pf_host, sizeof(h));
+      SymInfo si;
+      int fl = 0;
+      std::memcpy(&fl, &h[2], sizeof(int));
+      si.max_abs = h[0];
+      si.defect = h[1];
+      si.bitwise = (fl & 1) == 0;
+      si.nonfinite = (fl & 2) != 0;
+      PSD_TRY(judge(si));
+    } else if (f32) {
       SymInfo si;
       PSD_TRY(symcheck32(p, x32, n, ldx, raw, &si, st));
       PSD_TRY(judge(si));
@@ -1236,6 +1335,7 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
   QrInfo qi;
   auto start_prefetch = [&]() {
     if (prefetch_next) launch_prefetch(p, hint_x, hint_n, hint_ldx, st);
+    if (prefetch_next32) launch_prefetch32(p, hint_x32, hint_n, hint_ldx, st);
   };
   PSD_TRY(range_finder_core(p, mul, n, n, omega, ldo_eff, w, q, f32, (flags & PSD_FLAG_STRICT) != 0,
                             bufs, &qb, &wk, &qi, st, resolve_sym,
@@ -1424,12 +1524,23 @@ int psd_ran_proj_f32(psd_plan* p, const float* x, int64_t n, int64_t ldx, const 
   if (!p || !x || !omega) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
   DeviceGuard g(p->device);
   std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  cudaStream_t st = caller;
+  const bool piped = (p->hint_x32 || p->pf_ready) && p->work;   // see psd_ran_proj
+  if (piped) {
+    cudaEventRecord(p->ev_in, caller);
+    cudaStreamWaitEvent(p->work, p->ev_in, 0);
+    st = p->work;
+  }
   int status;
   {
     Stage total(p, PSD_STAGE_TOTAL, st);
     status = ran_proj_impl(p, nullptr, x, n, ldx, nullptr, omega, ldo, k, l, q, alpha, flags, nullptr,
-                           result, ldr, factors_w, ldw, factors_d, rep, stream);
+                           result, ldr, factors_w, ldw, factors_d, rep, st);
+  }
+  if (piped) {
+    cudaEventRecord(p->ev_out, st);
+    cudaStreamWaitEvent(caller, p->ev_out, 0);
   }
   if (p->prof) {
     cudaStreamSynchronize(st);

@@ -1284,7 +1284,7 @@ int gemm_tf32x3(const Tc32Op& op, cudaStream_t st) {
 }
 
 void symsplit_f32(const float* x, long long n, long long ldx, double* stats, float* hi, float* lo,
-                  long long ldh, cudaStream_t st) {
+                  long long ldh, cudaStream_t st, long long grid) {
   cudaMemsetAsync(stats, 0, 3 * sizeof(double), st);
   const long long nt = (n + tc32::kSST - 1) / tc32::kSST;
   const long long npairs = nt * (nt + 1) / 2;
@@ -1292,7 +1292,7 @@ void symsplit_f32(const float* x, long long n, long long ldx, double* stats, flo
     const char* e = getenv("PSD_SYMSPLIT_BPS");
     return e ? std::max(1, atoi(e)) : 8;
   }();
-  const long long blocks = std::min<long long>(npairs, (long long)device_info().sms * per_sm);
+  const long long blocks = std::min<long long>(npairs, grid > 0 ? grid : (long long)device_info().sms * per_sm);
   const bool vec = hi == nullptr && n % 4 == 0 && ldx % 4 == 0 && ldh % 4 == 0 &&
                    (uintptr_t)x % 16 == 0 && (uintptr_t)lo % 16 == 0;
   if (vec)

@@ -129,7 +129,7 @@ long long tc32_ws_elems(long long M, int N, int max_splits);
 // require_symmetric statistics of a square fp32 X (as sym_stats) fused with its tf32 hi/lo split;
 // hi == nullptr (also for split_rows_f32): raw mode, X itself serves as hi, only lo is written.
 void symsplit_f32(const float* x, long long n, long long ldx, double* stats, float* hi, float* lo,
-                  long long ldh, cudaStream_t st);
+                  long long ldh, cudaStream_t st, long long grid = 0);
 void split_rows_f32(const float* x, long long rows, long long cols, long long ldx, float* hi,
                     float* lo, long long ldh, long long cols_pad, cudaStream_t st);
 void split_rows_f64(const double* x, long long rows, int cols, long long ldx, const double* scale,

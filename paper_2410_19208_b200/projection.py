@@ -126,10 +126,10 @@ def _prefetch_hint(lib, plan, prefetch, n, op):
     call's CholeskyQR / eigensolver run).  FP64 n×n contiguous CUDA tensors only; anything
     else clears the hint."""
     ok = (isinstance(prefetch, torch.Tensor) and prefetch.is_cuda and prefetch.device == op.device
-          and prefetch.dtype == torch.float64 and op.t.dtype == torch.float64
-          and tuple(prefetch.shape) == (n, n) and prefetch.stride(1) == 1)
-    _native.check(lib.psd_plan_prefetch(plan.handle, _native.ptr(prefetch) if ok else None, n,
-                                        prefetch.stride(0) if ok else n))
+          and prefetch.dtype == op.t.dtype and tuple(prefetch.shape) == (n, n) and prefetch.stride(1) == 1)
+    entry = lib.psd_plan_prefetch_f32 if op.t.dtype == torch.float32 else lib.psd_plan_prefetch
+    _native.check(entry(plan.handle, _native.ptr(prefetch) if ok else None, n,
+                        prefetch.stride(0) if ok else n))
     plan.prefetch_ref = prefetch if ok else None   # keep the tensor alive until it is consumed
 
 

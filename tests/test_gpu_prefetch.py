@@ -121,3 +121,26 @@ def test_first_call_of_a_fresh_plan_can_be_hinted(psd):
     base = [psd.ran_proj(x, params, None, omega=o) for x, o in zip(xs, oms)]
     for b, p in zip(base, piped):
         assert torch.equal(p.result, b.result)
+
+
+def test_fp32_prefetch_bitwise_identical(psd):
+    xs, oms = _mats(3, seed=60), _omegas(3)
+    xs = [x.float().contiguous() for x in xs]
+    oms = [o.float() for o in oms]
+    params = psd.RangeParams(k=K, l=L, q=Q)
+    base = [psd.ran_proj(x, params, None, omega=o, dtype="fp32").result for x, o in zip(xs, oms)]
+    piped = [psd.ran_proj(x, params, None, omega=o, dtype="fp32", prefetch=xs[i + 1] if i < 2 else None).result
+             for i, (x, o) in enumerate(zip(xs, oms))]
+    for b, p in zip(base, piped):
+        assert p.dtype == torch.float32 and torch.equal(p, b)
+
+
+def test_fp32_prefetched_verdict_raises(psd):
+    xs, oms = _mats(2, seed=70), _omegas(2)
+    xs = [x.float().contiguous() for x in xs]
+    bad = xs[1].clone()
+    bad[4, 11] += 1e-2 * bad.abs().max()
+    params = psd.RangeParams(k=K, l=L, q=Q)
+    psd.ran_proj(xs[0], params, None, omega=oms[0].float(), dtype="fp32", prefetch=bad)
+    with pytest.raises(psd.AsymmetricMatrixError):
+        psd.ran_proj(bad, params, None, omega=oms[1].float(), dtype="fp32")
