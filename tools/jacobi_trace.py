@@ -15,3 +15,13 @@ print("round period us median", np.median(per), "solve work (ready->done) med", 
 # hop latencies: solve ready vs max of A done previous round
 hopAS=t[1:,S,1].min(1)-t[:-1,A,2].max(1); hopSA=t[:,A,1].max(1)-t[:,S,2].max(1)
 print("hop A(R-1)done->S(R)ready med", np.median(hopAS), " S(R)done->A(R)ready(max) med", np.median(hopSA))
+# critical path per solve task: what it waited on (readiness vs the previous round's solves / A-items / V-items)
+sdone_prev = t[:-1, S, 2].max(1)            # last solve of round R-1 done
+sready = t[1:, S, 1]                         # each solve of round R ready
+astart = t[1:, S, 0]
+print("solve R: start-after-prev-solve-done med", np.median(astart.min(1) - sdone_prev),
+      " ready-after-prev-solves-done med", np.median(sready.max(1) - sdone_prev),
+      " ready spread med", np.median(sready.max(1) - sready.min(1)))
+vdone_prev2 = t[:-2, V, 2].max(1); adone_prev2 = t[:-2, A, 2].max(1)
+print("V(R-2) done - S(R) ready med", np.median(vdone_prev2 - t[2:, S, 1].max(1)),
+      " A(R-2) done - S(R) ready med", np.median(adone_prev2 - t[2:, S, 1].max(1)))
