@@ -1001,14 +1001,12 @@ void launch_prefetch(psd_plan* p, const double* x, ll n, ll ldx, cudaStream_t st
   cudaStreamWaitEvent(p->side, p->ev_fork, 0);
   static const int pairs = [] { const char* e = getenv("PSD_PF_PAIRS"); return e ? std::max(1, atoi(e)) : 16; }();
   static const int rows = [] { const char* e = getenv("PSD_PF_ROWS"); return e ? std::max(1, atoi(e)) : 2; }();
-  static const int pad = [] { const char* e = getenv("PSD_PF_SMEM"); return e ? atoi(e) : 0; }();
   const ll nt = (n + 63) / 64;
-  psd::sym_stats(x, n, ldx, p->stats_alt, p->side, p->oz_rowmax_alt, std::max<ll>(1, nt * (nt + 1) / 2 / pairs),
-                 pad > 36 * 1024 ? pad - 36 * 1024 : 0);
+  psd::sym_stats(x, n, ldx, p->stats_alt, p->side, p->oz_rowmax_alt, std::max<ll>(1, nt * (nt + 1) / 2 / pairs));
   psd::copy_to_mapped(p->pf_dev, p->stats_alt, 3 * sizeof(double), p->side);
   cudaEventRecord(p->ev_pf_stats, p->side);
   psd::oz_prepare_rows_max(x, n, n, ldx, p->oz_rowmax_alt, p->oz_e_alt, p->oz_ar_alt, p->oz_ldk, p->side,
-                           std::max<ll>(1, n / rows), pad);
+                           std::max<ll>(1, n / rows));
   cudaEventRecord(p->ev_pf_done, p->side);
   p->pf_x = x;
   p->pf_x32 = nullptr;

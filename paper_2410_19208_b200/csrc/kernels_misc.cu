@@ -149,19 +149,14 @@ __global__ void __launch_bounds__(256, PSD_SYM_MINB) sym_stats_kernel(const T* _
 
 template <typename T>
 static void sym_stats_t(const T* x, long long n, long long ldx, double* stats, unsigned* rowmax,
-                        cudaStream_t st, long long grid = 0, int pad_smem = 0) {
+                        cudaStream_t st, long long grid = 0) {
   cudaMemsetAsync(stats, 0, 3 * sizeof(double), st);
   if (rowmax) cudaMemsetAsync(rowmax, 0, (size_t)n * sizeof(unsigned), st);
   const long long nt = (n + kSymT - 1) / kSymT;
   const long long npairs = nt * (nt + 1) / 2;
   const long long blocks = std::min<long long>(npairs, grid > 0 ? grid : (long long)device_info().sms * PSD_SYM_MINB * 2);
   static const int diag = [] { const char* e = getenv("PSD_SYM_ORDER"); return e && e[0] == 'd' ? 1 : 0; }();
-  static int pad_set = 0;
-  if (pad_smem > pad_set) {
-    cudaFuncSetAttribute(sym_stats_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad_smem);
-    pad_set = pad_smem;
-  }
-  sym_stats_kernel<T><<<(unsigned)blocks, 256, pad_smem, st>>>(x, n, ldx, npairs, stats, rowmax, diag);
+  sym_stats_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, npairs, stats, rowmax, diag);
   count_launch();
 }
 // Off-diagonal block pair of a row-sharded X (SURVEY §8(e) symmetry check):
@@ -264,8 +259,8 @@ void identity_defect(const double* g, int w, long long ldg, double* out, cudaStr
 }
 
 void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st,
-               unsigned* rowmax, long long grid, int pad_smem) {
-  sym_stats_t(x, n, ldx, stats, rowmax, st, grid, pad_smem);
+               unsigned* rowmax, long long grid) {
+  sym_stats_t(x, n, ldx, stats, rowmax, st, grid);
 }
 void sym_stats_f32(const float* x, long long n, long long ldx, double* stats, cudaStream_t st) {
   sym_stats_t(x, n, ldx, stats, static_cast<unsigned*>(nullptr), st);

@@ -108,7 +108,7 @@ long long oz_max_k();   // largest K the exact CRT reconstruction admits (2^18)
 // low-priority side stream that must yield SMs to the caller's stream — the pipelined prefetch)
 void oz_prepare_rows_max(const double* x, long long rows, long long cols, long long ldx,
                          const unsigned* rowmax_hi, int* e, int8_t* r, long long ldr, cudaStream_t st,
-                         long long grid = 0, int pad_smem = 0);
+                         long long grid = 0);
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
                      long long ldr, cudaStream_t st);
 int oz_gemm(const OzOp& op, cudaStream_t st);
@@ -143,7 +143,7 @@ void split_transpose(const double* P, long long n, int w, long long ldp, float* 
 void pair_defect(const double* a, long long lda, const double* b, long long ldb, long long rows,
                  long long cols, double* stats, bool reset, cudaStream_t st);
 void sym_stats(const double* x, long long n, long long ldx, double* stats, cudaStream_t st,
-               unsigned* rowmax = nullptr, long long grid = 0, int pad_smem = 0);
+               unsigned* rowmax = nullptr, long long grid = 0);
 // out[0] = max |G − I| over a w×w Gram (single block)
 void identity_defect(const double* g, int w, long long ldg, double* out, cudaStream_t st);
 void sym_stats_f32(const float* x, long long n, long long ldx, double* stats, cudaStream_t st);

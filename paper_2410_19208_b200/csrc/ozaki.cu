@@ -897,18 +897,11 @@ long long oz_max_k() { return oz::kMaxK; }
 
 void oz_prepare_rows_max(const double* x, long long rows, long long cols, long long ldx,
                          const unsigned* rowmax, int* e, int8_t* r, long long ldr, cudaStream_t st,
-                         long long grid_req, int pad_smem) {
+                         long long grid_req) {
   ensure_oz_constants();
   if (cols % 8 == 0 && ldx % 2 == 0 && ldr % 8 == 0 && (uintptr_t)x % 16 == 0) {
     const unsigned grid = (unsigned)std::min<long long>(rows, grid_req > 0 ? grid_req : (long long)device_info().sms * 8);
-    // pad_smem: unused dynamic shared memory that caps the CTAs resident per SM (a side-stream
-    // launch leaving room for the caller's kernels)
-    static int pad_set = 0;
-    if (pad_smem > pad_set) {
-      cudaFuncSetAttribute(oz::residues_rows_max_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pad_smem);
-      pad_set = pad_smem;
-    }
-    oz::residues_rows_max_kernel<<<grid, 256, pad_smem, st>>>(x, rows, cols, ldx, rowmax, e, r, ldr, ldr * rows);
+    oz::residues_rows_max_kernel<<<grid, 256, 0, st>>>(x, rows, cols, ldx, rowmax, e, r, ldr, ldr * rows);
     count_launch();
   } else {
     oz_prepare_rows(x, rows, cols, ldx, e, r, ldr, st);
