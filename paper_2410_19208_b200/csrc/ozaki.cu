@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(256) crt_kernel(const uint8_t* __restrict__ re
 template <int L>
 __host__ __device__ constexpr uint32_t kwt() { return (uint32_t)((134217728.0 / mod_at(L)) + 0.5); }   // ⌊2^27/m⌉
 
-__global__ void __launch_bounds__(256) crt1_kernel(const uint8_t* __restrict__ res, long long M, int N, long long ldo,
+__global__ void __launch_bounds__(256, 3) crt1_kernel(const uint8_t* __restrict__ res, long long M, int N, long long ldo,
                                                    const int* __restrict__ e, const int* __restrict__ f,
                                                    double* __restrict__ C, long long ldc, double alpha,
                                                    const double* __restrict__ S, long long lds) {
