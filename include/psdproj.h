@@ -125,6 +125,12 @@ int psd_power_iteration(psd_plan* plan, const double* x, int64_t n, int64_t ldx,
 int psd_min_eig_magnitude(psd_plan* plan, const double* x, int64_t n, int64_t ldx,
                           const double* v1, const double* v2, int32_t n_iter, double* result,
                           void* stream);
+/* The same with flags: PSD_FLAG_ASSUME_SYMMETRIC (the caller verified X bitwise symmetric, as
+ * project() does with require_symmetric first, projection.py:189) lets every product read only
+ * X's lower triangle (n % 64 == 0): half the HBM bytes of the 2(N+1) passes. */
+int psd_min_eig_magnitude_ex(psd_plan* plan, const double* x, int64_t n, int64_t ldx,
+                             const double* v1, const double* v2, int32_t n_iter, uint32_t flags,
+                             double* result, void* stream);
 
 /* range_finder — sketch.py:53-93: basis (m x width, ld ldb) of the range of
  * (X X^T)^q X Omega for an m x n X, Omega = omega (n x width, ld ldo).  alpha > 0 sketches

@@ -39,6 +39,9 @@ struct psd_plan {
   size_t jws_elems = 0;
   double *gy = nullptr, *gv = nullptr, *gpart = nullptr, *stats = nullptr, *scal = nullptr;
   double* qrstat = nullptr;
+  double* symv_ws = nullptr;   // tile partials of the symmetric GEMV (power iteration on a bitwise-symmetric X)
+  size_t symv_elems = 0;
+  bool symv_failed = false;
   double* dinv = nullptr;  // ceil(w/32) diagonal-block inverses (32×32) for chol_fast
   double *L1 = nullptr, *Rinv1 = nullptr, *dinv1 = nullptr;   // shifted CholeskyQR candidate
   bool oz_gram = false;   // CholeskyQR Grams on the INT8 engine (set per call by psd_ran_proj)
@@ -754,18 +757,35 @@ int psd_require_symmetric(psd_plan* p, const double* x, int64_t n, int64_t ldx, 
   return PSD_OK;
 }
 
+// sym: X is bitwise symmetric (caller-checked) — the products read only its lower triangle
+// (psd::symv_shift, half the HBM bytes) when the shape allows, else the row GEMV
 static int power_iteration_impl(psd_plan* p, const double* x, ll n, ll ldx, double shift,
-                                const double* v0, int n_iter, double* result, cudaStream_t st) {
+                                const double* v0, int n_iter, double* result, cudaStream_t st,
+                                bool sym = false) {
   const double floor = 2.2250738585072014e-308 * (double)n;  // finfo.tiny·n (sketch.py:107)
   int* flag = p->ints + p->w + 2;
   PSD_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int), st), "flag");
+  if (sym && psd::symv_ok(x, n, ldx, v0) && !p->symv_failed && p->symv_elems < psd::symv_ws_elems(n)) {
+    p->symv_ws = alloc(p, psd::symv_ws_elems(p->n));   // once per plan (the old block is kept, small)
+    if (p->symv_ws) {
+      p->symv_elems = psd::symv_ws_elems(p->n);
+    } else {
+      cudaGetLastError();
+      p->symv_failed = true;
+    }
+  }
+  const bool use_symv = sym && psd::symv_ok(x, n, ldx, v0) && p->symv_elems >= psd::symv_ws_elems(n);
+  auto product = [&](const double* v) {
+    return use_symv ? psd::symv_shift(x, n, ldx, v, shift, p->gy, p->gpart, p->symv_ws, st)
+                    : psd::gemv_shift(x, n, ldx, v, shift, p->gy, p->gpart, st);
+  };
   const double* v = v0;
   for (int it = 0; it < n_iter; ++it) {
-    const int nb = psd::gemv_shift(x, n, ldx, v, shift, p->gy, p->gpart, st);
+    const int nb = product(v);
     psd::normalize(p->gy, p->gpart, nb, n, floor, p->gv, p->scal, flag, st);
     v = p->gv;
   }
-  const int nb = psd::gemv_shift(x, n, ldx, v, shift, p->gy, p->gpart, st);
+  const int nb = product(v);
   psd::sum_partials(p->gpart, nb, p->scal + 1, 1, st);
   double h[2];
   int hflag = 0;
@@ -789,15 +809,21 @@ int psd_power_iteration(psd_plan* p, const double* x, int64_t n, int64_t ldx, do
 
 int psd_min_eig_magnitude(psd_plan* p, const double* x, int64_t n, int64_t ldx, const double* v1,
                           const double* v2, int32_t n_iter, double* result, void* stream) {
+  return psd_min_eig_magnitude_ex(p, x, n, ldx, v1, v2, n_iter, 0u, result, stream);
+}
+
+int psd_min_eig_magnitude_ex(psd_plan* p, const double* x, int64_t n, int64_t ldx, const double* v1,
+                             const double* v2, int32_t n_iter, uint32_t flags, double* result, void* stream) {
   if (!p || !x || !v1 || !v2 || !result) return fail(PSD_ERR_INVALID_PARAMS, "null argument");
   if (n_iter < 1) return fail(PSD_ERR_INVALID_PARAMS, "power iteration needs n_iter >= 1, got %d", n_iter);
   if (n < 1 || n > p->n) return fail(PSD_ERR_INVALID_PARAMS, "n=%lld outside plan", (ll)n);
   DeviceGuard g(p->device);
   std::lock_guard<std::recursive_mutex> dev_lock(device_mutex(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool sym = (flags & PSD_FLAG_ASSUME_SYMMETRIC) != 0;
   double s1 = 0.0, s2 = 0.0;
-  PSD_TRY(power_iteration_impl(p, x, n, ldx, 0.0, v1, n_iter, &s1, st));   // sketch.py:126
-  PSD_TRY(power_iteration_impl(p, x, n, ldx, s1, v2, n_iter, &s2, st));    // sketch.py:127-128
+  PSD_TRY(power_iteration_impl(p, x, n, ldx, 0.0, v1, n_iter, &s1, st, sym));   // sketch.py:126
+  PSD_TRY(power_iteration_impl(p, x, n, ldx, s1, v2, n_iter, &s2, st, sym));    // sketch.py:127-128
   *result = std::fabs(s1 - s2);
   return PSD_OK;
 }

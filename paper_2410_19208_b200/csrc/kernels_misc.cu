@@ -486,6 +486,108 @@ int gemv_shift(const double* x, long long n, long long ldx, const double* v, dou
   return blocks;
 }
 
+// a8 for a BITWISE-symmetric X: y = (X − σI)v reading only the lower triangle of 64×64
+// tiles (half the HBM bytes of the row GEMV).  Pass 1: each lower tile (I, J) yields its row
+// sums X_IJ·v_J and, off the diagonal, its column sums X_IJᵀ·v_I (= the (J, I) tile's row
+// sums), stored per tile; pass 2 adds them per row in a fixed order (deterministic) and
+// writes y and per-block Σy² like the GEMV.  n % 64 == 0, 16-byte rows.
+constexpr int kSymvT = 64;
+
+__global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restrict__ x, long long ldx,
+                                                         const double* __restrict__ v, long long ntri,
+                                                         double* __restrict__ pr, double* __restrict__ pc) {
+  __shared__ double cs[8][kSymvT];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (long long t = blockIdx.x; t < ntri; t += gridDim.x) {
+    long long I = (long long)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    while (I * (I + 1) / 2 > t) --I;
+    const long long J = t - I * (I + 1) / 2;
+    const long long r0 = I * kSymvT + warp * 8, c0 = J * kSymvT + 2 * lane;
+    const double2 vc = *reinterpret_cast<const double2*>(v + c0);
+    const bool off = I != J;
+    double acc[8], ca0 = 0.0, ca1 = 0.0;
+    double2 xx[8];
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) xx[rr] = __ldcs(reinterpret_cast<const double2*>(x + (r0 + rr) * ldx + c0));
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) {
+      acc[rr] = fma(xx[rr].x, vc.x, xx[rr].y * vc.y);
+      if (off) {
+        const double vr = v[r0 + rr];
+        ca0 = fma(xx[rr].x, vr, ca0);
+        ca1 = fma(xx[rr].y, vr, ca1);
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) {
+      const double s = warp_sum(acc[rr]);
+      if (lane == 0) pr[t * kSymvT + warp * 8 + rr] = s;
+    }
+    if (off) {
+      cs[warp][2 * lane] = ca0;
+      cs[warp][2 * lane + 1] = ca1;
+    }
+    __syncthreads();
+    if (off && threadIdx.x < kSymvT) {
+      double c = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) c += cs[w][threadIdx.x];
+      pc[t * kSymvT + threadIdx.x] = c;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) symv_reduce_kernel(const double* __restrict__ pr, const double* __restrict__ pc,
+                                                          long long nt, long long n, const double* __restrict__ v,
+                                                          double shift, double* __restrict__ y,
+                                                          double* __restrict__ partials) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double sq = 0.0;
+  if (i < n) {
+    const long long K = i / kSymvT, o = i % kSymvT;
+    double s = 0.0;
+    for (long long J = 0; J <= K; ++J) s += pr[(K * (K + 1) / 2 + J) * kSymvT + o];    // row sums of (K, J)
+    for (long long I = K + 1; I < nt; ++I) s += pc[(I * (I + 1) / 2 + K) * kSymvT + o];   // columns of (I, K)
+    s -= shift * v[i];
+    y[i] = s;
+    sq = s * s;
+  }
+  sq = warp_sum(sq);
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += red[w];
+    partials[blockIdx.x] = tot;
+  }
+}
+
+size_t symv_ws_elems(long long n) {
+  const long long nt = n / kSymvT;
+  return (size_t)nt * (nt + 1) / 2 * kSymvT * 2;
+}
+
+bool symv_ok(const double* x, long long n, long long ldx, const double* v) {
+  return n % kSymvT == 0 && n >= kSymvT && ldx % 2 == 0 && (uintptr_t)x % 16 == 0 && (uintptr_t)v % 16 == 0;
+}
+
+int symv_shift(const double* x, long long n, long long ldx, const double* v, double shift, double* y,
+               double* partials, double* ws, cudaStream_t st) {
+  const long long nt = n / kSymvT, ntri = nt * (nt + 1) / 2;
+  double* pr = ws;
+  double* pc = ws + ntri * kSymvT;
+  const long long blocks = std::min<long long>(ntri, (long long)device_info().sms * 8);
+  symv_tiles_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, ldx, v, ntri, pr, pc);
+  const int rb = (int)((n + 255) / 256);
+  symv_reduce_kernel<<<rb, 256, 0, st>>>(pr, pc, nt, n, v, shift, y, partials);
+  count_launch(2);
+  return rb;
+}
+
 __global__ void normalize_kernel(const double* __restrict__ y, const double* __restrict__ partials,
                                  int nparts, long long n, double floor, double* __restrict__ v,
                                  double* out, int* flag) {

@@ -160,6 +160,12 @@ void sym_gaussian_rows(double* out, long long ldo, long long r0, long long rows,
 int gemv_shift(const double* x, long long n, long long ldx, const double* v, double shift,
                double* y, double* partials, cudaStream_t st);
 int gemv_blocks(long long n);
+// the same product for a BITWISE-symmetric X from its lower triangle (n % 64 == 0, see symv_ok);
+// ws ≥ symv_ws_elems(n) doubles; returns the partials count (≤ gemv_blocks(n))
+bool symv_ok(const double* x, long long n, long long ldx, const double* v);
+size_t symv_ws_elems(long long n);
+int symv_shift(const double* x, long long n, long long ldx, const double* v, double shift, double* y,
+               double* partials, double* ws, cudaStream_t st);
 // nrm = sqrt(Σ partials); if nrm ≤ floor set *flag; v = y / nrm. out[0] = nrm.
 void normalize(const double* y, const double* partials, int nparts, long long n, double floor,
                double* v, double* out, int* flag, cudaStream_t st);

@@ -292,7 +292,10 @@ def project(x, cfg, rng=None, *, omega=None, assume_symmetric=False):
     elif op.t.dtype == torch.float32:  # α estimate on the fp32 values, in FP64
         alpha = min_eig_magnitude_device(type(op)(op.t.double(), op.kind, op.device), cfg.power_N, rng)
     else:
-        alpha = min_eig_magnitude_device(op, cfg.power_N, rng)   # projection.py:206
+        # require_symmetric first, as the reference does (projection.py:189); a bitwise-symmetric
+        # X lets the 2(N+1) products of the estimate read only its lower triangle
+        bitwise = check_symmetric_device(op).bitwise if validate else True
+        alpha = min_eig_magnitude_device(op, cfg.power_N, rng, bitwise_symmetric=bitwise)   # :206
     alpha *= cfg.scale_factor
     try:
         report = _ran_proj_scal_op(op, cfg.params, alpha, rng, cfg.collect_diagnostics,

@@ -101,15 +101,23 @@ def power_iteration(x, n_iter, rng, *, v0=None):
     return _power_iteration_device(op, n_iter, v)
 
 
-def min_eig_magnitude_device(op, n_iter, rng, v1=None, v2=None):
+def min_eig_magnitude_device(op, n_iter, rng, v1=None, v2=None, bitwise_symmetric=False):
+    """``bitwise_symmetric``: the caller verified X == Xᵀ exactly (project() runs
+    require_symmetric first, projection.py:189), so the 2(N+1) products read only X's lower
+    triangle (psd_min_eig_magnitude_ex, half the HBM traffic)."""
     n = require_square(op)
     if n_iter < 1:
         raise errors.error("InvalidParams", f"power iteration needs n_iter >= 1, got {n_iter}")
     a = as_device(v1, op.device).t if v1 is not None else draw_gaussian(rng, n, op.device)
-    s1 = _power_iteration_device(op, n_iter, a)                       # sketch.py:126
     b = as_device(v2, op.device).t if v2 is not None else draw_gaussian(rng, n, op.device)
-    s2 = _power_iteration_device(op, n_iter, b, shift=s1)             # sketch.py:127-128
-    return abs(s1 - s2)
+    lib = _native.load_library()
+    plan = _native.get_plan(n, 1, op.device)
+    res = ctypes.c_double(0.0)
+    flags = _native.FLAG_ASSUME_SYMMETRIC if bitwise_symmetric else 0
+    _native.check(lib.psd_min_eig_magnitude_ex(plan.handle, _native.ptr(op.t), n, n, _native.ptr(a),
+                                               _native.ptr(b), int(n_iter), flags, ctypes.byref(res),
+                                               _native.stream_handle(op.device)))   # sketch.py:126-129
+    return res.value
 
 
 def min_eig_magnitude(x, n_iter, rng, *, v1=None, v2=None):

@@ -168,3 +168,25 @@ def test_mirrored_syrk_deterministic_tma_path():
     assert float((ref - exact).abs().max() / exact.abs().max()) < 1e-13
     for _ in range(30):
         assert torch.equal(recon(), ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [256, 4096])
+def test_symmetric_alpha_estimate_matches_row_gemv(n):
+    """min_eig_magnitude (Alg. 5, sketch.py:117-129) with the lower-triangle products of a
+    bitwise-symmetric X (psd_min_eig_magnitude_ex) against the row-GEMV chains on the same
+    start vectors, and against the CPU oracle."""
+    import torch
+    import paper_2410_19208_b200 as psd
+    from paper_2410_19208_b200._tensors import as_device
+    from paper_2410_19208_b200.sketch import min_eig_magnitude_device
+    from oracle import psd_oracle as orc
+    x = orc.wigner(n, seed=7) + 0.3 * np.eye(n)
+    g = np.random.default_rng(3)
+    v1, v2 = g.standard_normal(n), g.standard_normal(n)
+    op = as_device(torch.from_numpy(x).cuda())
+    a = min_eig_magnitude_device(op, 10, None, v1=v1, v2=v2, bitwise_symmetric=True)
+    b = min_eig_magnitude_device(op, 10, None, v1=v1, v2=v2, bitwise_symmetric=False)
+    ref = orc.min_eig_magnitude(x, 10, v1=v1, v2=v2)
+    assert abs(a - b) <= 1e-12 * max(1.0, abs(b))
+    assert abs(a - ref) <= 1e-10 * max(1.0, abs(ref))
