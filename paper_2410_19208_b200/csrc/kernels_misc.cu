@@ -539,31 +539,41 @@ __global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restric
   }
 }
 
+// one block per 64-row tile K: thread (q, o) adds every 4th of the row's nt partials — the
+// (K, J) row sums for J ≤ K, then the (I, K) column sums for I > K — in a fixed order, and
+// the four quarters are added in a fixed order (deterministic, independent loads in flight)
 __global__ void __launch_bounds__(256) symv_reduce_kernel(const double* __restrict__ pr, const double* __restrict__ pc,
                                                           long long nt, long long n, const double* __restrict__ v,
                                                           double shift, double* __restrict__ y,
                                                           double* __restrict__ partials) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double qs[4][kSymvT];
+  const long long K = blockIdx.x;
+  const int q = threadIdx.x >> 6, o = threadIdx.x & 63;
+  double s0 = 0.0, s1 = 0.0;
+  long long e = q;
+#pragma unroll 4
+  for (; e + 4 < nt; e += 8) {
+    const long long e2 = e + 4;
+    const double a = e <= K ? pr[(K * (K + 1) / 2 + e) * kSymvT + o] : pc[(e * (e + 1) / 2 + K) * kSymvT + o];
+    const double b = e2 <= K ? pr[(K * (K + 1) / 2 + e2) * kSymvT + o] : pc[(e2 * (e2 + 1) / 2 + K) * kSymvT + o];
+    s0 += a;
+    s1 += b;
+  }
+  if (e < nt) s0 += e <= K ? pr[(K * (K + 1) / 2 + e) * kSymvT + o] : pc[(e * (e + 1) / 2 + K) * kSymvT + o];
+  qs[q][o] = s0 + s1;
+  __syncthreads();
   double sq = 0.0;
-  if (i < n) {
-    const long long K = i / kSymvT, o = i % kSymvT;
-    double s = 0.0;
-    for (long long J = 0; J <= K; ++J) s += pr[(K * (K + 1) / 2 + J) * kSymvT + o];    // row sums of (K, J)
-    for (long long I = K + 1; I < nt; ++I) s += pc[(I * (I + 1) / 2 + K) * kSymvT + o];   // columns of (I, K)
-    s -= shift * v[i];
-    y[i] = s;
-    sq = s * s;
+  if (threadIdx.x < kSymvT) {
+    const long long i = K * kSymvT + threadIdx.x;
+    const double yi = ((qs[0][threadIdx.x] + qs[1][threadIdx.x]) + (qs[2][threadIdx.x] + qs[3][threadIdx.x])) -
+                      shift * v[i];
+    y[i] = yi;
+    sq = yi * yi;
   }
   sq = warp_sum(sq);
-  __shared__ double red[8];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  if (threadIdx.x == 0) partials[blockIdx.x] = sq;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double tot = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) tot += red[w];
-    partials[blockIdx.x] = tot;
-  }
+  if (threadIdx.x == 32) partials[blockIdx.x] += sq;   // the second warp of the 64 rows
 }
 
 size_t symv_ws_elems(long long n) {
@@ -582,7 +592,7 @@ int symv_shift(const double* x, long long n, long long ldx, const double* v, dou
   double* pc = ws + ntri * kSymvT;
   const long long blocks = std::min<long long>(ntri, (long long)device_info().sms * 8);
   symv_tiles_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, ldx, v, ntri, pr, pc);
-  const int rb = (int)((n + 255) / 256);
+  const int rb = (int)nt;
   symv_reduce_kernel<<<rb, 256, 0, st>>>(pr, pc, nt, n, v, shift, y, partials);
   count_launch(2);
   return rb;
