@@ -42,6 +42,7 @@ struct psd_plan {
   double* symv_ws = nullptr;   // tile partials of the symmetric GEMV (power iteration on a bitwise-symmetric X)
   size_t symv_elems = 0;
   bool symv_failed = false;
+  bool span_host = false;   // power-step QRs on the host-driven loop (set while redoing a call)
   double* dinv = nullptr;  // ceil(w/32) diagonal-block inverses (32×32) for chol_fast
   double *L1 = nullptr, *Rinv1 = nullptr, *dinv1 = nullptr;   // shifted CholeskyQR candidate
   bool oz_gram = false;   // CholeskyQR Grams on the INT8 engine (set per call by psd_ran_proj)
@@ -411,13 +412,37 @@ __global__ void clip_values_kernel(const double* vals, int m, double offset, dou
   if (i < m) out[i] = (vals[i] - offset) * scale;
 }
 
+constexpr int kSpanRedo = -100;   // internal: redo the range finder with host-decided power-step QRs
+
 struct QrInfo {
   int passes = 0;
   int shifted = 0;
   double frob = 0.0;  // ‖Y‖_F of the input panel
   bool zero = false;  // Y == 0
   std::vector<double> rdiag;   // |R_ii| when read together with the last status (no extra round trip)
+  int span_redo = 0;           // a device-decided power-step QR missed its one-pass acceptance
 };
+
+// Power-step (span-only) CholeskyQR without a host round trip: the candidate choice of the
+// host loop below (shift iff Cholesky breakdown or κ-estimate > 3e6) made on the device, and
+// a flag raised when the pass would not have been accepted there (shifted, κ-estimate > 1e4,
+// zero or non-finite Gram); the final QR reads the flag with its status, and a raised flag
+// makes the caller redo the range finder with the host-driven loop.
+__global__ void qr_select_kernel(const double* __restrict__ stat, double* __restrict__ rinv,
+                                 const double* __restrict__ rinv1, long long elems, int* redo) {
+  __shared__ int shift_s;
+  if (threadIdx.x == 0) {
+    const double info = stat[0], trace = stat[1], mn = stat[2], mx = stat[3];
+    const bool bad = info != 0.0 || !isfinite(mn) || !isfinite(mx);
+    const double kest = mn > 0.0 ? mx / mn : INFINITY;
+    const bool shift = bad || kest > 3e6;
+    shift_s = shift ? 1 : 0;
+    if (shift || kest > 1e4 || !(trace > 0.0) || !isfinite(trace) || stat[8] != 0.0) atomicOr(redo, 1);
+  }
+  __syncthreads();
+  if (shift_s)
+    for (long long e = threadIdx.x; e < elems; e += blockDim.x) rinv[e] = rinv1[e];
+}
 
 // CholeskyQR2 with shifted passes (shifted CholeskyQR3 when ill-conditioned).
 // Orthonormalises the n×w panel in `bufs[cur]`; `bufs[tmp]` is scratch.
@@ -429,9 +454,23 @@ struct QrInfo {
 // result depends on the span alone — so one unshifted pass with κ²u ≲ 1e-12
 // is accepted instead of two.
 int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rdiag, int* qidx,
-           QrInfo* info, cudaStream_t st, bool span_only = false) {
+           QrInfo* info, cudaStream_t st, bool span_only = false, bool device_decided = false) {
   Stage mark(p, PSD_STAGE_QR, st);
   const ll ld = p->ldp;
+  const double u0 = 1.1102230246251565e-16;
+  if (span_only && device_decided) {   // one pass, candidate chosen on the device (see qr_select_kernel)
+    PSD_TRY(panel_tn(p, bufs[cur], bufs[cur], ld, n, w, p->G, true, st));
+    const double sfac = 11.0 * ((double)n * w + (double)w * (w + 1)) * u0;
+    if (psd::chol_fast(p->G, w, w, 0.0, p->L, w, p->Rinv, w, p->dinv, p->qrstat, st, sfac, p->L1,
+                       p->Rinv1, p->dinv1, p->qrstat + 8) != 0)
+      return fail(PSD_ERR_INVALID_PARAMS, "width %d too large for the CholeskyQR kernel", w);
+    qr_select_kernel<<<1, 1024, 0, st>>>(p->qrstat, p->Rinv, p->Rinv1, (long long)w * w, p->ints + p->w + 4);
+    launched(1);
+    PSD_TRY(panel_nn(p, bufs[cur], ld, p->Rinv, w, bufs[tmp], ld, n, w, w, st));
+    info->passes = 1;
+    *qidx = tmp;
+    return PSD_OK;
+  }
   if (rdiag) {
     fill_value_kernel<<<(w + 255) / 256, 256, 0, st>>>(rdiag, w, 1.0);
     launched(1);
@@ -467,7 +506,9 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
                        p->Rinv1, p->dinv1, p->qrstat + 8) != 0)
       return fail(PSD_ERR_INVALID_PARAMS, "width %d too large for the CholeskyQR kernel", w);
     double hs2[16];
-    PSD_CUDA_CHECK(psd::read_small(hs2, p->qrstat, sizeof(hs2), st), "qr status");
+    PSD_CUDA_CHECK(psd::read_small2(hs2, p->qrstat, sizeof(hs2), &info->span_redo, p->ints + p->w + 4,
+                                    sizeof(int), st),
+                   "qr status");
     PSD_TRY(sync(st, "cholesky"));
     std::memcpy(hs, hs2, sizeof(hs));
     const double trace = hs[1];
@@ -545,6 +586,10 @@ int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* o
   const ll ld = p->ldp;
   p->gq_P = nullptr;   // planes of an earlier call's panels are never reused
   const bool stabilize = q >= 2 || always_stabilize;               // sketch.py:74
+  // power-step QRs decided on the device (no host round trip) unless a redo asked otherwise
+  static const bool dev_span_on = [] { const char* e = getenv("PSD_SPAN_DEVICE"); return !(e && e[0] == '0'); }();
+  const bool dev_span = stabilize && !p->span_host && dev_span_on;
+  if (dev_span) PSD_CUDA_CHECK(cudaMemsetAsync(p->ints + p->w + 4, 0, sizeof(int), st), "span flag");
   int y = 0;
   PSD_TRY(mul(omega, ldo, w, bufs[0], ld, false));                 // :75
   // deferred input validation (psd_ran_proj): the host collects the symmetry statistics
@@ -552,12 +597,12 @@ int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* o
   if (after_first) PSD_TRY(after_first());
   for (int it = 0; it < q; ++it) {                                 // :76-82
     QrInfo tmp;
-    if (stabilize) PSD_TRY(cholqr(p, bufs, y, (y + 1) % 3, m, w, nullptr, &y, &tmp, st, true));
+    if (stabilize) PSD_TRY(cholqr(p, bufs, y, (y + 1) % 3, m, w, nullptr, &y, &tmp, st, true, dev_span));
     const int z = (y + 1) % 3;
     // z = xᵀ @ y (sketch.py:79); for bitwise-symmetric X this equals X·Y exactly
     PSD_TRY(mul(bufs[y], ld, w, bufs[z], ld, true));
     int zq = z;
-    if (stabilize) PSD_TRY(cholqr(p, bufs, z, (z + 1) % 3, n, w, nullptr, &zq, &tmp, st, true));
+    if (stabilize) PSD_TRY(cholqr(p, bufs, z, (z + 1) % 3, n, w, nullptr, &zq, &tmp, st, true, dev_span));
     const int ny = (zq + 1) % 3;
     PSD_TRY(mul(bufs[zq], ld, w, bufs[ny], ld, false));
     y = ny;
@@ -567,7 +612,13 @@ int range_finder_core(psd_plan* p, const MulFn& mul, ll m, ll n, const double* o
   // next matrix's preparation here (psd_plan_prefetch)
   if (before_final_qr) before_final_qr();
   int qb = y;
-  PSD_TRY(cholqr(p, bufs, y, (y + 1) % 3, n, w, p->rdiag, &qb, qi, st));   // :84-85
+  const int rcq = cholqr(p, bufs, y, (y + 1) % 3, n, w, p->rdiag, &qb, qi, st);   // :84-85
+  if (dev_span) {   // a power step needed the host loop (also when the final QR failed after it): redo
+    int fl = qi->span_redo;
+    if (rcq != PSD_OK && psd::read_small(&fl, p->ints + p->w + 4, sizeof(int), st) != cudaSuccess) fl = 0;
+    if (fl) return kSpanRedo;
+  }
+  PSD_TRY(rcq);
   if (qi->zero) {
     *width_out = 0;
     *qidx = qb;
@@ -857,8 +908,16 @@ int psd_range_finder(psd_plan* p, const double* x, int64_t m, int64_t n, int64_t
   const MulFn mul = [&](const double* P, ll ldP, int w, double* out, ll ldo2, bool t) {
     return xmul_rect(p, x, m, n, ldx, P, ldP, w, out, ldo2, alpha, t && use_t, st);
   };
-  PSD_TRY(range_finder_core(p, mul, m, n, omega, ldo, width, q, false,
-                            (flags & PSD_FLAG_STRICT) != 0, bufs, &qb, &wk, &qi, st));
+  int rc = range_finder_core(p, mul, m, n, omega, ldo, width, q, false, (flags & PSD_FLAG_STRICT) != 0, bufs,
+                             &qb, &wk, &qi, st);
+  if (rc == kSpanRedo) {   // a device-decided power-step QR needed more passes: host-driven redo
+    qi = QrInfo();
+    p->span_host = true;
+    rc = range_finder_core(p, mul, m, n, omega, ldo, width, q, false, (flags & PSD_FLAG_STRICT) != 0, bufs,
+                           &qb, &wk, &qi, st);
+    p->span_host = false;
+  }
+  PSD_TRY(rc);
   if (wk > 0) {
     psd::copy_matrix(bufs[qb], p->ldp, basis, ldb, m, wk, st);
   }
@@ -1361,9 +1420,24 @@ static int ran_proj_impl(psd_plan* p, const double* x64, const float* x32, int64
     if (prefetch_next) launch_prefetch(p, hint_x, hint_n, hint_ldx, st);
     if (prefetch_next32) launch_prefetch32(p, hint_x32, hint_n, hint_ldx, st);
   };
-  PSD_TRY(range_finder_core(p, mul, n, n, omega, ldo_eff, w, q, f32, (flags & PSD_FLAG_STRICT) != 0,
-                            bufs, &qb, &wk, &qi, st, resolve_sym,
-                            pf_at == 1 ? std::function<void()>(start_prefetch) : nullptr));
+  bool pf_started = false;
+  auto start_once = [&]() {
+    if (!pf_started) start_prefetch();
+    pf_started = true;
+  };
+  auto run_rf = [&]() {
+    return range_finder_core(p, mul, n, n, omega, ldo_eff, w, q, f32, (flags & PSD_FLAG_STRICT) != 0, bufs,
+                             &qb, &wk, &qi, st, resolve_sym,
+                             pf_at == 1 ? std::function<void()>(start_once) : nullptr);
+  };
+  int rc = run_rf();
+  if (rc == kSpanRedo) {   // a device-decided power-step QR needed more passes: host-driven redo
+    qi = QrInfo();
+    p->span_host = true;
+    rc = run_rf();
+    p->span_host = false;
+  }
+  PSD_TRY(rc);
   PSD_TRY(resolve_sym());
   r.qr_passes = qi.passes;
   r.qr_shifted = qi.shifted;
