@@ -190,3 +190,24 @@ def test_symmetric_alpha_estimate_matches_row_gemv(n):
     ref = orc.min_eig_magnitude(x, 10, v1=v1, v2=v2)
     assert abs(a - b) <= 1e-12 * max(1.0, abs(b))
     assert abs(a - ref) <= 1e-10 * max(1.0, abs(ref))
+
+
+@pytest.mark.gpu
+def test_power_step_qr_redo_path():
+    """q = 2 on a graded spectrum: the power-step samples are ill-conditioned (κ ≫ 1e4), so a
+    device-decided one-pass QR raises its flag and the range finder is redone with the
+    host-driven loop (api.cu, kSpanRedo); the result must match the CPU oracle."""
+    import paper_2410_19208_b200 as psd
+    from oracle import psd_oracle as orc
+    n, k, l, q = 512, 24, 8, 2
+    g = np.random.default_rng(11)
+    u, _ = np.linalg.qr(g.standard_normal((n, n)))
+    lam = np.concatenate([np.geomspace(1e4, 1e-4, 20), -np.geomspace(1e2, 1e-3, 20), np.zeros(n - 40)])
+    x = (u * lam) @ u.T
+    x = (x + x.T) / 2
+    om = g.standard_normal((n, k + l))
+    rep = psd.ran_proj(x, psd.RangeParams(k=k, l=l, q=q), None, omega=om)
+    ref = orc.ran_proj(x, k, l, q, omega=om)
+    assert rep.basis_width == ref.basis_width and rep.effective_rank == ref.effective_rank
+    err = np.linalg.norm(rep.result - ref.result) / np.linalg.norm(ref.result)
+    assert err <= 1e-10, err
