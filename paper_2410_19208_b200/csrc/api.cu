@@ -423,6 +423,30 @@ struct QrInfo {
   int span_redo = 0;           // a device-decided power-step QR missed its one-pass acceptance
 };
 
+// The final QR's first two passes without host round trips: the same candidate rule on the
+// device, |R_ii| accumulated from the chosen factor, and the pass's status (plus the power-step
+// redo flag) saved for the host to replay the decisions after one read (cholqr below).
+__global__ void qr_select_final_kernel(const double* __restrict__ stat, double* __restrict__ rinv,
+                                       const double* __restrict__ rinv1, const double* __restrict__ l,
+                                       const double* __restrict__ l1, int w, double* __restrict__ rdiag,
+                                       double* __restrict__ save, const int* __restrict__ redo) {
+  __shared__ int shift_s;
+  if (threadIdx.x == 0) {
+    const double info = stat[0], mn = stat[2], mx = stat[3];
+    const bool bad = info != 0.0 || !isfinite(mn) || !isfinite(mx);
+    const double kest = mn > 0.0 ? mx / mn : INFINITY;
+    shift_s = (bad || kest > 3e6) ? 1 : 0;
+  }
+  if (threadIdx.x < 16) save[threadIdx.x] = threadIdx.x == 15 ? (double)*redo : stat[threadIdx.x];
+  __syncthreads();
+  const bool shift = shift_s != 0;
+  const double* ls = shift ? l1 : l;
+  if (rdiag)
+    for (int i = threadIdx.x; i < w; i += blockDim.x) rdiag[i] *= fabs(ls[(long long)i * w + i]);
+  if (shift)
+    for (long long e = threadIdx.x; e < (long long)w * w; e += blockDim.x) rinv[e] = rinv1[e];
+}
+
 // Power-step (span-only) CholeskyQR without a host round trip: the candidate choice of the
 // host loop below (shift iff Cholesky breakdown or κ-estimate > 3e6) made on the device, and
 // a flag raised when the pass would not have been accepted there (shifted, κ-estimate > 1e4,
@@ -479,8 +503,77 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
   double kest0 = 0.0;
   bool verified = false;
   const double u = 1.1102230246251565e-16;
-  double hs[4];
-  for (int pass = 0; pass < 10; ++pass) {
+  // host decision of one pass from its status (the loop below, or replayed for deferred passes)
+  // → 1: stop with Y == 0, < 0: error; sets shift
+  auto decide = [&](const double* hs2, int pass, bool& shift) -> int {
+    const double trace = hs2[1];
+    if (pass == 0) {
+      info->frob = std::sqrt(std::max(trace, 0.0));
+      if (trace == 0.0) {
+        info->zero = true;
+        return 1;
+      }
+    }
+    if (!std::isfinite(trace)) return fail(PSD_ERR_CONVERGENCE, "non-finite Gram matrix in QR");
+    const bool bad = hs2[0] != 0.0 || !std::isfinite(hs2[2]) || !std::isfinite(hs2[3]);
+    const double kest = (hs2[2] > 0.0) ? hs2[3] / hs2[2] : INFINITY;
+    if (pass == 0) kest0 = kest;
+    shift = bad || kest > 3e6;
+    if (shift) {
+      // Fukaya et al. shifted CholeskyQR: s = 11(mn + n(n+1))·u·‖Y‖² (candidate 1)
+      if (hs2[8] != 0.0)
+        return fail(PSD_ERR_CONVERGENCE, "shifted CholeskyQR broke down (pivot %d)", (int)hs2[8]);
+      info->shifted = 1;
+    }
+    info->passes++;
+    unshifted_run = shift ? 0 : unshifted_run + 1;
+    if ((unshifted_run >= 2 && kest0 <= 1e4) || (span_only && !shift && kest <= 1e4)) verified = true;
+    return PSD_OK;
+  };
+  int first = 0;
+  static const bool defer_on = [] { const char* e = getenv("PSD_QR_DEFER"); return !(e && e[0] == '0'); }();
+  if (!span_only && defer_on) {
+    // the first two passes with device-side candidate choice, then ONE read of both statuses
+    // (and |R_ii|): the host replays the loop's decisions; identical kernels and results
+    constexpr int kDefer = 2;
+    const int c0 = cur;
+    const double sfac = 11.0 * ((double)n * w + (double)w * (w + 1)) * u;
+    for (int pass = 0; pass < kDefer; ++pass) {
+      PSD_TRY(panel_tn(p, bufs[cur], bufs[cur], ld, n, w, p->G, true, st));
+      if (psd::chol_fast(p->G, w, w, 0.0, p->L, w, p->Rinv, w, p->dinv, p->qrstat, st, sfac, p->L1,
+                         p->Rinv1, p->dinv1, p->qrstat + 8) != 0)
+        return fail(PSD_ERR_INVALID_PARAMS, "width %d too large for the CholeskyQR kernel", w);
+      qr_select_final_kernel<<<1, 1024, 0, st>>>(p->qrstat, p->Rinv, p->Rinv1, p->L, p->L1, w, rdiag,
+                                                 p->qrstat + 16 + 16 * pass, p->ints + p->w + 4);
+      launched(1);
+      PSD_TRY(panel_nn(p, bufs[cur], ld, p->Rinv, w, bufs[tmp], ld, n, w, w, st));
+      std::swap(cur, tmp);
+    }
+    double saved[2 * 16];
+    if (rdiag) info->rdiag.assign(w, 0.0);
+    PSD_CUDA_CHECK(psd::read_small2(saved, p->qrstat + 16, sizeof(saved), rdiag ? info->rdiag.data() : nullptr,
+                                    rdiag, rdiag ? w * sizeof(double) : 0, st),
+                   "qr status");
+    PSD_TRY(sync(st, "cholesky"));
+    info->span_redo = (int)saved[16 + 15];
+    for (int pass = 0; pass < kDefer; ++pass) {
+      bool shift = false;
+      const int r = decide(saved + 16 * pass, pass, shift);
+      if (r == 1) {   // Y == 0 (the passes after it computed nothing the caller uses)
+        *qidx = c0;
+        return PSD_OK;
+      }
+      if (r != PSD_OK) return r;
+      if (verified) break;   // only after the second pass (unshifted_run ≥ 2 or span rule)
+    }
+    if (verified) {
+      *qidx = cur;
+      return PSD_OK;
+    }
+    info->rdiag.clear();   // not final yet
+    first = kDefer;
+  }
+  for (int pass = first; pass < 10; ++pass) {
     PSD_TRY(panel_tn(p, bufs[cur], bufs[cur], ld, n, w, p->G, true, st));
     if (unshifted_run >= 2) {
       // verification Gram after two unshifted passes: accept if ‖QᵀQ − I‖_max small
@@ -510,38 +603,19 @@ int cholqr(psd_plan* p, double** bufs, int cur, int tmp, ll n, int w, double* rd
                                     sizeof(int), st),
                    "qr status");
     PSD_TRY(sync(st, "cholesky"));
-    std::memcpy(hs, hs2, sizeof(hs));
-    const double trace = hs[1];
-    if (pass == 0) {
-      info->frob = std::sqrt(std::max(trace, 0.0));
-      if (trace == 0.0) {
-        info->zero = true;
-        *qidx = cur;
-        return PSD_OK;
-      }
+    bool shift = false;
+    const int r = decide(hs2, pass, shift);
+    if (r == 1) {
+      *qidx = cur;
+      return PSD_OK;
     }
-    if (!std::isfinite(trace)) return fail(PSD_ERR_CONVERGENCE, "non-finite Gram matrix in QR");
-    const bool bad = hs[0] != 0.0 || !std::isfinite(hs[2]) || !std::isfinite(hs[3]);
-    const double kest = (hs[2] > 0.0) ? hs[3] / hs[2] : INFINITY;
-    if (pass == 0) kest0 = kest;
-    const bool shift = bad || kest > 3e6;
-    if (shift) {
-      // Fukaya et al. shifted CholeskyQR: s = 11(mn + n(n+1))·u·‖Y‖² (candidate 1 above)
-      if (hs2[8] != 0.0)
-        return fail(PSD_ERR_CONVERGENCE, "shifted CholeskyQR broke down (pivot %d)", (int)hs2[8]);
-      info->shifted = 1;
-    }
+    if (r != PSD_OK) return r;
     const double* Lsel = shift ? p->L1 : p->L;
     const double* Rsel = shift ? p->Rinv1 : p->Rinv;
     if (rdiag) psd::accumulate_diag(Lsel, w, w, rdiag, st);
     PSD_TRY(panel_nn(p, bufs[cur], ld, Rsel, w, bufs[tmp], ld, n, w, w, st));
     std::swap(cur, tmp);
-    info->passes++;
-    unshifted_run = shift ? 0 : unshifted_run + 1;
-    if ((unshifted_run >= 2 && kest0 <= 1e4) || (span_only && !shift && kest <= 1e4)) {
-      verified = true;
-      break;
-    }
+    if (verified) break;
   }
   if (!verified) return fail(PSD_ERR_CONVERGENCE, "CholeskyQR did not reach orthogonality");
   *qidx = cur;
@@ -710,7 +784,7 @@ int psd_plan_create(psd_plan** out, int64_t n, int32_t width, int32_t device) {
   ok &= (p->gpart = alloc(p, p->gparts)) != nullptr;
   ok &= (p->stats = alloc(p, 4)) != nullptr;
   ok &= (p->scal = alloc(p, 8)) != nullptr;
-  ok &= (p->qrstat = alloc(p, 16)) != nullptr;   // [0, 8): unshifted candidate, [8, 16): shifted
+  ok &= (p->qrstat = alloc(p, 48)) != nullptr;   // [0, 8): unshifted candidate, [8, 16): shifted; [16, 48): deferred passes
   ok &= (p->dinv = alloc(p, (size_t)((width + 31) / 32) * 1024)) != nullptr;
   psd::GemmOp rop;
   rop.M = (int)n;
