@@ -735,11 +735,20 @@ def run_solver(a):
     randomized projection each; value = solver iterations/s."""
     import numpy as np
 
-    from oracle import sdls_oracle as so
+    from paper_2410_19208_b200 import workloads
     cfg = CONFIGS["c5"]
     n, m = a.n, cfg["m"]
-    prob = so.config5_instance(n, m, nnz_per=4, seed=5)
-    beta = so.lipschitz_beta(prob)
+    sp = workloads.c5_problem(n, m, nnz_per=4, seed=5)
+    beta = workloads.c5_step_size(sp)
+
+    def cpu_solve(its):
+        """The CPU arm of this line (reference arm / cpu_baseline leg only): the
+        oracle's sparse-COO restatement of psdcone.solve on the same instance."""
+        from oracle import sdls_oracle as so
+        prob = so.SparseProblem(sp.c, sp.rho, sp.con, sp.rows, sp.cols, sp.vals, sp.b)
+        t0 = time.perf_counter()
+        so.solve(prob, "randomized", a.k, a.p, a.q, beta=beta, epsilon=1e-300, max_iter=its, rng=1)
+        return its / (time.perf_counter() - t0)
     metric = "SDLS solver iterations/s at n=4096, m=20000, k=64, q=1 (config 5)"
     conf = {"workload": f"BASELINE config 5: sdls.solve, n={n}, m={m}, k={a.k}, p={a.p}, q={a.q}, "
                         f"randomized projector, beta=1/L={beta:.4g}, {a.steps} iterations",
@@ -749,9 +758,7 @@ def run_solver(a):
         return
     if a.impl == "reference":
         its = max(1, min(a.steps, 3))
-        t0 = time.perf_counter()
-        so.solve(prob, "randomized", a.k, a.p, a.q, beta=beta, epsilon=1e-300, max_iter=its, rng=1)
-        value = its / (time.perf_counter() - t0)
+        value = cpu_solve(its)
         cores = cpu_cores()
         print(json.dumps({"metric": metric, "value": value, "unit": "iterations/s", "impl": "reference",
                           "n_gpus": 1, "steps": its, "warmup": 0, "ms_per_step": 1000 / value,
@@ -767,7 +774,6 @@ def run_solver(a):
 
     import paper_2410_19208_b200 as psd
     dev = torch.device("cuda", 0)
-    sp = psd.SparseSdlsProblem(prob.c, 1.0, prob.con, prob.rows, prob.cols, prob.vals, prob.b)
     pcfg = psd.ProjectorConfig(method="randomized", params=psd.RangeParams(k=a.k, l=a.p, q=a.q))
     # y0 / Ω from the device Philox stream (perf mode, as the C3 line); the numpy
     # stream (reference draw order) costs ~3 ms of host RNG per iteration
@@ -786,9 +792,7 @@ def run_solver(a):
             "timing": "wall clock around solve() incl. per-iteration host syncs, problem upload "
                       "and the final dense reconstruction; y0 and Ω from the device Philox stream"}
     if not a.no_cpu_baseline:
-        t0 = time.perf_counter()
-        so.solve(prob, "randomized", a.k, a.p, a.q, beta=beta, epsilon=1e-300, max_iter=2, rng=1)
-        v = 2 / (time.perf_counter() - t0)
+        v = cpu_solve(2)
         line["cpu_baseline"] = {"value": v, "unit": "iterations/s", "cores": cpu_cores(), "kind": "port",
                                 "sample": "2 iterations of the oracle sparse-COO restatement of psdcone.solve"}
     print(json.dumps(line), flush=True)

@@ -82,3 +82,49 @@ def c4_rows(n, r0, r1, seed=0, rank=200, device="cuda", chunk_rows=None):
                                             int(seed) & 0xFFFFFFFFFFFFFFFF,
                                             1e-3 / math.sqrt(2.0 * n), 1.0, st))
     return x
+
+
+def c5_problem(n=4096, m=20000, nnz_per=4, seed=0, rank=10):
+    """BASELINE config 5 as a ``SparseSdlsProblem`` (host COO triplets; the
+    solver uploads them): constraint i holds ``nnz_per`` seeded off-diagonal
+    N(0,1) entries, each stored at (r, c) and (c, r); b = A(Z Zᵀ) with Z n×rank
+    Gaussian; C = Wigner + 2I; ρ = 1.  The draw order (positions, values, Z, G)
+    is the one tests/ pin against the CPU restatement."""
+    import numpy as np
+
+    from .sdls import SparseSdlsProblem
+    rng = np.random.default_rng(seed)
+    r = rng.integers(0, n, size=(m, nnz_per))
+    c = rng.integers(0, n - 1, size=(m, nnz_per))
+    c += c >= r                                            # skip the diagonal
+    v = rng.standard_normal((m, nnz_per))
+    z = rng.standard_normal((n, rank))
+    g = rng.standard_normal((n, n))
+    rows = np.stack([r, c], axis=-1).reshape(-1)           # (r, c) then its mirror
+    cols = np.stack([c, r], axis=-1).reshape(-1)
+    vals = np.repeat(v, 2, axis=1).reshape(-1)
+    con = np.repeat(np.arange(m), 2 * nnz_per)
+    cmat = (g + g.T) / (2.0 * math.sqrt(n)) + 2.0 * np.eye(n)
+    x0 = z @ z.T
+    b = np.zeros(m)
+    np.add.at(b, con, vals * x0[rows, cols])               # bᵢ = ⟨Aᵢ, X₀⟩
+    return SparseSdlsProblem(cmat, 1.0, con, rows, cols, vals, b)
+
+
+def c5_step_size(problem, iters=50, seed=0):
+    """β = 1/L, L = λ_max of the constraint Gram ⟨Aᵢ, Aⱼ⟩_F, by power iteration
+    on v ↦ A(A*(v)) over the COO triplets (host, set-up only)."""
+    import numpy as np
+    n, m = problem.n, problem.m
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(m)
+    v /= np.linalg.norm(v)
+    lam = 0.0
+    for _ in range(iters):
+        adj = np.zeros((n, n))
+        np.add.at(adj, (problem.rows, problem.cols), v[problem.con] * problem.vals)
+        w = np.zeros(m)
+        np.add.at(w, problem.con, problem.vals * adj[problem.rows, problem.cols])
+        lam = float(np.linalg.norm(w))
+        v = w / lam
+    return 1.0 / lam

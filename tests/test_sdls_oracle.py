@@ -58,3 +58,18 @@ def test_config5_instance_shapes():
     np.testing.assert_array_equal(x, x.T)
     beta = so.lipschitz_beta(p)
     assert 0 < beta < 1
+
+
+def test_product_config5_generator_matches_the_oracle_instance():
+    """bench.py's own arm builds config 5 with the package's generator
+    (workloads.c5_problem / c5_step_size); the CPU arm solves the oracle's
+    SparseProblem of the same triplets — both must be the same instance."""
+    from oracle import sdls_oracle as so
+    from paper_2410_19208_b200 import workloads
+    ours = workloads.c5_problem(192, 300, nnz_per=4, seed=5)
+    ref = so.config5_instance(192, 300, nnz_per=4, seed=5)
+    for name in ("c", "con", "rows", "cols", "vals", "b"):
+        assert np.array_equal(getattr(ours, name), getattr(ref, name)), name
+    assert ours.rho == ref.rho
+    assert np.all(ours.rows != ours.cols)
+    assert workloads.c5_step_size(ours, iters=20) == so.lipschitz_beta(ref, iters=20)
