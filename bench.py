@@ -537,6 +537,24 @@ def run_ours(a):
     traffic = load_traffic("oz_traffic.json" if engine == 1 else "gemm_traffic.json")
     stages = {k: round(v[0] / a.steps, 3) for k, v in prof.items() if v[1]}
 
+    # the same K steps with no prefetch hints (every projection validates and prepares its
+    # own X on the caller's stream): reported beside the pipelined headline value
+    unpipelined = None
+    if a.config != "c1" and not a.no_prefetch:
+        for i in range(min(nwarm, 2)):
+            psd.ran_proj(pool[i % a.pool], params, rng, out=out64)
+        torch.cuda.synchronize(dev)
+        u0 = torch.cuda.Event(enable_timing=True)
+        u1 = torch.cuda.Event(enable_timing=True)
+        u0.record()
+        for i in range(a.steps):
+            psd.ran_proj(pool[i % a.pool], params, rng, out=out64)
+        u1.record()
+        torch.cuda.synchronize(dev)
+        ums = _max_over_ranks(torch, dist, world, u0.elapsed_time(u1), dev)
+        unpipelined = {"value": world * a.steps / (ums / 1000.0), "unit": UNIT, "ms_per_step": ums / a.steps,
+                       "steps": a.steps, "note": "same pool and steps, ran_proj without prefetch= hints"}
+
     fp32 = None
     if a.config == "c3" and not a.no_fp32:
         fp32 = run_fp32_leg(a, torch, psd, pool, params, rng, dev, world, peaks)
@@ -607,6 +625,8 @@ def run_ours(a):
         line["cpu_baseline"] = cpu
     if e2e:
         line["e2e"] = e2e
+    if unpipelined:
+        line["unpipelined"] = unpipelined
     if fp32:
         line["fp32"] = fp32
     if scaled:

@@ -13,7 +13,7 @@ timeout 1500 python bench.py --impl reference --steps 16 --warmup 3 > $O/bench_r
 F="--steps 2 --warmup 1 --pool 1 --no-peaks --no-fp32 --no-scaled --no-e2e --no-cpu-baseline --no-c4"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 450 -c 1500 --csv --log-file $O/launches_bench.csv python bench.py $F --no-prefetch > $O/ncu_list.log 2>&1
 timeout 600 python tools/selfcheck.py 10 > $O/selfcheck.log 2>&1
-for K in i8_gemm2 residues_rows_max i8_syrk sym_stats gemv_kernel tc32_gemm2 jacobi_persistent crt1_kernel; do
+for K in i8_gemm2 residues_rows_max i8_syrk sym_stats symv_tiles tc32_gemm2 jacobi_persistent crt1_kernel; do
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:$K -s 2 -c 1 -o $O/full_$K python bench.py --steps 1 --warmup 1 --pool 1 --no-peaks --no-e2e --no-cpu-baseline --no-c4 > $O/ncu_full_$K.log 2>&1
 done
 tail -n 3 $O/pytest_gpu.log $O/smoke.log $O/selfcheck.log
