@@ -8,7 +8,7 @@ GEMM summation order does).  Rank-deficient sketches (width > numerical rank of
 X at q = 1) and clipping thresholds inside a near-degenerate eigenvalue cluster
 leave the result determined by roundoff at the 1e-9..1e-8 level in ANY FP64
 implementation; a case passes when the GPU result is within 1e-10 of the oracle
-or within 10× that self-sensitivity.
+or within 2× that self-sensitivity (the bar of tests/test_gpu_ozaki_syrk.py).
 
     python tools/stress_parity.py [cases] [seed]
 """
@@ -49,12 +49,28 @@ def main():
         else:
             o = orc.ran_proj(x, k, l, q, omega=om)
         t_cpu = time.perf_counter() - t0
-        e = rs.choice([-1.0, 1.0], (n, n))
-        e = np.triu(e) + np.triu(e, 1).T
-        xp = x * (1 + 2.0 ** -53 * e)
-        op = orc.ran_proj_scal(xp, k, l, q, alpha, omega=om) if alpha > 0 else orc.ran_proj(xp, k, l, q, omega=om)
-        self_sens = np.linalg.norm(op.result - o.result) / max(np.linalg.norm(o.result), 1e-300)
-        del e, xp
+        # the reference's own sensitivity: the larger of two independent one-ulp perturbations
+        # (as tests/test_gpu_ozaki_syrk.py), a third when the first two sit above the bar
+        self_sens, samples = 0.0, 0
+        while samples < 2 or (samples < 3 and self_sens > 1e-10):
+            e = rs.choice([-1.0, 1.0], (n, n))
+            e = np.triu(e) + np.triu(e, 1).T
+            xp = x * (1 + 2.0 ** -53 * e)
+            op = orc.ran_proj_scal(xp, k, l, q, alpha, omega=om) if alpha > 0 else orc.ran_proj(xp, k, l, q, omega=om)
+            self_sens = max(self_sens, np.linalg.norm(op.result - o.result) / max(np.linalg.norm(o.result), 1e-300))
+            samples += 1
+            del e, xp
+        # ... and under a re-ordering of its own sums: the same problem with rows/columns
+        # symmetrically permuted (P X Pᵀ, P Ω) is the same projection, P X̂₊ Pᵀ, computed by
+        # the same reference code with every GEMM / QR / eigh summing in a different order
+        ulp_sens = self_sens
+        perm = rs.permutation(n)
+        inv = np.argsort(perm)
+        xq, omq = np.ascontiguousarray(x[np.ix_(perm, perm)]), np.ascontiguousarray(om[perm])
+        oq = orc.ran_proj_scal(xq, k, l, q, alpha, omega=omq) if alpha > 0 else orc.ran_proj(xq, k, l, q, omega=omq)
+        perm_sens = np.linalg.norm(oq.result[np.ix_(inv, inv)] - o.result) / max(np.linalg.norm(o.result), 1e-300)
+        self_sens = max(self_sens, perm_sens)
+        del xq, omq, oq
         xd, omd = torch.from_numpy(x).cuda(), torch.from_numpy(om).cuda()
         prm = psd.RangeParams(k=k, l=l, q=q)
         if alpha > 0:
@@ -78,10 +94,10 @@ def main():
         worst["fp32"] = max(worst["fp32"], e32)
         info = r.device_info
         # FP32: ≤1e-4 unless the problem is roundoff-determined even in FP64 (then FP32 is moot)
-        ok = (e64 <= max(1e-10, 10 * self_sens) and (e32 <= 1e-4 or self_sens > 1e-12) and sym
+        ok = (e64 <= max(1e-10, 2 * self_sens) and (e32 <= 1e-4 or self_sens > 1e-12) and sym
               and r.effective_rank == o.effective_rank and r.basis_width == o.basis_width)
         print(f"case {c:2d} {kind:7s} n={n} k={k} l={l} q={q} alpha={alpha:.3f} rank={r.effective_rank}/"
-              f"{o.effective_rank} width={r.basis_width}/{o.basis_width} engines={info['sketch_engine']}/{info['recon_engine']} fp64 {e64:.2e} (ref 1-ulp {self_sens:.1e}) "
+              f"{o.effective_rank} width={r.basis_width}/{o.basis_width} engines={info['sketch_engine']}/{info['recon_engine']} fp64 {e64:.2e} (ref 1-ulp {ulp_sens:.1e}, re-ordered {perm_sens:.1e}) "
               f"sym={sym} fp32 {e32:.2e} cpu {t_cpu:.1f}s {'OK' if ok else 'FAIL'}", flush=True)
     print(f"worst fp64 {worst['fp64']:.2e} (bar 1e-10), fp32 {worst['fp32']:.2e} (bar 1e-4)")
 
