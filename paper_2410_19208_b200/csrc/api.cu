@@ -1164,8 +1164,9 @@ void launch_prefetch(psd_plan* p, const double* x, ll n, ll ldx, cudaStream_t st
   psd::sym_stats(x, n, ldx, p->stats_alt, p->side, p->oz_rowmax_alt, std::max<ll>(1, nt * (nt + 1) / 2 / pairs));
   psd::copy_to_mapped(p->pf_dev, p->stats_alt, 3 * sizeof(double), p->side);
   cudaEventRecord(p->ev_pf_stats, p->side);
+  static const int pf_threads = [] { const char* e = getenv("PSD_PF_THREADS"); return e ? atoi(e) : 256; }();
   psd::oz_prepare_rows_max(x, n, n, ldx, p->oz_rowmax_alt, p->oz_e_alt, p->oz_ar_alt, p->oz_ldk, p->side,
-                           std::max<ll>(1, n / rows));
+                           std::max<ll>(1, n / rows), pf_threads);
   cudaEventRecord(p->ev_pf_done, p->side);
   p->pf_x = x;
   p->pf_x32 = nullptr;

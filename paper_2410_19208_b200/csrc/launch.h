@@ -108,7 +108,7 @@ long long oz_max_k();   // largest K the exact CRT reconstruction admits (2^18)
 // low-priority side stream that must yield SMs to the caller's stream — the pipelined prefetch)
 void oz_prepare_rows_max(const double* x, long long rows, long long cols, long long ldx,
                          const unsigned* rowmax_hi, int* e, int8_t* r, long long ldr, cudaStream_t st,
-                         long long grid = 0);
+                         long long grid = 0, int threads = 256);
 void oz_prepare_rows(const double* x, long long rows, long long cols, long long ldx, int* e, int8_t* r,
                      long long ldr, cudaStream_t st);
 int oz_gemm(const OzOp& op, cudaStream_t st);

@@ -897,11 +897,13 @@ long long oz_max_k() { return oz::kMaxK; }
 
 void oz_prepare_rows_max(const double* x, long long rows, long long cols, long long ldx,
                          const unsigned* rowmax, int* e, int8_t* r, long long ldr, cudaStream_t st,
-                         long long grid_req) {
+                         long long grid_req, int threads) {
   ensure_oz_constants();
   if (cols % 8 == 0 && ldx % 2 == 0 && ldr % 8 == 0 && (uintptr_t)x % 16 == 0) {
     const unsigned grid = (unsigned)std::min<long long>(rows, grid_req > 0 ? grid_req : (long long)device_info().sms * 8);
-    oz::residues_rows_max_kernel<<<grid, 256, 0, st>>>(x, rows, cols, ldx, rowmax, e, r, ldr, ldr * rows);
+    // threads < 256 (side-stream use): smaller CTAs pack beside the caller's register-heavy kernels
+    const unsigned block = (unsigned)std::min(256, std::max(32, threads / 32 * 32));
+    oz::residues_rows_max_kernel<<<grid, block, 0, st>>>(x, rows, cols, ldx, rowmax, e, r, ldr, ldr * rows);
     count_launch();
   } else {
     oz_prepare_rows(x, rows, cols, ldx, e, r, ldr, st);
