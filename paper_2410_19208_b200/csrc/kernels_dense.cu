@@ -506,7 +506,8 @@ PSD_DEVINL double chol_src(const double* __restrict__ G, long long ldg, const do
 // Dual candidates (gridDim.x == 2): CTA 0 factors G + shift·I into (L, Dinv, status), CTA 1
 // factors G + shift_factor·trace(G)·I into (L1, Dinv1, status1) at the same time — the
 // shifted CholeskyQR fallback is then ready without a second launch and host round trip.
-__global__ void __launch_bounds__(256, 1)
+template <int kNT>
+__global__ void __launch_bounds__(kNT, 1)
     chol_blocked_kernel(const double* __restrict__ G, long long ldg, int m, double shift, double* L,
                         long long ldl, double* Dinv, double* status, double shift_factor, double* L1,
                         double* Dinv1, double* status1) {
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(256, 1)
   __shared__ double red[32];
   __shared__ __align__(16) double colb[kFB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int kNT = 256, kNW = 8;
+  constexpr int kNW = kNT / 32;
   double tr = 0.0;
   for (int i = tid; i < m; i += kNT) tr += G[(long long)i * ldg + i];
   tr = warp_sum(tr);
@@ -837,7 +838,8 @@ int chol_fast(const double* G, long long ldg, int m, double shift, double* L, lo
   int dev = 0;
   cudaGetDevice(&dev);
   if (smem1 > attr1[dev]) {
-    cudaFuncSetAttribute(chol_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+    cudaFuncSetAttribute(chol_blocked_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+    cudaFuncSetAttribute(chol_blocked_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
     attr1[dev] = smem1;
   }
   if (smem2 > attr2[dev]) {
@@ -851,8 +853,14 @@ int chol_fast(const double* G, long long ldg, int m, double shift, double* L, lo
     cudaMemcpyToSymbolAsync(g_chol_t, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
   }
   const bool dual = L1 != nullptr;
-  chol_blocked_kernel<<<dual ? 2 : 1, 256, smem1, st>>>(G, ldg, m, shift, L, ldl, Dinv, status,
-                                                       shift_factor, L1, Dinv1, status1);
+  // 16 warps: the TRSM and trailing-update rounds per warp (dependent global round trips) halve
+  static const int chol_nt = [] { const char* e = getenv("PSD_CHOL_NT"); return e ? atoi(e) : 512; }();
+  if (chol_nt == 512 && m > 64)
+    chol_blocked_kernel<512><<<dual ? 2 : 1, 512, smem1, st>>>(G, ldg, m, shift, L, ldl, Dinv, status,
+                                                             shift_factor, L1, Dinv1, status1);
+  else
+    chol_blocked_kernel<256><<<dual ? 2 : 1, 256, smem1, st>>>(G, ldg, m, shift, L, ldl, Dinv, status,
+                                                             shift_factor, L1, Dinv1, status1);
   count_launch();
   tri_inv_blocked_kernel<<<dim3(nblk, dual ? 2 : 1), 256, smem2, st>>>(L, ldl, m, Dinv, Rinv, ldr, L1,
                                                                      Dinv1, Rinv1);
