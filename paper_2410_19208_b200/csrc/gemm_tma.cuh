@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
             if (m < p.M && m > n) crow[m] = Cs[r * Cfg::C_LD + c];
           }
         }
+        __threadfence_block();   // the tile's reads are done before the consumers may overwrite it
         named_arrive(2, kEpiBarCount);
         ++j;
       }
@@ -369,6 +370,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1)
 #pragma unroll
           for (int e = 0; e < 2; ++e) Cs[r * Cfg::C_LD + b_col<Cfg>(wn * N8W + j, 2 * t + e)] = acc[i][j][e];
       }
+      // bar.arrive does not wait for this warp's shared-memory stores: make the parked tile
+      // visible to the CTA before signalling the store warps (a rare stale-row race otherwise:
+      // 2 of 2080 tiles of the C4-shape reconstruction)
+      __threadfence_block();
       named_arrive(1, kEpiBarCount);
       ++stage_j;
       continue;
